@@ -1,0 +1,384 @@
+#!/usr/bin/env python3
+"""Headline benchmark: Megopolis particles resampled per second on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1)
+
+Workload (BASELINE.json config 4 / metric): Megopolis resampling of N = 2^24
+particles per GPU, Gaussian-family float32 weights with y = 4 (high variance),
+B from the epsilon = 0.01 rule (B = 354), the reference's megores random stream
+(bit-exact with the reference).  One step = one pass of the hot path over one
+batch: weight statistics -> B (host, like the reference) -> Megopolis kernel.
+Inputs are resident in HBM for ``value``; ``e2e`` runs the same step through the
+host-buffer C-ABI entry (pinned host weights in, pinned host ancestors out).
+
+Multi-GPU (weak scaling): rank r owns particles [r*2^24, (r+1)*2^24) of a global
+population of N*G; each step all-gathers the weight slices over NCCL (the
+replicated-weights exchange of SURVEY 8e), computes B on the replicated array and
+resamples its own slice.
+
+The L2 (126 MB) would hold the 64 MiB weight array across steps, so a 256 MiB
+buffer is written between timed steps (outside the CUDA-event windows).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Megopolis particles resampled/sec (N=2^24, 1/2/4/8 B200); % roofline; offspring MSE"
+N_PER_GPU = 1 << 24
+Y = 4.0
+EPS = 0.01
+RUN_SEED = 7
+WEIGHT_SEED = 20240
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=N_PER_GPU, help="particles per GPU")
+    ap.add_argument("--rng", default="megores", choices=["megores", "philox"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--quality-runs", type=int, default=8)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """NVML clock / throttle-reason sampling during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the CPU oracle port (oracle/), all host threads
+
+
+def cpu_rate(oracle, w, b, budget_s, nthreads):
+    """Particles/s of the oracle on a bounded prefix sample of the workload."""
+    n = len(w)
+    p = 4096
+    t0 = time.perf_counter()
+    oracle.megopolis(w, b, seed=RUN_SEED, threads=nthreads, p0=0, p1=p)
+    dt = time.perf_counter() - t0
+    rate = p / max(dt, 1e-6)
+    p = int(min(n, max(4096, rate * budget_s)))
+    p -= p % 32
+    t0 = time.perf_counter()
+    oracle.megopolis(w, b, seed=RUN_SEED, threads=nthreads, p0=0, p1=p)
+    dt = time.perf_counter() - t0
+    return p / dt, p, dt
+
+
+def host_weights(n_global, rank_slice=None):
+    """Synthetic Gaussian-family weights (M/weights.py:100-104) via the device generator."""
+    import paper_2109_13504_b200 as mg
+
+    return mg.gen_gaussian_weights(mg.GaussianWeightParams(Y, n_global), WEIGHT_SEED, "single").values
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle
+
+    import torch
+
+    n = args.n
+    if torch.cuda.is_available():
+        w = host_weights(n).cpu().numpy()
+    else:
+        w = oracle.gen_gaussian_weights(Y, n, WEIGHT_SEED, "single")
+    mean, mx = oracle.weight_mean_max(w)
+    b = oracle.compute_iterations(EPS, mean, mx)
+    threads = oracle.num_threads()
+    per_step_budget = max(2.0, min(15.0, 150.0 / max(1, args.steps + args.warmup)))
+    rate, p, dt = cpu_rate(oracle, w, b, per_step_budget, threads)
+    times = []
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.megopolis(w, b, seed=RUN_SEED, threads=threads, p0=0, p1=p)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    value = p / t
+    sample = f"particles [0, {p}) of N={n} (y=4, B={b}), {args.steps} steps of {t:.2f}s"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3 * n / p,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"megopolis N=2^{int(math.log2(n))} y=4 f32 weights B={b} eps=0.01 megores stream",
+                   "N": n, "B": b},
+        "cpu_baseline": {"value": value, "unit": "particles/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "particles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2109_13504_b200 as mg
+    from paper_2109_13504_b200 import _lib
+    from paper_2109_13504_b200 import _device as D
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    L = _lib.lib()
+    n_loc = args.n
+    n_glob = n_loc * world
+    rng_id = _lib.RNG[args.rng]
+
+    # weights: each rank generates its slice of the global population (device generator,
+    # same per-particle stream as the reference generator) then all-gathers.
+    full = host_weights(n_glob) if world == 1 else None
+    if world > 1:
+        gen_full = host_weights(n_glob)  # deterministic; slice it to emulate per-rank production
+        local_w = gen_full[rank * n_loc:(rank + 1) * n_loc].clone()
+        del gen_full
+        full = torch.empty(n_glob, dtype=torch.float32, device=dev)
+    else:
+        local_w = full
+    stats = torch.empty(8, dtype=torch.float64, device=dev)
+    anc = torch.empty(n_loc, dtype=torch.int64, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sp = ctypes.c_void_p(stream.cuda_stream)
+
+    def gather_weights():
+        if world > 1:
+            dist.all_gather_into_tensor(full, local_w)
+
+    def step(ev=None):
+        """One hot-path pass: (all-gather) -> stats -> B -> megopolis(slice)."""
+        gather_weights()
+        _lib.check(L.mgp_weight_stats(D.ptr(full), 0, n_glob, D.ptr(stats), sp))
+        host = stats.cpu().numpy()  # 64 B; the reference also derives B on the host
+        mean, mx = float(host[1]), float(host[2])
+        b = mg.compute_iterations(EPS, mean, mx).b
+        flags = _lib.FLAG_POSITIVE_NORMAL if host.view(np.int64)[7] == 0 else 0
+        if ev is not None:
+            ev[0].record(stream)
+        _lib.check(L.mgp_resample_range(_lib.KIND["megopolis"], D.ptr(full), 0, n_glob, b, RUN_SEED, 32, 0, 1,
+                                         rng_id, flags, rank * n_loc, (rank + 1) * n_loc, D.ptr(anc), sp))
+        if ev is not None:
+            ev[1].record(stream)
+        return b
+
+    # warm-up
+    for _ in range(max(args.warmup, 3)):
+        b = step()
+    torch.cuda.synchronize()
+
+    # timed region: K steps, each bracketed by CUDA events; L2 flushed between steps
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            flush.fill_(float(s))
+            starts[s].record(stream)
+            b = step(kev[s])
+            ends[s].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [starts[s].elapsed_time(ends[s]) for s in range(args.steps)]
+    kern_ms = [kev[s][0].elapsed_time(kev[s][1]) for s in range(args.steps)]
+    t_total = sum(step_ms)
+    if world > 1:
+        tt = torch.tensor([t_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_total = float(tt.item())
+    ms_per_step = t_total / args.steps
+    value = n_glob / (ms_per_step / 1e3)  # all ranks' particles per second
+    launches = args.steps * (2 + math.ceil(b / 1024))  # stats (2 kernels) + megopolis launches
+
+    # roofline: algorithmic bytes of one Megopolis launch: N*B*4 + N*4 + N*8 + 8*B
+    kern_avg = statistics.mean(kern_ms) / 1e3
+    alg_bytes = n_loc * b * 4 + n_loc * 4 + n_loc * 8 + 8 * b
+    peak, peak_src = load_peaks()
+    achieved = alg_bytes / kern_avg / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "megopolis_traffic.json")) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    # e2e through the host-buffer C-ABI entry (pinned buffers), rank-local population
+    e2e = None
+    if not args.no_e2e:
+        h_w = local_w.cpu().pin_memory() if world > 1 else full.cpu().pin_memory()
+        h_anc = torch.empty(n_loc, dtype=torch.int64).pin_memory()
+        bu = ctypes.c_int32(0)
+
+        def e2e_step():
+            _lib.check(L.mgp_resample_host(_lib.KIND["megopolis"], D.ptr(h_w), 0, n_loc, 0, EPS, RUN_SEED, 32, 0, 1,
+                                           rng_id, D.ptr(h_anc), ctypes.byref(bu), local))
+
+        for _ in range(3):
+            e2e_step()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        reps = max(3, min(args.steps, 10))
+        for _ in range(reps):
+            e2e_step()
+        te = (time.perf_counter() - t0) / reps
+        if world > 1:
+            tt = torch.tensor([te], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": n_loc * world / te, "unit": "particles/s", "h2d_bytes_per_step": 4 * n_loc,
+               "d2h_bytes_per_step": 8 * n_loc, "ms_per_step": te * 1e3, "B": int(bu.value),
+               "path": "mgp_resample_host (pinned host weights -> device -> pinned host ancestors)"}
+
+    # quality (offspring MSE / bias, M/metrics.py) outside the timed region, rank 0
+    quality = None
+    if rank == 0 and args.quality_runs >= 2 and world == 1:
+        qs = {}
+        wv = mg.WeightVector(full, "single")
+        for kind in ("megopolis", "metropolis"):
+            acc = mg.QualityAccumulator(n_glob)
+            fn = mg.make_resampler(kind)
+            for k in range(args.quality_runs):
+                acc.add(mg.ancestors_to_offspring(fn(wv, b, mg.derive_seed(2002, k)), n_glob), wv)
+            st = acc.finalize()
+            qs[kind] = {"mse_per_particle": st.mse_per_particle, "bias_contribution": st.bias_contribution}
+        quality = {"runs": args.quality_runs, **qs, "paper_megopolis_y4": 0.6508, "paper_metropolis": 1.0}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        from oracle import oracle
+
+        w_np = full[:n_loc].cpu().numpy() if world == 1 else local_w.cpu().numpy()
+        rate, p, dt = cpu_rate(oracle, w_np, b, 12.0, oracle.num_threads())
+        cpu = {"value": rate, "unit": "particles/s", "cores": oracle.num_threads(), "kind": "port",
+               "sample": f"oracle/mgp_oracle.c megopolis, particles [0, {p}) of the same N=2^24 y=4 B={b} "
+                         f"workload, {dt:.1f}s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {
+                "workload": f"megopolis N=2^{int(math.log2(n_loc))}/GPU y=4 f32 Gaussian weights, B={b} "
+                            f"(eps=0.01 rule), {args.rng} stream",
+                "N_per_gpu": n_loc, "N_global": n_glob, "B": b, "rng": args.rng,
+                "step": "weight stats -> B (host) -> megopolis" + (" (+ NCCL all-gather)" if world > 1 else ""),
+                "l2": "flushed between timed steps (256 MiB write, outside the event windows)",
+                "parallelism": f"dp{world} weak (replicated weights, particle slices)",
+            },
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "k_megopolis_w32", "kernel_ms": kern_avg * 1e3,
+                         "alg_bytes_per_launch": alg_bytes},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "quality": quality,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

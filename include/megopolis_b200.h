@@ -1,0 +1,145 @@
+/*
+ * megopolis_b200.h -- C ABI of libmgp.so, the B200 (sm_100a) implementation of the
+ * resampling hot path of arXiv 2109.13504 ("The Megopolis Resampler").
+ *
+ * The reference (pkg/src/megores, "M/" below) is a pure-Python/numba package; its
+ * plug-in surface for this path is the Python resampler API
+ *     fn(w: WeightVector, b: int, seed) -> np.int64[N]      (M/resample.py:431-455)
+ * Each entry point below names the reference interface it replaces.  The Python
+ * package paper_2109_13504_b200 binds these with ctypes and mirrors the reference
+ * API (names, arguments, defaults, errors); INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  "d_" pointers are device (HBM) pointers,
+ *     "h_" pointers are host pointers (pinned for asynchronous copies).
+ *   - stream: a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Device-pointer calls are asynchronous on that stream and run on the calling
+ *     thread's current device.
+ *   - dtype: MGP_F32 / MGP_F64 weights (the reference's "single" / "double",
+ *     M/weights.py:39).  Ancestors and offspring counts are int64 (the reference's
+ *     np.int64 results, M/resample.py:128, 368).
+ *   - rng: MGP_RNG_MEGORES is the reference's keyed splitmix64 stream
+ *     (M/rng.py:85-121), bit-exact with the reference; MGP_RNG_PHILOX is
+ *     Philox4x32-10 with the same counter layout.
+ *   - Return codes: 0 = ok; MGP_EINVAL (< 0) = invalid argument, the reference's
+ *     ValueError (message via mgp_last_error(), same text as the reference);
+ *     MGP_EUNSUPPORTED = size/feature outside this build; > 0 = cudaError_t.
+ *   - Thread-safe: no global mutable state; scratch is stream-ordered
+ *     (cudaMallocAsync); mgp_last_error() is thread-local.
+ *   - Particle counts are limited to N < 2^31 (32-bit index arithmetic on device).
+ */
+#ifndef MEGOPOLIS_B200_H
+#define MEGOPOLIS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MGP_ABI_VERSION 1
+
+enum { MGP_F32 = 0, MGP_F64 = 1 };
+enum { MGP_RNG_MEGORES = 0, MGP_RNG_PHILOX = 1 };
+enum { MGP_KIND_METROPOLIS = 0, MGP_KIND_C1 = 1, MGP_KIND_C2 = 2, MGP_KIND_MEGOPOLIS = 3 };
+enum { MGP_OK = 0, MGP_EINVAL = -1, MGP_EUNSUPPORTED = -2 };
+
+/* flags: MGP_FLAG_POSITIVE_NORMAL asserts that every weight is a positive normal
+ * float32 (mgp_weight_stats: n_notnormal == 0), enabling the exact fast compare. */
+enum { MGP_FLAG_POSITIVE_NORMAL = 1 };
+
+/* Weight statistics (device-resident result).  sum/mean are bit-identical to
+ * numpy's np.asarray(w, float64).sum()/.mean() (pairwise summation), which feeds
+ * the B rule at M/bench.py:119-120 and T/conftest.py:29-30. */
+typedef struct {
+    double sum;
+    double mean;
+    double max;          /* float64 max (M/bench.py:120) */
+    int64_t n_pos;       /* w > 0 and finite           */
+    int64_t n_zero;      /* w == 0 (incl. -0.0)        */
+    int64_t n_neg;       /* w < 0                      */
+    int64_t n_nonfinite; /* inf / nan                  */
+    int64_t n_notnormal; /* zero, subnormal, negative or non-finite */
+} mgp_weight_stats_t;
+
+int mgp_abi_version(void);
+const char *mgp_last_error(void);
+
+/* Replaces the f64 mean/max scan feeding compute_iterations (M/weights.py:114-131,
+ * M/bench.py:119-120) and the WeightVector / _check_weights scans
+ * (M/weights.py:49-59, M/resample.py:96-100).  One fused HBM pass. */
+int mgp_weight_stats(const void *d_w, int dtype, int64_t n, mgp_weight_stats_t *d_out, void *stream);
+
+/* B = ceil(ln eps / ln(1 - mean/max)), clamped >= 1 (M/weights.py:114-131; same
+ * ValueErrors).  Host arithmetic, libm log as the reference's math.log. */
+int mgp_compute_iterations(double epsilon, double mean_w, double max_w, int32_t *b_out);
+
+/* megopolis_offsets (M/resample.py:263-265): B offsets on GLOBAL_OFFSET_LANE. */
+int mgp_offsets_host(uint64_t seed, int64_t n, int32_t b, int rng, int64_t *h_off);
+int mgp_offsets(uint64_t seed, int64_t n, int32_t b, int rng, int64_t *d_off, void *stream);
+
+/* Resamplers (device pointers).  Preconditions are checked like the reference
+ * wrappers check them (B >= 1, strict N % W, partition geometry); the
+ * data-dependent "all weights are zero" check (M/resample.py:96-100) needs the
+ * weight statistics and is done by the caller (the Python package does it) or by
+ * mgp_resample_host. */
+/* megopolis(w, b, warp, seed, strict)          M/resample.py:268-282 */
+int mgp_megopolis(const void *d_w, int dtype, int64_t n, int32_t b, uint64_t seed, int32_t warp, int strict,
+                  int rng, int flags, int64_t *d_anc, void *stream);
+/* metropolis(w, b, seed)                       M/resample.py:201-206 */
+int mgp_metropolis(const void *d_w, int dtype, int64_t n, int32_t b, uint64_t seed, int rng, int flags,
+                   int64_t *d_anc, void *stream);
+/* metropolis_c1(w, b, part, warp, seed, strict) M/resample.py:209-225; partition_bytes
+ * is PartitionConfig.partition_bytes, word size 4 bytes (M/resample.py:64, 84-93) */
+int mgp_metropolis_c1(const void *d_w, int dtype, int64_t n, int32_t b, uint64_t seed, int32_t warp,
+                      int32_t partition_bytes, int strict, int rng, int flags, int64_t *d_anc, void *stream);
+/* metropolis_c2(w, b, part, warp, seed, strict) M/resample.py:228-244 */
+int mgp_metropolis_c2(const void *d_w, int dtype, int64_t n, int32_t b, uint64_t seed, int32_t warp,
+                      int32_t partition_bytes, int strict, int rng, int flags, int64_t *d_anc, void *stream);
+
+/* Particle slice [p0, p1) of any resampler (sharded multi-GPU / pipelined use):
+ * ancestors for particle i land in d_anc_slice[i - p0]; the weights are the full
+ * (replicated) array.  For the W = 32 paths p0 must be a multiple of 32. */
+int mgp_resample_range(int kind, const void *d_w, int dtype, int64_t n, int32_t b, uint64_t seed, int32_t warp,
+                       int32_t partition_bytes, int strict, int rng, int flags, int64_t p0, int64_t p1,
+                       int64_t *d_anc_slice, void *stream);
+
+/* Host-buffer drop-in for make_resampler(kind, ...)(w, b, seed) (M/resample.py:431-455):
+ * copies h_w to the device, validates (WeightVector + _check_weights), derives B
+ * from epsilon when b <= 0 (reporting it in *b_used), resamples, and streams the
+ * ancestors back into h_anc overlapped with the remaining compute. */
+int mgp_resample_host(int kind, const void *h_w, int dtype, int64_t n, int32_t b, double epsilon, uint64_t seed,
+                      int32_t warp, int32_t partition_bytes, int strict, int rng, int64_t *h_anc, int32_t *b_used,
+                      int device);
+
+/* ancestors_to_offspring (M/resample.py:361-368): d_counts[j] = #{i : anc[i] == j};
+ * *d_bad set to 1 if an ancestor is outside [0, n) (the reference's ValueError). */
+int mgp_offspring(const int64_t *d_anc, int64_t n_anc, int64_t n, int64_t *d_counts, int32_t *d_bad,
+                  void *stream);
+
+/* QualityAccumulator (M/metrics.py:55-110), float64, bit-identical to numpy:
+ *   expected:  d_e = N * w / sum(w)              (_expected_offspring, :55-60)
+ *   add:       sum += o; sum_sq += o*o; se_total += sum((o - e)^2)      (:86-93)
+ *   finalize:  variance = sum(sum_sq/k - mean^2), bias_sq = sum((mean - e)^2) (:95-110) */
+int mgp_expected_offspring(const void *d_w, int dtype, int64_t n, double *d_e, double *d_total, void *stream);
+int mgp_quality_add(const int64_t *d_counts, const double *d_e, int64_t n, double *d_sum, double *d_sumsq,
+                    double *d_se_total, double *d_se_run, void *stream);
+int mgp_quality_finalize(const double *d_sum, const double *d_sumsq, const double *d_e, int64_t n, int64_t k,
+                         double *d_variance, double *d_bias_sq, void *stream);
+/* squared_error (M/metrics.py:63-68) for one offspring vector */
+int mgp_squared_error(const int64_t *d_counts, const double *d_e, int64_t n, double *d_out, void *stream);
+
+/* apply_ancestors (M/resample.py:371-377): out[i] = states[anc[i]], rows of row_bytes */
+int mgp_gather(const void *d_states, int64_t row_bytes, const int64_t *d_anc, int64_t n, void *d_out, void *stream);
+
+/* gen_gaussian_weights (M/weights.py:100-104) on the device (synthetic inputs) */
+int mgp_gen_gaussian(double y, int64_t n, uint64_t seed, int dtype, void *d_out, void *stream);
+
+/* Self-check: our Philox4x32-10 vs curand_Philox4x32_10 for counters {i, c1, c2, c3}.
+ * Writes 4*n words each; returns the number of mismatching words in *h_mismatch. */
+int mgp_philox_selftest(uint64_t key, uint32_t c1, uint32_t c2, uint32_t c3, int64_t n, int64_t *h_mismatch);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MEGOPOLIS_B200_H */

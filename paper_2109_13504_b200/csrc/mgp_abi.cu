@@ -1,0 +1,651 @@
+// mgp_abi.cu -- extern "C" entry points of libmgp.so (see include/megopolis_b200.h).
+//
+// Host-side responsibilities: argument validation with the reference's error texts
+// (pkg/src/megores/resample.py:84-108, weights.py:114-131), kernel selection, the
+// Megopolis offsets (computed on the host like M/resample.py:263-265 and carried to
+// the device in the kernel parameter space), stream-ordered scratch, and the
+// host-buffer path that overlaps ancestor download with compute.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <curand_philox4x32_x.h>
+
+#include "megopolis_b200.h"
+#include "mgp_kernels.cuh"
+
+using namespace mgp;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_err(cudaError_t e, const char* what) {
+  return set_err((int)e, "CUDA error %d (%s) in %s", (int)e, cudaGetErrorString(e), what);
+}
+
+#define CUDA_TRY(x)                                   \
+  do {                                                \
+    cudaError_t e_ = (x);                             \
+    if (e_ != cudaSuccess) return cuda_err(e_, #x);   \
+  } while (0)
+
+#define LAUNCH_CHECK(what)                                  \
+  do {                                                      \
+    cudaError_t e_ = cudaGetLastError();                    \
+    if (e_ != cudaSuccess) return cuda_err(e_, what);       \
+  } while (0)
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+inline uint32_t ilog2(uint64_t v) { uint32_t r = 0; while ((1ull << r) < v) ++r; return r; }
+
+constexpr int64_t MAX_N = (1ll << 31) - 1;
+
+int check_common(int dtype, int64_t n, int32_t b, int rng) {
+  if (dtype != MGP_F32 && dtype != MGP_F64) return set_err(MGP_EINVAL, "dtype must be MGP_F32 or MGP_F64, got %d", dtype);
+  if (rng != MGP_RNG_MEGORES && rng != MGP_RNG_PHILOX) return set_err(MGP_EINVAL, "unknown rng stream %d", rng);
+  if (n < 1) return set_err(MGP_EINVAL, "weights must be a non-empty 1-d sequence");
+  if (n > MAX_N) return set_err(MGP_EUNSUPPORTED, "N=%lld exceeds this build's limit of 2^31-1 particles", (long long)n);
+  if (b < 1) return set_err(MGP_EINVAL, "B must be >= 1, got %d", b);
+  return 0;
+}
+
+int check_warp(int64_t n, int32_t warp, int strict, const char* name) {  // M/resample.py:59-75, 103-108
+  if (warp < 1) return set_err(MGP_EINVAL, "warp_size must be positive, got %d", warp);
+  if (strict && n % warp)
+    return set_err(MGP_EINVAL, "%s requires N (%lld) to be a multiple of the warp size (%d) in strict mode", name,
+                   (long long)n, warp);
+  return 0;
+}
+
+int check_partition(int64_t n, int32_t part_bytes, int64_t* n_w, int64_t* n_part) {  // M/resample.py:84-93
+  if (part_bytes < 1 || part_bytes % 4) return set_err(MGP_EINVAL, "partition_bytes must be a positive multiple of word_bytes");
+  *n_w = part_bytes / 4;
+  if (n % *n_w) return set_err(MGP_EINVAL, "N=%lld is not divisible by the partition width %lld", (long long)n, (long long)*n_w);
+  *n_part = n / *n_w;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// pairwise reduction plumbing
+
+int pw_depth(int64_t n) {
+  std::vector<int64_t> sizes{n}, next;
+  int d = 0;
+  for (;;) {
+    int64_t mx = 0;
+    for (int64_t s : sizes) mx = s > mx ? s : mx;
+    if (mx <= PW_CHUNK) return d;
+    next.clear();
+    for (int64_t s : sizes) {
+      int64_t n2 = s / 2;
+      n2 -= n2 % 8;
+      next.push_back(n2);
+      next.push_back(s - n2);
+    }
+    std::sort(next.begin(), next.end());
+    next.erase(std::unique(next.begin(), next.end()), next.end());
+    sizes.swap(next);
+    ++d;
+  }
+}
+
+template <class Elem, typename WT, bool STATS>
+int pw_reduce(const Elem& e, const WT* wraw, int64_t n, PwOut out, cudaStream_t st) {
+  const int depth = pw_depth(n);
+  const int64_t nch = 1ll << depth;
+  double* heap = nullptr;
+  WStats* cst = nullptr;
+  CUDA_TRY(cudaMallocAsync(&heap, sizeof(double) * 2 * nch, st));
+  if (STATS) CUDA_TRY(cudaMallocAsync(&cst, sizeof(WStats) * nch, st));
+  k_pw_chunks<Elem, WT, STATS><<<(unsigned)nch, PW_THREADS, 0, st>>>(e, wraw, n, depth, heap, cst);
+  LAUNCH_CHECK("k_pw_chunks");
+  k_pw_final<<<1, 1024, 0, st>>>(heap, depth, n, cst, out);
+  LAUNCH_CHECK("k_pw_final");
+  CUDA_TRY(cudaFreeAsync(heap, st));
+  if (cst) CUDA_TRY(cudaFreeAsync(cst, st));
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// host offsets
+
+void offsets_host(uint64_t seed, int64_t n, int32_t b, int rng, int64_t* out) {
+  const uint64_t base = megores_base(seed);
+  for (int32_t t = 0; t < b; ++t) {
+    if (rng == MGP_RNG_MEGORES) out[t] = below_from_hash(mix64(megores_key(base, GLOBAL_OFFSET_LANE, (uint64_t)t)), n);
+    else out[t] = below_from_word(p4_word(philox_block(seed, GLOBAL_OFFSET_LANE, (uint64_t)t >> 2), t & 3), n);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// kernel dispatch helpers
+
+template <int RNG, typename WT, bool POW2, bool FAST>
+int launch_mego_w32(const ResampleArgs& a, const OffChunk& oc, cudaStream_t st) {
+  const unsigned grid = (unsigned)((a.p_end - a.p0 + RS_THREADS - 1) / RS_THREADS);
+  k_megopolis_w32<RNG, WT, POW2, FAST><<<grid, RS_THREADS, 0, st>>>(a, oc);
+  LAUNCH_CHECK("k_megopolis_w32");
+  return 0;
+}
+
+template <int RNG, typename WT>
+int dispatch_mego_w32(const ResampleArgs& a, const OffChunk& oc, bool pow2, bool fast, cudaStream_t st) {
+  if constexpr (sizeof(WT) == 4) {
+    if (fast) return pow2 ? launch_mego_w32<RNG, WT, true, true>(a, oc, st) : launch_mego_w32<RNG, WT, false, true>(a, oc, st);
+  }
+  return pow2 ? launch_mego_w32<RNG, WT, true, false>(a, oc, st) : launch_mego_w32<RNG, WT, false, false>(a, oc, st);
+}
+
+template <int RNG, typename WT, bool POW2, bool FAST>
+int launch_metro(const ResampleArgs& a, cudaStream_t st) {
+  const unsigned grid = (unsigned)((a.p_end - a.p0 + RS_THREADS - 1) / RS_THREADS);
+  k_metropolis<RNG, WT, POW2, FAST><<<grid, RS_THREADS, 0, st>>>(a);
+  LAUNCH_CHECK("k_metropolis");
+  return 0;
+}
+
+template <int RNG, typename WT>
+int dispatch_metro(const ResampleArgs& a, bool pow2, bool fast, cudaStream_t st) {
+  if constexpr (sizeof(WT) == 4) {
+    if (fast) return pow2 ? launch_metro<RNG, WT, true, true>(a, st) : launch_metro<RNG, WT, false, true>(a, st);
+  }
+  return pow2 ? launch_metro<RNG, WT, true, false>(a, st) : launch_metro<RNG, WT, false, false>(a, st);
+}
+
+constexpr int C1_SMEM_MAX = 96 * 1024;
+
+template <int RNG, typename WT, bool POW2, bool FAST, bool C2, bool STAGE>
+int launch_c12(const ResampleArgs& a, cudaStream_t st) {
+  const unsigned grid = (unsigned)((a.p_end - a.p0 + RS_THREADS - 1) / RS_THREADS);
+  size_t smem = STAGE ? (size_t)(RS_THREADS / 32) * a.n_w * sizeof(WT) : 0;
+  auto kern = k_c12_w32<RNG, WT, POW2, FAST, C2, STAGE>;
+  if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<grid, RS_THREADS, smem, st>>>(a);
+  LAUNCH_CHECK("k_c12_w32");
+  return 0;
+}
+
+template <int RNG, typename WT, bool C2>
+int dispatch_c12(const ResampleArgs& a, bool pow2, bool fast, cudaStream_t st) {
+  const bool stage = !C2 && (size_t)(RS_THREADS / 32) * a.n_w * sizeof(WT) <= (size_t)C1_SMEM_MAX;
+#define C12_CASE(P, F)                                                        \
+  if (pow2 == P && fast == F) {                                               \
+    if constexpr (!F || sizeof(WT) == 4) {                                    \
+      if (stage) return launch_c12<RNG, WT, P, F, C2, !C2>(a, st);            \
+      return launch_c12<RNG, WT, P, F, C2, false>(a, st);                     \
+    }                                                                         \
+  }
+  C12_CASE(true, true)
+  C12_CASE(false, true)
+  C12_CASE(true, false)
+  C12_CASE(false, false)
+#undef C12_CASE
+  return launch_c12<RNG, WT, false, false, C2, false>(a, st);
+}
+
+template <int RNG, typename WT>
+int launch_generic(int kind, GenericArgs ga, cudaStream_t st) {
+  const unsigned grid = (unsigned)((ga.p_end - ga.p0 + RS_THREADS - 1) / RS_THREADS);
+  if (kind == MGP_KIND_C1) k_generic<RNG, WT, 1><<<grid, RS_THREADS, 0, st>>>(ga);
+  else if (kind == MGP_KIND_C2) k_generic<RNG, WT, 2><<<grid, RS_THREADS, 0, st>>>(ga);
+  else k_generic<RNG, WT, 3><<<grid, RS_THREADS, 0, st>>>(ga);
+  LAUNCH_CHECK("k_generic");
+  return 0;
+}
+
+// One resampler call over particles [p0, p_end).  Arguments already validated.
+struct Plan {
+  int kind, dtype, rng;
+  bool fast;
+  const void* w;
+  int64_t n, n_w, n_part;
+  int32_t b, warp;
+  uint64_t seed;
+  std::vector<int64_t> off;  // Megopolis offsets (host)
+  int64_t* d_off = nullptr;  // device copy for the generic path
+  int32_t* kstate = nullptr;
+};
+
+bool plan_uses_w32(const Plan& p) {
+  if (p.kind == MGP_KIND_METROPOLIS) return true;
+  return p.warp == 32 && p.n % 32 == 0;
+}
+
+int run_range(Plan& p, int64_t p0, int64_t p_end, int64_t* anc, cudaStream_t st) {
+  if (p0 >= p_end) return 0;
+  if (!plan_uses_w32(p)) {
+    GenericArgs ga{p.w, p.n, (int64_t)p.warp, p.n_w, p.n_part, (int64_t)p.b, p0, p_end, p.seed, megores_base(p.seed),
+                   p.d_off, anc};
+    if (p.rng == MGP_RNG_MEGORES)
+      return p.dtype == MGP_F32 ? launch_generic<RNG_MEGORES, float>(p.kind, ga, st)
+                                : launch_generic<RNG_MEGORES, double>(p.kind, ga, st);
+    return p.dtype == MGP_F32 ? launch_generic<RNG_PHILOX, float>(p.kind, ga, st)
+                              : launch_generic<RNG_PHILOX, double>(p.kind, ga, st);
+  }
+  ResampleArgs a{};
+  a.w = p.w;
+  a.n = (uint32_t)p.n;
+  a.p0 = (uint32_t)p0;
+  a.p_end = (uint32_t)p_end;
+  a.n_w = (uint32_t)p.n_w;
+  a.n_part = (uint32_t)p.n_part;
+  a.seed = p.seed;
+  a.base = megores_base(p.seed);
+  a.kstate = p.kstate;
+  a.anc = anc;
+  const int cap = (p.kind == MGP_KIND_MEGOPOLIS) ? OFF_CAP : p.b;  // only Megopolis carries params
+  for (int b0 = 0; b0 < p.b; b0 += cap) {
+    a.b0 = b0;
+    a.cnt = std::min(cap, p.b - b0);
+    a.first = (b0 == 0);
+    a.last = (b0 + a.cnt >= p.b);
+    int rc = 0;
+    if (p.kind == MGP_KIND_MEGOPOLIS) {
+      static thread_local OffChunk oc;
+      for (int t = 0; t < a.cnt; ++t) oc.o[t] = (uint32_t)p.off[b0 + t];
+      const bool pow2 = is_pow2(p.n);
+      if (p.rng == MGP_RNG_MEGORES)
+        rc = p.dtype == MGP_F32 ? dispatch_mego_w32<RNG_MEGORES, float>(a, oc, pow2, p.fast, st)
+                                : dispatch_mego_w32<RNG_MEGORES, double>(a, oc, pow2, p.fast, st);
+      else
+        rc = p.dtype == MGP_F32 ? dispatch_mego_w32<RNG_PHILOX, float>(a, oc, pow2, p.fast, st)
+                                : dispatch_mego_w32<RNG_PHILOX, double>(a, oc, pow2, p.fast, st);
+    } else if (p.kind == MGP_KIND_METROPOLIS) {
+      const bool pow2 = is_pow2(p.n) && p.n >= 2;
+      a.log2 = ilog2((uint64_t)p.n);
+      if (p.rng == MGP_RNG_MEGORES)
+        rc = p.dtype == MGP_F32 ? dispatch_metro<RNG_MEGORES, float>(a, pow2, p.fast, st)
+                                : dispatch_metro<RNG_MEGORES, double>(a, pow2, p.fast, st);
+      else
+        rc = p.dtype == MGP_F32 ? dispatch_metro<RNG_PHILOX, float>(a, pow2, p.fast, st)
+                                : dispatch_metro<RNG_PHILOX, double>(a, pow2, p.fast, st);
+    } else {
+      const bool pow2 = is_pow2(p.n_w) && p.n_w >= 2;
+      a.log2 = ilog2((uint64_t)p.n_w);
+      const bool c2 = p.kind == MGP_KIND_C2;
+#define C12_GO(R, T) (c2 ? dispatch_c12<R, T, true>(a, pow2, p.fast, st) : dispatch_c12<R, T, false>(a, pow2, p.fast, st))
+      if (p.rng == MGP_RNG_MEGORES)
+        rc = p.dtype == MGP_F32 ? C12_GO(RNG_MEGORES, float) : C12_GO(RNG_MEGORES, double);
+      else
+        rc = p.dtype == MGP_F32 ? C12_GO(RNG_PHILOX, float) : C12_GO(RNG_PHILOX, double);
+#undef C12_GO
+    }
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+// Validate + build a plan (no data access).
+int make_plan(Plan& p, int kind, const void* w, int dtype, int64_t n, int32_t b, uint64_t seed, int32_t warp,
+              int32_t part_bytes, int strict, int rng, int flags) {
+  int rc = check_common(dtype, n, b, rng);
+  if (rc) return rc;
+  p.kind = kind;
+  p.w = w;
+  p.dtype = dtype;
+  p.n = n;
+  p.b = b;
+  p.seed = seed;
+  p.rng = rng;
+  p.warp = warp;
+  p.n_w = 0;
+  p.n_part = 0;
+  p.fast = (flags & MGP_FLAG_POSITIVE_NORMAL) && dtype == MGP_F32;
+  if (kind == MGP_KIND_MEGOPOLIS) {
+    if ((rc = check_warp(n, warp, strict, "megopolis"))) return rc;
+    p.off.resize((size_t)b);
+    offsets_host(seed, n, b, rng, p.off.data());
+  } else if (kind == MGP_KIND_C1 || kind == MGP_KIND_C2) {
+    if ((rc = check_warp(n, warp, strict, kind == MGP_KIND_C1 ? "metropolis_c1" : "metropolis_c2"))) return rc;
+    if ((rc = check_partition(n, part_bytes, &p.n_w, &p.n_part))) return rc;
+  } else if (kind != MGP_KIND_METROPOLIS) {
+    return set_err(MGP_EINVAL, "unknown resampler kind %d", kind);
+  }
+  return 0;
+}
+
+int plan_alloc(Plan& p, cudaStream_t st) {
+  if (!plan_uses_w32(p) && p.kind == MGP_KIND_MEGOPOLIS) {
+    CUDA_TRY(cudaMallocAsync(&p.d_off, sizeof(int64_t) * p.b, st));
+    CUDA_TRY(cudaMemcpyAsync(p.d_off, p.off.data(), sizeof(int64_t) * p.b, cudaMemcpyHostToDevice, st));
+  }
+  if (plan_uses_w32(p) && p.kind == MGP_KIND_MEGOPOLIS && p.b > OFF_CAP)
+    CUDA_TRY(cudaMallocAsync(&p.kstate, sizeof(int32_t) * p.n, st));
+  return 0;
+}
+
+int plan_free(Plan& p, cudaStream_t st) {
+  if (p.d_off) CUDA_TRY(cudaFreeAsync(p.d_off, st));
+  if (p.kstate) CUDA_TRY(cudaFreeAsync(p.kstate, st));
+  p.d_off = nullptr;
+  p.kstate = nullptr;
+  return 0;
+}
+
+int resample_device(int kind, const void* w, int dtype, int64_t n, int32_t b, uint64_t seed, int32_t warp,
+                    int32_t part_bytes, int strict, int rng, int flags, int64_t* anc, void* stream) {
+  Plan p;
+  int rc = make_plan(p, kind, w, dtype, n, b, seed, warp, part_bytes, strict, rng, flags);
+  if (rc) return rc;
+  if (!w || !anc) return set_err(MGP_EINVAL, "null pointer");
+  cudaStream_t st = S(stream);
+  if ((rc = plan_alloc(p, st))) return rc;
+  rc = run_range(p, 0, n, anc, st);
+  int rc2 = plan_free(p, st);
+  return rc ? rc : rc2;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int mgp_abi_version(void) { return MGP_ABI_VERSION; }
+
+const char* mgp_last_error(void) { return g_err.c_str(); }
+
+int mgp_weight_stats(const void* d_w, int dtype, int64_t n, mgp_weight_stats_t* d_out, void* stream) {
+  if (dtype != MGP_F32 && dtype != MGP_F64) return set_err(MGP_EINVAL, "dtype must be MGP_F32 or MGP_F64");
+  if (n < 1) return set_err(MGP_EINVAL, "weights must be a non-empty 1-d sequence");
+  PwOut out{&d_out->sum, &d_out->mean, nullptr, reinterpret_cast<WStats*>(&d_out->max)};
+  static_assert(sizeof(WStats) == 6 * 8, "WStats layout");
+  if (dtype == MGP_F32) {
+    const float* w = (const float*)d_w;
+    return pw_reduce<ElemWeight<float>, float, true>(ElemWeight<float>{w}, w, n, out, S(stream));
+  }
+  const double* w = (const double*)d_w;
+  return pw_reduce<ElemWeight<double>, double, true>(ElemWeight<double>{w}, w, n, out, S(stream));
+}
+
+int mgp_compute_iterations(double epsilon, double mean_w, double max_w, int32_t* b_out) {  // M/weights.py:114-131
+  if (!(0.0 < epsilon && epsilon <= 1.0)) return set_err(MGP_EINVAL, "epsilon must be in (0, 1], got %.17g", epsilon);
+  if (mean_w <= 0 || max_w <= 0) return set_err(MGP_EINVAL, "mean_w and max_w must be positive");
+  if (mean_w > max_w) return set_err(MGP_EINVAL, "mean_w (%.17g) exceeds max_w (%.17g)", mean_w, max_w);
+  const double ratio = mean_w / max_w;
+  if (ratio >= 1.0 || epsilon == 1.0) { *b_out = 1; return 0; }
+  const double v = std::ceil(std::log(epsilon) / std::log(1.0 - ratio));
+  if (!(v < 2147483647.0)) return set_err(MGP_EUNSUPPORTED, "B=%.17g exceeds the int32 range", v);
+  *b_out = v < 1.0 ? 1 : (int32_t)v;
+  return 0;
+}
+
+int mgp_offsets_host(uint64_t seed, int64_t n, int32_t b, int rng, int64_t* h_off) {
+  if (n < 1) return set_err(MGP_EINVAL, "n must be >= 1, got %lld", (long long)n);
+  if (b < 0) return set_err(MGP_EINVAL, "B must be >= 0");
+  if (rng != MGP_RNG_MEGORES && rng != MGP_RNG_PHILOX) return set_err(MGP_EINVAL, "unknown rng stream %d", rng);
+  offsets_host(seed, n, b, rng, h_off);
+  return 0;
+}
+
+int mgp_offsets(uint64_t seed, int64_t n, int32_t b, int rng, int64_t* d_off, void* stream) {
+  if (n < 1) return set_err(MGP_EINVAL, "n must be >= 1, got %lld", (long long)n);
+  if (b <= 0) return b == 0 ? 0 : set_err(MGP_EINVAL, "B must be >= 0");
+  const unsigned grid = (unsigned)((b + 255) / 256);
+  if (rng == MGP_RNG_MEGORES) k_offsets<RNG_MEGORES><<<grid, 256, 0, S(stream)>>>(megores_base(seed), seed, n, b, d_off);
+  else if (rng == MGP_RNG_PHILOX) k_offsets<RNG_PHILOX><<<grid, 256, 0, S(stream)>>>(0, seed, n, b, d_off);
+  else return set_err(MGP_EINVAL, "unknown rng stream %d", rng);
+  LAUNCH_CHECK("k_offsets");
+  return 0;
+}
+
+int mgp_megopolis(const void* d_w, int dtype, int64_t n, int32_t b, uint64_t seed, int32_t warp, int strict, int rng,
+                  int flags, int64_t* d_anc, void* stream) {
+  return resample_device(MGP_KIND_MEGOPOLIS, d_w, dtype, n, b, seed, warp, 0, strict, rng, flags, d_anc, stream);
+}
+
+int mgp_metropolis(const void* d_w, int dtype, int64_t n, int32_t b, uint64_t seed, int rng, int flags,
+                   int64_t* d_anc, void* stream) {
+  return resample_device(MGP_KIND_METROPOLIS, d_w, dtype, n, b, seed, 32, 0, 0, rng, flags, d_anc, stream);
+}
+
+int mgp_metropolis_c1(const void* d_w, int dtype, int64_t n, int32_t b, uint64_t seed, int32_t warp,
+                      int32_t partition_bytes, int strict, int rng, int flags, int64_t* d_anc, void* stream) {
+  return resample_device(MGP_KIND_C1, d_w, dtype, n, b, seed, warp, partition_bytes, strict, rng, flags, d_anc, stream);
+}
+
+int mgp_metropolis_c2(const void* d_w, int dtype, int64_t n, int32_t b, uint64_t seed, int32_t warp,
+                      int32_t partition_bytes, int strict, int rng, int flags, int64_t* d_anc, void* stream) {
+  return resample_device(MGP_KIND_C2, d_w, dtype, n, b, seed, warp, partition_bytes, strict, rng, flags, d_anc, stream);
+}
+
+int mgp_resample_range(int kind, const void* d_w, int dtype, int64_t n, int32_t b, uint64_t seed, int32_t warp,
+                       int32_t partition_bytes, int strict, int rng, int flags, int64_t p0, int64_t p1,
+                       int64_t* d_anc_slice, void* stream) {
+  Plan p;
+  int rc = make_plan(p, kind, d_w, dtype, n, b, seed, warp, partition_bytes, strict, rng, flags);
+  if (rc) return rc;
+  if (!d_w || !d_anc_slice) return set_err(MGP_EINVAL, "null pointer");
+  if (p0 < 0 || p1 > n || p0 > p1) return set_err(MGP_EINVAL, "particle range [%lld, %lld) outside [0, %lld)",
+                                                  (long long)p0, (long long)p1, (long long)n);
+  if (plan_uses_w32(p) && p0 % 32) return set_err(MGP_EINVAL, "p0 must be a multiple of 32, got %lld", (long long)p0);
+  cudaStream_t st = S(stream);
+  if ((rc = plan_alloc(p, st))) return rc;
+  rc = run_range(p, p0, p1, d_anc_slice - p0, st);
+  int rc2 = plan_free(p, st);
+  return rc ? rc : rc2;
+}
+
+int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b, double epsilon, uint64_t seed,
+                      int32_t warp, int32_t partition_bytes, int strict, int rng, int64_t* h_anc, int32_t* b_used,
+                      int device) {
+  if (!h_w || !h_anc) return set_err(MGP_EINVAL, "null pointer");
+  if (dtype != MGP_F32 && dtype != MGP_F64) return set_err(MGP_EINVAL, "dtype must be MGP_F32 or MGP_F64");
+  if (n < 1) return set_err(MGP_EINVAL, "weights must be a non-empty 1-d sequence");
+  if (n > MAX_N) return set_err(MGP_EUNSUPPORTED, "N exceeds 2^31-1");
+  if (device >= 0) CUDA_TRY(cudaSetDevice(device));
+  cudaStream_t st, cp;
+  CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
+  const size_t wbytes = (size_t)n * (dtype == MGP_F32 ? 4 : 8);
+  void* d_w = nullptr;
+  int64_t* d_anc = nullptr;
+  mgp_weight_stats_t* d_stats = nullptr;
+  mgp_weight_stats_t hs{};
+  int rc = 0;
+  Plan p;
+  std::vector<cudaEvent_t> evs;
+  auto cleanup = [&]() {
+    cudaStreamSynchronize(cp);
+    cudaStreamSynchronize(st);
+    if (d_w) cudaFreeAsync(d_w, st);
+    if (d_anc) cudaFreeAsync(d_anc, st);
+    if (d_stats) cudaFreeAsync(d_stats, st);
+    plan_free(p, st);
+    cudaStreamSynchronize(st);
+    for (auto e : evs) cudaEventDestroy(e);
+    cudaStreamDestroy(cp);
+    cudaStreamDestroy(st);
+  };
+#define HTRY(x)                 \
+  do {                          \
+    rc = (x);                   \
+    if (rc) { cleanup(); return rc; } \
+  } while (0)
+#define HCUDA(x)                                        \
+  do {                                                  \
+    cudaError_t e_ = (x);                               \
+    if (e_ != cudaSuccess) { rc = cuda_err(e_, #x); cleanup(); return rc; } \
+  } while (0)
+  HCUDA(cudaMallocAsync(&d_w, wbytes, st));
+  HCUDA(cudaMallocAsync(&d_anc, sizeof(int64_t) * n, st));
+  HCUDA(cudaMallocAsync(&d_stats, sizeof(mgp_weight_stats_t), st));
+  HCUDA(cudaMemcpyAsync(d_w, h_w, wbytes, cudaMemcpyHostToDevice, st));
+  HTRY(mgp_weight_stats(d_w, dtype, n, d_stats, st));
+  HCUDA(cudaMemcpyAsync(&hs, d_stats, sizeof hs, cudaMemcpyDeviceToHost, st));
+  HCUDA(cudaStreamSynchronize(st));
+  // WeightVector.__post_init__ (M/weights.py:56-59) and _check_weights (M/resample.py:96-100)
+  if (hs.n_nonfinite) { rc = set_err(MGP_EINVAL, "weights must be finite"); cleanup(); return rc; }
+  if (hs.n_neg) { rc = set_err(MGP_EINVAL, "weights must be non-negative"); cleanup(); return rc; }
+  if (hs.n_pos == 0) { rc = set_err(MGP_EINVAL, "all weights are zero"); cleanup(); return rc; }
+  if (b <= 0) HTRY(mgp_compute_iterations(epsilon, hs.mean, hs.max, &b));
+  if (b_used) *b_used = b;
+  const int flags = (hs.n_notnormal == 0) ? MGP_FLAG_POSITIVE_NORMAL : 0;
+  HTRY(make_plan(p, kind, d_w, dtype, n, b, seed, warp, partition_bytes, strict, rng, flags));
+  HTRY(plan_alloc(p, st));
+  // Overlap the ancestor download with the remaining compute: particle chunks are
+  // independent given (w, offsets, seed); each chunk's D2H waits only on its kernel.
+  const bool chunkable = !(plan_uses_w32(p) && p.kind == MGP_KIND_MEGOPOLIS && p.b > OFF_CAP);
+  const int64_t nchunk = (chunkable && n >= (1 << 20)) ? 4 : 1;
+  int64_t step = (n + nchunk - 1) / nchunk;
+  step = (step + 255) / 256 * 256;
+  for (int64_t c0 = 0; c0 < n; c0 += step) {
+    const int64_t c1 = std::min(n, c0 + step);
+    HTRY(run_range(p, c0, c1, d_anc, st));
+    cudaEvent_t ev;
+    HCUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    evs.push_back(ev);
+    HCUDA(cudaEventRecord(ev, st));
+    HCUDA(cudaStreamWaitEvent(cp, ev, 0));
+    HCUDA(cudaMemcpyAsync(h_anc + c0, d_anc + c0, sizeof(int64_t) * (c1 - c0), cudaMemcpyDeviceToHost, cp));
+  }
+  HCUDA(cudaStreamSynchronize(cp));
+  HCUDA(cudaStreamSynchronize(st));
+  cleanup();
+#undef HTRY
+#undef HCUDA
+  return 0;
+}
+
+int mgp_offspring(const int64_t* d_anc, int64_t n_anc, int64_t n, int64_t* d_counts, int32_t* d_bad, void* stream) {
+  if (n < 0 || n_anc < 0) return set_err(MGP_EINVAL, "negative size");
+  cudaStream_t st = S(stream);
+  if (n) CUDA_TRY(cudaMemsetAsync(d_counts, 0, sizeof(int64_t) * n, st));
+  if (d_bad) CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int32_t), st));
+  if (n_anc == 0) return 0;
+  int32_t* bad = d_bad;
+  if (!bad) CUDA_TRY(cudaMallocAsync(&bad, sizeof(int32_t), st));
+  const unsigned grid = (unsigned)((n_anc + 255) / 256);
+  k_offspring<int64_t><<<grid, 256, 0, st>>>(d_anc, n_anc, n, d_counts, bad);
+  LAUNCH_CHECK("k_offspring");
+  if (!d_bad) CUDA_TRY(cudaFreeAsync(bad, st));
+  return 0;
+}
+
+int mgp_expected_offspring(const void* d_w, int dtype, int64_t n, double* d_e, double* d_total, void* stream) {
+  if (n < 1) return set_err(MGP_EINVAL, "weights must be a non-empty 1-d sequence");
+  cudaStream_t st = S(stream);
+  PwOut out{d_total, nullptr, nullptr, nullptr};
+  int rc;
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  if (dtype == MGP_F32) {
+    const float* w = (const float*)d_w;
+    if ((rc = pw_reduce<ElemWeight<float>, float, false>(ElemWeight<float>{w}, w, n, out, st))) return rc;
+    k_expected<float><<<grid, 256, 0, st>>>(w, n, d_total, d_e);
+  } else if (dtype == MGP_F64) {
+    const double* w = (const double*)d_w;
+    if ((rc = pw_reduce<ElemWeight<double>, double, false>(ElemWeight<double>{w}, w, n, out, st))) return rc;
+    k_expected<double><<<grid, 256, 0, st>>>(w, n, d_total, d_e);
+  } else {
+    return set_err(MGP_EINVAL, "dtype must be MGP_F32 or MGP_F64");
+  }
+  LAUNCH_CHECK("k_expected");
+  return 0;
+}
+
+int mgp_quality_add(const int64_t* d_counts, const double* d_e, int64_t n, double* d_sum, double* d_sumsq,
+                    double* d_se_total, double* d_se_run, void* stream) {
+  if (n < 1) return set_err(MGP_EINVAL, "n must be >= 1");
+  cudaStream_t st = S(stream);
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  k_quality_accum<int64_t><<<grid, 256, 0, st>>>(d_counts, n, d_sum, d_sumsq);
+  LAUNCH_CHECK("k_quality_accum");
+  PwOut out{d_se_run, nullptr, d_se_total, nullptr};
+  return pw_reduce<ElemSqErr<int64_t>, float, false>(ElemSqErr<int64_t>{d_counts, d_e}, nullptr, n, out, st);
+}
+
+int mgp_squared_error(const int64_t* d_counts, const double* d_e, int64_t n, double* d_out, void* stream) {
+  if (n < 1) return set_err(MGP_EINVAL, "n must be >= 1");
+  PwOut out{d_out, nullptr, nullptr, nullptr};
+  return pw_reduce<ElemSqErr<int64_t>, float, false>(ElemSqErr<int64_t>{d_counts, d_e}, nullptr, n, out, S(stream));
+}
+
+int mgp_quality_finalize(const double* d_sum, const double* d_sumsq, const double* d_e, int64_t n, int64_t k,
+                         double* d_variance, double* d_bias_sq, void* stream) {
+  if (k < 2) return set_err(MGP_EINVAL, "need at least 2 runs to estimate variance, got %lld", (long long)k);
+  if (n < 1) return set_err(MGP_EINVAL, "n must be >= 1");
+  cudaStream_t st = S(stream);
+  int rc;
+  PwOut o1{d_variance, nullptr, nullptr, nullptr};
+  if ((rc = pw_reduce<ElemVar, float, false>(ElemVar{d_sum, d_sumsq, (double)k}, nullptr, n, o1, st))) return rc;
+  PwOut o2{d_bias_sq, nullptr, nullptr, nullptr};
+  return pw_reduce<ElemBias, float, false>(ElemBias{d_sum, d_e, (double)k}, nullptr, n, o2, st);
+}
+
+int mgp_gather(const void* d_states, int64_t row_bytes, const int64_t* d_anc, int64_t n, void* d_out, void* stream) {
+  if (row_bytes < 0 || n < 0) return set_err(MGP_EINVAL, "negative size");
+  if (n == 0 || row_bytes == 0) return 0;
+  cudaStream_t st = S(stream);
+  const uintptr_t al = (uintptr_t)d_states | (uintptr_t)d_out | (uintptr_t)row_bytes;
+  const int64_t total_bytes = n * row_bytes;
+  auto grid_for = [&](int64_t elems) { return (unsigned)std::min<int64_t>((elems + 255) / 256, 148 * 32); };
+  if ((al & 15) == 0) {
+    k_gather<uint4><<<grid_for(total_bytes / 16), 256, 0, st>>>((const uint4*)d_states, d_anc, n, row_bytes / 16, (uint4*)d_out);
+  } else if ((al & 7) == 0) {
+    k_gather<uint2><<<grid_for(total_bytes / 8), 256, 0, st>>>((const uint2*)d_states, d_anc, n, row_bytes / 8, (uint2*)d_out);
+  } else if ((al & 3) == 0) {
+    k_gather<uint32_t><<<grid_for(total_bytes / 4), 256, 0, st>>>((const uint32_t*)d_states, d_anc, n, row_bytes / 4, (uint32_t*)d_out);
+  } else {
+    k_gather<uint8_t><<<grid_for(total_bytes), 256, 0, st>>>((const uint8_t*)d_states, d_anc, n, row_bytes, (uint8_t*)d_out);
+  }
+  LAUNCH_CHECK("k_gather");
+  return 0;
+}
+
+int mgp_gen_gaussian(double y, int64_t n, uint64_t seed, int dtype, void* d_out, void* stream) {
+  if (y < 0) return set_err(MGP_EINVAL, "y must be >= 0, got %.17g", y);
+  if (n < 1) return set_err(MGP_EINVAL, "n must be >= 1, got %lld", (long long)n);
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
+  if (dtype == MGP_F32) k_gen_gaussian<float><<<grid, 256, 0, S(stream)>>>(y, n, seed, (float*)d_out);
+  else if (dtype == MGP_F64) k_gen_gaussian<double><<<grid, 256, 0, S(stream)>>>(y, n, seed, (double*)d_out);
+  else return set_err(MGP_EINVAL, "dtype must be MGP_F32 or MGP_F64");
+  LAUNCH_CHECK("k_gen_gaussian");
+  return 0;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Philox self-test against curand's device implementation.
+namespace {
+__global__ void k_philox_selftest(uint64_t key, uint32_t c1, uint32_t c2, uint32_t c3, int64_t n,
+                                  unsigned long long* mismatch) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const P4 a = philox4x32_10((uint32_t)i, c1, c2, c3, (uint32_t)key, (uint32_t)(key >> 32));
+    const uint4 b = curand_Philox4x32_10(make_uint4((uint32_t)i, c1, c2, c3),
+                                         make_uint2((uint32_t)key, (uint32_t)(key >> 32)));
+    const int bad = (a.x != b.x) + (a.y != b.y) + (a.z != b.z) + (a.w != b.w);
+    if (bad) atomicAdd(mismatch, (unsigned long long)bad);
+  }
+}
+}  // namespace
+
+extern "C" int mgp_philox_selftest(uint64_t key, uint32_t c1, uint32_t c2, uint32_t c3, int64_t n,
+                                   int64_t* h_mismatch) {
+  unsigned long long* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, sizeof *d));
+  CUDA_TRY(cudaMemset(d, 0, sizeof *d));
+  k_philox_selftest<<<148 * 4, 256>>>(key, c1, c2, c3, n, d);
+  LAUNCH_CHECK("k_philox_selftest");
+  unsigned long long h = 0;
+  CUDA_TRY(cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaFree(d));
+  *h_mismatch = (int64_t)h;
+  return 0;
+}

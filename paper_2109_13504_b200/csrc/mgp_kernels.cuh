@@ -1,0 +1,611 @@
+// mgp_kernels.cuh -- sm_100a kernels for the Megopolis hot path.
+//
+// Reference (pkg/src/megores, abbreviated M/):
+//   Megopolis   M/resample.py:180-198, 263-282
+//   Metropolis  M/resample.py:125-138, 201-206
+//   C1 / C2     M/resample.py:141-177, 209-244
+//   B rule      M/weights.py:114-131 fed by np.asarray(w, float64).mean()/max() (M/bench.py:119-120)
+//   offspring   M/resample.py:361-368     quality  M/metrics.py:55-110     gather M/resample.py:371-377
+//
+// Layout in HBM: weights are the caller's contiguous f32[N] / f64[N]; ancestors int64[N]
+// (the reference's dtype); particle index arithmetic is 32-bit (N < 2^31).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "mgp_device.cuh"
+
+namespace mgp {
+
+constexpr int RS_THREADS = 256;   // resampler CTA size (8 warps)
+constexpr int OFF_CAP = 1024;     // Megopolis offsets carried per launch in the param space
+
+// Offsets o_b for rounds [b0, b0+cnt) of one launch.  Kernel parameter space is a
+// constant bank: the warp-uniform o_b reads never touch the LSU/L1 path.
+struct OffChunk {
+  uint32_t o[OFF_CAP];
+};
+
+struct ResampleArgs {
+  const void* w;
+  uint32_t n;        // particles
+  uint32_t p0, p_end;  // particles [p0, p_end) handled by this launch (p0 % 256 == 0)
+  uint32_t n_w;      // partition width (C1/C2)
+  uint32_t n_part;   // number of partitions (C1/C2)
+  uint32_t log2;     // log2(n) (Metropolis pow2) or log2(n_w) (C1/C2 pow2)
+  uint64_t seed;     // run seed (philox key)
+  uint64_t base;     // mix(seed + M_LANE) (megores stream key)
+  int b0, cnt;       // rounds [b0, b0 + cnt)
+  int first, last;   // first launch reads k = i; last launch writes ancestors
+  int32_t* kstate;   // carried ancestor between launches (B > OFF_CAP)
+  int64_t* anc;      // output ancestors
+};
+
+// ---------------------------------------------------------------------------
+// weight loads
+
+template <typename WT, bool FAST>
+__device__ __forceinline__ double wload(const WT* __restrict__ w, uint32_t j) {
+  if constexpr (sizeof(WT) == 4) {
+    if constexpr (FAST) {
+      return f32n_to_f64(__ldg(reinterpret_cast<const uint32_t*>(w) + j));
+    } else {
+      return (double)__ldg(reinterpret_cast<const float*>(w) + j);
+    }
+  } else {
+    return __ldg(reinterpret_cast<const double*>(w) + j);
+  }
+}
+
+template <bool FAST>
+__device__ __forceinline__ bool accept_rule(double u, double wk, double wj) {
+  if constexpr (FAST) return u * wk <= wj;  // all weights positive: the zero rule can never fire
+  else return accepts(u, wk, wj);
+}
+
+// Megopolis partner for W = 32, N % 32 == 0 (M/resample.py:187-193):
+//   j = ((i_al + o_al) mod N) | ((lane + o) & 31)
+template <bool POW2>
+__device__ __forceinline__ uint32_t mego_j(uint32_t i_al, uint32_t lane, uint32_t o, uint32_t n) {
+  uint32_t a = i_al + (o & ~31u);
+  if constexpr (POW2) a &= (n - 1);
+  else a = (a >= n) ? a - n : a;
+  return a | ((lane + o) & 31u);
+}
+
+// ---------------------------------------------------------------------------
+// Megopolis, W = 32 (the hot path).  One particle per thread; the warp's 32 partner
+// weights for round b are one 128-byte line (4 sectors) -- the paper's coalescing.
+// The accepted round index is carried instead of j (j is a pure function of (i, o_b)).
+
+template <int RNG, typename WT, bool POW2, bool FAST>
+__global__ void __launch_bounds__(RS_THREADS) k_megopolis_w32(const ResampleArgs a,
+                                                              const __grid_constant__ OffChunk oc) {
+  const uint32_t i = a.p0 + blockIdx.x * RS_THREADS + threadIdx.x;
+  if (i >= a.p_end) return;
+  const WT* __restrict__ w = reinterpret_cast<const WT*>(a.w);
+  const uint32_t lane = threadIdx.x & 31u, i_al = i - lane, n = a.n;
+  uint32_t k = a.first ? i : (uint32_t)a.kstate[i];
+  double wk = wload<WT, FAST>(w, k);
+  int bstar = -1;
+  if constexpr (RNG == RNG_MEGORES) {
+    uint64_t x = megores_key(a.base, i, (uint64_t)a.b0);
+#pragma unroll 4
+    for (int t = 0; t < a.cnt; ++t) {
+      const uint32_t o = oc.o[t];
+      const double wj = wload<WT, FAST>(w, mego_j<POW2>(i_al, lane, o, n));
+      const uint64_t m = mix64_m53(x);
+      x += M_CTR;
+      const double u = FAST ? u53_fast(m) : (double)m * 0x1p-53;
+      if (accept_rule<FAST>(u, wk, wj)) { wk = wj; bstar = t; }
+    }
+  } else {
+    // philox: draw t = b0 + t; block (t >> 2), word (t & 3); b0 % 4 == 0.
+    for (int t0 = 0; t0 < a.cnt; t0 += 4) {
+      const P4 blk = philox_block(a.seed, i, (uint64_t)(a.b0 + t0) >> 2);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int t = t0 + q;
+        if (t < a.cnt) {
+          const uint32_t o = oc.o[t];
+          const double wj = wload<WT, FAST>(w, mego_j<POW2>(i_al, lane, o, n));
+          const double u = (double)p4_word(blk, q) * 0x1p-32;
+          if (accept_rule<FAST>(u, wk, wj)) { wk = wj; bstar = t; }
+        }
+      }
+    }
+  }
+  if (bstar >= 0) k = mego_j<POW2>(i_al, lane, oc.o[bstar], n);
+  if (a.last) a.anc[i] = (int64_t)k;
+  else a.kstate[i] = (int32_t)k;
+}
+
+// ---------------------------------------------------------------------------
+// Metropolis (uniform random partner; the uncoalesced baseline, M/resample.py:125-138)
+
+template <int RNG, typename WT, bool POW2, bool FAST>
+__global__ void __launch_bounds__(RS_THREADS) k_metropolis(const ResampleArgs a) {
+  const uint32_t i = a.p0 + blockIdx.x * RS_THREADS + threadIdx.x;
+  if (i >= a.p_end) return;
+  const WT* __restrict__ w = reinterpret_cast<const WT*>(a.w);
+  const uint32_t n = a.n;
+  uint32_t k = a.first ? i : (uint32_t)a.kstate[i];
+  double wk = wload<WT, FAST>(w, k);
+  if constexpr (RNG == RNG_MEGORES) {
+    uint64_t x = megores_key(a.base, i, 2ull * (uint64_t)a.b0);
+#pragma unroll 2
+    for (int t = 0; t < a.cnt; ++t) {
+      const uint64_t m = mix64_m53(x);
+      x += M_CTR;
+      const uint64_t hj = mix64(x);
+      x += M_CTR;
+      uint32_t j;
+      if constexpr (POW2) j = (a.log2 == 0) ? 0u : (uint32_t)(hj >> 32) >> (32 - a.log2);
+      else j = (uint32_t)below_from_hash(hj, (int64_t)n);
+      const double wj = wload<WT, FAST>(w, j);
+      const double u = FAST ? u53_fast(m) : (double)m * 0x1p-53;
+      if (accept_rule<FAST>(u, wk, wj)) { wk = wj; k = j; }
+    }
+  } else {
+    // u at draw 2b, j at draw 2b+1: one philox block per two rounds.
+    for (int t = 0; t < a.cnt; ++t) {
+      const uint64_t d = 2ull * (uint64_t)(a.b0 + t);
+      const P4 blk = philox_block(a.seed, i, d >> 2);
+      const uint32_t q = (uint32_t)(d & 3);
+      const uint32_t wu = q == 0 ? blk.x : blk.z, wjw = q == 0 ? blk.y : blk.w;
+      const uint32_t j = __umulhi(wjw, n);
+      const double wj = wload<WT, FAST>(w, j);
+      const double u = (double)wu * 0x1p-32;
+      if (accept_rule<FAST>(u, wk, wj)) { wk = wj; k = j; }
+    }
+  }
+  if (a.last) a.anc[i] = (int64_t)k;
+  else a.kstate[i] = (int32_t)k;
+}
+
+// ---------------------------------------------------------------------------
+// Metropolis-C1 (one partition per warp for all rounds, M/resample.py:141-158) and
+// C2 (a fresh partition per warp and round, M/resample.py:161-177) for W = 32.
+// C1 stages its partition in shared memory once and serves all B rounds from it.
+// C2 draws the 32 upcoming partitions cooperatively (lane l draws round b0+l) and
+// broadcasts them with a shuffle; its partner loads are partition-local gathers.
+
+template <int RNG>
+__device__ __forceinline__ uint32_t below_n(uint64_t h_or_word, uint32_t n, uint32_t log2, bool pow2) {
+  if (RNG == RNG_MEGORES) {
+    if (pow2) return log2 == 0 ? 0u : (uint32_t)(h_or_word >> 32) >> (32 - log2);
+    return (uint32_t)below_from_hash(h_or_word, (int64_t)n);
+  }
+  return __umulhi((uint32_t)h_or_word, n);
+}
+
+template <int RNG, typename WT, bool POW2, bool FAST, bool C2, bool STAGE>
+__global__ void __launch_bounds__(RS_THREADS) k_c12_w32(const ResampleArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t i = a.p0 + blockIdx.x * RS_THREADS + threadIdx.x;
+  if (i >= a.p_end) return;  // n % 32 == 0: whole warps leave together
+  const WT* __restrict__ w = reinterpret_cast<const WT*>(a.w);
+  const uint32_t lane = threadIdx.x & 31u, warp_g = i >> 5;
+  const uint32_t n_w = a.n_w;
+  const uint64_t wlane = WARP_LANE_BASE + warp_g;
+  uint32_t k = a.first ? i : (uint32_t)a.kstate[i];
+  double wk = wload<WT, FAST>(w, k);
+  uint32_t lo = 0;
+  WT* part = reinterpret_cast<WT*>(smem_raw) + (threadIdx.x >> 5) * n_w;
+  if constexpr (!C2) {
+    lo = (uint32_t)draw_below<RNG>(a.base, a.seed, wlane, 0, (int64_t)a.n_part) * n_w;
+    if constexpr (STAGE) {
+      for (uint32_t q = lane; q < n_w; q += 32) part[q] = w[lo + q];
+      __syncwarp();
+    }
+  }
+  uint32_t preg = 0;
+  if constexpr (RNG == RNG_MEGORES) {
+    uint64_t x = megores_key(a.base, i, 2ull * (uint64_t)a.b0);
+    for (int t = 0; t < a.cnt; ++t) {
+      if constexpr (C2) {
+        if ((t & 31) == 0)
+          preg = (uint32_t)draw_below<RNG>(a.base, a.seed, wlane, (uint64_t)(a.b0 + t + (int)lane), (int64_t)a.n_part);
+        lo = __shfl_sync(0xffffffffu, preg, t & 31) * n_w;
+      }
+      const uint64_t m = mix64_m53(x);
+      x += M_CTR;
+      const uint32_t jl = below_n<RNG>(mix64(x), n_w, a.log2, POW2);
+      x += M_CTR;
+      double wj;
+      if constexpr (STAGE && !C2) {
+        if constexpr (sizeof(WT) == 4 && FAST) wj = f32n_to_f64(reinterpret_cast<const uint32_t*>(part)[jl]);
+        else wj = (double)part[jl];
+      } else {
+        wj = wload<WT, FAST>(w, lo + jl);
+      }
+      const double u = FAST ? u53_fast(m) : (double)m * 0x1p-53;
+      if (accept_rule<FAST>(u, wk, wj)) { wk = wj; k = lo + jl; }
+    }
+  } else {
+    for (int t = 0; t < a.cnt; ++t) {
+      if constexpr (C2) {
+        if ((t & 31) == 0)
+          preg = (uint32_t)draw_below<RNG>(a.base, a.seed, wlane, (uint64_t)(a.b0 + t + (int)lane), (int64_t)a.n_part);
+        lo = __shfl_sync(0xffffffffu, preg, t & 31) * n_w;
+      }
+      const uint64_t d = 2ull * (uint64_t)(a.b0 + t);
+      const P4 blk = philox_block(a.seed, i, d >> 2);
+      const uint32_t q = (uint32_t)(d & 3);
+      const uint32_t wu = q == 0 ? blk.x : blk.z, wjw = q == 0 ? blk.y : blk.w;
+      const uint32_t jl = __umulhi(wjw, n_w);
+      double wj;
+      if constexpr (STAGE && !C2) wj = (double)part[jl];
+      else wj = wload<WT, FAST>(w, lo + jl);
+      const double u = (double)wu * 0x1p-32;
+      if (accept_rule<FAST>(u, wk, wj)) { wk = wj; k = lo + jl; }
+    }
+  }
+  if (a.last) a.anc[i] = (int64_t)k;
+  else a.kstate[i] = (int32_t)k;
+}
+
+// ---------------------------------------------------------------------------
+// Generic path: any logical warp size W (semantic, M/resample.py:59-75), any N
+// (permissive mode, M/resample.py:103-108), f32 or f64.  64-bit index arithmetic,
+// exact draws, exact acceptance.  kind: 1 = C1, 2 = C2, 3 = Megopolis.
+
+struct GenericArgs {
+  const void* w;
+  int64_t n, warp, n_w, n_part, b, p0, p_end;
+  uint64_t seed, base;
+  const int64_t* off;  // Megopolis offsets (device)
+  int64_t* anc;
+};
+
+template <int RNG, typename WT, int KIND>
+__global__ void __launch_bounds__(RS_THREADS) k_generic(const GenericArgs a) {
+  const int64_t i = a.p0 + (int64_t)blockIdx.x * RS_THREADS + threadIdx.x;
+  if (i >= a.p_end) return;
+  const WT* __restrict__ w = reinterpret_cast<const WT*>(a.w);
+  Stream<RNG> s(a.base, a.seed, (uint64_t)i, 0);
+  int64_t k = i;
+  const uint64_t wlane = WARP_LANE_BASE + (uint64_t)(i / a.warp);
+  int64_t lo = 0;
+  if (KIND == 1) lo = draw_below<RNG>(a.base, a.seed, wlane, 0, a.n_part) * a.n_w;
+  const int64_t i_al = i - i % a.warp;
+  for (int64_t b = 0; b < a.b; ++b) {
+    int64_t j;
+    double u;
+    if (KIND == 3) {
+      const int64_t ob = a.off[b];
+      j = (i_al + (ob - ob % a.warp) + (i + ob) % a.warp) % a.n;
+      u = s.u();
+    } else {
+      u = s.u();
+      if (KIND == 2) lo = draw_below<RNG>(a.base, a.seed, wlane, (uint64_t)b, a.n_part) * a.n_w;
+      j = lo + s.below(a.n_w);
+    }
+    if (accepts(u, (double)w[k], (double)w[j])) k = j;
+  }
+  a.anc[i] = k;
+}
+
+// Megopolis offsets on the device: o_b = uint_below(seed, GLOBAL_OFFSET_LANE, b, N)
+template <int RNG>
+__global__ void k_offsets(uint64_t base, uint64_t seed, int64_t n, int64_t b, int64_t* out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < b) out[t] = draw_below<RNG>(base, seed, GLOBAL_OFFSET_LANE, (uint64_t)t, n);
+}
+
+// ---------------------------------------------------------------------------
+// numpy-exact pairwise reduction.
+//
+// np.add.reduce over a contiguous float64 array is the recursive pairwise sum
+// (blocks of <= 128 with 8 accumulators; split n2 = n/2 - (n/2)%8).  This is what
+// np.asarray(w, float64).mean() (B rule), .sum() (expected offspring total) and the
+// QualityAccumulator sums evaluate.  We reproduce the same tree: the top D levels
+// form a complete binary tree of "chunks" (<= PW_CHUNK elements each, one CTA per
+// chunk, sub-tree built level by level in shared memory), then one CTA combines the
+// chunk sums in the same pairwise order.  The result is bit-identical to numpy.
+
+constexpr int PW_CHUNK = 32768;
+constexpr int PW_HEAP = 2048;
+constexpr int PW_THREADS = 256;
+
+__host__ __device__ inline void pw_chunk_span(int64_t n, int depth, int64_t c, int64_t& lo, int64_t& len) {
+  lo = 0;
+  len = n;
+  for (int d = depth - 1; d >= 0; --d) {
+    int64_t n2 = len / 2;
+    n2 -= n2 % 8;
+    if ((c >> d) & 1) { lo += n2; len -= n2; }
+    else len = n2;
+  }
+}
+
+struct WStats {  // per-chunk and final weight statistics
+  double max;
+  int64_t n_pos, n_zero, n_neg, n_nonfinite, n_notnormal;
+};
+
+// Element functors: value(i) in float64, exactly as numpy evaluates it.
+template <typename WT>
+struct ElemWeight {
+  const WT* w;
+  __device__ __forceinline__ double operator()(int64_t i) const { return (double)w[i]; }
+};
+template <typename CT>
+struct ElemSqErr {  // (o - E)**2, M/metrics.py:68, 93
+  const CT* counts;
+  const double* e;
+  __device__ __forceinline__ double operator()(int64_t i) const {
+    double d = __dsub_rn((double)counts[i], e[i]);
+    return __dmul_rn(d, d);
+  }
+};
+struct ElemVar {  // sum_sq/k - mean*mean, M/metrics.py:101
+  const double *s, *s2;
+  double k;
+  __device__ __forceinline__ double operator()(int64_t i) const {
+    double m = __ddiv_rn(s[i], k);
+    return __dsub_rn(__ddiv_rn(s2[i], k), __dmul_rn(m, m));
+  }
+};
+struct ElemBias {  // (mean - expected)**2, M/metrics.py:102
+  const double *s, *e;
+  double k;
+  __device__ __forceinline__ double operator()(int64_t i) const {
+    double d = __dsub_rn(__ddiv_rn(s[i], k), e[i]);
+    return __dmul_rn(d, d);
+  }
+};
+
+template <class Elem>
+__device__ __forceinline__ double pw_leaf(const Elem& e, int64_t lo, int64_t n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, e(lo + i));
+    return res;
+  }
+  double r0 = e(lo), r1 = e(lo + 1), r2 = e(lo + 2), r3 = e(lo + 3);
+  double r4 = e(lo + 4), r5 = e(lo + 5), r6 = e(lo + 6), r7 = e(lo + 7);
+  int64_t i = 8;
+  const int64_t m = n - (n % 8);
+  for (; i < m; i += 8) {
+    r0 = __dadd_rn(r0, e(lo + i)); r1 = __dadd_rn(r1, e(lo + i + 1));
+    r2 = __dadd_rn(r2, e(lo + i + 2)); r3 = __dadd_rn(r3, e(lo + i + 3));
+    r4 = __dadd_rn(r4, e(lo + i + 4)); r5 = __dadd_rn(r5, e(lo + i + 5));
+    r6 = __dadd_rn(r6, e(lo + i + 6)); r7 = __dadd_rn(r7, e(lo + i + 7));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
+                         __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
+  for (; i < n; ++i) res = __dadd_rn(res, e(lo + i));
+  return res;
+}
+
+template <typename WT>
+__device__ __forceinline__ void wstat_observe(WStats& s, WT v) {
+  if constexpr (sizeof(WT) == 4) {
+    const uint32_t bits = __float_as_uint(v);
+    const uint32_t ex = (bits >> 23) & 0xFFu;
+    const bool neg = (bits >> 31) != 0;
+    const bool zero = (bits & 0x7FFFFFFFu) == 0;
+    if (ex == 0xFFu) s.n_nonfinite++;
+    else if (zero) s.n_zero++;
+    else if (neg) s.n_neg++;
+    else s.n_pos++;
+    if (ex == 0u || ex == 0xFFu || neg) s.n_notnormal++;
+  } else {
+    const uint64_t bits = (uint64_t)__double_as_longlong(v);
+    const uint32_t ex = (uint32_t)(bits >> 52) & 0x7FFu;
+    const bool neg = (bits >> 63) != 0;
+    const bool zero = (bits & 0x7FFFFFFFFFFFFFFFull) == 0;
+    if (ex == 0x7FFu) s.n_nonfinite++;
+    else if (zero) s.n_zero++;
+    else if (neg) s.n_neg++;
+    else s.n_pos++;
+    if (ex == 0u || ex == 0x7FFu || neg) s.n_notnormal++;
+  }
+  const double d = (double)v;
+  if (d > s.max) s.max = d;
+}
+
+// heap: [2^D, 2^(D+1)) receives the chunk sums; stats (optional) one per chunk.
+template <class Elem, typename WT, bool STATS>
+__global__ void __launch_bounds__(PW_THREADS) k_pw_chunks(Elem e, const WT* wraw, int64_t n, int depth,
+                                                          double* heap, WStats* cstats) {
+  __shared__ int32_t s_lo[PW_HEAP];
+  __shared__ int32_t s_len[PW_HEAP];
+  __shared__ double s_val[PW_HEAP];
+  __shared__ WStats s_red[PW_THREADS / 32];
+  int64_t lo0, len0;
+  pw_chunk_span(n, depth, blockIdx.x, lo0, len0);
+  for (int h = threadIdx.x; h < PW_HEAP; h += PW_THREADS) s_len[h] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) { s_lo[1] = 0; s_len[1] = (int32_t)len0; }
+  __syncthreads();
+  for (int lvl = 0; lvl < 10; ++lvl) {  // build the subtree top-down
+    const int h0 = 1 << lvl, h1 = min(2 << lvl, PW_HEAP / 2);
+    for (int h = h0 + threadIdx.x; h < h1; h += PW_THREADS) {
+      const int32_t len = s_len[h];
+      if (len > 128) {
+        int32_t n2 = len / 2;
+        n2 -= n2 % 8;
+        s_lo[2 * h] = s_lo[h];
+        s_len[2 * h] = n2;
+        s_lo[2 * h + 1] = s_lo[h] + n2;
+        s_len[2 * h + 1] = len - n2;
+      }
+    }
+    __syncthreads();
+  }
+  WStats st{-1.0, 0, 0, 0, 0, 0};
+  for (int h = 1 + threadIdx.x; h < PW_HEAP; h += PW_THREADS) {  // leaves
+    const int32_t len = s_len[h];
+    if (len > 0 && len <= 128) {
+      const int64_t lo = lo0 + s_lo[h];
+      s_val[h] = pw_leaf(e, lo, len);
+      if constexpr (STATS)
+        for (int32_t q = 0; q < len; ++q) wstat_observe<WT>(st, wraw[lo + q]);
+    }
+  }
+  __syncthreads();
+  for (int lvl = 9; lvl >= 0; --lvl) {  // combine bottom-up in the same order as numpy
+    const int h0 = 1 << lvl, h1 = min(2 << lvl, PW_HEAP / 2);
+    for (int h = h0 + threadIdx.x; h < h1; h += PW_THREADS)
+      if (s_len[h] > 128) s_val[h] = __dadd_rn(s_val[2 * h], s_val[2 * h + 1]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) heap[(1ll << depth) + blockIdx.x] = len0 > 0 ? s_val[1] : 0.0;
+  if constexpr (STATS) {
+    // warp then block reduction of the stats (integer counts + max: order-free)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      st.max = fmax(st.max, __shfl_xor_sync(0xffffffffu, st.max, off));
+      st.n_pos += __shfl_xor_sync(0xffffffffu, st.n_pos, off);
+      st.n_zero += __shfl_xor_sync(0xffffffffu, st.n_zero, off);
+      st.n_neg += __shfl_xor_sync(0xffffffffu, st.n_neg, off);
+      st.n_nonfinite += __shfl_xor_sync(0xffffffffu, st.n_nonfinite, off);
+      st.n_notnormal += __shfl_xor_sync(0xffffffffu, st.n_notnormal, off);
+    }
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = st;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      WStats t = s_red[0];
+      for (int q = 1; q < PW_THREADS / 32; ++q) {
+        t.max = fmax(t.max, s_red[q].max);
+        t.n_pos += s_red[q].n_pos; t.n_zero += s_red[q].n_zero; t.n_neg += s_red[q].n_neg;
+        t.n_nonfinite += s_red[q].n_nonfinite; t.n_notnormal += s_red[q].n_notnormal;
+      }
+      cstats[blockIdx.x] = t;
+    }
+  }
+}
+
+// Combine the complete top tree heap[1 .. 2^(D+1)) in place (single CTA) and emit
+//   out[0] = sum, and, when requested, mean = sum / n, accumulation into *accum.
+struct PwOut {
+  double* sum;       // may be null
+  double* mean;      // may be null
+  double* accum;     // may be null: *accum += sum (sequential, like Python float +=)
+  WStats* stats;     // may be null
+};
+
+__global__ void __launch_bounds__(1024) k_pw_final(double* heap, int depth, int64_t n, const WStats* cstats,
+                                                   PwOut out) {
+  for (int lvl = depth - 1; lvl >= 0; --lvl) {
+    const int64_t h0 = 1ll << lvl, h1 = 2ll << lvl;
+    for (int64_t h = h0 + threadIdx.x; h < h1; h += blockDim.x) heap[h] = __dadd_rn(heap[2 * h], heap[2 * h + 1]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double s = heap[1];
+    if (out.sum) *out.sum = s;
+    if (out.mean) *out.mean = __ddiv_rn(s, (double)n);
+    if (out.accum) *out.accum = __dadd_rn(*out.accum, s);
+  }
+  if (out.stats && cstats) {
+    __shared__ WStats red[32];
+    WStats st{-1.0, 0, 0, 0, 0, 0};
+    const int64_t nch = 1ll << depth;
+    for (int64_t c = threadIdx.x; c < nch; c += blockDim.x) {
+      const WStats& q = cstats[c];
+      st.max = fmax(st.max, q.max);
+      st.n_pos += q.n_pos; st.n_zero += q.n_zero; st.n_neg += q.n_neg;
+      st.n_nonfinite += q.n_nonfinite; st.n_notnormal += q.n_notnormal;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      st.max = fmax(st.max, __shfl_xor_sync(0xffffffffu, st.max, off));
+      st.n_pos += __shfl_xor_sync(0xffffffffu, st.n_pos, off);
+      st.n_zero += __shfl_xor_sync(0xffffffffu, st.n_zero, off);
+      st.n_neg += __shfl_xor_sync(0xffffffffu, st.n_neg, off);
+      st.n_nonfinite += __shfl_xor_sync(0xffffffffu, st.n_nonfinite, off);
+      st.n_notnormal += __shfl_xor_sync(0xffffffffu, st.n_notnormal, off);
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = st;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      WStats t = red[0];
+      for (int q = 1; q < (int)(blockDim.x + 31) / 32; ++q) {
+        t.max = fmax(t.max, red[q].max);
+        t.n_pos += red[q].n_pos; t.n_zero += red[q].n_zero; t.n_neg += red[q].n_neg;
+        t.n_nonfinite += red[q].n_nonfinite; t.n_notnormal += red[q].n_notnormal;
+      }
+      *out.stats = t;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Offspring histogram (M/resample.py:361-368): counts[a] += 1 with warp-aggregated
+// atomics -- lanes holding the same ancestor elect one leader that adds the
+// popcount, so the heavy ancestors of degenerate (y = 4) weights do not serialise
+// 32 atomics per warp.  Out-of-range ancestors set *bad.
+
+template <typename CT>
+__global__ void k_offspring(const int64_t* __restrict__ anc, int64_t n_anc, int64_t n, CT* counts, int* bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = i < n_anc;
+  int64_t a = live ? anc[i] : -1;
+  const bool ok = live && a >= 0 && a < n;
+  if (live && !ok) atomicExch(bad, 1);
+  const unsigned act = __ballot_sync(0xffffffffu, ok);
+  if (!ok) return;
+  const unsigned peers = __match_any_sync(act, (unsigned long long)a);
+  const int leader = __ffs(peers) - 1;
+  if ((int)(threadIdx.x & 31) == leader) {
+    if constexpr (sizeof(CT) == 8)
+      atomicAdd(reinterpret_cast<unsigned long long*>(counts) + a, (unsigned long long)__popc(peers));
+    else
+      atomicAdd(reinterpret_cast<unsigned int*>(counts) + a, (unsigned int)__popc(peers));
+  }
+}
+
+// QualityAccumulator.add element update (M/metrics.py:90-92): sum += o, sum_sq += o*o
+template <typename CT>
+__global__ void k_quality_accum(const CT* __restrict__ counts, int64_t n, double* sum, double* sumsq) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double o = (double)counts[i];
+    sum[i] = __dadd_rn(sum[i], o);
+    sumsq[i] = __dadd_rn(sumsq[i], __dmul_rn(o, o));
+  }
+}
+
+// expected offspring N * w / sum(w)  (M/metrics.py:55-60: len(values) * values / total)
+template <typename WT>
+__global__ void k_expected(const WT* __restrict__ w, int64_t n, const double* total, double* e) {
+  const double t = *total;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    e[i] = __ddiv_rn(__dmul_rn((double)n, (double)w[i]), t);
+}
+
+// ---------------------------------------------------------------------------
+// Ancestor-driven particle-state gather (M/resample.py:371-377): out[i] = states[anc[i]].
+// Rows of row_bytes; vector width V (16/8/4/1 bytes) chosen by alignment.
+
+template <typename V>
+__global__ void k_gather(const V* __restrict__ src, const int64_t* __restrict__ anc, int64_t n, int64_t row_v,
+                         V* __restrict__ dst) {
+  const int64_t total = n * row_v;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / row_v, c = t - i * row_v;
+    dst[t] = __ldg(src + anc[i] * row_v + c);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Synthetic Gaussian-family weights on the device (M/weights.py:100-104 with the
+// Box-Muller draw of M/rng.py:152-161).  Same formula and stream; libm rounding of
+// exp/log/cos may differ from the host's in the last float64 bit.
+
+template <typename WT>
+__global__ void k_gen_gaussian(double y, int64_t n, uint64_t seed, WT* out) {
+  const uint64_t base = megores_base(seed);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = megores_key(base, (uint64_t)i, 0);
+    const uint64_t h1 = mix64(x), h2 = mix64(x + M_SALT);
+    const double u1 = ((double)(h1 >> 11) + 0.5) * 0x1p-53;
+    const double u2 = (double)(h2 >> 11) * 0x1p-53;
+    const double z = sqrt(-2.0 * log(u1)) * cos(2.0 * 3.141592653589793 * u2);
+    const double d = z - y;
+    out[i] = (WT)(exp(-0.5 * (d * d)) * 0.3989422804014327);
+  }
+}
+
+}  // namespace mgp

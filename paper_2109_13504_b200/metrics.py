@@ -1,0 +1,127 @@
+"""Resampling quality statistics on the B200 (mirrors M/metrics.py:33-121).
+
+The offspring bias / MSE metric of the paper (and of BASELINE.json).  All
+accumulators live in HBM as float64 and every reduction uses numpy's pairwise
+summation order, so the statistics are bit-identical to the reference's
+``QualityAccumulator`` for the same offspring vectors.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _device as D
+from . import _lib
+from .weights import _as_weight_vector
+
+
+@dataclass(frozen=True)
+class QualityStats:  # M/metrics.py:33-39
+    mse: float
+    variance: float
+    bias_sq: float
+    bias_contribution: float
+    mse_per_particle: float
+
+
+def _dev_weights(w):
+    t = D.torch()
+    wv = _as_weight_vector(w)
+    vals = wv.values if wv.on_device else t.from_numpy(np.ascontiguousarray(wv.values)).cuda()
+    return vals
+
+
+def _dev_counts(offspring, device):
+    t = D.torch()
+    if D.is_tensor(offspring):
+        return offspring.to(device=device, dtype=t.int64).contiguous()
+    return t.from_numpy(np.ascontiguousarray(offspring, dtype=np.int64)).to(device)
+
+
+def _expected(vals):
+    t = D.torch()
+    e = t.empty(vals.numel(), dtype=t.float64, device=vals.device)
+    total = t.empty(1, dtype=t.float64, device=vals.device)
+    with t.cuda.device(vals.device):
+        _lib.check(_lib.lib().mgp_expected_offspring(D.ptr(vals), D.wdtype(vals), vals.numel(), D.ptr(e),
+                                                     D.ptr(total), D.stream_ptr()))
+    if not float(total.item()) > 0:  # M/metrics.py:57-59
+        raise ValueError("total weight must be positive")
+    return e
+
+
+def squared_error(offspring, w) -> float:
+    """Sum of squared deviations from the expected offspring counts (M/metrics.py:63-68)."""
+    D.require_cuda()
+    t = D.torch()
+    vals = _dev_weights(w)
+    n_off = offspring.shape[0] if D.is_tensor(offspring) else len(offspring)
+    if n_off != vals.numel():
+        raise ValueError(f"length mismatch: {n_off} offspring vs {vals.numel()} weights")
+    e = _expected(vals)
+    o = _dev_counts(offspring, vals.device)
+    out = t.empty(1, dtype=t.float64, device=vals.device)
+    with t.cuda.device(vals.device):
+        _lib.check(_lib.lib().mgp_squared_error(D.ptr(o), D.ptr(e), o.numel(), D.ptr(out), D.stream_ptr()))
+    return float(out.item())
+
+
+class QualityAccumulator:
+    """Streaming mean/variance over K offspring vectors (M/metrics.py:71-110), in HBM."""
+
+    def __init__(self, n: int, device=None):
+        D.require_cuda()
+        t = D.torch()
+        self.n = n
+        self.k = 0
+        self.device = t.device("cuda") if device is None else t.device(device)
+        self._sum = t.zeros(n, dtype=t.float64, device=self.device)
+        self._sum_sq = t.zeros(n, dtype=t.float64, device=self.device)
+        self._se = t.zeros(2, dtype=t.float64, device=self.device)  # [se_total, se_last_run]
+        self._expected = None
+
+    def add(self, offspring, w) -> None:
+        t = D.torch()
+        if self._expected is None:
+            self._expected = _expected(_dev_weights(w).to(self.device))
+        o = _dev_counts(offspring, self.device)
+        self.k += 1
+        with t.cuda.device(self.device):
+            _lib.check(_lib.lib().mgp_quality_add(D.ptr(o), D.ptr(self._expected), self.n, D.ptr(self._sum),
+                                                  D.ptr(self._sum_sq), D.ptr(self._se),
+                                                  D.ptr(self._se[1:]), D.stream_ptr()))
+
+    @property
+    def _se_total(self) -> float:
+        return float(self._se[0].item())
+
+    def finalize(self) -> QualityStats:
+        if self.k < 2:
+            raise ValueError(f"need at least 2 runs to estimate variance, got {self.k}")
+        t = D.torch()
+        out = t.empty(2, dtype=t.float64, device=self.device)
+        with t.cuda.device(self.device):
+            _lib.check(_lib.lib().mgp_quality_finalize(D.ptr(self._sum), D.ptr(self._sum_sq), D.ptr(self._expected),
+                                                       self.n, self.k, D.ptr(out), D.ptr(out[1:]), D.stream_ptr()))
+        variance, bias_sq = (float(x) for x in out.cpu().numpy())
+        mse = self._se_total / self.k
+        contribution = bias_sq / mse if mse > 0 else 0.0
+        return QualityStats(mse=mse, variance=variance, bias_sq=bias_sq, bias_contribution=contribution,
+                            mse_per_particle=mse / self.n)
+
+
+def quality_stats(runs, w) -> QualityStats:
+    """MSE / variance / squared-bias over a (K, N) stack of offspring vectors (M/metrics.py:113-121)."""
+    if D.is_tensor(runs):
+        shape = tuple(runs.shape)
+    else:
+        runs = np.asarray(runs)
+        shape = runs.shape
+    if len(shape) != 2:
+        raise ValueError("runs must have shape (K, N)")
+    acc = QualityAccumulator(shape[1])
+    for row in runs:
+        acc.add(row, w)
+    return acc.finalize()

@@ -1,0 +1,254 @@
+"""Metropolis-family resamplers on the B200 -- drop-in for pkg/src/megores/resample.py.
+
+Same names, signatures, defaults, return types and errors as the reference
+(M/ = pkg/src/megores/):
+  metropolis      M/resample.py:201-206     metropolis_c1  :209-225
+  metropolis_c2   :228-244                  megopolis      :268-282
+  make_resampler  :431-455                  megopolis_offsets :263-265
+  ancestors_to_offspring :361-368           apply_ancestors   :371-377
+  WarpConfig :59-75, PartitionConfig :78-93, METROPOLIS_FAMILY / ALGORITHMS :55-56
+
+Inputs: a WeightVector (this package's or the reference's), a numpy array, or a
+CUDA tensor.  Host inputs go through the host-buffer C-ABI entry
+(``mgp_resample_host``: upload, validate, resample, overlapped download) and
+return ``np.int64`` arrays like the reference.  CUDA-tensor inputs stay in HBM,
+run asynchronously on the current torch stream after one validation pass, and
+return an int64 CUDA tensor.
+
+Extra keyword ``rng``: "megores" (default; the reference's stream, bit-exact with
+the reference) or "philox" (Philox4x32-10).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _device as D
+from . import _lib
+from .weights import WeightVector, _as_weight_vector
+
+METROPOLIS_FAMILY = ("metropolis", "c1", "c2", "megopolis")
+ALGORITHMS = METROPOLIS_FAMILY  # prefix-sum resamplers are not on the B200 hot path
+
+
+@dataclass(frozen=True)
+class WarpConfig:
+    """Logical warp geometry (M/resample.py:59-75).  W is semantic: it fixes the
+    Megopolis partner index and the C1/C2 partition owner, independent of hardware."""
+
+    warp_size: int = 32
+    word_bytes: int = 4
+    segment_bytes: int = 32
+
+    def __post_init__(self):
+        if self.warp_size < 1:
+            raise ValueError(f"warp_size must be positive, got {self.warp_size}")
+        if self.word_bytes < 1 or self.segment_bytes % self.word_bytes:
+            raise ValueError("segment_bytes must be a positive multiple of word_bytes")
+
+    @property
+    def words_per_segment(self) -> int:
+        return self.segment_bytes // self.word_bytes
+
+
+@dataclass(frozen=True)
+class PartitionConfig:
+    """Partition geometry for the c1/c2 variants (M/resample.py:78-93)."""
+
+    partition_bytes: int
+
+    def n_weights(self, warp: WarpConfig) -> int:
+        if self.partition_bytes < 1 or self.partition_bytes % warp.word_bytes:
+            raise ValueError("partition_bytes must be a positive multiple of word_bytes")
+        return self.partition_bytes // warp.word_bytes
+
+    def n_partitions(self, n: int, warp: WarpConfig) -> int:
+        n_w = self.n_weights(warp)
+        if n % n_w:
+            raise ValueError(f"N={n} is not divisible by the partition width {n_w}")
+        return n // n_w
+
+
+def _seed(seed) -> int:
+    return int(np.uint64(seed)) if not isinstance(seed, int) else seed & (2**64 - 1)
+
+
+def _rng(rng: str) -> int:
+    try:
+        return _lib.RNG[rng]
+    except KeyError:
+        raise ValueError(f"unknown rng stream {rng!r} (choose 'megores' or 'philox')") from None
+
+
+def _validate(w: WeightVector, b, warp, strict, part, name):
+    """Argument checks in the reference's order (M/resample.py:96-108, 84-93); the
+    all-zero check needs the data, so it is consulted only when deciding which
+    error the reference would raise first or on the device path."""
+    n = len(w)
+    errs = []
+    if b < 1:
+        errs.append(f"B must be >= 1, got {b}")
+    elif warp is not None and strict and n % warp.warp_size:
+        errs.append(f"{name} requires N ({n}) to be a multiple of the warp size "
+                    f"({warp.warp_size}) in strict mode")
+    elif part is not None:
+        try:
+            part.n_partitions(n, warp)
+        except ValueError as e:
+            errs.append(str(e))
+    if errs:
+        if not w.on_device and not np.any(w.values > 0):
+            raise ValueError("all weights are zero")
+        if w.on_device and w.stats().n_pos == 0:
+            raise ValueError("all weights are zero")
+        raise ValueError(errs[0])
+
+
+def _resample(kind, w, b, seed, warp, part, strict, rng, name):
+    w = _as_weight_vector(w)
+    b = int(b)
+    _validate(w, b, warp, strict, part, name)
+    L = _lib.lib()
+    ws = warp.warp_size if warp is not None else 32
+    pb = part.partition_bytes if part is not None else 0
+    if w.on_device:
+        t = D.torch()
+        vals = w.values
+        st = w.stats()
+        if st.n_pos == 0:
+            raise ValueError("all weights are zero")
+        flags = _lib.FLAG_POSITIVE_NORMAL if st.positive_normal else 0
+        out = t.empty(len(w), dtype=t.int64, device=vals.device)
+        with t.cuda.device(vals.device):
+            s = D.stream_ptr()
+            args = (D.ptr(vals), D.wdtype(vals), len(w), b, _seed(seed))
+            if kind == "megopolis":
+                rc = L.mgp_megopolis(*args, ws, int(bool(strict)), _rng(rng), flags, D.ptr(out), s)
+            elif kind == "metropolis":
+                rc = L.mgp_metropolis(*args, _rng(rng), flags, D.ptr(out), s)
+            elif kind == "c1":
+                rc = L.mgp_metropolis_c1(*args, ws, pb, int(bool(strict)), _rng(rng), flags, D.ptr(out), s)
+            else:
+                rc = L.mgp_metropolis_c2(*args, ws, pb, int(bool(strict)), _rng(rng), flags, D.ptr(out), s)
+        _lib.check(rc)
+        return out
+    D.require_cuda()
+    vals = np.ascontiguousarray(w.values)
+    out = np.empty(len(vals), dtype=np.int64)
+    b_used = ctypes.c_int32(0)
+    rc = L.mgp_resample_host(_lib.KIND[kind], D.ptr(vals), D.wdtype(vals), len(vals), b, 0.0, _seed(seed), ws, pb,
+                             int(bool(strict)), _rng(rng), D.ptr(out), ctypes.byref(b_used), -1)
+    _lib.check(rc)
+    return out
+
+
+def metropolis(w, b: int, seed, *, rng: str = "megores"):
+    """Independent per-particle random comparisons; fully random access (M/resample.py:201-206)."""
+    return _resample("metropolis", w, b, seed, None, None, False, rng, "metropolis")
+
+
+def metropolis_c1(w, b: int, part: PartitionConfig, warp: WarpConfig = WarpConfig(), seed=0, strict: bool = True,
+                  *, rng: str = "megores"):
+    """One shared partition per warp for all B rounds (M/resample.py:209-225)."""
+    return _resample("c1", w, b, seed, warp, part, strict, rng, "metropolis_c1")
+
+
+def metropolis_c2(w, b: int, part: PartitionConfig, warp: WarpConfig = WarpConfig(), seed=0, strict: bool = True,
+                  *, rng: str = "megores"):
+    """A fresh shared partition per warp at every round (M/resample.py:228-244)."""
+    return _resample("c2", w, b, seed, warp, part, strict, rng, "metropolis_c2")
+
+
+def megopolis(w, b: int, warp: WarpConfig = WarpConfig(), seed=0, strict: bool = True, *, rng: str = "megores"):
+    """Shared global offsets with warp-aligned wrapped-sequential reads (M/resample.py:268-282)."""
+    return _resample("megopolis", w, b, seed, warp, None, strict, rng, "megopolis")
+
+
+def megopolis_index(i: int, o_b: int, warp: WarpConfig, n: int) -> int:
+    """Wrapped-sequential comparison index (M/resample.py:247-260); host helper."""
+    if not (0 <= i < n) or not (0 <= o_b < n):
+        raise ValueError("i and o_b must lie in [0, N)")
+    ws = warp.warp_size
+    return (i - i % ws + o_b - o_b % ws + (i + o_b) % ws) % n
+
+
+def megopolis_offsets(n: int, b: int, seed, *, rng: str = "megores") -> np.ndarray:
+    """The shared offset list: B uniform integers on the reserved global lane (M/resample.py:263-265)."""
+    out = np.empty(max(int(b), 1), dtype=np.int64)
+    _lib.check(_lib.lib().mgp_offsets_host(_seed(seed), int(n), int(b), _rng(rng), D.ptr(out)))
+    return out[: int(b)]
+
+
+def make_resampler(kind: str, warp: WarpConfig = WarpConfig(), partition_bytes: int | None = None,
+                   strict: bool = True, *, rng: str = "megores"):
+    """Bind an algorithm id to a uniform ``fn(w, b, seed) -> ancestors`` (M/resample.py:431-455)."""
+    if kind == "metropolis":
+        return lambda w, b, seed: metropolis(w, b, seed, rng=rng)
+    if kind in ("c1", "c2"):
+        if partition_bytes is None:
+            raise ValueError(f"{kind} requires a partition size")
+        part = PartitionConfig(partition_bytes)
+        fn = metropolis_c1 if kind == "c1" else metropolis_c2
+        return lambda w, b, seed: fn(w, b, part, warp, seed, strict, rng=rng)
+    if kind == "megopolis":
+        return lambda w, b, seed: megopolis(w, b, warp, seed, strict, rng=rng)
+    if kind in ("multinomial", "systematic"):
+        raise NotImplementedError(f"{kind!r} is a prefix-sum resampler outside the B200 hot path (SURVEY 8f)")
+    raise ValueError(f"unknown resampler {kind!r}")
+
+
+def ancestors_to_offspring(ancestors, n: int | None = None):
+    """Count how many particles chose each index as their ancestor (M/resample.py:361-368).
+
+    Device histogram with warp-aggregated atomics.  numpy in -> numpy out;
+    CUDA tensor in -> CUDA tensor out."""
+    D.require_cuda()
+    t = D.torch()
+    host = not D.is_cuda_tensor(ancestors)
+    dev = t.device("cuda") if host else ancestors.device
+    a = D.as_index_tensor(ancestors, dev)
+    n = a.numel() if n is None else int(n)
+    counts = t.empty(max(n, 1), dtype=t.int64, device=dev)
+    bad = t.zeros(1, dtype=t.int32, device=dev)
+    with t.cuda.device(dev):
+        _lib.check(_lib.lib().mgp_offspring(D.ptr(a), a.numel(), n, D.ptr(counts), D.ptr(bad), D.stream_ptr()))
+        if a.numel() and int(bad.item()):
+            raise ValueError("ancestor indices out of range")
+    counts = counts[:n]
+    return counts.cpu().numpy() if host else counts
+
+
+def apply_ancestors(states, ancestors):
+    """Gather states by ancestor index into a fresh array (M/resample.py:371-377).
+
+    Rows of any dtype/shape (states[N, ...]); numpy in -> numpy out."""
+    D.require_cuda()
+    t = D.torch()
+    host = not D.is_cuda_tensor(states)
+    if host:
+        s_np = np.ascontiguousarray(np.asarray(states))
+        n_states = len(s_np)
+    else:
+        n_states = states.shape[0]
+    n_anc = len(ancestors) if not D.is_tensor(ancestors) else ancestors.shape[0]
+    if n_states != n_anc:
+        raise ValueError(f"length mismatch: {n_states} states vs {n_anc} ancestors")
+    dev = t.device("cuda") if host else states.device
+    a = D.as_index_tensor(ancestors, dev)
+    if a.numel() and (int(a.min()) < 0 or int(a.max()) >= n_states):
+        raise IndexError("ancestor index out of range")
+    if host:
+        src = t.from_numpy(s_np.view(np.uint8).reshape(n_states, -1) if s_np.size else
+                           np.zeros((n_states, 0), np.uint8)).to(dev)
+    else:
+        src = states.contiguous()
+    out = t.empty_like(src)
+    row_bytes = (src.numel() * src.element_size()) // max(n_states, 1)
+    with t.cuda.device(dev):
+        _lib.check(_lib.lib().mgp_gather(D.ptr(src), row_bytes, D.ptr(a), n_states, D.ptr(out), D.stream_ptr()))
+    if host:
+        return out.cpu().numpy().view(s_np.dtype).reshape(s_np.shape)
+    return out

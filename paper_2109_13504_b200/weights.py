@@ -1,0 +1,191 @@
+"""Weight vectors and the iteration budget (the B rule) on the B200.
+
+Mirrors pkg/src/megores/weights.py (M/weights.py):
+  * ``WeightVector``        M/weights.py:42-62 (same validation and errors; values may
+                            also be a CUDA tensor, validated by one fused device pass)
+  * ``compute_iterations``  M/weights.py:114-131 (host arithmetic, identical)
+  * ``iterations_for``      the f64 mean/max of M/bench.py:119-120 computed on the
+                            device (numpy-exact pairwise sum) then ``compute_iterations``
+  * ``gen_gaussian_weights`` M/weights.py:100-104 evaluated on the device
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _device as D
+from . import _lib
+
+GAUSSIAN_PEAK = 1.0 / math.sqrt(2.0 * math.pi)  # M/weights.py:37
+_DTYPES = {"single": np.float32, "double": np.float64}
+_TORCH_DTYPES = {"single": "float32", "double": "float64"}
+
+
+class _StatsStruct(ctypes.Structure):  # mgp_weight_stats_t
+    _fields_ = [("sum", ctypes.c_double), ("mean", ctypes.c_double), ("max", ctypes.c_double),
+                ("n_pos", ctypes.c_int64), ("n_zero", ctypes.c_int64), ("n_neg", ctypes.c_int64),
+                ("n_nonfinite", ctypes.c_int64), ("n_notnormal", ctypes.c_int64)]
+
+
+@dataclass(frozen=True)
+class WeightStats:
+    """One fused device pass over the weights (mgp_weight_stats)."""
+
+    n: int
+    sum: float
+    mean: float
+    max: float
+    n_pos: int
+    n_zero: int
+    n_neg: int
+    n_nonfinite: int
+    n_notnormal: int
+
+    @property
+    def positive_normal(self) -> bool:
+        return self.n_notnormal == 0
+
+
+def device_stats(values) -> WeightStats:
+    """Weight statistics of a CUDA tensor (synchronises to read 64 bytes back)."""
+    t = D.torch()
+    values = values.contiguous()
+    out = t.empty(8, dtype=t.float64, device=values.device)
+    with t.cuda.device(values.device):
+        _lib.check(_lib.lib().mgp_weight_stats(D.ptr(values), D.wdtype(values), values.numel(),
+                                               D.ptr(out), D.stream_ptr()))
+        host = out.cpu().numpy()
+    s = _StatsStruct.from_buffer_copy(host.tobytes())
+    return WeightStats(values.numel(), s.sum, s.mean, s.max, s.n_pos, s.n_zero, s.n_neg, s.n_nonfinite,
+                       s.n_notnormal)
+
+
+class WeightVector:
+    """Non-negative particle weights; normalisation is not required (M/weights.py:42-62).
+
+    ``values`` may be anything numpy accepts (validated on the host exactly like the
+    reference) or a CUDA tensor (kept in HBM, validated by one device pass).
+    """
+
+    def __init__(self, values, precision: str = "single"):
+        if precision not in _DTYPES:
+            raise ValueError(f"precision must be 'single' or 'double', got {precision!r}")
+        self.precision = precision
+        self._stats = None
+        if D.is_cuda_tensor(values):
+            t = D.torch()
+            values = values.to(getattr(t, _TORCH_DTYPES[precision])).contiguous()
+            if values.dim() != 1 or values.numel() < 1:
+                raise ValueError("weights must be a non-empty 1-d sequence")
+            st = device_stats(values)
+            if st.n_nonfinite:
+                raise ValueError("weights must be finite")
+            if st.n_neg:
+                raise ValueError("weights must be non-negative")
+            self._stats = st
+            self.values = values
+            return
+        if D.is_tensor(values):
+            values = values.detach().cpu().numpy()
+        values = np.asarray(values, dtype=_DTYPES[precision])
+        if values.ndim != 1 or len(values) < 1:
+            raise ValueError("weights must be a non-empty 1-d sequence")
+        if not np.all(np.isfinite(values)):
+            raise ValueError("weights must be finite")
+        if np.any(values < 0):
+            raise ValueError("weights must be non-negative")
+        self.values = values
+
+    def __len__(self) -> int:
+        return int(self.values.shape[0])
+
+    @property
+    def on_device(self) -> bool:
+        return D.is_cuda_tensor(self.values)
+
+    def stats(self) -> WeightStats:
+        """Device statistics (cached for device-resident weights)."""
+        if self._stats is None:
+            D.require_cuda()
+            t = D.torch()
+            vals = self.values if self.on_device else t.from_numpy(np.ascontiguousarray(self.values)).cuda()
+            self._stats = device_stats(vals)
+        return self._stats
+
+
+@dataclass(frozen=True)
+class GaussianWeightParams:  # M/weights.py:65-74
+    y: float
+    n: int
+
+    def __post_init__(self):
+        if self.y < 0:
+            raise ValueError(f"y must be >= 0, got {self.y}")
+        if self.n < 1:
+            raise ValueError(f"n must be >= 1, got {self.n}")
+
+
+@dataclass(frozen=True)
+class IterationBudget:  # M/weights.py:90-97
+    b: int
+    epsilon: float
+
+    def __post_init__(self):
+        if self.b < 1:
+            raise ValueError(f"B must be >= 1, got {self.b}")
+
+
+def compute_iterations(epsilon: float, mean_w: float, max_w: float) -> IterationBudget:
+    """B = ceil(ln(eps) / ln(1 - mean_w / max_w)), clamped to >= 1 (M/weights.py:114-131)."""
+    if not (0.0 < epsilon <= 1.0):
+        raise ValueError(f"epsilon must be in (0, 1], got {epsilon}")
+    if mean_w <= 0 or max_w <= 0:
+        raise ValueError("mean_w and max_w must be positive")
+    if mean_w > max_w:
+        raise ValueError(f"mean_w ({mean_w}) exceeds max_w ({max_w})")
+    ratio = mean_w / max_w
+    if ratio >= 1.0 or epsilon == 1.0:
+        return IterationBudget(1, epsilon)
+    b = math.ceil(math.log(epsilon) / math.log(1.0 - ratio))
+    return IterationBudget(max(b, 1), epsilon)
+
+
+def _as_weight_vector(w) -> WeightVector:
+    if isinstance(w, WeightVector):
+        return w
+    if hasattr(w, "values") and hasattr(w, "precision"):  # the reference's WeightVector
+        return WeightVector(w.values, w.precision)
+    if D.is_tensor(w) or isinstance(w, np.ndarray):
+        prec = "double" if str(w.dtype).endswith("float64") else "single"
+        return WeightVector(w, prec)
+    return WeightVector(w)
+
+
+def iterations_for(w, epsilon: float = 0.01) -> IterationBudget:
+    """The benchmark's B rule: f64 mean and max of the weights (M/bench.py:119-120),
+    computed on the device with numpy's pairwise summation order, then
+    ``compute_iterations``.  Bit-identical to the reference's B."""
+    st = _as_weight_vector(w).stats()
+    if st.n_pos == 0:
+        raise ValueError("mean_w and max_w must be positive")
+    return compute_iterations(epsilon, st.mean, st.max)
+
+
+def gen_gaussian_weights(params: GaussianWeightParams, seed, precision="single", device=None) -> WeightVector:
+    """w_i = exp(-(x_i - y)^2 / 2) / sqrt(2 pi), x_i ~ N(0,1) by Box-Muller on the
+    reference's stream (M/weights.py:100-104, M/rng.py:152-161), generated in HBM.
+    libm rounding on the device may differ from the host's in the last float64 bit."""
+    D.require_cuda()
+    t = D.torch()
+    if precision not in _DTYPES:
+        raise ValueError(f"precision must be 'single' or 'double', got {precision!r}")
+    dev = t.device("cuda") if device is None else t.device(device)
+    out = t.empty(params.n, dtype=getattr(t, _TORCH_DTYPES[precision]), device=dev)
+    with t.cuda.device(dev):
+        _lib.check(_lib.lib().mgp_gen_gaussian(float(params.y), params.n, int(seed) & (2**64 - 1),
+                                               D.wdtype(out), D.ptr(out), D.stream_ptr()))
+    return WeightVector(out, precision)

@@ -1,0 +1,366 @@
+"""GPU parity: libmgp.so (through the public API / C ABI) vs the reference's golden
+vectors and the CPU oracle.  Bit-exact for every integer / index result and for the
+float64 statistics (numpy summation order reproduced)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:32]
+
+
+@pytest.fixture(scope="module")
+def mg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2109_13504_b200 as m
+    from paper_2109_13504_b200 import build
+
+    build.build()
+    return m
+
+
+def run_case(mg, c, w, rng="megores"):
+    kind = c["kind"]
+    W = mg.WarpConfig(warp_size=c["warp"])
+    if kind == "megopolis":
+        return mg.megopolis(w, c["b"], W, c["seed"], c["strict"], rng=rng)
+    if kind == "metropolis":
+        return mg.metropolis(w, c["b"], c["seed"], rng=rng)
+    part = mg.PartitionConfig(c["part"])
+    fn = mg.metropolis_c1 if kind == "c1" else mg.metropolis_c2
+    return fn(w, c["b"], part, W, c["seed"], c["strict"], rng=rng)
+
+
+def to_np(a):
+    return a.cpu().numpy() if torch.is_tensor(a) else a
+
+
+def test_golden_cases_host_buffers(mg, golden):
+    """Every stored reference case through the numpy (host-buffer C-ABI) path."""
+    meta, z = golden
+    n = 0
+    for c in meta["cases"]:
+        if "w" not in c:
+            continue
+        wv = mg.WeightVector(z[c["w"]], c["precision"])
+        got = run_case(mg, c, wv)
+        assert isinstance(got, np.ndarray) and got.dtype == np.int64
+        assert np.array_equal(got, z[c["anc"]]), f"{c['tag']}/{c['kind']}"
+        n += 1
+    assert n > 250
+
+
+def test_golden_cases_device_tensors(mg, golden):
+    """Same cases with weights resident in HBM (async device path)."""
+    meta, z = golden
+    for c in meta["cases"]:
+        if "w" not in c:
+            continue
+        w = torch.from_numpy(z[c["w"]]).cuda()
+        got = run_case(mg, c, mg.WeightVector(w, c["precision"]))
+        assert got.is_cuda and got.dtype == torch.int64
+        assert np.array_equal(got.cpu().numpy(), z[c["anc"]]), f"{c['tag']}/{c['kind']}"
+
+
+def test_philox_stream_vs_oracle(mg, golden, oracle):
+    meta, z = golden
+    for c in meta["cases"]:
+        if "w" not in c:
+            continue
+        w = z[c["w"]]
+        got = to_np(run_case(mg, c, mg.WeightVector(w, c["precision"]), rng="philox"))
+        kw = dict(rng="philox")
+        if c["kind"] == "megopolis":
+            ref = oracle.megopolis(w, c["b"], c["warp"], c["seed"], c["strict"], **kw)
+        elif c["kind"] == "metropolis":
+            ref = oracle.metropolis(w, c["b"], c["seed"], **kw)
+        else:
+            fn = oracle.metropolis_c1 if c["kind"] == "c1" else oracle.metropolis_c2
+            ref = fn(w, c["b"], c["part"], c["warp"], c["seed"], c["strict"], **kw)
+        assert np.array_equal(got, ref), f"philox {c['tag']}/{c['kind']}"
+
+
+def test_philox_matches_curand(mg):
+    import ctypes
+
+    from paper_2109_13504_b200 import _lib
+
+    bad = ctypes.c_int64(-1)
+    for key, c1, c2, c3 in [(0, 0, 0, 0), (2**64 - 1, 7, 9, 11), (0x0123456789ABCDEF, 1 << 31, 5, 0)]:
+        _lib.check(_lib.lib().mgp_philox_selftest(key, c1, c2, c3, 1 << 20, ctypes.byref(bad)))
+        assert bad.value == 0
+
+
+def test_config1_golden(mg, golden):
+    meta, z = golden
+    w_np = z["config1_w"]
+    for dev in (False, True):
+        w = mg.WeightVector(torch.from_numpy(w_np).cuda() if dev else w_np, "single")
+        budget = mg.iterations_for(w, 0.01)
+        assert budget.b == meta["config1"]["b"] == 6
+        st = w.stats()
+        assert st.mean == meta["config1"]["mean"] and st.max == meta["config1"]["max"]
+        for c in meta["cases"]:
+            if c["tag"] == "config1":
+                got = to_np(run_case(mg, c, w))
+                assert sha(got) == c["anc_sha"], c["kind"]
+                assert np.array_equal(got[z[c["sample_pos"]]], z[c["sample_anc"]])
+
+
+def mean_input(n, seed=81):
+    r = np.random.default_rng([seed, n])
+    mant = r.integers(0, 2**23, n, dtype=np.uint32)
+    expo = r.integers(127 - 20, 127 + 20, n, dtype=np.uint32)
+    return ((expo << np.uint32(23)) | mant).view(np.float32)
+
+
+def test_weight_stats_numpy_exact(mg, golden):
+    meta, _ = golden
+    from paper_2109_13504_b200.weights import device_stats
+
+    for r in meta["means"]:
+        a = mean_input(r["n"])
+        for dt in (np.float32, np.float64):
+            st = device_stats(torch.from_numpy(a.astype(dt)).cuda())
+            assert st.sum == r["sum"] and st.mean == r["mean"], (r["n"], dt)
+            assert st.max == float(a.max())
+            assert st.n_pos == r["n"] and st.n_notnormal == 0
+    # odd sizes across the chunk boundary vs numpy directly
+    rr = np.random.default_rng(5)
+    for n in (32767, 32768, 32769, 65536 * 3 + 17, 2**20 - 3, 5_000_001):
+        a = rr.random(n).astype(np.float64) ** 3
+        st = device_stats(torch.from_numpy(a).cuda())
+        assert st.sum == float(a.sum()) and st.mean == float(a.mean()), n
+    # flags
+    a = np.array([0.0, -0.0, 1e-40, 1.0, 2.0], dtype=np.float32)
+    st = device_stats(torch.from_numpy(a).cuda())
+    assert (st.n_zero, st.n_pos, st.n_notnormal) == (2, 3, 3)
+    a = np.array([1.0, np.inf, -1.0, np.nan], dtype=np.float64)
+    st = device_stats(torch.from_numpy(a).cuda())
+    assert st.n_nonfinite == 2 and st.n_neg == 1
+
+
+def test_b_rule_golden(mg, golden, oracle):
+    meta, _ = golden
+    for r in meta["b_rule"]:
+        if "n" not in r:
+            continue
+        w = oracle.gen_gaussian_weights(r["y"], r["n"], oracle.derive_seed(71, r["n"], int(r["y"])), r["precision"])
+        if sha(w) != r["w_sha"]:
+            continue
+        wv = mg.WeightVector(torch.from_numpy(w).cuda(), r["precision"])
+        assert mg.iterations_for(wv, r["eps"]).b == r["b"]
+        assert wv.stats().mean == r["mean"] and wv.stats().max == r["max"]
+
+
+def test_quality_bit_exact(mg, golden):
+    meta, z = golden
+    for q in meta["quality"]:
+        w = z[q["w"]]
+        offs = z[q["offspring"]]
+        acc = mg.QualityAccumulator(q["n"])
+        for o in offs:
+            acc.add(torch.from_numpy(o).cuda(), mg.WeightVector(w, "double"))
+        st = acc.finalize()
+        for key in ("mse", "variance", "bias_sq", "bias_contribution", "mse_per_particle"):
+            assert getattr(st, key) == q[key], (q["kind"], key)
+        assert mg.squared_error(offs[0], mg.WeightVector(w, "double")) == q["se0"]
+
+
+def test_offspring_histogram(mg):
+    rr = np.random.default_rng(3)
+    for n in (1, 31, 1000, 1 << 16):
+        for heavy in (False, True):
+            a = rr.integers(0, n, n) if not heavy else rr.choice(np.arange(min(n, 5)), n)
+            got = mg.ancestors_to_offspring(a, n)
+            assert np.array_equal(got, np.bincount(a, minlength=n))
+            gd = mg.ancestors_to_offspring(torch.from_numpy(a).cuda(), n)
+            assert np.array_equal(gd.cpu().numpy(), got)
+    with pytest.raises(ValueError):
+        mg.ancestors_to_offspring(np.array([0, 7]), 4)
+    with pytest.raises(ValueError):
+        mg.ancestors_to_offspring(np.array([-1, 0]), 4)
+    assert list(mg.ancestors_to_offspring(np.array([2, 2, 0, 5, 5, 5]))) == [1, 0, 2, 0, 0, 3]
+
+
+def test_gather(mg):
+    rr = np.random.default_rng(4)
+    for shape, dt in [((1000,), np.float64), ((1000,), np.float32), ((513, 3), np.float32), ((64, 7), np.uint8),
+                      ((300, 4), np.float64), ((77, 2, 5), np.int16)]:
+        s = (rr.random(shape) * 100).astype(dt)
+        a = rr.integers(0, shape[0], shape[0])
+        assert np.array_equal(mg.apply_ancestors(s, a), s[a])
+        sd = torch.from_numpy(s).cuda()
+        assert np.array_equal(mg.apply_ancestors(sd, torch.from_numpy(a).cuda()).cpu().numpy(), s[a])
+    s = np.array([1.0, 2.0])
+    out = mg.apply_ancestors(s, np.array([1, 0]))
+    assert list(s) == [1.0, 2.0] and list(out) == [2.0, 1.0]
+    with pytest.raises(ValueError):
+        mg.apply_ancestors(np.arange(4.0), np.arange(3))
+
+
+@pytest.mark.parametrize("kind", ["megopolis", "metropolis", "c1", "c2"])
+@pytest.mark.parametrize("rng", ["megores", "philox"])
+def test_oracle_sweep(mg, oracle, kind, rng):
+    """Shapes the golden set does not cover: non-pow2 N multiples of 32, B above the
+    per-launch offset capacity (chunked launches), f64, zeros, wide partitions."""
+    rr = np.random.default_rng(11)
+    configs = [(96 * 32, 17, "single"), (5 * 1024, 2500, "single"), (3 * 4096, 61, "double"),
+               (1 << 15, 40, "single"), (4096, 1030, "double")]
+    for n, b, prec in configs:
+        w = oracle.gen_gaussian_weights(float(rr.uniform(0, 4)), n, int(rr.integers(1 << 62)), prec)
+        if prec == "single" and n == 3 * 4096:
+            w[rr.random(n) < 0.3] = 0
+        seed = int(rr.integers(1 << 63))
+        for dev in (False, True):
+            wv = mg.WeightVector(torch.from_numpy(w).cuda() if dev else w, prec)
+            if kind == "megopolis":
+                got = mg.megopolis(wv, b, seed=seed, rng=rng)
+                ref = oracle.megopolis(w, b, seed=seed, rng=rng)
+            elif kind == "metropolis":
+                got = mg.metropolis(wv, b, seed, rng=rng)
+                ref = oracle.metropolis(w, b, seed, rng=rng)
+            else:
+                ps = 128 * int(rr.choice([1, 2, 4, 16]))
+                fn = mg.metropolis_c1 if kind == "c1" else mg.metropolis_c2
+                ofn = oracle.metropolis_c1 if kind == "c1" else oracle.metropolis_c2
+                got = fn(wv, b, mg.PartitionConfig(ps), seed=seed, rng=rng)
+                ref = ofn(w, b, ps, seed=seed, rng=rng)
+            assert np.array_equal(to_np(got), ref), (kind, rng, n, b, prec, dev)
+
+
+def test_config2_full_size(mg, golden, oracle):
+    """N=2^20, y sweep: reference shas (when the weights regenerate bit-identically on
+    this host) and the oracle on a particle sample."""
+    meta, z = golden
+    for c in meta["cases"]:
+        if not (c["tag"].startswith("config2_y") or c["tag"].startswith("config3_y")):
+            continue
+        y = float(c["tag"].split("_y")[1])
+        w = oracle.gen_gaussian_weights(y, 2**20, oracle.derive_seed(2, 20, int(1000 * y), 0), "single")
+        wd = torch.from_numpy(w).cuda()
+        got = to_np(run_case(mg, c, mg.WeightVector(wd, "single")))
+        assert np.array_equal(got[z[c["sample_pos"]]], z[c["sample_anc"]]) or sha(w) != c["w_sha"]
+        if sha(w) == c["w_sha"]:
+            assert sha(got) == c["anc_sha"], c["tag"] + c["kind"]
+        # independent of the weight bytes: the oracle on two particle ranges
+        for p0 in (0, 2**19 + 4096):
+            kw = dict(p0=p0, p1=p0 + 2048)
+            if c["kind"] == "megopolis":
+                ref = oracle.megopolis(w, c["b"], seed=c["seed"], **kw)
+            elif c["kind"] == "metropolis":
+                ref = oracle.metropolis(w, c["b"], c["seed"], **kw)
+            else:
+                fn = oracle.metropolis_c1 if c["kind"] == "c1" else oracle.metropolis_c2
+                ref = fn(w, c["b"], c["part"], seed=c["seed"], **kw)
+            assert np.array_equal(got[p0:p0 + 2048], ref[p0:p0 + 2048])
+
+
+def test_config4_megopolis_2p24(mg, golden, oracle):
+    """N=2^24, y=4, B=354: the reference's full-size hash, plus size-independent
+    properties (conservation; offspring bound adopters <= B)."""
+    meta, z = golden
+    c = [c for c in meta["cases"] if c["tag"] == "config4_y4"][0]
+    w = oracle.gen_gaussian_weights(4.0, 2**24, oracle.derive_seed(2, 24, 4000, 0), "single")
+    wv = mg.WeightVector(torch.from_numpy(w).cuda(), "single")
+    assert mg.iterations_for(wv).b == c["b"] == 354
+    anc = mg.megopolis(wv, c["b"], seed=c["seed"])
+    got = anc.cpu().numpy()
+    assert np.array_equal(got[z[c["sample_pos"]]], z[c["sample_anc"]])
+    if sha(w) == c["w_sha"]:
+        assert sha(got) == c["anc_sha"]
+    ref = oracle.megopolis(w, c["b"], seed=c["seed"], p0=2**23, p1=2**23 + 1024)
+    assert np.array_equal(got[2**23:2**23 + 1024], ref[2**23:2**23 + 1024])
+    off = mg.ancestors_to_offspring(anc, 2**24)
+    assert int(off.sum()) == 2**24
+    adopters = off - (anc == torch.arange(2**24, device=anc.device)).long()
+    assert int(adopters.max()) <= c["b"]
+
+
+def test_uniform_weights_permutation_large(mg):
+    """Megopolis with equal weights is the last offset's permutation (T/test_resample.py:154-171)."""
+    n = 1 << 22
+    w = mg.WeightVector(torch.ones(n, device="cuda", dtype=torch.float32), "single")
+    for b in (1, 7):
+        anc = mg.megopolis(w, b, seed=5)
+        last = int(mg.megopolis_offsets(n, b, 5)[-1])
+        i = torch.arange(n, device="cuda", dtype=torch.int64)
+        expect = (i - i % 32 + last - last % 32 + (i + last) % 32) % n
+        assert torch.equal(anc, expect)
+
+
+def test_resample_host_with_epsilon(mg, oracle):
+    import ctypes
+
+    from paper_2109_13504_b200 import _lib
+
+    w = oracle.gen_gaussian_weights(3.0, 1 << 18, 99, "single")
+    out = np.empty(len(w), dtype=np.int64)
+    b = ctypes.c_int32(0)
+    _lib.check(_lib.lib().mgp_resample_host(_lib.KIND["megopolis"], w.ctypes.data_as(ctypes.c_void_p), 0, len(w), 0,
+                                            0.01, 12345, 32, 0, 1, 0, out.ctypes.data_as(ctypes.c_void_p),
+                                            ctypes.byref(b), -1))
+    mean, mx = oracle.weight_mean_max(w)
+    assert b.value == oracle.compute_iterations(0.01, mean, mx)
+    assert np.array_equal(out, oracle.megopolis(w, b.value, seed=12345))
+
+
+def test_errors_match_reference(mg):
+    with pytest.raises(ValueError, match="all weights are zero"):
+        mg.metropolis(mg.WeightVector(np.zeros(4), "double"), 4, seed=0)
+    with pytest.raises(ValueError, match="all weights are zero"):
+        mg.megopolis(mg.WeightVector(torch.zeros(64, device="cuda"), "single"), 4, seed=0)
+    with pytest.raises(ValueError, match="B must be >= 1"):
+        mg.metropolis(mg.WeightVector(np.ones(4), "double"), 0, seed=0)
+    with pytest.raises(ValueError, match="multiple of the warp size"):
+        mg.megopolis(mg.WeightVector(np.ones(33), "double"), 4, seed=0)
+    anc = mg.megopolis(mg.WeightVector(np.ones(33), "double"), 4, seed=0, strict=False)
+    assert anc.min() >= 0 and anc.max() < 33
+    with pytest.raises(ValueError):
+        mg.WeightVector(torch.tensor([1.0, float("inf")], device="cuda"), "single")
+    with pytest.raises(ValueError):
+        mg.WeightVector(torch.tensor([1.0, -2.0], device="cuda"), "single")
+
+
+def test_nondefault_stream(mg, oracle):
+    w = oracle.gen_gaussian_weights(2.0, 1 << 16, 5, "single")
+    s = torch.cuda.Stream()
+    wd = torch.from_numpy(w).cuda()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        anc = mg.megopolis(mg.WeightVector(wd, "single"), 16, seed=3)
+    s.synchronize()
+    assert np.array_equal(anc.cpu().numpy(), oracle.megopolis(w, 16, seed=3))
+
+
+def test_shim_routes_reference_api(mg, golden):
+    """The shim replaces megores' resamplers when the reference package is importable
+    (in the build container); on the GPU box the reference is absent."""
+    megores = pytest.importorskip("megores")
+    from paper_2109_13504_b200 import shim
+
+    saved = shim.install(megores)
+    try:
+        w = megores.WeightVector(np.arange(1, 65, dtype=np.float32), "single")
+        fn = megores.make_resampler("megopolis")
+        assert list(fn(w, 5, 3)[:8]) == [21, 22, 23, 29, 25, 26, 27, 28]
+    finally:
+        shim.uninstall(megores, saved)
+
+
+def test_device_weight_generator(mg, oracle):
+    n = 1 << 16
+    for y in (0.0, 4.0):
+        wv = mg.gen_gaussian_weights(mg.GaussianWeightParams(y, n), 123, "double")
+        host = oracle.gen_gaussian_weights(y, n, 123, "double")
+        assert np.allclose(wv.values.cpu().numpy(), host, rtol=1e-13, atol=0)
+        w32 = mg.gen_gaussian_weights(mg.GaussianWeightParams(y, n), 123, "single")
+        assert (w32.values.cpu().numpy() != host.astype(np.float32)).mean() < 1e-3
