@@ -303,9 +303,11 @@ __global__ void k_offsets(uint64_t base, uint64_t seed, int64_t n, int64_t b, in
 // chunk, sub-tree built level by level in shared memory), then one CTA combines the
 // chunk sums in the same pairwise order.  The result is bit-identical to numpy.
 
-constexpr int PW_CHUNK = 32768;
-constexpr int PW_HEAP = 2048;
+constexpr int PW_CHUNK = 4096;   // elements per CTA (staged as float64 in shared memory)
+constexpr int PW_HEAP = 256;     // heap slots of one chunk's subtree (depth <= 7)
 constexpr int PW_THREADS = 256;
+constexpr int PW_PAD = 8;        // +8 doubles per 128: 8-lane leaf groups hit disjoint banks
+__host__ __device__ constexpr int pw_sidx(int e) { return e + (e >> 7) * PW_PAD; }
 
 __host__ __device__ inline void pw_chunk_span(int64_t n, int depth, int64_t c, int64_t& lo, int64_t& len) {
   lo = 0;
@@ -355,29 +357,6 @@ struct ElemBias {  // (mean - expected)**2, M/metrics.py:102
   }
 };
 
-template <class Elem>
-__device__ __forceinline__ double pw_leaf(const Elem& e, int64_t lo, int64_t n) {
-  if (n < 8) {
-    double res = 0.0;
-    for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, e(lo + i));
-    return res;
-  }
-  double r0 = e(lo), r1 = e(lo + 1), r2 = e(lo + 2), r3 = e(lo + 3);
-  double r4 = e(lo + 4), r5 = e(lo + 5), r6 = e(lo + 6), r7 = e(lo + 7);
-  int64_t i = 8;
-  const int64_t m = n - (n % 8);
-  for (; i < m; i += 8) {
-    r0 = __dadd_rn(r0, e(lo + i)); r1 = __dadd_rn(r1, e(lo + i + 1));
-    r2 = __dadd_rn(r2, e(lo + i + 2)); r3 = __dadd_rn(r3, e(lo + i + 3));
-    r4 = __dadd_rn(r4, e(lo + i + 4)); r5 = __dadd_rn(r5, e(lo + i + 5));
-    r6 = __dadd_rn(r6, e(lo + i + 6)); r7 = __dadd_rn(r7, e(lo + i + 7));
-  }
-  double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
-                         __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
-  for (; i < n; ++i) res = __dadd_rn(res, e(lo + i));
-  return res;
-}
-
 template <typename WT>
 __device__ __forceinline__ void wstat_observe(WStats& s, WT v) {
   if constexpr (sizeof(WT) == 4) {
@@ -405,47 +384,81 @@ __device__ __forceinline__ void wstat_observe(WStats& s, WT v) {
   if (d > s.max) s.max = d;
 }
 
-// heap: [2^D, 2^(D+1)) receives the chunk sums; stats (optional) one per chunk.
+// One CTA per chunk.  The chunk's elements are staged (coalesced) into shared memory as
+// float64; its subtree is built level by level; each leaf (<= 128 elements) is summed by
+// 8 lanes, lane j owning numpy's accumulator r[j] (elements j, j+8, j+16, ...), then
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) by xor-shuffles (IEEE addition commutes exactly),
+// then the n % 8 tail sequentially -- numpy's leaf order.  Internal nodes are combined
+// bottom-up.  heap[2^D + c] receives the chunk sum.
 template <class Elem, typename WT, bool STATS>
 __global__ void __launch_bounds__(PW_THREADS) k_pw_chunks(Elem e, const WT* wraw, int64_t n, int depth,
                                                           double* heap, WStats* cstats) {
+  __shared__ double s_el[pw_sidx(PW_CHUNK)];
   __shared__ int32_t s_lo[PW_HEAP];
   __shared__ int32_t s_len[PW_HEAP];
   __shared__ double s_val[PW_HEAP];
+  __shared__ int32_t s_leaf[PW_HEAP];
+  __shared__ int32_t s_nleaf;
   __shared__ WStats s_red[PW_THREADS / 32];
   int64_t lo0, len0;
   pw_chunk_span(n, depth, blockIdx.x, lo0, len0);
+  const int len = (int)len0;
   for (int h = threadIdx.x; h < PW_HEAP; h += PW_THREADS) s_len[h] = 0;
+  if (threadIdx.x == 0) s_nleaf = 0;
+  // stage (coalesced; each element read exactly once)
+  WStats st{-1.0, 0, 0, 0, 0, 0};
+#pragma unroll 4
+  for (int q = threadIdx.x; q < len; q += PW_THREADS) {
+    s_el[pw_sidx(q)] = e(lo0 + q);
+    if constexpr (STATS) wstat_observe<WT>(st, wraw[lo0 + q]);
+  }
   __syncthreads();
-  if (threadIdx.x == 0) { s_lo[1] = 0; s_len[1] = (int32_t)len0; }
+  if (threadIdx.x == 0) { s_lo[1] = 0; s_len[1] = len; }
   __syncthreads();
-  for (int lvl = 0; lvl < 10; ++lvl) {  // build the subtree top-down
-    const int h0 = 1 << lvl, h1 = min(2 << lvl, PW_HEAP / 2);
+  for (int lvl = 0; lvl < 8; ++lvl) {  // build the subtree top-down
+    const int h0 = 1 << lvl, h1 = min(2 << lvl, PW_HEAP);
     for (int h = h0 + threadIdx.x; h < h1; h += PW_THREADS) {
-      const int32_t len = s_len[h];
-      if (len > 128) {
-        int32_t n2 = len / 2;
+      const int32_t ln = s_len[h];
+      if (ln > 128 && 2 * h + 1 < PW_HEAP) {
+        int32_t n2 = ln / 2;
         n2 -= n2 % 8;
         s_lo[2 * h] = s_lo[h];
         s_len[2 * h] = n2;
         s_lo[2 * h + 1] = s_lo[h] + n2;
-        s_len[2 * h + 1] = len - n2;
+        s_len[2 * h + 1] = ln - n2;
+      } else if (ln > 0) {
+        s_leaf[atomicAdd(&s_nleaf, 1)] = h;
       }
     }
     __syncthreads();
   }
-  WStats st{-1.0, 0, 0, 0, 0, 0};
-  for (int h = 1 + threadIdx.x; h < PW_HEAP; h += PW_THREADS) {  // leaves
-    const int32_t len = s_len[h];
-    if (len > 0 && len <= 128) {
-      const int64_t lo = lo0 + s_lo[h];
-      s_val[h] = pw_leaf(e, lo, len);
-      if constexpr (STATS)
-        for (int32_t q = 0; q < len; ++q) wstat_observe<WT>(st, wraw[lo + q]);
+  const int nleaf = s_nleaf;
+  const int grp = threadIdx.x >> 3, jl = threadIdx.x & 7;
+  for (int q0 = 0; q0 < nleaf; q0 += PW_THREADS / 8) {  // warp-uniform trip count
+    const int q = q0 + grp;
+    const bool live = q < nleaf;
+    const int h = live ? s_leaf[q] : 0;
+    const int lo = live ? s_lo[h] : 0, ln = live ? s_len[h] : 0;
+    double r = 0.0;
+    if (ln >= 8) {
+      r = s_el[pw_sidx(lo + jl)];
+      const int m = ln - (ln % 8);
+      for (int i = 8; i < m; i += 8) r = __dadd_rn(r, s_el[pw_sidx(lo + i + jl)]);
+    }
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+    if (live && jl == 0) {
+      double res;
+      int i;
+      if (ln < 8) { res = 0.0; i = 0; }
+      else { res = r; i = ln - (ln % 8); }
+      for (; i < ln; ++i) res = __dadd_rn(res, s_el[pw_sidx(lo + i)]);
+      s_val[h] = res;
     }
   }
   __syncthreads();
-  for (int lvl = 9; lvl >= 0; --lvl) {  // combine bottom-up in the same order as numpy
+  for (int lvl = 7; lvl >= 0; --lvl) {  // combine bottom-up in the same order as numpy
     const int h0 = 1 << lvl, h1 = min(2 << lvl, PW_HEAP / 2);
     for (int h = h0 + threadIdx.x; h < h1; h += PW_THREADS)
       if (s_len[h] > 128) s_val[h] = __dadd_rn(s_val[2 * h], s_val[2 * h + 1]);
@@ -453,7 +466,6 @@ __global__ void __launch_bounds__(PW_THREADS) k_pw_chunks(Elem e, const WT* wraw
   }
   if (threadIdx.x == 0) heap[(1ll << depth) + blockIdx.x] = len0 > 0 ? s_val[1] : 0.0;
   if constexpr (STATS) {
-    // warp then block reduction of the stats (integer counts + max: order-free)
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       st.max = fmax(st.max, __shfl_xor_sync(0xffffffffu, st.max, off));
