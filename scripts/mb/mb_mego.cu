@@ -197,6 +197,40 @@ __global__ void __launch_bounds__(256) k_vx(const ResampleArgs a, const __grid_c
   a.anc[i] = (int64_t)k;
 }
 
+
+// Combined candidates: exponent-hack u (exact), texture or F2F partner, mux, 32-bit state.
+template <int WMODE, bool STATE32, int UNROLL, bool XMUL>
+__global__ void __launch_bounds__(256) k_vy(const ResampleArgs a, const __grid_constant__ OffChunk oc,
+                                            cudaTextureObject_t tex) {
+  const uint32_t i = a.p0 + blockIdx.x * 256 + threadIdx.x;
+  if (i >= a.p_end) return;
+  const uint32_t* __restrict__ w = reinterpret_cast<const uint32_t*>(a.w);
+  const uint32_t lane = threadIdx.x & 31u, i_al = i - lane;
+  const uint32_t cmask = (a.n - 1) & ~31u;
+  uint32_t wkb = __ldg(w + i);
+  double wk = (double)__uint_as_float(wkb);
+  int bstar = -1;
+  const uint64_t x0 = megores_key(a.base, i, (uint64_t)a.b0);
+  uint64_t x = x0;
+#pragma unroll UNROLL
+  for (int t = 0; t < a.cnt; ++t) {
+    const uint32_t o = oc.o[t];
+    const uint32_t j = mux3(i_al + (o & ~31u), lane + (o & 31u), cmask);
+    double wj;
+    uint32_t wjb;
+    if (WMODE == 1) { wjb = __ldg(w + j); wj = (double)__uint_as_float(wjb); }
+    else { float f = tex1Dfetch<float>(tex, (int)j); wjb = __float_as_uint(f); wj = (double)f; }
+    const uint64_t xx = XMUL ? x0 + (uint64_t)(uint32_t)t * M_CTR : x;
+    const double u = u_ref(xx);
+    x += M_CTR;
+    const double wkd = STATE32 ? (double)__uint_as_float(wkb) : wk;
+    if (u * wkd <= wj) { if (STATE32) wkb = wjb; else wk = wj; bstar = t; }
+  }
+  uint32_t k = i;
+  if (bstar >= 0) k = mego_j<true>(i_al, lane, oc.o[bstar], a.n);
+  a.anc[i] = (int64_t)k;
+}
+
 // ---------------------------------------------------------------------------
 
 template <class K>
@@ -272,6 +306,16 @@ int main(int argc, char** argv) {
   check("u1w1s", time_it([&]() { k_vx<1, 1, true><<<grid, 256>>>(b, oc, tex); }, 7));
   check("u0w2", time_it([&]() { k_vx<0, 2, false><<<grid, 256>>>(b, oc, tex); }, 7));
   check("u1w2", time_it([&]() { k_vx<1, 2, false><<<grid, 256>>>(b, oc, tex); }, 7));
+  check("y1s4", time_it([&]() { k_vy<1, true, 4, false><<<grid, 256>>>(b, oc, tex); }, 7));
+  check("y2s4", time_it([&]() { k_vy<2, true, 4, false><<<grid, 256>>>(b, oc, tex); }, 7));
+  check("y2d4", time_it([&]() { k_vy<2, false, 4, false><<<grid, 256>>>(b, oc, tex); }, 7));
+  check("y2s8", time_it([&]() { k_vy<2, true, 8, false><<<grid, 256>>>(b, oc, tex); }, 7));
+  check("y2s2", time_it([&]() { k_vy<2, true, 2, false><<<grid, 256>>>(b, oc, tex); }, 7));
+  check("y2s4m", time_it([&]() { k_vy<2, true, 4, true><<<grid, 256>>>(b, oc, tex); }, 7));
+  {
+    float tp = time_it([&]() { k_megopolis_w32<1, float, true, true><<<grid, 256>>>(b, oc); }, 7);
+    printf("philox(lib) %.3f ms  %.3f Gcmp/s  vs megores ref %.3f\n", tp, cmp / tp / 1e6, t0 / tp);
+  }
   check("u1w2s", time_it([&]() { k_vx<1, 2, true><<<grid, 256>>>(b, oc, tex); }, 7));
   return 0;
 }
