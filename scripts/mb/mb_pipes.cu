@@ -15,6 +15,8 @@ template <int K>
 __global__ void __launch_bounds__(256) kop(uint64_t* out, uint32_t s1, uint32_t s2, long long* cyc) {
   __syncthreads();
   long long c0 = clock64();
+  unsigned long long g0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
   uint32_t a0 = threadIdx.x, a1 = a0 * 3, a2 = a0 * 5, a3 = a0 * 7, a4 = a0 ^ 9, a5 = a0 + 11, a6 = a0 * 13, a7 = a0 + 17;
   uint32_t b0 = a0 + 1, b1 = a1 + 2, b2 = a2 + 3, b3 = a3 + 4, b4 = a4 + 5, b5 = a5 + 6, b6 = a6 + 7, b7 = a7 + 8;
   uint64_t dd = a0; double d0 = a0, d1 = a1, d2 = a2, d3 = a3, d4 = a4, d5 = a5, d6 = a6, d7 = a7;
@@ -91,25 +93,35 @@ __global__ void __launch_bounds__(256) kop(uint64_t* out, uint32_t s1, uint32_t 
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) cyc[blockIdx.x] = clock64() - c0;
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    unsigned long long g1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+    cyc[0] = clock64() - c0;
+    cyc[1] = (long long)(g1 - g0);
+  }
   out[blockIdx.x * 256 + threadIdx.x] = (uint64_t)(a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7) +
                                         dd + (uint64_t)(d0 + d1 + d2 + d3 + d4 + d5 + d6 + d7);
 }
 
 template <int K>
-void run(const char* name, uint64_t* out, long long* cyc, int sms) {
-  const int blocks = sms * 8;  // 64 warps per SM (one wave)
+void run(const char* name, uint64_t* out, long long* cyc, int sms, int nop) {
+  const int blocks = sms * 8 * 4;  // several waves
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
   kop<K><<<blocks, 256>>>(out, 3, 5, cyc);
   CK(cudaDeviceSynchronize());
+  CK(cudaEventRecord(e0));
   kop<K><<<blocks, 256>>>(out, 3, 5, cyc);
-  CK(cudaDeviceSynchronize());
-  long long* h = (long long*)malloc(sizeof(long long) * blocks);
-  CK(cudaMemcpy(h, cyc, sizeof(long long) * blocks, cudaMemcpyDeviceToHost));
-  double mean = 0;
-  for (int b = 0; b < blocks; ++b) mean += (double)h[b] / blocks;
-  free(h);
-  const double iters_per_smsp = 16.0 * ITERS;  // 16 warps per SMSP
-  printf("%-14s %.2f cycles / loop iteration / SMSP\n", name, mean / iters_per_smsp);
+  CK(cudaEventRecord(e1));
+  CK(cudaEventSynchronize(e1));
+  float ms;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  long long h[2];
+  CK(cudaMemcpy(h, cyc, sizeof h, cudaMemcpyDeviceToHost));
+  const double ghz = (double)h[0] / (double)h[1];
+  const double warp_instr = (double)blocks * 8 * ITERS * nop;  // op instructions
+  const double smsp_cycles = ms * 1e-3 * ghz * 1e9 * sms * 4;
+  printf("%-14s %7.3f ms  clk %.3f GHz  %.2f cycles per warp-op per SMSP\n", name, ms, ghz, smsp_cycles / warp_instr);
 }
 
 int main() {
@@ -120,20 +132,20 @@ int main() {
   long long* cyc;
   CK(cudaMalloc(&out, sizeof(uint64_t) * sms * 8 * 256));
   CK(cudaMalloc(&cyc, sizeof(long long) * sms * 8));
-  run<0>("LOP3 xor", out, cyc, sms);
-  run<11>("LOP3 3-in", out, cyc, sms);
-  run<1>("SHF.R.U32", out, cyc, sms);
-  run<2>("SHF funnel", out, cyc, sms);
-  run<6>("IADD reg", out, cyc, sms);
-  run<12>("IADD imm", out, cyc, sms);
-  run<10>("SEL", out, cyc, sms);
-  run<3>("IMAD", out, cyc, sms);
-  run<4>("IMAD.WIDE+x", out, cyc, sms);
-  run<5>("IMAD.HI", out, cyc, sms);
-  run<13>("LOP3|IMAD mix", out, cyc, sms);
-  run<14>("FFMA", out, cyc, sms);
-  run<7>("DMUL", out, cyc, sms);
-  run<8>("I2F.F64.U64+", out, cyc, sms);
-  run<9>("F2F.F64.F32+", out, cyc, sms);
+  run<0>("LOP3 xor", out, cyc, sms, 18);
+  run<11>("LOP3 3-in", out, cyc, sms, 32);
+  run<1>("SHF.R.U32", out, cyc, sms, 32);
+  run<2>("SHF funnel", out, cyc, sms, 32);
+  run<6>("IADD reg", out, cyc, sms, 32);
+  run<12>("IADD imm", out, cyc, sms, 4);
+  run<10>("SEL", out, cyc, sms, 32);
+  run<3>("IMAD", out, cyc, sms, 32);
+  run<4>("IMAD.WIDE+x", out, cyc, sms, 32);
+  run<5>("IMAD.HI", out, cyc, sms, 32);
+  run<13>("LOP3|IMAD mix", out, cyc, sms, 32);
+  run<14>("FFMA", out, cyc, sms, 32);
+  run<7>("DMUL", out, cyc, sms, 32);
+  run<8>("I2F.F64.U64+", out, cyc, sms, 32);
+  run<9>("F2F.F64.F32+", out, cyc, sms, 32);
   return 0;
 }
