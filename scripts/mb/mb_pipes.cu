@@ -130,7 +130,7 @@ int main() {
   const int sms = p.multiProcessorCount;
   uint64_t* out;
   long long* cyc;
-  CK(cudaMalloc(&out, sizeof(uint64_t) * sms * 8 * 256));
+  CK(cudaMalloc(&out, sizeof(uint64_t) * sms * 32 * 256));
   CK(cudaMalloc(&cyc, sizeof(long long) * sms * 8));
   run<0>("LOP3 xor", out, cyc, sms, 18);
   run<11>("LOP3 3-in", out, cyc, sms, 32);
