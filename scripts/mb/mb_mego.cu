@@ -231,6 +231,72 @@ __global__ void __launch_bounds__(256) k_vy(const ResampleArgs a, const __grid_c
   a.anc[i] = (int64_t)k;
 }
 
+
+// ---- optimized candidates ------------------------------------------------------
+// megores: texture partner fetch, F2F conversions, 32-bit state select, lop3 mux,
+// u = (double)m * 2^-53 on the FP64 pipe (exact for every m, incl. m == 0).
+template <bool XMUL>
+__global__ void __launch_bounds__(256) k_vz(const ResampleArgs a, const __grid_constant__ OffChunk oc,
+                                            cudaTextureObject_t tex) {
+  const uint32_t i = a.p0 + blockIdx.x * 256 + threadIdx.x;
+  if (i >= a.p_end) return;
+  const uint32_t lane = threadIdx.x & 31u, i_al = i - lane;
+  const uint32_t cmask = (a.n - 1) & ~31u;
+  float wkf = tex1Dfetch<float>(tex, (int)i);
+  int bstar = -1;
+  const uint64_t x0 = megores_key(a.base, i, (uint64_t)a.b0);
+  uint64_t x = x0;
+#pragma unroll 4
+  for (int t = 0; t < a.cnt; ++t) {
+    const uint32_t o = oc.o[t];
+    const uint32_t j = mux3(i_al + (o & ~31u), lane + (o & 31u), cmask);
+    const float wjf = tex1Dfetch<float>(tex, (int)j);
+    const uint64_t xx = XMUL ? x0 + (uint64_t)(uint32_t)t * M_CTR : x;
+    x += M_CTR;
+    const double u = (double)mix64_m53(xx) * 0x1p-53;
+    if (u * (double)wkf <= (double)wjf) { wkf = wjf; bstar = t; }
+  }
+  uint32_t k = i;
+  if (bstar >= 0) k = mego_j<true>(i_al, lane, oc.o[bstar], a.n);
+  a.anc[i] = (int64_t)k;
+}
+
+// philox: round keys in the param space (uniform), 4 draws per block.
+struct PhiloxKeys { uint32_t k0[10], k1[10]; };
+__global__ void __launch_bounds__(256) k_vp(const ResampleArgs a, const __grid_constant__ OffChunk oc,
+                                            cudaTextureObject_t tex, const __grid_constant__ PhiloxKeys pk) {
+  const uint32_t i = a.p0 + blockIdx.x * 256 + threadIdx.x;
+  if (i >= a.p_end) return;
+  const uint32_t lane = threadIdx.x & 31u, i_al = i - lane;
+  const uint32_t cmask = (a.n - 1) & ~31u;
+  float wkf = tex1Dfetch<float>(tex, (int)i);
+  int bstar = -1;
+  for (int t0 = 0; t0 < a.cnt; t0 += 4) {
+    uint32_t c0 = i, c1 = 0, c2 = (uint32_t)((a.b0 + t0) >> 2), c3 = 0;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+      const uint64_t p0 = (uint64_t)PHILOX_M0 * c0, p1 = (uint64_t)PHILOX_M1 * c2;
+      const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ pk.k0[r], n2 = (uint32_t)(p0 >> 32) ^ c3 ^ pk.k1[r];
+      c1 = (uint32_t)p1; c3 = (uint32_t)p0; c0 = n0; c2 = n2;
+    }
+    const uint32_t wd[4] = {c0, c1, c2, c3};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int t = t0 + q;
+      if (t < a.cnt) {
+        const uint32_t o = oc.o[t];
+        const uint32_t j = mux3(i_al + (o & ~31u), lane + (o & 31u), cmask);
+        const float wjf = tex1Dfetch<float>(tex, (int)j);
+        const double u = (double)wd[q] * 0x1p-32;
+        if (u * (double)wkf <= (double)wjf) { wkf = wjf; bstar = t; }
+      }
+    }
+  }
+  uint32_t k = i;
+  if (bstar >= 0) k = mego_j<true>(i_al, lane, oc.o[bstar], a.n);
+  a.anc[i] = (int64_t)k;
+}
+
 // ---------------------------------------------------------------------------
 
 template <class K>
@@ -312,6 +378,25 @@ int main(int argc, char** argv) {
   check("y2s8", time_it([&]() { k_vy<2, true, 8, false><<<grid, 256>>>(b, oc, tex); }, 7));
   check("y2s2", time_it([&]() { k_vy<2, true, 2, false><<<grid, 256>>>(b, oc, tex); }, 7));
   check("y2s4m", time_it([&]() { k_vy<2, true, 4, true><<<grid, 256>>>(b, oc, tex); }, 7));
+  check("vz", time_it([&]() { k_vz<false><<<grid, 256>>>(b, oc, tex); }, 7));
+  check("vzm", time_it([&]() { k_vz<true><<<grid, 256>>>(b, oc, tex); }, 7));
+  {
+    // philox reference (library kernel) vs optimized philox
+    static OffChunk ocp;
+    for (int t = 0; t < B; ++t) ocp.o[t] = (uint32_t)below_from_word(p4_word(philox_block(seed, GLOBAL_OFFSET_LANE, t >> 2), t & 3), n);
+    ResampleArgs c = a; c.anc = anc0;
+    float tpl = time_it([&]() { k_megopolis_w32<1, float, true, true><<<grid, 256>>>(c, ocp); }, 7);
+    CK(cudaMemcpy(h0.data(), anc0, 8ull * n, cudaMemcpyDeviceToHost));
+    PhiloxKeys pk;
+    uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+    for (int r = 0; r < 10; ++r) { pk.k0[r] = k0; pk.k1[r] = k1; k0 += PHILOX_W0; k1 += PHILOX_W1; }
+    printf("philox lib %.3f ms\n", tpl);
+    float tvp = time_it([&]() { k_vp<<<grid, 256>>>(b, ocp, tex, pk); }, 7);
+    CK(cudaMemcpy(h1.data(), anc1, 8ull * n, cudaMemcpyDeviceToHost));
+    size_t bad = 0;
+    for (uint32_t q = 0; q < n; ++q) bad += h0[q] != h1[q];
+    printf("vp (philox opt) %.3f ms  %.3f Gcmp/s  vs megores ref %.3f  mismatches %zu\n", tvp, cmp / tvp / 1e6, t0 / tvp, bad);
+  }
   {
     float tp = time_it([&]() { k_megopolis_w32<1, float, true, true><<<grid, 256>>>(b, oc); }, 7);
     printf("philox(lib) %.3f ms  %.3f Gcmp/s  vs megores ref %.3f\n", tp, cmp / tp / 1e6, t0 / tp);
