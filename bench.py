@@ -248,7 +248,7 @@ def main():
         host = stats.cpu().numpy()  # 64 B; the reference also derives B on the host
         mean, mx = float(host[1]), float(host[2])
         b = mg.compute_iterations(EPS, mean, mx).b
-        flags = _lib.FLAG_POSITIVE_NORMAL if host.view(np.int64)[7] == 0 else 0
+        flags = _lib.FLAG_NONZERO if host.view(np.int64)[4] == 0 else 0
         if ev is not None:
             ev[0].record(stream)
         _lib.check(L.mgp_resample_range(_lib.KIND["megopolis"], D.ptr(full), 0, n_glob, b, RUN_SEED, 32, 0, 1,

@@ -44,9 +44,11 @@ enum { MGP_RNG_MEGORES = 0, MGP_RNG_PHILOX = 1 };
 enum { MGP_KIND_METROPOLIS = 0, MGP_KIND_C1 = 1, MGP_KIND_C2 = 2, MGP_KIND_MEGOPOLIS = 3 };
 enum { MGP_OK = 0, MGP_EINVAL = -1, MGP_EUNSUPPORTED = -2 };
 
-/* flags: MGP_FLAG_POSITIVE_NORMAL asserts that every weight is a positive normal
- * float32 (mgp_weight_stats: n_notnormal == 0), enabling the exact fast compare. */
-enum { MGP_FLAG_POSITIVE_NORMAL = 1 };
+/* flags: MGP_FLAG_NONZERO asserts that no weight is zero (mgp_weight_stats:
+ * n_zero == 0), so the both-zero rejection of the acceptance rule
+ * (M/resample.py:118-122) can never fire and is compiled out.  Results are
+ * identical with or without the flag when it holds. */
+enum { MGP_FLAG_NONZERO = 1 };
 
 /* Weight statistics (device-resident result).  sum/mean are bit-identical to
  * numpy's np.asarray(w, float64).sum()/.mean() (pairwise summation), which feeds

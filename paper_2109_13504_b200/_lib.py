@@ -18,7 +18,7 @@ MGP_F32, MGP_F64 = 0, 1
 RNG = {"megores": 0, "philox": 1}
 KIND = {"metropolis": 0, "c1": 1, "c2": 2, "megopolis": 3}
 MGP_EINVAL, MGP_EUNSUPPORTED = -1, -2
-FLAG_POSITIVE_NORMAL = 1
+FLAG_NONZERO = 1
 
 _lib = None
 _lock = threading.Lock()

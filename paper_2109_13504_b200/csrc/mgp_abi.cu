@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include <curand_philox4x32_x.h>
@@ -137,45 +138,53 @@ void offsets_host(uint64_t seed, int64_t n, int32_t b, int rng, int64_t* out) {
 // ---------------------------------------------------------------------------
 // kernel dispatch helpers
 
-template <int RNG, typename WT, bool POW2, bool FAST>
+template <int RNG, typename WT, bool POW2, bool NZ, bool TEX>
 int launch_mego_w32(const ResampleArgs& a, const OffChunk& oc, cudaStream_t st) {
   const unsigned grid = (unsigned)((a.p_end - a.p0 + RS_THREADS - 1) / RS_THREADS);
-  k_megopolis_w32<RNG, WT, POW2, FAST><<<grid, RS_THREADS, 0, st>>>(a, oc);
+  k_megopolis_w32<RNG, WT, POW2, NZ, TEX><<<grid, RS_THREADS, 0, st>>>(a, oc);
   LAUNCH_CHECK("k_megopolis_w32");
   return 0;
 }
 
 template <int RNG, typename WT>
-int dispatch_mego_w32(const ResampleArgs& a, const OffChunk& oc, bool pow2, bool fast, cudaStream_t st) {
-  if constexpr (sizeof(WT) == 4) {
-    if (fast) return pow2 ? launch_mego_w32<RNG, WT, true, true>(a, oc, st) : launch_mego_w32<RNG, WT, false, true>(a, oc, st);
+int dispatch_mego_w32(const ResampleArgs& a, const OffChunk& oc, bool pow2, bool nz, cudaStream_t st) {
+#define MEGO_CASE(P, Z, T)                                                    \
+  if (pow2 == P && nz == Z && (a.tex != 0) == T) {                            \
+    if constexpr (!T || sizeof(WT) == 4) return launch_mego_w32<RNG, WT, P, Z, T>(a, oc, st); \
   }
-  return pow2 ? launch_mego_w32<RNG, WT, true, false>(a, oc, st) : launch_mego_w32<RNG, WT, false, false>(a, oc, st);
+  MEGO_CASE(true, true, true)
+  MEGO_CASE(true, false, true)
+  MEGO_CASE(false, true, true)
+  MEGO_CASE(false, false, true)
+  MEGO_CASE(true, true, false)
+  MEGO_CASE(true, false, false)
+  MEGO_CASE(false, true, false)
+  MEGO_CASE(false, false, false)
+#undef MEGO_CASE
+  return set_err(MGP_EINVAL, "internal: no megopolis variant");
 }
 
-template <int RNG, typename WT, bool POW2, bool FAST>
+template <int RNG, typename WT, bool POW2, bool NZ>
 int launch_metro(const ResampleArgs& a, cudaStream_t st) {
   const unsigned grid = (unsigned)((a.p_end - a.p0 + RS_THREADS - 1) / RS_THREADS);
-  k_metropolis<RNG, WT, POW2, FAST><<<grid, RS_THREADS, 0, st>>>(a);
+  k_metropolis<RNG, WT, POW2, NZ><<<grid, RS_THREADS, 0, st>>>(a);
   LAUNCH_CHECK("k_metropolis");
   return 0;
 }
 
 template <int RNG, typename WT>
-int dispatch_metro(const ResampleArgs& a, bool pow2, bool fast, cudaStream_t st) {
-  if constexpr (sizeof(WT) == 4) {
-    if (fast) return pow2 ? launch_metro<RNG, WT, true, true>(a, st) : launch_metro<RNG, WT, false, true>(a, st);
-  }
+int dispatch_metro(const ResampleArgs& a, bool pow2, bool nz, cudaStream_t st) {
+  if (nz) return pow2 ? launch_metro<RNG, WT, true, true>(a, st) : launch_metro<RNG, WT, false, true>(a, st);
   return pow2 ? launch_metro<RNG, WT, true, false>(a, st) : launch_metro<RNG, WT, false, false>(a, st);
 }
 
 constexpr int C1_SMEM_MAX = 96 * 1024;
 
-template <int RNG, typename WT, bool POW2, bool FAST, bool C2, bool STAGE>
+template <int RNG, typename WT, bool POW2, bool NZ, bool C2, bool STAGE>
 int launch_c12(const ResampleArgs& a, cudaStream_t st) {
   const unsigned grid = (unsigned)((a.p_end - a.p0 + RS_THREADS - 1) / RS_THREADS);
   size_t smem = STAGE ? (size_t)(RS_THREADS / 32) * a.n_w * sizeof(WT) : 0;
-  auto kern = k_c12_w32<RNG, WT, POW2, FAST, C2, STAGE>;
+  auto kern = k_c12_w32<RNG, WT, POW2, NZ, C2, STAGE>;
   if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<grid, RS_THREADS, smem, st>>>(a);
   LAUNCH_CHECK("k_c12_w32");
@@ -183,21 +192,61 @@ int launch_c12(const ResampleArgs& a, cudaStream_t st) {
 }
 
 template <int RNG, typename WT, bool C2>
-int dispatch_c12(const ResampleArgs& a, bool pow2, bool fast, cudaStream_t st) {
+int dispatch_c12(const ResampleArgs& a, bool pow2, bool nz, cudaStream_t st) {
   const bool stage = !C2 && (size_t)(RS_THREADS / 32) * a.n_w * sizeof(WT) <= (size_t)C1_SMEM_MAX;
-#define C12_CASE(P, F)                                                        \
-  if (pow2 == P && fast == F) {                                               \
-    if constexpr (!F || sizeof(WT) == 4) {                                    \
-      if (stage) return launch_c12<RNG, WT, P, F, C2, !C2>(a, st);            \
-      return launch_c12<RNG, WT, P, F, C2, false>(a, st);                     \
-    }                                                                         \
+#define C12_CASE(P, Z)                                                        \
+  if (pow2 == P && nz == Z) {                                                 \
+    if (stage) return launch_c12<RNG, WT, P, Z, C2, !C2>(a, st);              \
+    return launch_c12<RNG, WT, P, Z, C2, false>(a, st);                       \
   }
   C12_CASE(true, true)
   C12_CASE(false, true)
   C12_CASE(true, false)
   C12_CASE(false, false)
 #undef C12_CASE
-  return launch_c12<RNG, WT, false, false, C2, false>(a, st);
+  return set_err(MGP_EINVAL, "internal: no c1/c2 variant");
+}
+
+// ---------------------------------------------------------------------------
+// float32 weights as a 1-D linear texture: the texture unit does the partner-address
+// arithmetic.  Objects are cached per (device, pointer, length) and never destroyed
+// while the process lives (a kernel may still be reading through them).
+
+struct TexEntry {
+  int dev;
+  const void* ptr;
+  int64_t n;
+  cudaTextureObject_t tex;
+};
+std::mutex g_tex_mu;
+std::vector<TexEntry> g_tex;
+constexpr size_t TEX_CACHE_MAX = 1024;
+
+cudaTextureObject_t weights_texture(const float* w, int64_t n) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  std::lock_guard<std::mutex> lk(g_tex_mu);
+  for (const auto& e : g_tex)
+    if (e.dev == dev && e.ptr == (const void*)w && e.n == n) return e.tex;
+  if (g_tex.size() >= TEX_CACHE_MAX) return 0;
+  int maxw = 0, align = 0;
+  cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxTexture1DLinearWidth, dev);
+  cudaDeviceGetAttribute(&align, cudaDevAttrTextureAlignment, dev);
+  if (n > (int64_t)maxw || (align > 0 && ((uintptr_t)w % (uintptr_t)align) != 0)) return 0;
+  cudaResourceDesc rd{};
+  rd.resType = cudaResourceTypeLinear;
+  rd.res.linear.devPtr = const_cast<float*>(w);
+  rd.res.linear.desc = cudaCreateChannelDesc<float>();
+  rd.res.linear.sizeInBytes = sizeof(float) * (size_t)n;
+  cudaTextureDesc td{};
+  td.readMode = cudaReadModeElementType;
+  cudaTextureObject_t tex = 0;
+  if (cudaCreateTextureObject(&tex, &rd, &td, nullptr) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  g_tex.push_back({dev, (const void*)w, n, tex});
+  return tex;
 }
 
 template <int RNG, typename WT>
@@ -213,7 +262,7 @@ int launch_generic(int kind, GenericArgs ga, cudaStream_t st) {
 // One resampler call over particles [p0, p_end).  Arguments already validated.
 struct Plan {
   int kind, dtype, rng;
-  bool fast;
+  bool nz;  // no zero weights (caller asserted MGP_FLAG_NONZERO)
   const void* w;
   int64_t n, n_w, n_part;
   int32_t b, warp;
@@ -250,6 +299,11 @@ int run_range(Plan& p, int64_t p0, int64_t p_end, int64_t* anc, cudaStream_t st)
   a.base = megores_base(p.seed);
   a.kstate = p.kstate;
   a.anc = anc;
+  {
+    uint32_t k0 = (uint32_t)p.seed, k1 = (uint32_t)(p.seed >> 32);
+    for (int r = 0; r < 10; ++r) { a.pk0[r] = k0; a.pk1[r] = k1; k0 += PHILOX_W0; k1 += PHILOX_W1; }
+  }
+  if (p.kind == MGP_KIND_MEGOPOLIS && p.dtype == MGP_F32) a.tex = weights_texture((const float*)p.w, p.n);
   const int cap = (p.kind == MGP_KIND_MEGOPOLIS) ? OFF_CAP : p.b;  // only Megopolis carries params
   for (int b0 = 0; b0 < p.b; b0 += cap) {
     a.b0 = b0;
@@ -260,27 +314,27 @@ int run_range(Plan& p, int64_t p0, int64_t p_end, int64_t* anc, cudaStream_t st)
     if (p.kind == MGP_KIND_MEGOPOLIS) {
       static thread_local OffChunk oc;
       for (int t = 0; t < a.cnt; ++t) oc.o[t] = (uint32_t)p.off[b0 + t];
-      const bool pow2 = is_pow2(p.n);
+      const bool pow2 = is_pow2(p.n) && p.n >= 64;
       if (p.rng == MGP_RNG_MEGORES)
-        rc = p.dtype == MGP_F32 ? dispatch_mego_w32<RNG_MEGORES, float>(a, oc, pow2, p.fast, st)
-                                : dispatch_mego_w32<RNG_MEGORES, double>(a, oc, pow2, p.fast, st);
+        rc = p.dtype == MGP_F32 ? dispatch_mego_w32<RNG_MEGORES, float>(a, oc, pow2, p.nz, st)
+                                : dispatch_mego_w32<RNG_MEGORES, double>(a, oc, pow2, p.nz, st);
       else
-        rc = p.dtype == MGP_F32 ? dispatch_mego_w32<RNG_PHILOX, float>(a, oc, pow2, p.fast, st)
-                                : dispatch_mego_w32<RNG_PHILOX, double>(a, oc, pow2, p.fast, st);
+        rc = p.dtype == MGP_F32 ? dispatch_mego_w32<RNG_PHILOX, float>(a, oc, pow2, p.nz, st)
+                                : dispatch_mego_w32<RNG_PHILOX, double>(a, oc, pow2, p.nz, st);
     } else if (p.kind == MGP_KIND_METROPOLIS) {
       const bool pow2 = is_pow2(p.n) && p.n >= 2;
       a.log2 = ilog2((uint64_t)p.n);
       if (p.rng == MGP_RNG_MEGORES)
-        rc = p.dtype == MGP_F32 ? dispatch_metro<RNG_MEGORES, float>(a, pow2, p.fast, st)
-                                : dispatch_metro<RNG_MEGORES, double>(a, pow2, p.fast, st);
+        rc = p.dtype == MGP_F32 ? dispatch_metro<RNG_MEGORES, float>(a, pow2, p.nz, st)
+                                : dispatch_metro<RNG_MEGORES, double>(a, pow2, p.nz, st);
       else
-        rc = p.dtype == MGP_F32 ? dispatch_metro<RNG_PHILOX, float>(a, pow2, p.fast, st)
-                                : dispatch_metro<RNG_PHILOX, double>(a, pow2, p.fast, st);
+        rc = p.dtype == MGP_F32 ? dispatch_metro<RNG_PHILOX, float>(a, pow2, p.nz, st)
+                                : dispatch_metro<RNG_PHILOX, double>(a, pow2, p.nz, st);
     } else {
       const bool pow2 = is_pow2(p.n_w) && p.n_w >= 2;
       a.log2 = ilog2((uint64_t)p.n_w);
       const bool c2 = p.kind == MGP_KIND_C2;
-#define C12_GO(R, T) (c2 ? dispatch_c12<R, T, true>(a, pow2, p.fast, st) : dispatch_c12<R, T, false>(a, pow2, p.fast, st))
+#define C12_GO(R, T) (c2 ? dispatch_c12<R, T, true>(a, pow2, p.nz, st) : dispatch_c12<R, T, false>(a, pow2, p.nz, st))
       if (p.rng == MGP_RNG_MEGORES)
         rc = p.dtype == MGP_F32 ? C12_GO(RNG_MEGORES, float) : C12_GO(RNG_MEGORES, double);
       else
@@ -307,7 +361,7 @@ int make_plan(Plan& p, int kind, const void* w, int dtype, int64_t n, int32_t b,
   p.warp = warp;
   p.n_w = 0;
   p.n_part = 0;
-  p.fast = (flags & MGP_FLAG_POSITIVE_NORMAL) && dtype == MGP_F32;
+  p.nz = (flags & MGP_FLAG_NONZERO) != 0;
   if (kind == MGP_KIND_MEGOPOLIS) {
     if ((rc = check_warp(n, warp, strict, "megopolis"))) return rc;
     p.off.resize((size_t)b);
@@ -496,7 +550,7 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
   if (hs.n_pos == 0) { rc = set_err(MGP_EINVAL, "all weights are zero"); cleanup(); return rc; }
   if (b <= 0) HTRY(mgp_compute_iterations(epsilon, hs.mean, hs.max, &b));
   if (b_used) *b_used = b;
-  const int flags = (hs.n_notnormal == 0) ? MGP_FLAG_POSITIVE_NORMAL : 0;
+  const int flags = (hs.n_zero == 0) ? MGP_FLAG_NONZERO : 0;
   HTRY(make_plan(p, kind, d_w, dtype, n, b, seed, warp, partition_bytes, strict, rng, flags));
   HTRY(plan_alloc(p, st));
   // Overlap the ancestor download with the remaining compute: particle chunks are

@@ -144,20 +144,4 @@ __device__ __forceinline__ bool accepts(double u, double wk, double wj) {
   return !(wj == 0.0 && wk == 0.0) && (u * wk <= wj);
 }
 
-// float32 -> binary64 bits for a POSITIVE NORMAL float32 (one IMAD.WIDE.U32):
-//   hi = (bits >> 3) + ((1023 - 127) << 20), lo = bits << 29
-__device__ __forceinline__ double f32n_to_f64(uint32_t bits) {
-  uint64_t d = (uint64_t)bits * (1ull << 29) + (0x38000000ull << 32);
-  return __longlong_as_double((long long)d);
-}
-
-// m * 2^-53 for the fast path: exact for 1 <= m < 2^53 (exponent field - 53);
-// m == 0 yields a negative finite value, which accepts exactly like u == 0 does
-// when both weights are positive (the fast path's precondition).
-__device__ __forceinline__ double u53_fast(uint64_t m) {
-  double d = __ull2double_rn(m);
-  int hi = __double2hiint(d) - (53 << 20);
-  return __hiloint2double(hi, __double2loint(d));
-}
-
 }  // namespace mgp

@@ -38,78 +38,99 @@ struct ResampleArgs {
   int first, last;   // first launch reads k = i; last launch writes ancestors
   int32_t* kstate;   // carried ancestor between launches (B > OFF_CAP)
   int64_t* anc;      // output ancestors
+  cudaTextureObject_t tex;  // float32 weights as a 1-D linear texture (0: use LDG)
+  uint32_t pk0[10], pk1[10];  // Philox round keys (uniform; constant bank)
 };
 
 // ---------------------------------------------------------------------------
-// weight loads
+// weight loads.  float32 -> float64 conversion is F2F (exact for every float32,
+// subnormals included); it runs on the otherwise idle conversion pipe.
 
-template <typename WT, bool FAST>
-__device__ __forceinline__ double wload(const WT* __restrict__ w, uint32_t j) {
-  if constexpr (sizeof(WT) == 4) {
-    if constexpr (FAST) {
-      return f32n_to_f64(__ldg(reinterpret_cast<const uint32_t*>(w) + j));
-    } else {
-      return (double)__ldg(reinterpret_cast<const float*>(w) + j);
-    }
-  } else {
-    return __ldg(reinterpret_cast<const double*>(w) + j);
-  }
+template <typename WT, bool TEX>
+__device__ __forceinline__ WT wfetch(const WT* __restrict__ w, cudaTextureObject_t tex, uint32_t j) {
+  if constexpr (TEX && sizeof(WT) == 4) return tex1Dfetch<float>(tex, (int)j);
+  else return __ldg(w + j);
 }
 
-template <bool FAST>
-__device__ __forceinline__ bool accept_rule(double u, double wk, double wj) {
-  if constexpr (FAST) return u * wk <= wj;  // all weights positive: the zero rule can never fire
-  else return accepts(u, wk, wj);
+// accept j (M/resample.py:118-122).  NOZERO: no weight is zero, so the both-zero
+// rejection can never fire and is skipped.  u * w_k is exact-rounded binary64.
+template <bool NOZERO, typename WT>
+__device__ __forceinline__ bool accept_w(double u, WT wk, WT wj) {
+  const bool le = u * (double)wk <= (double)wj;
+  if constexpr (NOZERO) return le;
+  else return le && !(wj == (WT)0 && wk == (WT)0);
+}
+
+// (a & c) | (b & ~c) in one LOP3
+__device__ __forceinline__ uint32_t mux3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
 }
 
 // Megopolis partner for W = 32, N % 32 == 0 (M/resample.py:187-193):
 //   j = ((i_al + o_al) mod N) | ((lane + o) & 31)
+// POW2 (N >= 64 a power of two): one LOP3 mux with C = (N-1) & ~31.
 template <bool POW2>
 __device__ __forceinline__ uint32_t mego_j(uint32_t i_al, uint32_t lane, uint32_t o, uint32_t n) {
-  uint32_t a = i_al + (o & ~31u);
-  if constexpr (POW2) a &= (n - 1);
-  else a = (a >= n) ? a - n : a;
-  return a | ((lane + o) & 31u);
+  if constexpr (POW2) {
+    return mux3(i_al + (o & ~31u), lane + (o & 31u), (n - 1) & ~31u);
+  } else {
+    uint32_t a = i_al + (o & ~31u);
+    a = (a >= n) ? a - n : a;
+    return a | ((lane + o) & 31u);
+  }
 }
 
 // ---------------------------------------------------------------------------
 // Megopolis, W = 32 (the hot path).  One particle per thread; the warp's 32 partner
 // weights for round b are one 128-byte line (4 sectors) -- the paper's coalescing.
-// The accepted round index is carried instead of j (j is a pure function of (i, o_b)).
+// Per round: partner fetch (texture path, no address arithmetic), one stream draw,
+// one DMUL + DSETP, one 32-bit select.  The accepted round index is carried instead
+// of j (j is a pure function of (i, o_b)) and k is rebuilt once at the end.
 
-template <int RNG, typename WT, bool POW2, bool FAST>
-__global__ void __launch_bounds__(RS_THREADS) k_megopolis_w32(const ResampleArgs a,
+template <int RNG, typename WT, bool POW2, bool NOZERO, bool TEX>
+__global__ void __launch_bounds__(RS_THREADS) k_megopolis_w32(const __grid_constant__ ResampleArgs a,
                                                               const __grid_constant__ OffChunk oc) {
   const uint32_t i = a.p0 + blockIdx.x * RS_THREADS + threadIdx.x;
   if (i >= a.p_end) return;
   const WT* __restrict__ w = reinterpret_cast<const WT*>(a.w);
   const uint32_t lane = threadIdx.x & 31u, i_al = i - lane, n = a.n;
   uint32_t k = a.first ? i : (uint32_t)a.kstate[i];
-  double wk = wload<WT, FAST>(w, k);
+  WT wk = wfetch<WT, TEX>(w, a.tex, k);
   int bstar = -1;
   if constexpr (RNG == RNG_MEGORES) {
     uint64_t x = megores_key(a.base, i, (uint64_t)a.b0);
 #pragma unroll 4
     for (int t = 0; t < a.cnt; ++t) {
       const uint32_t o = oc.o[t];
-      const double wj = wload<WT, FAST>(w, mego_j<POW2>(i_al, lane, o, n));
-      const uint64_t m = mix64_m53(x);
+      const WT wj = wfetch<WT, TEX>(w, a.tex, mego_j<POW2>(i_al, lane, o, n));
+      const double u = (double)mix64_m53(x) * 0x1p-53;  // exact: u01 (M/rng.py:105-108)
       x += M_CTR;
-      const double u = FAST ? u53_fast(m) : (double)m * 0x1p-53;
-      if (accept_rule<FAST>(u, wk, wj)) { wk = wj; bstar = t; }
+      if (accept_w<NOZERO>(u, wk, wj)) { wk = wj; bstar = t; }
     }
   } else {
     // philox: draw t = b0 + t; block (t >> 2), word (t & 3); b0 % 4 == 0.
     for (int t0 = 0; t0 < a.cnt; t0 += 4) {
-      const P4 blk = philox_block(a.seed, i, (uint64_t)(a.b0 + t0) >> 2);
+      uint32_t c0 = i, c1 = 0, c2 = (uint32_t)((a.b0 + t0) >> 2), c3 = 0;
+#pragma unroll
+      for (int r = 0; r < 10; ++r) {
+        const uint64_t q0 = (uint64_t)PHILOX_M0 * c0, q1 = (uint64_t)PHILOX_M1 * c2;
+        const uint32_t n0 = (uint32_t)(q1 >> 32) ^ c1 ^ a.pk0[r], n2 = (uint32_t)(q0 >> 32) ^ c3 ^ a.pk1[r];
+        c1 = (uint32_t)q1;
+        c3 = (uint32_t)q0;
+        c0 = n0;
+        c2 = n2;
+      }
+      const uint32_t wd[4] = {c0, c1, c2, c3};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int t = t0 + q;
         if (t < a.cnt) {
           const uint32_t o = oc.o[t];
-          const double wj = wload<WT, FAST>(w, mego_j<POW2>(i_al, lane, o, n));
-          const double u = (double)p4_word(blk, q) * 0x1p-32;
-          if (accept_rule<FAST>(u, wk, wj)) { wk = wj; bstar = t; }
+          const WT wj = wfetch<WT, TEX>(w, a.tex, mego_j<POW2>(i_al, lane, o, n));
+          const double u = (double)wd[q] * 0x1p-32;
+          if (accept_w<NOZERO>(u, wk, wj)) { wk = wj; bstar = t; }
         }
       }
     }
@@ -122,28 +143,27 @@ __global__ void __launch_bounds__(RS_THREADS) k_megopolis_w32(const ResampleArgs
 // ---------------------------------------------------------------------------
 // Metropolis (uniform random partner; the uncoalesced baseline, M/resample.py:125-138)
 
-template <int RNG, typename WT, bool POW2, bool FAST>
-__global__ void __launch_bounds__(RS_THREADS) k_metropolis(const ResampleArgs a) {
+template <int RNG, typename WT, bool POW2, bool NOZERO>
+__global__ void __launch_bounds__(RS_THREADS) k_metropolis(const __grid_constant__ ResampleArgs a) {
   const uint32_t i = a.p0 + blockIdx.x * RS_THREADS + threadIdx.x;
   if (i >= a.p_end) return;
   const WT* __restrict__ w = reinterpret_cast<const WT*>(a.w);
   const uint32_t n = a.n;
   uint32_t k = a.first ? i : (uint32_t)a.kstate[i];
-  double wk = wload<WT, FAST>(w, k);
+  WT wk = __ldg(w + k);
   if constexpr (RNG == RNG_MEGORES) {
     uint64_t x = megores_key(a.base, i, 2ull * (uint64_t)a.b0);
 #pragma unroll 2
     for (int t = 0; t < a.cnt; ++t) {
-      const uint64_t m = mix64_m53(x);
+      const double u = (double)mix64_m53(x) * 0x1p-53;  // u at counter 2b
       x += M_CTR;
-      const uint64_t hj = mix64(x);
+      const uint64_t hj = mix64(x);                     // j at counter 2b+1
       x += M_CTR;
       uint32_t j;
-      if constexpr (POW2) j = (a.log2 == 0) ? 0u : (uint32_t)(hj >> 32) >> (32 - a.log2);
+      if constexpr (POW2) j = (uint32_t)(hj >> 32) >> (32 - a.log2);  // == uint_below for n = 2^k
       else j = (uint32_t)below_from_hash(hj, (int64_t)n);
-      const double wj = wload<WT, FAST>(w, j);
-      const double u = FAST ? u53_fast(m) : (double)m * 0x1p-53;
-      if (accept_rule<FAST>(u, wk, wj)) { wk = wj; k = j; }
+      const WT wj = __ldg(w + j);
+      if (accept_w<NOZERO>(u, wk, wj)) { wk = wj; k = j; }
     }
   } else {
     // u at draw 2b, j at draw 2b+1: one philox block per two rounds.
@@ -153,9 +173,8 @@ __global__ void __launch_bounds__(RS_THREADS) k_metropolis(const ResampleArgs a)
       const uint32_t q = (uint32_t)(d & 3);
       const uint32_t wu = q == 0 ? blk.x : blk.z, wjw = q == 0 ? blk.y : blk.w;
       const uint32_t j = __umulhi(wjw, n);
-      const double wj = wload<WT, FAST>(w, j);
-      const double u = (double)wu * 0x1p-32;
-      if (accept_rule<FAST>(u, wk, wj)) { wk = wj; k = j; }
+      const WT wj = __ldg(w + j);
+      if (accept_w<NOZERO>((double)wu * 0x1p-32, wk, wj)) { wk = wj; k = j; }
     }
   }
   if (a.last) a.anc[i] = (int64_t)k;
@@ -178,8 +197,8 @@ __device__ __forceinline__ uint32_t below_n(uint64_t h_or_word, uint32_t n, uint
   return __umulhi((uint32_t)h_or_word, n);
 }
 
-template <int RNG, typename WT, bool POW2, bool FAST, bool C2, bool STAGE>
-__global__ void __launch_bounds__(RS_THREADS) k_c12_w32(const ResampleArgs a) {
+template <int RNG, typename WT, bool POW2, bool NOZERO, bool C2, bool STAGE>
+__global__ void __launch_bounds__(RS_THREADS) k_c12_w32(const __grid_constant__ ResampleArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t i = a.p0 + blockIdx.x * RS_THREADS + threadIdx.x;
   if (i >= a.p_end) return;  // n % 32 == 0: whole warps leave together
@@ -188,13 +207,13 @@ __global__ void __launch_bounds__(RS_THREADS) k_c12_w32(const ResampleArgs a) {
   const uint32_t n_w = a.n_w;
   const uint64_t wlane = WARP_LANE_BASE + warp_g;
   uint32_t k = a.first ? i : (uint32_t)a.kstate[i];
-  double wk = wload<WT, FAST>(w, k);
+  WT wk = __ldg(w + k);
   uint32_t lo = 0;
   WT* part = reinterpret_cast<WT*>(smem_raw) + (threadIdx.x >> 5) * n_w;
   if constexpr (!C2) {
     lo = (uint32_t)draw_below<RNG>(a.base, a.seed, wlane, 0, (int64_t)a.n_part) * n_w;
     if constexpr (STAGE) {
-      for (uint32_t q = lane; q < n_w; q += 32) part[q] = w[lo + q];
+      for (uint32_t q = lane; q < n_w; q += 32) part[q] = __ldg(w + lo + q);
       __syncwarp();
     }
   }
@@ -207,19 +226,12 @@ __global__ void __launch_bounds__(RS_THREADS) k_c12_w32(const ResampleArgs a) {
           preg = (uint32_t)draw_below<RNG>(a.base, a.seed, wlane, (uint64_t)(a.b0 + t + (int)lane), (int64_t)a.n_part);
         lo = __shfl_sync(0xffffffffu, preg, t & 31) * n_w;
       }
-      const uint64_t m = mix64_m53(x);
+      const double u = (double)mix64_m53(x) * 0x1p-53;
       x += M_CTR;
       const uint32_t jl = below_n<RNG>(mix64(x), n_w, a.log2, POW2);
       x += M_CTR;
-      double wj;
-      if constexpr (STAGE && !C2) {
-        if constexpr (sizeof(WT) == 4 && FAST) wj = f32n_to_f64(reinterpret_cast<const uint32_t*>(part)[jl]);
-        else wj = (double)part[jl];
-      } else {
-        wj = wload<WT, FAST>(w, lo + jl);
-      }
-      const double u = FAST ? u53_fast(m) : (double)m * 0x1p-53;
-      if (accept_rule<FAST>(u, wk, wj)) { wk = wj; k = lo + jl; }
+      const WT wj = (STAGE && !C2) ? part[jl] : __ldg(w + lo + jl);
+      if (accept_w<NOZERO>(u, wk, wj)) { wk = wj; k = lo + jl; }
     }
   } else {
     for (int t = 0; t < a.cnt; ++t) {
@@ -233,11 +245,8 @@ __global__ void __launch_bounds__(RS_THREADS) k_c12_w32(const ResampleArgs a) {
       const uint32_t q = (uint32_t)(d & 3);
       const uint32_t wu = q == 0 ? blk.x : blk.z, wjw = q == 0 ? blk.y : blk.w;
       const uint32_t jl = __umulhi(wjw, n_w);
-      double wj;
-      if constexpr (STAGE && !C2) wj = (double)part[jl];
-      else wj = wload<WT, FAST>(w, lo + jl);
-      const double u = (double)wu * 0x1p-32;
-      if (accept_rule<FAST>(u, wk, wj)) { wk = wj; k = lo + jl; }
+      const WT wj = (STAGE && !C2) ? part[jl] : __ldg(w + lo + jl);
+      if (accept_w<NOZERO>((double)wu * 0x1p-32, wk, wj)) { wk = wj; k = lo + jl; }
     }
   }
   if (a.last) a.anc[i] = (int64_t)k;

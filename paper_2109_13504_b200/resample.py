@@ -120,7 +120,7 @@ def _resample(kind, w, b, seed, warp, part, strict, rng, name):
         st = w.stats()
         if st.n_pos == 0:
             raise ValueError("all weights are zero")
-        flags = _lib.FLAG_POSITIVE_NORMAL if st.positive_normal else 0
+        flags = _lib.FLAG_NONZERO if st.n_zero == 0 else 0
         out = t.empty(len(w), dtype=t.int64, device=vals.device)
         with t.cuda.device(vals.device):
             s = D.stream_ptr()

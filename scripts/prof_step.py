@@ -36,7 +36,7 @@ for _ in range(a.steps):
     _lib.check(L.mgp_weight_stats(D.ptr(w.values), dt, a.n, D.ptr(stats), sp))
     h = stats.cpu().numpy()
     b = mg.compute_iterations(0.01, float(h[1]), float(h[2])).b
-    flags = 1 if h.view("int64")[7] == 0 else 0
+    flags = 1 if h.view("int64")[4] == 0 else 0
     pb = a.part if a.kind in ("c1", "c2") else 0
     _lib.check(L.mgp_resample_range(_lib.KIND[a.kind], D.ptr(w.values), dt, a.n, b, 7, 32, pb, 1,
                                     _lib.RNG[a.rng], flags, 0, a.n, D.ptr(anc), sp))
