@@ -251,6 +251,7 @@ def main():
         flags = _lib.FLAG_NONZERO if host.view(np.int64)[4] == 0 else 0
         if ev is not None:
             ev[0].record(stream)
+            ev[2].record(stream)
         _lib.check(L.mgp_resample_range(_lib.KIND["megopolis"], D.ptr(full), 0, n_glob, b, RUN_SEED, 32, 0, 1,
                                          rng_id, flags, rank * n_loc, (rank + 1) * n_loc, D.ptr(anc), sp))
         if ev is not None:
@@ -265,7 +266,8 @@ def main():
     # timed region: K steps, each bracketed by CUDA events; L2 flushed between steps
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -280,6 +282,7 @@ def main():
         dist.barrier()
     step_ms = [starts[s].elapsed_time(ends[s]) for s in range(args.steps)]
     kern_ms = [kev[s][0].elapsed_time(kev[s][1]) for s in range(args.steps)]
+    pre_ms = [starts[s].elapsed_time(kev[s][2]) for s in range(args.steps)]
     t_total = sum(step_ms)
     if world > 1:
         tt = torch.tensor([t_total], dtype=torch.float64, device=dev)
@@ -372,6 +375,8 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
+            "step_breakdown_ms": {"step": [round(x, 3) for x in step_ms], "kernel": [round(x, 3) for x in kern_ms],
+                                  "stats_and_host_B": [round(x, 3) for x in pre_ms]},
             "clocks": clk.summary(),
             "quality": quality,
         }

@@ -1,6 +1,6 @@
 set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv
-python -c "import torch; p=torch.cuda.get_device_properties(0); print(p, p.L2_cache_size if hasattr(p,'L2_cache_size') else '')"
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -5
-timeout 1200 python -m pytest tests -x -q -m gpu 2>&1 | tail -30
-timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench1.json 2> gpurun_out/bench1.err; tail -3 gpurun_out/bench1.err; cat gpurun_out/bench1.json
+mkdir -p gpurun_out
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -3
+timeout 1200 python -m pytest tests -x -q -m gpu 2>&1 | tail -15
+timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err; cat gpurun_out/bench.json
+timeout 600 python bench.py --steps 10 --warmup 3 --rng philox --no-cpu-baseline --quality-runs 0 > gpurun_out/bench_philox.json 2>&1; cat gpurun_out/bench_philox.json | tail -2
