@@ -313,7 +313,10 @@ int run_range(Plan& p, int64_t p0, int64_t p_end, int64_t* anc, cudaStream_t st)
     int rc = 0;
     if (p.kind == MGP_KIND_MEGOPOLIS) {
       static thread_local OffChunk oc;
-      for (int t = 0; t < a.cnt; ++t) oc.o[t] = (uint32_t)p.off[b0 + t];
+      for (int t = 0; t < a.cnt; ++t) {
+        const uint32_t o = (uint32_t)p.off[b0 + t];
+        oc.o[t] = make_uint2(o & ~31u, o & 31u);
+      }
       const bool pow2 = is_pow2(p.n) && p.n >= 64;
       if (p.rng == MGP_RNG_MEGORES)
         rc = p.dtype == MGP_F32 ? dispatch_mego_w32<RNG_MEGORES, float>(a, oc, pow2, p.nz, st)

@@ -19,10 +19,11 @@ namespace mgp {
 constexpr int RS_THREADS = 256;   // resampler CTA size (8 warps)
 constexpr int OFF_CAP = 1024;     // Megopolis offsets carried per launch in the param space
 
-// Offsets o_b for rounds [b0, b0+cnt) of one launch.  Kernel parameter space is a
-// constant bank: the warp-uniform o_b reads never touch the LSU/L1 path.
+// Offsets o_b for rounds [b0, b0+cnt) of one launch, pre-split on the host into
+// {o & ~31, o & 31}.  Kernel parameter space is a constant bank: the warp-uniform
+// reads are uniform-datapath loads that never touch the LSU/L1 path.
 struct OffChunk {
-  uint32_t o[OFF_CAP];
+  uint2 o[OFF_CAP];
 };
 
 struct ResampleArgs {
@@ -72,14 +73,19 @@ __device__ __forceinline__ uint32_t mux3(uint32_t a, uint32_t b, uint32_t c) {
 //   j = ((i_al + o_al) mod N) | ((lane + o) & 31)
 // POW2 (N >= 64 a power of two): one LOP3 mux with C = (N-1) & ~31.
 template <bool POW2>
-__device__ __forceinline__ uint32_t mego_j(uint32_t i_al, uint32_t lane, uint32_t o, uint32_t n) {
+__device__ __forceinline__ uint32_t mego_j(uint32_t i_al, uint32_t lane, uint2 o, uint32_t n) {
   if constexpr (POW2) {
-    return mux3(i_al + (o & ~31u), lane + (o & 31u), (n - 1) & ~31u);
+    return mux3(i_al + o.x, lane + o.y, (n - 1) & ~31u);
   } else {
-    uint32_t a = i_al + (o & ~31u);
+    uint32_t a = i_al + o.x;
     a = (a >= n) ? a - n : a;
-    return a | ((lane + o) & 31u);
+    return a | ((lane + o.y) & 31u);
   }
+}
+
+// exact (double)w * 2^-32 for a 32-bit word: (2^52 + w) * 2^-32 - 2^20 in one DFMA
+__device__ __forceinline__ double u32_exact(uint32_t w) {
+  return fma(__hiloint2double(0x43300000, (int)w), 0x1p-32, -0x1p20);
 }
 
 // ---------------------------------------------------------------------------
@@ -100,13 +106,15 @@ __global__ void __launch_bounds__(RS_THREADS) k_megopolis_w32(const __grid_const
   WT wk = wfetch<WT, TEX>(w, a.tex, k);
   int bstar = -1;
   if constexpr (RNG == RNG_MEGORES) {
-    uint64_t x = megores_key(a.base, i, (uint64_t)a.b0);
+    // counter t's key x0 + t*M_CTR is formed with IMAD.WIDE (FMA pipe): the ALU pipe
+    // is the binding one (the splitmix xorshifts)
+    const uint64_t x0 = megores_key(a.base, i, (uint64_t)a.b0);
 #pragma unroll 4
     for (int t = 0; t < a.cnt; ++t) {
-      const uint32_t o = oc.o[t];
+      const uint2 o = oc.o[t];
       const WT wj = wfetch<WT, TEX>(w, a.tex, mego_j<POW2>(i_al, lane, o, n));
+      const uint64_t x = x0 + (uint64_t)(uint32_t)t * M_CTR;
       const double u = (double)mix64_m53(x) * 0x1p-53;  // exact: u01 (M/rng.py:105-108)
-      x += M_CTR;
       if (accept_w<NOZERO>(u, wk, wj)) { wk = wj; bstar = t; }
     }
   } else {
@@ -127,9 +135,9 @@ __global__ void __launch_bounds__(RS_THREADS) k_megopolis_w32(const __grid_const
       for (int q = 0; q < 4; ++q) {
         const int t = t0 + q;
         if (t < a.cnt) {
-          const uint32_t o = oc.o[t];
+          const uint2 o = oc.o[t];
           const WT wj = wfetch<WT, TEX>(w, a.tex, mego_j<POW2>(i_al, lane, o, n));
-          const double u = (double)wd[q] * 0x1p-32;
+          const double u = u32_exact(wd[q]);
           if (accept_w<NOZERO>(u, wk, wj)) { wk = wj; bstar = t; }
         }
       }
