@@ -109,7 +109,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.05)
+            time.sleep(0.1)
 
     def __enter__(self):
         if self.nv:
@@ -271,6 +271,10 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    import gc
+
+    gc.collect()
+    gc.disable()
     with ClockSampler(local) as clk:
         for s in range(args.steps):
             flush.fill_(float(s))
@@ -278,6 +282,7 @@ def main():
             b = step(kev[s])
             ends[s].record(stream)
         torch.cuda.synchronize()
+    gc.enable()
     if world > 1:
         dist.barrier()
     step_ms = [starts[s].elapsed_time(ends[s]) for s in range(args.steps)]

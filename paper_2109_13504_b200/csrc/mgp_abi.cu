@@ -84,6 +84,30 @@ int check_partition(int64_t n, int32_t part_bytes, int64_t* n_w, int64_t* n_part
 }
 
 // ---------------------------------------------------------------------------
+// Stream-ordered scratch.  The device's default memory pool keeps freed blocks
+// (release threshold raised once per device), so the per-call cudaMallocAsync of
+// reduction heaps / offsets / the host-path buffers is a pool hit instead of a
+// remap after every synchronisation.
+
+std::mutex g_pool_mu;
+std::vector<int> g_pool_ready;
+
+void ensure_pool() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  for (int d : g_pool_ready)
+    if (d == dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaGetLastError();
+  g_pool_ready.push_back(dev);
+}
+
+// ---------------------------------------------------------------------------
 // pairwise reduction plumbing
 
 int pw_depth(int64_t n) {
@@ -109,6 +133,7 @@ int pw_depth(int64_t n) {
 
 template <class Elem, typename WT, bool STATS>
 int pw_reduce(const Elem& e, const WT* wraw, int64_t n, PwOut out, cudaStream_t st) {
+  ensure_pool();
   const int depth = pw_depth(n);
   const int64_t nch = 1ll << depth;
   double* heap = nullptr;
@@ -379,6 +404,7 @@ int make_plan(Plan& p, int kind, const void* w, int dtype, int64_t n, int32_t b,
 }
 
 int plan_alloc(Plan& p, cudaStream_t st) {
+  ensure_pool();
   if (!plan_uses_w32(p) && p.kind == MGP_KIND_MEGOPOLIS) {
     CUDA_TRY(cudaMallocAsync(&p.d_off, sizeof(int64_t) * p.b, st));
     CUDA_TRY(cudaMemcpyAsync(p.d_off, p.off.data(), sizeof(int64_t) * p.b, cudaMemcpyHostToDevice, st));
@@ -507,6 +533,7 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
   if (n < 1) return set_err(MGP_EINVAL, "weights must be a non-empty 1-d sequence");
   if (n > MAX_N) return set_err(MGP_EUNSUPPORTED, "N exceeds 2^31-1");
   if (device >= 0) CUDA_TRY(cudaSetDevice(device));
+  ensure_pool();
   cudaStream_t st, cp;
   CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
@@ -586,6 +613,7 @@ int mgp_offspring(const int64_t* d_anc, int64_t n_anc, int64_t n, int64_t* d_cou
   if (n) CUDA_TRY(cudaMemsetAsync(d_counts, 0, sizeof(int64_t) * n, st));
   if (d_bad) CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int32_t), st));
   if (n_anc == 0) return 0;
+  ensure_pool();
   int32_t* bad = d_bad;
   if (!bad) CUDA_TRY(cudaMallocAsync(&bad, sizeof(int32_t), st));
   const unsigned grid = (unsigned)((n_anc + 255) / 256);
