@@ -134,6 +134,12 @@ int mgp_squared_error(const int64_t *d_counts, const double *d_e, int64_t n, dou
 /* apply_ancestors (M/resample.py:371-377): out[i] = states[anc[i]], rows of row_bytes */
 int mgp_gather(const void *d_states, int64_t row_bytes, const int64_t *d_anc, int64_t n, void *d_out, void *stream);
 
+/* Sharded apply_ancestors over peer memory: rank r owns rows [r*n_local, (r+1)*n_local)
+ * at peer_states[r] (device pointers valid on the calling device: NVLink P2P /
+ * symmetric-memory mappings); out[i] = row anc[i] read directly from its owner. */
+int mgp_gather_peers(const void *const *peer_states, int npeers, int64_t n_local, int64_t row_bytes,
+                     const int64_t *d_anc, int64_t n, void *d_out, void *stream);
+
 /* gen_gaussian_weights (M/weights.py:100-104) on the device (synthetic inputs) */
 int mgp_gen_gaussian(double y, int64_t n, uint64_t seed, int dtype, void *d_out, void *stream);
 

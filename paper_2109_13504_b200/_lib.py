@@ -46,6 +46,7 @@ SIGNATURES = {
     "mgp_quality_finalize": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
     "mgp_squared_error": (_i32, [_vp, _vp, _i64, _vp, _vp]),
     "mgp_gather": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp]),
+    "mgp_gather_peers": (_i32, [_vp, _i32, _i64, _i64, _vp, _i64, _vp, _vp]),
     "mgp_gen_gaussian": (_i32, [_dbl, _i64, _u64, _i32, _vp, _vp]),
     "mgp_philox_selftest": (_i32, [_u64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, _i64, _vp]),
 }

@@ -693,6 +693,32 @@ int mgp_gather(const void* d_states, int64_t row_bytes, const int64_t* d_anc, in
   return 0;
 }
 
+int mgp_gather_peers(const void* const* peer_states, int npeers, int64_t n_local, int64_t row_bytes,
+                     const int64_t* d_anc, int64_t n, void* d_out, void* stream) {
+  if (npeers < 1 || npeers > 64) return set_err(MGP_EINVAL, "npeers must be in [1, 64], got %d", npeers);
+  if (n_local < 1 || row_bytes < 0 || n < 0) return set_err(MGP_EINVAL, "invalid sizes");
+  if (n == 0 || row_bytes == 0) return 0;
+  PeerTable pt{};
+  uintptr_t al = (uintptr_t)d_out | (uintptr_t)row_bytes;
+  for (int r = 0; r < npeers; ++r) {
+    if (!peer_states[r]) return set_err(MGP_EINVAL, "null peer pointer %d", r);
+    pt.p[r] = peer_states[r];
+    al |= (uintptr_t)peer_states[r];
+  }
+  cudaStream_t st = S(stream);
+  const unsigned grid = (unsigned)std::min<int64_t>((n * row_bytes / 4 + 255) / 256 + 1, 148 * 32);
+  if ((al & 15) == 0)
+    k_gather_peers<uint4><<<grid, 256, 0, st>>>(pt, npeers, n_local, d_anc, n, row_bytes / 16, (uint4*)d_out);
+  else if ((al & 7) == 0)
+    k_gather_peers<uint2><<<grid, 256, 0, st>>>(pt, npeers, n_local, d_anc, n, row_bytes / 8, (uint2*)d_out);
+  else if ((al & 3) == 0)
+    k_gather_peers<uint32_t><<<grid, 256, 0, st>>>(pt, npeers, n_local, d_anc, n, row_bytes / 4, (uint32_t*)d_out);
+  else
+    k_gather_peers<uint8_t><<<grid, 256, 0, st>>>(pt, npeers, n_local, d_anc, n, row_bytes, (uint8_t*)d_out);
+  LAUNCH_CHECK("k_gather_peers");
+  return 0;
+}
+
 int mgp_gen_gaussian(double y, int64_t n, uint64_t seed, int dtype, void* d_out, void* stream) {
   if (y < 0) return set_err(MGP_EINVAL, "y must be >= 0, got %.17g", y);
   if (n < 1) return set_err(MGP_EINVAL, "n must be >= 1, got %lld", (long long)n);

@@ -618,6 +618,26 @@ __global__ void k_gather(const V* __restrict__ src, const int64_t* __restrict__ 
   }
 }
 
+// Sharded gather over peer memory (NVLink P2P / symmetric memory): rank r owns rows
+// [r*n_local, (r+1)*n_local); out[i] = peers[anc[i] / n_local][anc[i] % n_local].
+// The remote rows are read directly by this kernel -- no staging copy.
+struct PeerTable {
+  const void* p[64];
+};
+
+template <typename V>
+__global__ void k_gather_peers(const __grid_constant__ PeerTable peers, int npeers, int64_t n_local,
+                               const int64_t* __restrict__ anc, int64_t n, int64_t row_v, V* __restrict__ dst) {
+  const int64_t total = n * row_v;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / row_v, c = t - i * row_v;
+    const int64_t a = anc[i];
+    const int64_t owner = a / n_local, local = a - owner * n_local;
+    const V* src = reinterpret_cast<const V*>(peers.p[owner]);
+    dst[t] = src[local * row_v + c];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Synthetic Gaussian-family weights on the device (M/weights.py:100-104 with the
 // Box-Muller draw of M/rng.py:152-161).  Same formula and stream; libm rounding of

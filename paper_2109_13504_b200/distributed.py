@@ -1,0 +1,184 @@
+"""Sharded resampling across GPUs (one process per GPU, torch.distributed over NCCL).
+
+Layout: rank r owns particles [r*n_local, (r+1)*n_local) of a global
+population of N = world * n_local.  Each particle's ancestor depends on the FULL
+weight vector, the shared offsets and the seed only (M/resample.py:185-197), so:
+
+  1. weights: the per-rank slices are all-gathered into a replicated f32[N]
+     (the one real exchange of the path; 4N bytes over NVLink),
+  2. B rule: every rank reduces the replicated array with the same numpy-exact
+     pairwise tree, so every rank derives the identical B without a collective,
+  3. offsets: derived from the seed on every rank (no collective),
+  4. resample: each rank runs the kernel on its particle slice (global indices),
+  5. states: apply_ancestors needs rows owned by other ranks -- exchanged with
+     all-to-all (bucketed by owner) or read directly from peer memory
+     (``gather_from_peers`` / mgp_gather_peers) when the rows live in
+     NVLink-mapped symmetric memory.
+
+The concatenation of every rank's ancestors equals the single-GPU result, which
+equals the reference's, bit for bit.
+
+Compute goes through ``ops`` (default: libmgp.so on the current CUDA device).  The
+multi-process tests inject a CPU implementation to exercise the protocol with the
+gloo backend on machines without GPUs; the product path has no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+from . import _device as D
+from . import _lib
+from .resample import PartitionConfig, WarpConfig
+from .weights import compute_iterations, device_stats
+
+
+class CudaOps:
+    """libmgp.so on the calling rank's current CUDA device."""
+
+    def stats(self, w_full):
+        return device_stats(w_full)
+
+    def resample_range(self, kind, w_full, b, seed, warp, partition_bytes, strict, rng, nonzero, p0, p1):
+        t = D.torch()
+        out = t.empty(p1 - p0, dtype=t.int64, device=w_full.device)
+        flags = _lib.FLAG_NONZERO if nonzero else 0
+        _lib.check(_lib.lib().mgp_resample_range(
+            _lib.KIND[kind], D.ptr(w_full), D.wdtype(w_full), w_full.numel(), int(b), int(seed) & (2**64 - 1),
+            int(warp), int(partition_bytes or 0), int(bool(strict)), _lib.RNG[rng], flags, int(p0), int(p1),
+            D.ptr(out), D.stream_ptr()))
+        return out
+
+    def gather_rows(self, states, idx):
+        t = D.torch()
+        src = states.contiguous()
+        out = t.empty((idx.numel(),) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+        row_bytes = src[0].numel() * src.element_size() if src.shape[0] else 0
+        _lib.check(_lib.lib().mgp_gather(D.ptr(src), row_bytes, D.ptr(idx.contiguous()), idx.numel(), D.ptr(out),
+                                         D.stream_ptr()))
+        return out
+
+
+@dataclass
+class ShardedResampler:
+    """A Metropolis-family resampler over particles sharded across ranks."""
+
+    kind: str = "megopolis"
+    warp: WarpConfig = WarpConfig()
+    partition_bytes: int | None = None
+    strict: bool = True
+    rng: str = "megores"
+    group: object = None
+    ops: object = None
+
+    def __post_init__(self):
+        import torch.distributed as dist
+
+        self._dist = dist
+        self.rank = dist.get_rank(self.group)
+        self.world = dist.get_world_size(self.group)
+        if self.ops is None:
+            self.ops = CudaOps()
+        if self.kind in ("c1", "c2") and self.partition_bytes is None:
+            raise ValueError(f"{self.kind} requires a partition size")
+
+    # -- 1. replicated weights ---------------------------------------------
+    def replicate_weights(self, w_local):
+        """All-gather the per-rank weight slices into the full replicated vector."""
+        t = D.torch()
+        n_local = w_local.numel()
+        full = t.empty(n_local * self.world, dtype=w_local.dtype, device=w_local.device)
+        if self.world == 1:
+            full.copy_(w_local)
+            return full
+        try:
+            self._dist.all_gather_into_tensor(full, w_local.contiguous(), group=self.group)
+        except (RuntimeError, AttributeError, NotImplementedError):
+            parts = list(full.chunk(self.world))
+            self._dist.all_gather(parts, w_local.contiguous(), group=self.group)
+        return full
+
+    # -- 2-4. B rule + per-slice resample --------------------------------------
+    def resample(self, w_local, b: int | None = None, seed=0, epsilon: float = 0.01):
+        """Ancestors (global indices) for this rank's particle slice, and the B used."""
+        n_local = w_local.numel()
+        full = self.replicate_weights(w_local)
+        n = full.numel()
+        st = self.ops.stats(full)
+        if st.n_nonfinite:
+            raise ValueError("weights must be finite")
+        if st.n_neg:
+            raise ValueError("weights must be non-negative")
+        if st.n_pos == 0:
+            raise ValueError("all weights are zero")
+        if b is None:
+            b = compute_iterations(epsilon, st.mean, st.max).b
+        if b < 1:
+            raise ValueError(f"B must be >= 1, got {b}")
+        if self.kind in ("megopolis", "c1", "c2") and self.strict and n % self.warp.warp_size:
+            raise ValueError(f"{self.kind} requires N ({n}) to be a multiple of the warp size "
+                             f"({self.warp.warp_size}) in strict mode")
+        if self.kind in ("c1", "c2"):
+            PartitionConfig(self.partition_bytes).n_partitions(n, self.warp)
+        p0 = self.rank * n_local
+        anc = self.ops.resample_range(self.kind, full, b, seed, self.warp.warp_size, self.partition_bytes,
+                                      self.strict, self.rng, st.n_zero == 0, p0, p0 + n_local)
+        return anc, b
+
+    # -- 5. particle states ---------------------------------------------------
+    def exchange(self, states_local, anc_local):
+        """apply_ancestors across ranks: rows anc_local[i] (global) into a fresh local array.
+
+        Requests are bucketed by owner rank and exchanged with two all-to-alls
+        (indices out, rows back)."""
+        t = D.torch()
+        dist = self._dist
+        n_local = states_local.shape[0]
+        dev = states_local.device
+        anc = anc_local.to(device=dev, dtype=t.int64)
+        if self.world == 1:
+            return self.ops.gather_rows(states_local, anc)
+        owner = t.div(anc, n_local, rounding_mode="floor")
+        order = t.argsort(owner, stable=True)
+        send_idx = (anc - owner * n_local)[order].contiguous()
+        send_counts = t.bincount(owner, minlength=self.world).to(t.int64)
+        recv_counts = t.empty_like(send_counts)
+        dist.all_to_all_single(recv_counts, send_counts, group=self.group)
+        sc, rc = send_counts.tolist(), recv_counts.tolist()
+        recv_idx = t.empty(sum(rc), dtype=t.int64, device=dev)
+        dist.all_to_all_single(recv_idx, send_idx, output_split_sizes=rc, input_split_sizes=sc, group=self.group)
+        rows = self.ops.gather_rows(states_local, recv_idx)
+        reply = t.empty((sum(sc),) + tuple(states_local.shape[1:]), dtype=states_local.dtype, device=dev)
+        dist.all_to_all_single(reply, rows.contiguous(), output_split_sizes=sc, input_split_sizes=rc,
+                               group=self.group)
+        out = t.empty_like(reply)
+        out[order] = reply
+        return out
+
+
+def gather_from_peers(peer_states, n_local: int, anc, out=None):
+    """out[i] = row anc[i] read directly from its owner's memory (mgp_gather_peers).
+
+    ``peer_states``: one CUDA tensor (or raw device pointer) per rank, each holding
+    that rank's n_local rows and addressable from this device (NVLink P2P /
+    symmetric memory).  Single-kernel sharded gather: no staging, no all-to-all."""
+    t = D.torch()
+    ptrs = []
+    ref = None
+    for p in peer_states:
+        if D.is_tensor(p):
+            ref = p if ref is None else ref
+            ptrs.append(p.data_ptr())
+        else:
+            ptrs.append(int(p))
+    if ref is None:
+        raise ValueError("at least one peer must be given as a tensor (shape/dtype template)")
+    anc = anc.to(device=ref.device, dtype=t.int64).contiguous()
+    if out is None:
+        out = t.empty((anc.numel(),) + tuple(ref.shape[1:]), dtype=ref.dtype, device=ref.device)
+    row_bytes = ref[0].numel() * ref.element_size()
+    arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+    _lib.check(_lib.lib().mgp_gather_peers(ctypes.cast(arr, ctypes.c_void_p), len(ptrs), int(n_local), row_bytes,
+                                           D.ptr(anc), anc.numel(), D.ptr(out), D.stream_ptr()))
+    return out

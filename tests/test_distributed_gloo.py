@@ -1,0 +1,128 @@
+"""Multi-process (world_size 2 and 3, gloo, CPU) tests of the sharded protocol:
+weight all-gather, per-slice resampling with global indices, the B rule on the
+replicated array, and the cross-rank state exchange.
+
+The CUDA kernels are replaced by the CPU oracle through ShardedResampler's ``ops``
+hook (test infrastructure only); the GPU path is covered by tests/test_parity_gpu.py
+and by the peer-gather GPU test below.
+"""
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+class _Stats:
+    def __init__(self, w):
+        from oracle import oracle
+
+        v = w.numpy()
+        self.n_nonfinite = int((~np.isfinite(v)).sum())
+        self.n_neg = int((v < 0).sum())
+        self.n_pos = int((v > 0).sum())
+        self.n_zero = int((v == 0).sum())
+        self.mean, self.max = oracle.weight_mean_max(v)
+
+
+class OracleOps:
+    """CPU stand-in for CudaOps (test infrastructure)."""
+
+    def stats(self, w_full):
+        return _Stats(w_full)
+
+    def resample_range(self, kind, w_full, b, seed, warp, partition_bytes, strict, rng, nonzero, p0, p1):
+        from oracle import oracle
+
+        anc = oracle.resample(kind, w_full.numpy(), b, seed, warp, partition_bytes, strict, rng, p0=p0, p1=p1)
+        return torch.from_numpy(anc[p0:p1].copy())
+
+    def gather_rows(self, states, idx):
+        return states[idx]
+
+
+def _worker(rank, world, port, case, q):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle
+        from paper_2109_13504_b200.distributed import ShardedResampler
+        from paper_2109_13504_b200.resample import WarpConfig
+
+        kind, n_local, y, prec, rng, b = case
+        n = n_local * world
+        w_full = oracle.gen_gaussian_weights(y, n, 4242, prec)
+        w_local = torch.from_numpy(w_full[rank * n_local:(rank + 1) * n_local].copy())
+        sr = ShardedResampler(kind=kind, warp=WarpConfig(), partition_bytes=128 if kind in ("c1", "c2") else None,
+                              rng=rng, ops=OracleOps())
+        anc_local, b_used = sr.resample(w_local, b=b, seed=99)
+        # every rank derived the same B
+        bt = torch.tensor([b_used])
+        bs = [torch.zeros(1, dtype=bt.dtype) for _ in range(world)]
+        dist.all_gather(bs, bt)
+        parts = [torch.zeros(n_local, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(parts, anc_local)
+        # state exchange: states are (value, index) rows
+        states_full = np.stack([np.arange(n, dtype=np.float64) * 1.5, np.arange(n, dtype=np.float64)], axis=1)
+        s_local = torch.from_numpy(states_full[rank * n_local:(rank + 1) * n_local].copy())
+        new_local = sr.exchange(s_local, anc_local)
+        news = [torch.zeros_like(new_local) for _ in range(world)]
+        dist.all_gather(news, new_local)
+        if rank == 0:
+            q.put((int(b_used), [int(x) for x in bs], torch.cat(parts).numpy(), torch.cat(news).numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, case):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("case", [
+    ("megopolis", 512, 3.0, "single", "megores", None),
+    ("megopolis", 256, 1.0, "double", "philox", 9),
+    ("metropolis", 320, 2.0, "single", "megores", 7),
+    ("c1", 256, 4.0, "single", "megores", None),
+    ("c2", 256, 0.0, "single", "philox", 5),
+])
+def test_sharded_equals_single_process(oracle, world, case):
+    kind, n_local, y, prec, rng, b = case
+    b_used, bs, anc, states = _run(world, case)
+    n = n_local * world
+    w_full = oracle.gen_gaussian_weights(y, n, 4242, prec)
+    if b is None:
+        mean, mx = oracle.weight_mean_max(w_full)
+        assert b_used == oracle.compute_iterations(0.01, mean, mx)
+    assert bs == [b_used] * world
+    ref = oracle.resample(kind, w_full, b_used, 99, 32, 128 if kind in ("c1", "c2") else None, True, rng)
+    assert np.array_equal(anc, ref)
+    states_full = np.stack([np.arange(n) * 1.5, np.arange(n)], axis=1)
+    assert np.array_equal(states, states_full[ref])

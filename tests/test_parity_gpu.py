@@ -364,3 +364,46 @@ def test_device_weight_generator(mg, oracle):
         assert np.allclose(wv.values.cpu().numpy(), host, rtol=1e-13, atol=0)
         w32 = mg.gen_gaussian_weights(mg.GaussianWeightParams(y, n), 123, "single")
         assert (w32.values.cpu().numpy() != host.astype(np.float32)).mean() < 1e-3
+
+
+def test_gather_from_peers_kernel(mg):
+    """mgp_gather_peers with 4 'peer' shards living on this device (pointer table)."""
+    from paper_2109_13504_b200.distributed import gather_from_peers
+
+    rr = np.random.default_rng(9)
+    n_local, world = 1000, 4
+    for shape, dt in [((3,), np.float32), ((), np.float64), ((5,), np.uint8)]:
+        full = (rr.random((n_local * world,) + shape) * 100).astype(dt)
+        shards = [torch.from_numpy(full[r * n_local:(r + 1) * n_local].copy()).cuda() for r in range(world)]
+        anc = rr.integers(0, n_local * world, 2500)
+        out = gather_from_peers(shards, n_local, torch.from_numpy(anc))
+        assert np.array_equal(out.cpu().numpy(), full[anc])
+
+
+def test_sharded_resampler_cuda_ops_single_rank(mg, oracle):
+    """ShardedResampler through CudaOps on one rank (gloo group of size 1)."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2109_13504_b200.distributed import ShardedResampler
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        w = oracle.gen_gaussian_weights(2.0, 1 << 16, 5, "single")
+        sr = ShardedResampler()
+        anc, b = sr.resample(torch.from_numpy(w).cuda(), seed=31)
+        mean, mx = oracle.weight_mean_max(w)
+        assert b == oracle.compute_iterations(0.01, mean, mx)
+        assert np.array_equal(anc.cpu().numpy(), oracle.megopolis(w, b, seed=31))
+        st = torch.arange(1 << 16, dtype=torch.float64, device="cuda")
+        assert torch.equal(sr.exchange(st, anc), st[anc])
+    finally:
+        dist.destroy_process_group()
