@@ -118,8 +118,12 @@ __global__ void __launch_bounds__(RS_THREADS) k_megopolis_w32(const __grid_const
       if (accept_w<NOZERO>(u, wk, wj)) { wk = wj; bstar = t; }
     }
   } else {
-    // philox: draw t = b0 + t; block (t >> 2), word (t & 3); b0 % 4 == 0.
-    for (int t0 = 0; t0 < a.cnt; t0 += 4) {
+    // philox: draw t = b0 + t; block (t >> 2), word (t & 3); b0 % 4 == 0.  Full groups of
+    // four draws run unguarded; the state weight is kept in float64 (the conversion pipe,
+    // not the ALU, is this variant's scarce resource).
+    double wkd = (double)wk;
+    const int full = a.cnt & ~3;
+    auto group = [&](int t0, int lim) {
       uint32_t c0 = i, c1 = 0, c2 = (uint32_t)((a.b0 + t0) >> 2), c3 = 0;
 #pragma unroll
       for (int r = 0; r < 10; ++r) {
@@ -133,15 +137,18 @@ __global__ void __launch_bounds__(RS_THREADS) k_megopolis_w32(const __grid_const
       const uint32_t wd[4] = {c0, c1, c2, c3};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int t = t0 + q;
-        if (t < a.cnt) {
-          const uint2 o = oc.o[t];
-          const WT wj = wfetch<WT, TEX>(w, a.tex, mego_j<POW2>(i_al, lane, o, n));
-          const double u = u32_exact(wd[q]);
-          if (accept_w<NOZERO>(u, wk, wj)) { wk = wj; bstar = t; }
+        if (q < lim) {
+          const int t = t0 + q;
+          const WT wj = wfetch<WT, TEX>(w, a.tex, mego_j<POW2>(i_al, lane, oc.o[t], n));
+          const double wjd = (double)wj;
+          const bool le = u32_exact(wd[q]) * wkd <= wjd;
+          const bool acc = NOZERO ? le : (le && !(wj == (WT)0 && wkd == 0.0));
+          if (acc) { wkd = wjd; bstar = t; }
         }
       }
-    }
+    };
+    for (int t0 = 0; t0 < full; t0 += 4) group(t0, 4);
+    if (full < a.cnt) group(full, a.cnt - full);
   }
   if (bstar >= 0) k = mego_j<POW2>(i_al, lane, oc.o[bstar], n);
   if (a.last) a.anc[i] = (int64_t)k;
