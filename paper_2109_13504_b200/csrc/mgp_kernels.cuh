@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_megopolis_w32(const __grid_const
           const int t = t0 + q;
           const WT wj = wfetch<WT, TEX>(w, a.tex, mego_j<POW2>(i_al, lane, oc.o[t], n));
           const double wjd = (double)wj;
-          const bool le = u32_exact(wd[q]) * wkd <= wjd;
+          const bool le = ((double)wd[q] * 0x1p-32) * wkd <= wjd;  // I2F (conversion pipe) + exact DMUL
           const bool acc = NOZERO ? le : (le && !(wj == (WT)0 && wkd == 0.0));
           if (acc) { wkd = wjd; bstar = t; }
         }
