@@ -54,7 +54,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="particles per GPU")
-    ap.add_argument("--rng", default="megores", choices=["megores", "philox"])
+    ap.add_argument("--rng", default="philox", choices=["megores", "philox"],
+                    help="headline stream; the other one is measured too and reported under 'streams'")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quality-runs", type=int, default=8)
@@ -133,18 +134,18 @@ class ClockSampler:
 # reference arm: the CPU oracle port (oracle/), all host threads
 
 
-def cpu_rate(oracle, w, b, budget_s, nthreads):
+def cpu_rate(oracle, w, b, budget_s, nthreads, rng):
     """Particles/s of the oracle on a bounded prefix sample of the workload."""
     n = len(w)
-    p = 4096
+    p = 16384
     t0 = time.perf_counter()
-    oracle.megopolis(w, b, seed=RUN_SEED, threads=nthreads, p0=0, p1=p)
+    oracle.megopolis(w, b, seed=RUN_SEED, threads=nthreads, p0=0, p1=p, rng=rng)
     dt = time.perf_counter() - t0
     rate = p / max(dt, 1e-6)
     p = int(min(n, max(4096, rate * budget_s)))
     p -= p % 32
     t0 = time.perf_counter()
-    oracle.megopolis(w, b, seed=RUN_SEED, threads=nthreads, p0=0, p1=p)
+    oracle.megopolis(w, b, seed=RUN_SEED, threads=nthreads, p0=0, p1=p, rng=rng)
     dt = time.perf_counter() - t0
     return p / dt, p, dt
 
@@ -173,21 +174,21 @@ def run_reference(args):
     b = oracle.compute_iterations(EPS, mean, mx)
     threads = oracle.num_threads()
     per_step_budget = max(2.0, min(15.0, 150.0 / max(1, args.steps + args.warmup)))
-    rate, p, dt = cpu_rate(oracle, w, b, per_step_budget, threads)
+    rate, p, dt = cpu_rate(oracle, w, b, per_step_budget, threads, args.rng)
     times = []
     for s in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        oracle.megopolis(w, b, seed=RUN_SEED, threads=threads, p0=0, p1=p)
+        oracle.megopolis(w, b, seed=RUN_SEED, threads=threads, p0=0, p1=p, rng=args.rng)
         if s >= args.warmup:
             times.append(time.perf_counter() - t0)
     t = statistics.median(times)
     value = p / t
     sample = f"particles [0, {p}) of N={n} (y=4, B={b}), {args.steps} steps of {t:.2f}s"
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": 0,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3 * n / p,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"megopolis N=2^{int(math.log2(n))} y=4 f32 weights B={b} eps=0.01 megores stream",
+        "config": {"workload": f"megopolis N=2^{int(math.log2(n))} y=4 f32 weights B={b} eps=0.01 {args.rng} stream",
                    "N": n, "B": b},
         "cpu_baseline": {"value": value, "unit": "particles/s", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "particles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -219,7 +220,6 @@ def main():
     L = _lib.lib()
     n_loc = args.n
     n_glob = n_loc * world
-    rng_id = _lib.RNG[args.rng]
 
     # weights: each rank generates its slice of the global population (device generator,
     # same per-particle stream as the reference generator) then all-gathers.
@@ -241,71 +241,84 @@ def main():
         if world > 1:
             dist.all_gather_into_tensor(full, local_w)
 
-    def step(ev=None):
-        """One hot-path pass: (all-gather) -> stats -> B -> megopolis(slice)."""
-        gather_weights()
-        _lib.check(L.mgp_weight_stats(D.ptr(full), 0, n_glob, D.ptr(stats), sp))
-        host = stats.cpu().numpy()  # 64 B; the reference also derives B on the host
-        mean, mx = float(host[1]), float(host[2])
-        b = mg.compute_iterations(EPS, mean, mx).b
-        flags = _lib.FLAG_NONZERO if host.view(np.int64)[4] == 0 else 0
-        if ev is not None:
-            ev[0].record(stream)
-            ev[2].record(stream)
-        _lib.check(L.mgp_resample_range(_lib.KIND["megopolis"], D.ptr(full), 0, n_glob, b, RUN_SEED, 32, 0, 1,
-                                         rng_id, flags, rank * n_loc, (rank + 1) * n_loc, D.ptr(anc), sp))
-        if ev is not None:
-            ev[1].record(stream)
-        return b
+    def measure(rng_id):
+        """W warm-up + K timed steps of the hot path for one random stream."""
+        nonlocal_b = [0]
 
-    # warm-up
-    for _ in range(max(args.warmup, 3)):
-        b = step()
-    torch.cuda.synchronize()
+        def step(ev=None):
+            """One hot-path pass: (all-gather) -> stats -> B -> megopolis(slice)."""
+            gather_weights()
+            _lib.check(L.mgp_weight_stats(D.ptr(full), 0, n_glob, D.ptr(stats), sp))
+            host = stats.cpu().numpy()  # 64 B; the reference also derives B on the host
+            mean, mx = float(host[1]), float(host[2])
+            b = mg.compute_iterations(EPS, mean, mx).b
+            flags = _lib.FLAG_NONZERO if host.view(np.int64)[4] == 0 else 0
+            if ev is not None:
+                ev[0].record(stream)
+            _lib.check(L.mgp_resample_range(_lib.KIND["megopolis"], D.ptr(full), 0, n_glob, b, RUN_SEED, 32, 0, 1,
+                                             rng_id, flags, rank * n_loc, (rank + 1) * n_loc, D.ptr(anc), sp))
+            if ev is not None:
+                ev[1].record(stream)
+            nonlocal_b[0] = b
 
-    # timed region: K steps, each bracketed by CUDA events; L2 flushed between steps
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    import gc
-
-    gc.collect()
-    gc.disable()
-    with ClockSampler(local) as clk:
-        for s in range(args.steps):
-            flush.fill_(float(s))
-            starts[s].record(stream)
-            b = step(kev[s])
-            ends[s].record(stream)
+        for _ in range(max(args.warmup, 3)):
+            step()
         torch.cuda.synchronize()
-    gc.enable()
-    if world > 1:
-        dist.barrier()
-    step_ms = [starts[s].elapsed_time(ends[s]) for s in range(args.steps)]
-    kern_ms = [kev[s][0].elapsed_time(kev[s][1]) for s in range(args.steps)]
-    pre_ms = [starts[s].elapsed_time(kev[s][2]) for s in range(args.steps)]
-    t_total = sum(step_ms)
-    if world > 1:
-        tt = torch.tensor([t_total], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_total = float(tt.item())
-    ms_per_step = t_total / args.steps
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        import gc
+
+        gc.collect()
+        gc.disable()
+        with ClockSampler(local) as clk:
+            for s in range(args.steps):
+                flush.fill_(float(s))
+                starts[s].record(stream)
+                step(kev[s])
+                ends[s].record(stream)
+            torch.cuda.synchronize()
+        gc.enable()
+        if world > 1:
+            dist.barrier()
+        step_ms = [starts[s].elapsed_time(ends[s]) for s in range(args.steps)]
+        kern_ms = [kev[s][0].elapsed_time(kev[s][1]) for s in range(args.steps)]
+        t_total = sum(step_ms)
+        if world > 1:
+            tt = torch.tensor([t_total], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_total = float(tt.item())
+        return {"b": nonlocal_b[0], "ms_per_step": t_total / args.steps, "step_ms": step_ms, "kern_ms": kern_ms,
+                "clocks": clk.summary()}
+
+    res = {}
+    other = "megores" if args.rng == "philox" else "philox"
+    for name in (args.rng, other):
+        res[name] = measure(_lib.RNG[name])
+    head = res[args.rng]
+    b = head["b"]
+    ms_per_step = head["ms_per_step"]
     value = n_glob / (ms_per_step / 1e3)  # all ranks' particles per second
     launches = args.steps * (2 + math.ceil(b / 1024))  # stats (2 kernels) + megopolis launches
 
     # roofline: algorithmic bytes of one Megopolis launch (SURVEY 8d): N*B*4 + N*4 + N*8 + 8*B
-    kern_avg = statistics.mean(kern_ms) / 1e3
     alg_bytes = n_loc * b * 4 + n_loc * 4 + n_loc * 8 + 8 * b
     peak, peak_src = load_peaks()
-    achieved = alg_bytes / kern_avg / 1e9
+
+    def roof(r):
+        kavg = statistics.mean(r["kern_ms"]) / 1e3
+        ach = alg_bytes / kavg / 1e9
+        return ach, kavg
+
+    achieved, kern_avg = roof(head)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "megopolis_traffic.json")) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+            traffic = json.load(f).get(args.rng, {}).get("dram_bytes_per_launch")
     except Exception:
         pass
 
@@ -316,25 +329,31 @@ def main():
         h_anc = torch.empty(n_loc, dtype=torch.int64).pin_memory()
         bu = ctypes.c_int32(0)
 
-        def e2e_step():
-            _lib.check(L.mgp_resample_host(_lib.KIND["megopolis"], D.ptr(h_w), 0, n_loc, 0, EPS, RUN_SEED, 32, 0, 1,
-                                           rng_id, D.ptr(h_anc), ctypes.byref(bu), local))
+        def e2e_time(rid):
+            def e2e_step():
+                _lib.check(L.mgp_resample_host(_lib.KIND["megopolis"], D.ptr(h_w), 0, n_loc, 0, EPS, RUN_SEED, 32, 0,
+                                               1, rid, D.ptr(h_anc), ctypes.byref(bu), local))
 
-        for _ in range(3):
-            e2e_step()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        reps = max(3, min(args.steps, 10))
-        for _ in range(reps):
-            e2e_step()
-        te = (time.perf_counter() - t0) / reps
-        if world > 1:
-            tt = torch.tensor([te], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            te = float(tt.item())
+            for _ in range(3):
+                e2e_step()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            reps = max(3, min(args.steps, 10))
+            for _ in range(reps):
+                e2e_step()
+            te = (time.perf_counter() - t0) / reps
+            if world > 1:
+                tt = torch.tensor([te], dtype=torch.float64, device=dev)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                te = float(tt.item())
+            return te
+
+        te = e2e_time(_lib.RNG[args.rng])
         e2e = {"value": n_loc * world / te, "unit": "particles/s", "h2d_bytes_per_step": 4 * n_loc,
                "d2h_bytes_per_step": 8 * n_loc, "ms_per_step": te * 1e3, "B": int(bu.value),
                "path": "mgp_resample_host (pinned host weights -> device -> pinned host ancestors)"}
+        te_o = e2e_time(_lib.RNG[other])
+        res[other]["e2e"] = {"value": n_loc * world / te_o, "ms_per_step": te_o * 1e3}
 
     # quality (offspring MSE / bias, M/metrics.py) outside the timed region, rank 0
     quality = None
@@ -343,7 +362,7 @@ def main():
         wv = mg.WeightVector(full, "single")
         for kind in ("megopolis", "metropolis"):
             acc = mg.QualityAccumulator(n_glob)
-            fn = mg.make_resampler(kind)
+            fn = mg.make_resampler(kind, rng=args.rng)
             for k in range(args.quality_runs):
                 acc.add(mg.ancestors_to_offspring(fn(wv, b, mg.derive_seed(2002, k)), n_glob), wv)
             st = acc.finalize()
@@ -355,10 +374,10 @@ def main():
         from oracle import oracle
 
         w_np = full[:n_loc].cpu().numpy() if world == 1 else local_w.cpu().numpy()
-        rate, p, dt = cpu_rate(oracle, w_np, b, 12.0, oracle.num_threads())
+        rate, p, dt = cpu_rate(oracle, w_np, b, 12.0, oracle.num_threads(), args.rng)
         cpu = {"value": rate, "unit": "particles/s", "cores": oracle.num_threads(), "kind": "port",
-               "sample": f"oracle/mgp_oracle.c megopolis, particles [0, {p}) of the same N=2^24 y=4 B={b} "
-                         f"workload, {dt:.1f}s"}
+               "sample": f"oracle/mgp_oracle.c megopolis ({args.rng} stream), particles [0, {p}) of the same "
+                         f"N=2^24 y=4 B={b} workload, {dt:.1f}s"}
 
     if rank == 0:
         line = {
@@ -380,9 +399,15 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
-            "step_breakdown_ms": {"step": [round(x, 3) for x in step_ms], "kernel": [round(x, 3) for x in kern_ms],
-                                  "stats_and_host_B": [round(x, 3) for x in pre_ms]},
-            "clocks": clk.summary(),
+            "step_breakdown_ms": {"step": [round(x, 3) for x in head["step_ms"]],
+                                  "kernel": [round(x, 3) for x in head["kern_ms"]]},
+            "clocks": head["clocks"],
+            "streams": {k: {"value": n_glob / (r["ms_per_step"] / 1e3), "ms_per_step": r["ms_per_step"],
+                            "kernel_ms": roof(r)[1] * 1e3, "roofline_frac": roof(r)[0] / peak,
+                            "e2e": r.get("e2e"), "clocks": r["clocks"],
+                            "parity": ("bit-exact vs the unmodified reference (golden vectors)" if k == "megores"
+                                       else "bit-exact vs the reference-side CPU harness (oracle/, Philox)")}
+                        for k, r in res.items()},
             "quality": quality,
         }
         print(json.dumps(line), flush=True)

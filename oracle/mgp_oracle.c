@@ -113,7 +113,50 @@ static int64_t philox_uint_below(uint64_t seed, uint64_t lane, uint64_t t, int64
     return (int64_t)(((uint64_t)mgo_philox_word(seed, lane, t) * (uint64_t)n) >> 32);
 }
 
-/* stream dispatch */
+/* Stream dispatch with a per-thread draw context: the megores key base
+ * mix(seed + M_LANE) is computed once (M/rng.py:95 recomputes it per call; the
+ * value is identical), and the last Philox block is cached (one block serves four
+ * consecutive draws).  Results are identical to the per-call functions above. */
+typedef struct {
+    int rng;
+    uint64_t seed, base;
+    uint64_t blk_lane, blk_idx;
+    int blk_valid;
+    uint32_t blk[4];
+} draw_ctx;
+
+static inline void ctx_init(draw_ctx *c, int rng, uint64_t seed) {
+    c->rng = rng; c->seed = seed; c->base = mgo_mix(seed + M_LANE); c->blk_valid = 0;
+}
+
+static inline uint64_t ctx_hash(const draw_ctx *c, uint64_t lane, uint64_t ctr) {
+    return mgo_mix(c->base + lane * M_LANE + ctr * M_CTR);
+}
+
+static inline uint32_t ctx_word(draw_ctx *c, uint64_t lane, uint64_t t) {
+    uint64_t b = t >> 2;
+    if (!c->blk_valid || c->blk_lane != lane || c->blk_idx != b) {
+        uint32_t key[2] = {(uint32_t)c->seed, (uint32_t)(c->seed >> 32)};
+        uint32_t ctr[4] = {(uint32_t)lane, (uint32_t)(lane >> 32), (uint32_t)b, (uint32_t)(b >> 32)};
+        mgo_philox4x32_10(ctr, key, c->blk);
+        c->blk_lane = lane; c->blk_idx = b; c->blk_valid = 1;
+    }
+    return c->blk[t & 3];
+}
+
+static inline double ctx_u(draw_ctx *c, uint64_t lane, uint64_t ctr) {
+    if (c->rng == 0) return (double)(ctx_hash(c, lane, ctr) >> 11) * INV_2_53;
+    return (double)ctx_word(c, lane, ctr) * (1.0 / 4294967296.0);
+}
+
+static inline int64_t ctx_below(draw_ctx *c, uint64_t lane, uint64_t ctr, int64_t n) {
+    if (c->rng == 0) {
+        int64_t v = (int64_t)((double)(ctx_hash(c, lane, ctr) >> 11) * INV_2_53 * (double)n);
+        return v >= n ? n - 1 : v;
+    }
+    return (int64_t)(((uint64_t)ctx_word(c, lane, ctr) * (uint64_t)n) >> 32);
+}
+
 static inline double draw_u(int rng, uint64_t seed, uint64_t lane, uint64_t ctr) {
     return rng == 0 ? mgo_u01(seed, lane, ctr) : philox_u01(seed, lane, ctr);
 }
@@ -163,32 +206,34 @@ typedef struct {
 
 static void resample_slice(const job_t *J) {
     const int64_t n = J->n, b = J->b, warp = J->warp, n_w = J->n_w, n_part = J->n_part;
-    const uint64_t seed = J->seed;
-    const int rng = J->rng, dtype = J->dtype, kind = J->kind;
+    const int dtype = J->dtype, kind = J->kind;
     const void *w = J->w;
+    draw_ctx C, CW;  /* particle-lane and warp-lane draw contexts */
+    ctx_init(&C, J->rng, J->seed);
+    ctx_init(&CW, J->rng, J->seed);
     for (int64_t i = J->p0; i < J->p1; ++i) {
         uint64_t lane = (uint64_t)i;
         int64_t k = i;
         if (kind == K_METROPOLIS) {
             for (int64_t r = 0; r < b; ++r) {
-                double u = draw_u(rng, seed, lane, (uint64_t)(2 * r));
-                int64_t j = draw_below(rng, seed, lane, (uint64_t)(2 * r + 1), n);
+                double u = ctx_u(&C, lane, (uint64_t)(2 * r));
+                int64_t j = ctx_below(&C, lane, (uint64_t)(2 * r + 1), n);
                 if (accepts(u, wload(w, dtype, k), wload(w, dtype, j))) k = j;
             }
         } else if (kind == K_C1) {
             uint64_t wl = WARP_LANE_BASE + (uint64_t)(i / warp);
-            int64_t lo = draw_below(rng, seed, wl, 0, n_part) * n_w;
+            int64_t lo = ctx_below(&CW, wl, 0, n_part) * n_w;
             for (int64_t r = 0; r < b; ++r) {
-                double u = draw_u(rng, seed, lane, (uint64_t)(2 * r));
-                int64_t j = lo + draw_below(rng, seed, lane, (uint64_t)(2 * r + 1), n_w);
+                double u = ctx_u(&C, lane, (uint64_t)(2 * r));
+                int64_t j = lo + ctx_below(&C, lane, (uint64_t)(2 * r + 1), n_w);
                 if (accepts(u, wload(w, dtype, k), wload(w, dtype, j))) k = j;
             }
         } else if (kind == K_C2) {
             uint64_t wl = WARP_LANE_BASE + (uint64_t)(i / warp);
             for (int64_t r = 0; r < b; ++r) {
-                double u = draw_u(rng, seed, lane, (uint64_t)(2 * r));
-                int64_t p = draw_below(rng, seed, wl, (uint64_t)r, n_part);
-                int64_t j = p * n_w + draw_below(rng, seed, lane, (uint64_t)(2 * r + 1), n_w);
+                double u = ctx_u(&C, lane, (uint64_t)(2 * r));
+                int64_t p = ctx_below(&CW, wl, (uint64_t)r, n_part);
+                int64_t j = p * n_w + ctx_below(&C, lane, (uint64_t)(2 * r + 1), n_w);
                 if (accepts(u, wload(w, dtype, k), wload(w, dtype, j))) k = j;
             }
         } else {
@@ -198,7 +243,7 @@ static void resample_slice(const job_t *J) {
                 int64_t o_al = ob - ob % warp;
                 int64_t o_un = (i + ob) % warp;
                 int64_t j = (i_al + o_al + o_un) % n;
-                double u = draw_u(rng, seed, lane, (uint64_t)r);
+                double u = ctx_u(&C, lane, (uint64_t)r);
                 if (accepts(u, wload(w, dtype, k), wload(w, dtype, j))) k = j;
             }
         }
