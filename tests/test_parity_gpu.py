@@ -407,3 +407,28 @@ def test_sharded_resampler_cuda_ops_single_rank(mg, oracle):
         assert torch.equal(sr.exchange(st, anc), st[anc])
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("rng", ["philox", "megores"])
+def test_config5_2p28_single_gpu(mg, oracle, rng):
+    """N=2^28 (1 GiB f32 weights, beyond L2; config 5 on one GPU): device-generated weights,
+    B from the device stats, oracle bit-exact on particle samples (particles are independent
+    given w, offsets and seed), conservation on the full vector."""
+    n = 1 << 28
+    free, _ = torch.cuda.mem_get_info()
+    if free < 6 * n * 4:
+        pytest.skip("not enough device memory")
+    wv = mg.gen_gaussian_weights(mg.GaussianWeightParams(4.0, n), 777, "single")
+    b = mg.iterations_for(wv, 0.01).b
+    anc = mg.megopolis(wv, b, seed=123, rng=rng)
+    w_np = wv.values.cpu().numpy()
+    mean, mx = oracle.weight_mean_max(w_np)
+    assert b == oracle.compute_iterations(0.01, mean, mx)
+    got = anc.cpu().numpy()
+    for p0 in (0, (n // 2) - 4096, n - 2048):
+        ref = oracle.megopolis(w_np, b, seed=123, rng=rng, p0=p0, p1=p0 + 2048)
+        assert np.array_equal(got[p0:p0 + 2048], ref[p0:p0 + 2048]), p0
+    off = mg.ancestors_to_offspring(anc, n)
+    assert int(off.sum()) == n
+    del anc, off, wv
+    torch.cuda.empty_cache()
