@@ -140,7 +140,10 @@ int pw_reduce(const Elem& e, const WT* wraw, int64_t n, PwOut out, cudaStream_t 
   WStats* cst = nullptr;
   CUDA_TRY(cudaMallocAsync(&heap, sizeof(double) * 2 * nch, st));
   if (STATS) CUDA_TRY(cudaMallocAsync(&cst, sizeof(WStats) * nch, st));
-  k_pw_chunks<Elem, WT, STATS><<<(unsigned)nch, PW_THREADS, 0, st>>>(e, wraw, n, depth, heap, cst);
+  if (n == (int64_t)PW_CHUNK << depth)  // power-of-two N >= 4096: perfect 32-leaf chunk subtrees
+    k_pw_chunks4096<Elem, WT, STATS><<<(unsigned)nch, PW_THREADS, 0, st>>>(e, wraw, depth, heap, cst);
+  else
+    k_pw_chunks<Elem, WT, STATS><<<(unsigned)nch, PW_THREADS, 0, st>>>(e, wraw, n, depth, heap, cst);
   LAUNCH_CHECK("k_pw_chunks");
   k_pw_final<<<1, 1024, 0, st>>>(heap, depth, n, cst, out);
   LAUNCH_CHECK("k_pw_final");

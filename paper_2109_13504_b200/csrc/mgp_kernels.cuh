@@ -83,6 +83,21 @@ __device__ __forceinline__ uint32_t mego_j(uint32_t i_al, uint32_t lane, uint2 o
   }
 }
 
+// Philox4x32-10 block with the round keys from the parameter space (uniform registers)
+__device__ __forceinline__ P4 philox_keys(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                          const uint32_t* pk0, const uint32_t* pk1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t q0 = (uint64_t)PHILOX_M0 * c0, q1 = (uint64_t)PHILOX_M1 * c2;
+    const uint32_t n0 = (uint32_t)(q1 >> 32) ^ c1 ^ pk0[r], n2 = (uint32_t)(q0 >> 32) ^ c3 ^ pk1[r];
+    c1 = (uint32_t)q1;
+    c3 = (uint32_t)q0;
+    c0 = n0;
+    c2 = n2;
+  }
+  return P4{c0, c1, c2, c3};
+}
+
 // exact (double)w * 2^-32 for a 32-bit word: (2^52 + w) * 2^-32 - 2^20 in one DFMA
 __device__ __forceinline__ double u32_exact(uint32_t w) {
   return fma(__hiloint2double(0x43300000, (int)w), 0x1p-32, -0x1p20);
@@ -181,15 +196,21 @@ __global__ void __launch_bounds__(RS_THREADS) k_metropolis(const __grid_constant
       if (accept_w<NOZERO>(u, wk, wj)) { wk = wj; k = j; }
     }
   } else {
-    // u at draw 2b, j at draw 2b+1: one philox block per two rounds.
-    for (int t = 0; t < a.cnt; ++t) {
-      const uint64_t d = 2ull * (uint64_t)(a.b0 + t);
-      const P4 blk = philox_block(a.seed, i, d >> 2);
-      const uint32_t q = (uint32_t)(d & 3);
-      const uint32_t wu = q == 0 ? blk.x : blk.z, wjw = q == 0 ? blk.y : blk.w;
-      const uint32_t j = __umulhi(wjw, n);
-      const WT wj = __ldg(w + j);
-      if (accept_w<NOZERO>((double)wu * 0x1p-32, wk, wj)) { wk = wj; k = j; }
+    // u at draw 2b, j at draw 2b+1: one philox block serves rounds (2m, 2m+1).
+    for (int t = 0; t < a.cnt;) {
+      const uint32_t blkidx = (uint32_t)(((uint64_t)(a.b0 + t) * 2) >> 2);
+      const P4 blk = philox_keys(i, 0, blkidx, 0, a.pk0, a.pk1);
+      const int first_half = ((a.b0 + t) & 1) == 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if ((h == 0 && first_half) || (h == 1 && t < a.cnt)) {
+          const uint32_t wu = h == 0 ? blk.x : blk.z, wjw = h == 0 ? blk.y : blk.w;
+          const uint32_t j = __umulhi(wjw, n);
+          const WT wj = __ldg(w + j);
+          if (accept_w<NOZERO>((double)wu * 0x1p-32, wk, wj)) { wk = wj; k = j; }
+          ++t;
+        }
+      }
     }
   }
   if (a.last) a.anc[i] = (int64_t)k;
@@ -249,19 +270,27 @@ __global__ void __launch_bounds__(RS_THREADS) k_c12_w32(const __grid_constant__ 
       if (accept_w<NOZERO>(u, wk, wj)) { wk = wj; k = lo + jl; }
     }
   } else {
-    for (int t = 0; t < a.cnt; ++t) {
-      if constexpr (C2) {
-        if ((t & 31) == 0)
-          preg = (uint32_t)draw_below<RNG>(a.base, a.seed, wlane, (uint64_t)(a.b0 + t + (int)lane), (int64_t)a.n_part);
-        lo = __shfl_sync(0xffffffffu, preg, t & 31) * n_w;
+    // u at draw 2b, j at draw 2b+1: one philox block serves rounds (2m, 2m+1).
+    for (int t = 0; t < a.cnt;) {
+      const uint32_t blkidx = (uint32_t)(((uint64_t)(a.b0 + t) * 2) >> 2);
+      const P4 blk = philox_keys(i, 0, blkidx, 0, a.pk0, a.pk1);
+      const int first_half = ((a.b0 + t) & 1) == 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if ((h == 0 && first_half) || (h == 1 && t < a.cnt)) {
+          if constexpr (C2) {
+            if ((t & 31) == 0)
+              preg = (uint32_t)draw_below<RNG>(a.base, a.seed, wlane, (uint64_t)(a.b0 + t + (int)lane),
+                                               (int64_t)a.n_part);
+            lo = __shfl_sync(0xffffffffu, preg, t & 31) * n_w;
+          }
+          const uint32_t wu = h == 0 ? blk.x : blk.z, wjw = h == 0 ? blk.y : blk.w;
+          const uint32_t jl = __umulhi(wjw, n_w);
+          const WT wj = (STAGE && !C2) ? part[jl] : __ldg(w + lo + jl);
+          if (accept_w<NOZERO>((double)wu * 0x1p-32, wk, wj)) { wk = wj; k = lo + jl; }
+          ++t;
+        }
       }
-      const uint64_t d = 2ull * (uint64_t)(a.b0 + t);
-      const P4 blk = philox_block(a.seed, i, d >> 2);
-      const uint32_t q = (uint32_t)(d & 3);
-      const uint32_t wu = q == 0 ? blk.x : blk.z, wjw = q == 0 ? blk.y : blk.w;
-      const uint32_t jl = __umulhi(wjw, n_w);
-      const WT wj = (STAGE && !C2) ? part[jl] : __ldg(w + lo + jl);
-      if (accept_w<NOZERO>((double)wu * 0x1p-32, wk, wj)) { wk = wj; k = lo + jl; }
     }
   }
   if (a.last) a.anc[i] = (int64_t)k;
@@ -509,6 +538,63 @@ __global__ void __launch_bounds__(PW_THREADS) k_pw_chunks(Elem e, const WT* wraw
         t.n_nonfinite += s_red[q].n_nonfinite; t.n_notnormal += s_red[q].n_notnormal;
       }
       cstats[blockIdx.x] = t;
+    }
+  }
+}
+
+// Fast path for chunks of exactly 4096 elements (every chunk when N = 4096 * 2^D): the
+// subtree is the perfect binary tree over 32 leaves of 128.  Lane j (0..7) of leaf L owns
+// numpy's accumulator r[j] = sum_q a[L*128 + j + 8q]; the 8-lane shuffle tree forms
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)); the 32 leaf sums are then combined pairwise by one
+// warp -- the same tree, no shared-memory staging, two barriers.
+template <class Elem, typename WT, bool STATS>
+__global__ void __launch_bounds__(PW_THREADS) k_pw_chunks4096(Elem e, const WT* wraw, int depth, double* heap,
+                                                              WStats* cstats) {
+  __shared__ double s_leaf[32];
+  __shared__ WStats s_red[PW_THREADS / 32];
+  const int64_t lo0 = (int64_t)blockIdx.x * PW_CHUNK;
+  const int leaf = threadIdx.x >> 3, jl = threadIdx.x & 7;
+  const int64_t base = lo0 + leaf * 128 + jl;
+  double r = e(base);
+  WStats st{-1.0, 0, 0, 0, 0, 0};
+  if constexpr (STATS) wstat_observe<WT>(st, wraw[base]);
+#pragma unroll
+  for (int q = 1; q < 16; ++q) {
+    r = __dadd_rn(r, e(base + 8 * q));
+    if constexpr (STATS) wstat_observe<WT>(st, wraw[base + 8 * q]);
+  }
+  r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+  r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+  r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+  if (jl == 0) s_leaf[leaf] = r;
+  if constexpr (STATS) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      st.max = fmax(st.max, __shfl_xor_sync(0xffffffffu, st.max, off));
+      st.n_pos += __shfl_xor_sync(0xffffffffu, st.n_pos, off);
+      st.n_zero += __shfl_xor_sync(0xffffffffu, st.n_zero, off);
+      st.n_neg += __shfl_xor_sync(0xffffffffu, st.n_neg, off);
+      st.n_nonfinite += __shfl_xor_sync(0xffffffffu, st.n_nonfinite, off);
+      st.n_notnormal += __shfl_xor_sync(0xffffffffu, st.n_notnormal, off);
+    }
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = st;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = s_leaf[threadIdx.x];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if (threadIdx.x == 0) heap[(1ll << depth) + blockIdx.x] = v;
+    if constexpr (STATS) {
+      if (threadIdx.x == 0) {
+        WStats t = s_red[0];
+        for (int q = 1; q < PW_THREADS / 32; ++q) {
+          t.max = fmax(t.max, s_red[q].max);
+          t.n_pos += s_red[q].n_pos; t.n_zero += s_red[q].n_zero; t.n_neg += s_red[q].n_neg;
+          t.n_nonfinite += s_red[q].n_nonfinite; t.n_notnormal += s_red[q].n_notnormal;
+        }
+        cstats[blockIdx.x] = t;
+      }
     }
   }
 }
