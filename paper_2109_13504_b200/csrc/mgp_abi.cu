@@ -589,7 +589,8 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
   // Overlap the ancestor download with the remaining compute: particle chunks are
   // independent given (w, offsets, seed); each chunk's D2H waits only on its kernel.
   const bool chunkable = !(plan_uses_w32(p) && p.kind == MGP_KIND_MEGOPOLIS && p.b > OFF_CAP);
-  const int64_t nchunk = (chunkable && n >= (1 << 20)) ? 4 : 1;
+  // ~16 chunks of >= 2^20 particles: the D2H tail after the last kernel is ~1/16 of the download
+  const int64_t nchunk = chunkable ? std::max<int64_t>(1, std::min<int64_t>(16, n >> 20)) : 1;
   int64_t step = (n + nchunk - 1) / nchunk;
   step = (step + 255) / 256 * 256;
   for (int64_t c0 = 0; c0 < n; c0 += step) {
