@@ -140,6 +140,25 @@ int mgp_gather(const void *d_states, int64_t row_bytes, const int64_t *d_anc, in
 int mgp_gather_peers(const void *const *peer_states, int npeers, int64_t n_local, int64_t row_bytes,
                      const int64_t *d_anc, int64_t n, void *d_out, void *stream);
 
+/* np.mean of a float64 / float32 vector (numpy pairwise order), e.g. the filter estimate
+ * (M/pfilter.py:162). */
+int mgp_mean(const void *d_x, int dtype, int64_t n, double *d_out, void *stream);
+
+/* SIR particle filter stages (M/pfilter.py:129-165), float64:
+ *   mgp_pf_init: x_i = gaussian_at(seed, i, 0) * sqrt(process_var)          (init_state)
+ *   mgp_pf_predict_update: noise = gaussian_at(seed, i, 0) * sqrt(process_var);
+ *     x' = transition(x, t, noise) with cos_term = 8 cos(1.2 t) (M/pfilter.py:86-89);
+ *     w = max(likelihood(z, x', obs_var), tiny) cast to dtype (M/pfilter.py:92-103). */
+int mgp_pf_init(int64_t n, uint64_t seed, double sqrt_process_var, double *d_x, void *stream);
+int mgp_pf_predict_update(const double *d_x, int64_t n, double cos_term, double sqrt_process_var, uint64_t seed,
+                          double z, double obs_var, int dtype, double *d_xpred, void *d_w, void *stream);
+
+/* estimate_ratio (M/weights.py:134-154) statistics: d_out = {mean, max} (float64) of the
+ * subset formed by the first `subset` entries of the stable argsort of uniform01_at(seed, i, 0)
+ * (the full array when subset == n).  ratio = mean / max is formed by the caller. */
+int mgp_estimate_ratio_stats(const void *d_w, int dtype, int64_t n, int64_t subset, uint64_t seed, double *d_out,
+                             void *stream);
+
 /* gen_gaussian_weights (M/weights.py:100-104) on the device (synthetic inputs) */
 int mgp_gen_gaussian(double y, int64_t n, uint64_t seed, int dtype, void *d_out, void *stream);
 

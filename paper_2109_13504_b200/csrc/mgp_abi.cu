@@ -14,6 +14,7 @@
 #include <mutex>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
 #include <curand_philox4x32_x.h>
 
 #include "megopolis_b200.h"
@@ -721,6 +722,97 @@ int mgp_gather_peers(const void* const* peer_states, int npeers, int64_t n_local
     k_gather_peers<uint8_t><<<grid, 256, 0, st>>>(pt, npeers, n_local, d_anc, n, row_bytes, (uint8_t*)d_out);
   LAUNCH_CHECK("k_gather_peers");
   return 0;
+}
+
+int mgp_mean(const void* d_x, int dtype, int64_t n, double* d_out, void* stream) {
+  if (n < 1) return set_err(MGP_EINVAL, "n must be >= 1");
+  PwOut out{nullptr, d_out, nullptr, nullptr};
+  if (dtype == MGP_F32) {
+    const float* x = (const float*)d_x;
+    return pw_reduce<ElemWeight<float>, float, false>(ElemWeight<float>{x}, x, n, out, S(stream));
+  }
+  if (dtype == MGP_F64) {
+    const double* x = (const double*)d_x;
+    return pw_reduce<ElemWeight<double>, double, false>(ElemWeight<double>{x}, x, n, out, S(stream));
+  }
+  return set_err(MGP_EINVAL, "dtype must be MGP_F32 or MGP_F64");
+}
+
+int mgp_pf_init(int64_t n, uint64_t seed, double sqrt_process_var, double* d_x, void* stream) {
+  if (n < 1) return set_err(MGP_EINVAL, "n_particles must be positive");
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  k_pf_init<<<grid, 256, 0, S(stream)>>>(n, megores_base(seed), sqrt_process_var, d_x);
+  LAUNCH_CHECK("k_pf_init");
+  return 0;
+}
+
+int mgp_pf_predict_update(const double* d_x, int64_t n, double cos_term, double sqrt_process_var, uint64_t seed,
+                          double z, double obs_var, int dtype, double* d_xpred, void* d_w, void* stream) {
+  if (n < 1) return set_err(MGP_EINVAL, "n_particles must be positive");
+  if (!(obs_var > 0)) return set_err(MGP_EINVAL, "obs_var must be positive");
+  const double norm = std::sqrt(2.0 * 3.141592653589793 * obs_var);  // math.sqrt(2.0 * math.pi * obs_var)
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  const uint64_t base = megores_base(seed);
+  if (dtype == MGP_F32)
+    k_pf_predict_update<float><<<grid, 256, 0, S(stream)>>>(d_x, n, cos_term, sqrt_process_var, base, z, obs_var, norm,
+                                                            d_xpred, (float*)d_w);
+  else if (dtype == MGP_F64)
+    k_pf_predict_update<double><<<grid, 256, 0, S(stream)>>>(d_x, n, cos_term, sqrt_process_var, base, z, obs_var, norm,
+                                                             d_xpred, (double*)d_w);
+  else
+    return set_err(MGP_EINVAL, "dtype must be MGP_F32 or MGP_F64");
+  LAUNCH_CHECK("k_pf_predict_update");
+  return 0;
+}
+
+int mgp_estimate_ratio_stats(const void* d_w, int dtype, int64_t n, int64_t subset, uint64_t seed, double* d_out,
+                             void* stream) {
+  if (subset < 1 || subset > n) return set_err(MGP_EINVAL, "subset_size must be in [1, %lld], got %lld", (long long)n,
+                                               (long long)subset);
+  if (dtype != MGP_F32 && dtype != MGP_F64) return set_err(MGP_EINVAL, "dtype must be MGP_F32 or MGP_F64");
+  if (n > MAX_N) return set_err(MGP_EUNSUPPORTED, "N exceeds 2^31-1");
+  ensure_pool();
+  cudaStream_t st = S(stream);
+  mgp_weight_stats_t* ws = nullptr;
+  CUDA_TRY(cudaMallocAsync(&ws, sizeof *ws, st));
+  int rc = 0;
+  if (subset == n) {  // the full array in natural order (M/weights.py:146-147)
+    rc = mgp_weight_stats(d_w, dtype, n, ws, st);
+  } else {
+    uint64_t *k_in = nullptr, *k_out = nullptr;
+    int32_t *i_in = nullptr, *i_out = nullptr;
+    double* sub = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    CUDA_TRY(cudaMallocAsync(&k_in, 8 * n, st));
+    CUDA_TRY(cudaMallocAsync(&k_out, 8 * n, st));
+    CUDA_TRY(cudaMallocAsync(&i_in, 4 * n, st));
+    CUDA_TRY(cudaMallocAsync(&i_out, 4 * n, st));
+    CUDA_TRY(cudaMallocAsync(&sub, 8 * subset, st));
+    const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    k_ratio_keys<<<grid, 256, 0, st>>>(n, megores_base(seed), k_in, i_in);
+    LAUNCH_CHECK("k_ratio_keys");
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, i_in, i_out, (int)n, 0, 53, st));
+    CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, st));
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k_in, k_out, i_in, i_out, (int)n, 0, 53, st));
+    const unsigned g2 = (unsigned)std::min<int64_t>((subset + 255) / 256, 148 * 16);
+    if (dtype == MGP_F32) k_gather_f64<float><<<g2, 256, 0, st>>>((const float*)d_w, i_out, subset, sub);
+    else k_gather_f64<double><<<g2, 256, 0, st>>>((const double*)d_w, i_out, subset, sub);
+    LAUNCH_CHECK("k_gather_f64");
+    rc = mgp_weight_stats(sub, MGP_F64, subset, ws, st);
+    cudaFreeAsync(tmp, st);
+    cudaFreeAsync(sub, st);
+    cudaFreeAsync(i_out, st);
+    cudaFreeAsync(i_in, st);
+    cudaFreeAsync(k_out, st);
+    cudaFreeAsync(k_in, st);
+  }
+  if (!rc) {
+    CUDA_TRY(cudaMemcpyAsync(d_out, &ws->mean, sizeof(double), cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(d_out + 1, &ws->max, sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+  cudaFreeAsync(ws, st);
+  return rc;
 }
 
 int mgp_gen_gaussian(double y, int64_t n, uint64_t seed, int dtype, void* d_out, void* stream) {

@@ -750,4 +750,58 @@ __global__ void k_gen_gaussian(double y, int64_t n, uint64_t seed, WT* out) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// SIR particle filter stages (M/pfilter.py:86-165), float64 like numpy.
+// gaussian_at(seed, i, 0) (M/rng.py:152-161): Box-Muller on salts 0/1.
+
+__device__ __forceinline__ double gaussian_at_dev(uint64_t base, uint64_t i) {
+  const uint64_t x = megores_key(base, i, 0);
+  const uint64_t h1 = mix64(x), h2 = mix64(x + M_SALT);
+  const double u1 = __dmul_rn(__dadd_rn((double)(h1 >> 11), 0.5), 0x1p-53);
+  const double u2 = __dmul_rn((double)(h2 >> 11), 0x1p-53);
+  return __dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(6.283185307179586, u2)));
+}
+
+// init_state (M/pfilter.py:129-133): x_i = gaussian_at(seed_init, i, 0) * sqrt(process_var)
+__global__ void k_pf_init(int64_t n, uint64_t base, double sqrt_pv, double* __restrict__ x) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = __dmul_rn(gaussian_at_dev(base, (uint64_t)i), sqrt_pv);
+}
+
+// stage 1 of sir_step (M/pfilter.py:149-153): process noise, transition (M/pfilter.py:86-89),
+// likelihood with the float64-tiny floor (M/pfilter.py:92-103), cast to the weight precision.
+template <typename WT>
+__global__ void k_pf_predict_update(const double* __restrict__ x, int64_t n, double cos_term, double sqrt_pv,
+                                    uint64_t base, double z, double obs_var, double norm,
+                                    double* __restrict__ xp, WT* __restrict__ w) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = __dmul_rn(gaussian_at_dev(base, (uint64_t)i), sqrt_pv);
+    const double xi = x[i];
+    // x / 2.0 + 25.0 * x / (1.0 + x * x) + 8.0 * cos(1.2 t) + noise   (left to right)
+    const double a = __dadd_rn(__ddiv_rn(xi, 2.0), __ddiv_rn(__dmul_rn(25.0, xi), __dadd_rn(1.0, __dmul_rn(xi, xi))));
+    const double xn = __dadd_rn(__dadd_rn(a, cos_term), v);
+    xp[i] = xn;
+    // residual = z - x*x/20; exp(-0.5 * r * r / obs_var) / sqrt(2 pi obs_var); max(., tiny)
+    const double r = __dsub_rn(z, __ddiv_rn(__dmul_rn(xn, xn), 20.0));
+    double dens = __ddiv_rn(exp(__ddiv_rn(__dmul_rn(__dmul_rn(-0.5, r), r), obs_var)), norm);
+    dens = dens > 2.2250738585072014e-308 ? dens : 2.2250738585072014e-308;
+    w[i] = (WT)dens;
+  }
+}
+
+// estimate_ratio subset (M/weights.py:134-154): keys = the 53-bit draw of uniform01_at(seed, i, 0)
+// (a stable radix sort by key reproduces np.argsort(kind="stable")); gather w in that order.
+__global__ void k_ratio_keys(int64_t n, uint64_t base, uint64_t* __restrict__ keys, int32_t* __restrict__ idx) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = mix64(megores_key(base, (uint64_t)i, 0)) >> 11;
+    idx[i] = (int32_t)i;
+  }
+}
+
+template <typename WT>
+__global__ void k_gather_f64(const WT* __restrict__ w, const int32_t* __restrict__ idx, int64_t m, double* __restrict__ out) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x)
+    out[q] = (double)w[idx[q]];
+}
+
 }  // namespace mgp

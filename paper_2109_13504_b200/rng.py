@@ -27,3 +27,40 @@ def derive_seed(seed, *parts) -> int:
     for p in parts:
         h = _mix(h ^ (((int(p) & _MASK) * _M_CTR + _M_SALT) & _MASK))
     return h
+
+
+# ---------------------------------------------------------------------------
+# Host (numpy) draws for the small host-side sequences of the filter harness
+# (trajectory noise, M/pfilter.py:106-126).  The per-particle draws run on the
+# device (csrc/mgp_kernels.cuh gaussian_at_dev).
+
+
+def _hash_np(seed, lane, counter, salt=0):  # M/rng.py:73-82
+    import numpy as np
+
+    m1, m2 = np.uint64(0xBF58476D1CE4E5B9), np.uint64(0x94D049BB133111EB)
+
+    def mix(x):
+        x = (x ^ (x >> np.uint64(30))) * m1
+        x = (x ^ (x >> np.uint64(27))) * m2
+        return x ^ (x >> np.uint64(31))
+
+    with np.errstate(over="ignore"):
+        base = mix(np.uint64(int(seed) & _MASK) + np.uint64(_M_LANE))
+        x = (base + np.asarray(lane, dtype=np.uint64) * np.uint64(_M_LANE)
+             + np.asarray(counter, dtype=np.uint64) * np.uint64(_M_CTR)
+             + np.asarray(salt, dtype=np.uint64) * np.uint64(_M_SALT))
+        return mix(x)
+
+
+def gaussian_at(seed, lane, counter, mean=0.0, stddev=1.0):  # M/rng.py:152-161
+    import numpy as np
+
+    if stddev < 0:
+        raise ValueError(f"stddev must be >= 0, got {stddev}")
+    h1 = _hash_np(seed, lane, counter, 0)
+    h2 = _hash_np(seed, lane, counter, 1)
+    u1 = ((h1 >> np.uint64(11)).astype(np.float64) + 0.5) * (1.0 / 9007199254740992.0)
+    u2 = (h2 >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+    z = np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * np.pi * u2)
+    return mean + stddev * z

@@ -1,0 +1,118 @@
+"""SIR particle filter on the B200 (paper_2109_13504_b200.pfilter) against golden data from
+the unmodified reference (tests/golden/make_golden_pf.py; M/pfilter.py).
+
+exp/log/cos on the device come from libdevice, not the host libm, so float64 particle values
+may differ in the last bit: stage outputs are compared to 1e-12 relative, the float32 weights
+and the estimate_ratio statistics (sort + pairwise mean, no transcendental) exactly, and the
+filter estimates / benchmark RMSE within tolerance."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.fixture(scope="module")
+def pf():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2109_13504_b200 import pfilter
+
+    return pfilter
+
+
+@pytest.fixture(scope="module")
+def g():
+    z = np.load(os.path.join(HERE, "golden", "pf_golden.npz"))
+    with open(os.path.join(HERE, "golden", "pf_golden.json")) as f:
+        return z, json.load(f)
+
+
+def test_host_helpers_match_reference(pf, g):
+    z, _ = g
+    t = pf.generate_trajectory(20, 0.0, 7)
+    assert np.array_equal(t.truth, z["traj_truth"]) and np.array_equal(t.observations, z["traj_obs"])
+    assert pf.transition(0.0, 1) == pytest.approx(8 * np.cos(1.2))
+    assert pf.likelihood(5.0, 10.0) == pytest.approx(0.39894, abs=1e-5)
+    with pytest.raises(ValueError):
+        pf.FilterConfig(n_particles=0)
+    with pytest.raises(ValueError):
+        pf.Trajectory(np.zeros(3), np.zeros(4))
+
+
+def test_init_and_predict_update(pf, g):
+    from paper_2109_13504_b200 import _device as D
+    from paper_2109_13504_b200 import _lib
+
+    z, _ = g
+    cfg = pf.FilterConfig(n_particles=2**12)
+    st = pf.init_state(cfg, 5)
+    x0 = st.particles.cpu().numpy()
+    assert np.allclose(x0, z["init_particles"], rtol=1e-12, atol=0)
+    assert (x0 == z["init_particles"]).mean() > 0.99
+    # one predict/update from the reference's own initial cloud
+    x = torch.from_numpy(z["init_particles"]).cuda()
+    xp = torch.empty_like(x)
+    w = torch.empty(x.numel(), dtype=torch.float32, device="cuda")
+    from paper_2109_13504_b200.rng import derive_seed
+
+    _lib.check(_lib.lib().mgp_pf_predict_update(D.ptr(x), x.numel(), 8.0 * np.cos(1.2 * 1), np.sqrt(10.0),
+                                                derive_seed(5, 2, 1), float(z["traj_obs"][0]), 1.0, 0, D.ptr(xp),
+                                                D.ptr(w), D.stream_ptr()))
+    assert np.allclose(xp.cpu().numpy(), z["step1_pred"], rtol=1e-12, atol=1e-12)
+    assert (w.cpu().numpy() == z["step1_w"]).mean() > 0.999
+
+
+def test_estimate_ratio_exact(pf, g):
+    """Sorted subset + numpy pairwise mean: bit-identical to megores.estimate_ratio."""
+    z, meta = g
+    for r in meta["ratios"]:
+        w = torch.from_numpy(z[r.get("w", "step1_w")]).cuda()
+        out = torch.empty(2, dtype=torch.float64, device="cuda")
+        from paper_2109_13504_b200 import _device as D
+        from paper_2109_13504_b200 import _lib
+
+        _lib.check(_lib.lib().mgp_estimate_ratio_stats(D.ptr(w), 0, w.numel(), r["subset"], r["seed"], D.ptr(out),
+                                                       D.stream_ptr()))
+        mean, mx = out.cpu().numpy()
+        assert mean / mx == r["ratio"], r
+
+
+def test_run_filter_matches_reference(pf, g):
+    z, meta = g
+    traj = pf.Trajectory(z["traj_truth"], z["traj_obs"])
+    for name, c in meta["runs"].items():
+        cfg = pf.FilterConfig(n_particles=c["n"], resampler=c["resampler"], b_fixed=c["b_fixed"],
+                              partition_bytes=c["partition_bytes"], precision=c["precision"], epsilon=c["epsilon"])
+        est, tm = pf.run_filter(cfg, traj, 42)
+        ref = z[f"est_{name}"]
+        assert np.all(np.isfinite(est)) and tm.stage1 >= 0 and tm.stage2 > 0
+        assert np.allclose(est, ref, rtol=1e-9, atol=1e-9), (name, np.abs(est - ref).max())
+
+
+def test_filter_deterministic(pf, g):
+    z, _ = g
+    traj = pf.Trajectory(z["traj_truth"], z["traj_obs"])
+    cfg = pf.FilterConfig(n_particles=2**10, resampler="c2", partition_bytes=128, b_fixed=8)
+    e1, _ = pf.run_filter(cfg, traj, 3)
+    e2, _ = pf.run_filter(cfg, traj, 3)
+    assert np.array_equal(e1, e2)
+
+
+def test_benchmark_rmse(pf, g):
+    from paper_2109_13504_b200.rng import derive_seed
+
+    _, meta = g
+    trajs = [pf.generate_trajectory(30, 0.0, derive_seed(1100, i)) for i in range(2)]
+    rows = pf.run_benchmark(pf.FilterConfig(n_particles=2**14), trajs, 4, [16, 64], [("megopolis", None), ("c1", 128)],
+                            derive_seed(1101))
+    for r, ref in zip(rows, meta["bench_rows"]):
+        assert (r["algorithm"], r["b"]) == (ref["algorithm"], ref["b"])
+        assert abs(r["rmse"] - ref["rmse"]) <= 1e-6 * ref["rmse"], (r, ref)
+        assert 0.0 < r["resample_ratio"] < 1.0
