@@ -43,6 +43,59 @@ __global__ void __launch_bounds__(256) k_vw(const __grid_constant__ ResampleArgs
   a.anc[i] = (int64_t)k;
 }
 
+
+// Philox, two particles per thread (i and i + 128 of a 256-particle block): two independent
+// Philox chains interleaved per thread.
+template <int PPT>
+__global__ void __launch_bounds__(256 / PPT) k_vp2(const __grid_constant__ ResampleArgs a, const __grid_constant__ OffChunk oc) {
+  const uint32_t blk = a.p0 + blockIdx.x * 256;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t cmask = (a.n - 1) & ~31u;
+  uint32_t ii[PPT], ial[PPT];
+  double wkd[PPT];
+  int bstar[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    ii[p] = blk + threadIdx.x + p * (256 / PPT);
+    ial[p] = ii[p] - lane;
+    wkd[p] = (double)tex1Dfetch<float>(a.tex, (int)ii[p]);
+    bstar[p] = -1;
+  }
+  const int full = a.cnt & ~3;
+  for (int t0 = 0; t0 < full; t0 += 4) {
+    uint32_t c0[PPT], c1[PPT], c2[PPT], c3[PPT];
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) { c0[p] = ii[p]; c1[p] = 0; c2[p] = (uint32_t)((a.b0 + t0) >> 2); c3[p] = 0; }
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) {
+        const uint64_t q0 = (uint64_t)PHILOX_M0 * c0[p], q1 = (uint64_t)PHILOX_M1 * c2[p];
+        const uint32_t n0 = (uint32_t)(q1 >> 32) ^ c1[p] ^ a.pk0[r], n2 = (uint32_t)(q0 >> 32) ^ c3[p] ^ a.pk1[r];
+        c1[p] = (uint32_t)q1; c3[p] = (uint32_t)q0; c0[p] = n0; c2[p] = n2;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int t = t0 + q;
+      const uint2 o = oc.o[t];
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) {
+        const uint32_t wd = q == 0 ? c0[p] : q == 1 ? c1[p] : q == 2 ? c2[p] : c3[p];
+        const uint32_t j = mux3(ial[p] + o.x, lane + o.y, cmask);
+        const double wjd = (double)tex1Dfetch<float>(a.tex, (int)j);
+        if (((double)wd * 0x1p-32) * wkd[p] <= wjd) { wkd[p] = wjd; bstar[p] = t; }
+      }
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    uint32_t k = ii[p];
+    if (bstar[p] >= 0) { const uint2 o = oc.o[bstar[p]]; k = mux3(ial[p] + o.x, lane + o.y, cmask); }
+    a.anc[ii[p]] = (int64_t)k;
+  }
+}
+
 template <class K>
 float time_it(K launch, int reps) {
   cudaEvent_t e0, e1;
@@ -110,6 +163,29 @@ int main(int argc, char** argv) {
     printf("%-6s %.3f ms  %.1f Gcmp/s  speedup %.3f  mismatches %zu\n", name, ms, cmp / ms / 1e6, t0 / ms, bad);
     CK(cudaMemset(anc1, 0xff, 8ull * n));
   };
+  {
+    static OffChunk ocp;
+    for (int t = 0; t < B; ++t) {
+      const uint32_t o = (uint32_t)below_from_word(p4_word(philox_block(seed, GLOBAL_OFFSET_LANE, t >> 2), t & 3), n);
+      ocp.o[t] = make_uint2(o & ~31u, o & 31u);
+    }
+    ResampleArgs c = a;
+    uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+    for (int r = 0; r < 10; ++r) { c.pk0[r] = k0; c.pk1[r] = k1; k0 += PHILOX_W0; k1 += PHILOX_W1; }
+    c.anc = anc0;
+    float tp = time_it([&]() { k_megopolis_w32<1, float, true, true, true><<<grid, 256>>>(c, ocp); }, 7);
+    CK(cudaMemcpy(h0.data(), anc0, 8ull * n, cudaMemcpyDeviceToHost));
+    printf("philox lib %.3f ms\n", tp);
+    ResampleArgs d = c; d.anc = anc1;
+    float t1 = time_it([&]() { k_vp2<1><<<grid, 256>>>(d, ocp); }, 7);
+    check("vp2_1", t1);
+    float t2 = time_it([&]() { k_vp2<2><<<grid, 128>>>(d, ocp); }, 7);
+    check("vp2_2", t2);
+    CK(cudaMemcpy(h0.data(), anc0, 8ull * n, cudaMemcpyDeviceToHost));
+  }
+  CK(cudaMemcpy(h0.data(), anc0, 8ull * n, cudaMemcpyDeviceToHost));
+  t0 = time_it([&]() { k_megopolis_w32<0, float, true, true, true><<<grid, 256>>>(a, oc); }, 3);
+  CK(cudaMemcpy(h0.data(), anc0, 8ull * n, cudaMemcpyDeviceToHost));
   check("vw4", time_it([&]() { k_vw<false, 4><<<grid, 256>>>(b, o4); }, 7));
   check("vwt4", time_it([&]() { k_vw<true, 4><<<grid, 256>>>(b, o4); }, 7));
   check("vwt2", time_it([&]() { k_vw<true, 2><<<grid, 256>>>(b, o4); }, 7));
