@@ -110,64 +110,99 @@ __device__ __forceinline__ double u32_exact(uint32_t w) {
 // one DMUL + DSETP, one 32-bit select.  The accepted round index is carried instead
 // of j (j is a pure function of (i, o_b)) and k is rebuilt once at the end.
 
-template <int RNG, typename WT, bool POW2, bool NOZERO, bool TEX>
-__global__ void __launch_bounds__(RS_THREADS) k_megopolis_w32(const __grid_constant__ ResampleArgs a,
-                                                              const __grid_constant__ OffChunk oc) {
-  const uint32_t i = a.p0 + blockIdx.x * RS_THREADS + threadIdx.x;
-  if (i >= a.p_end) return;
+template <int RNG, typename WT, bool POW2, bool NOZERO, bool TEX, int PPT>
+__global__ void __launch_bounds__(RS_THREADS / PPT) k_megopolis_w32(const __grid_constant__ ResampleArgs a,
+                                                                    const __grid_constant__ OffChunk oc) {
+  // PPT particles per thread: i + p*(256/PPT) of this CTA's 256-particle block -- same lane,
+  // different warps, so the lane part of the partner index is shared and the independent
+  // random-stream chains interleave (ILP).  p_end is a multiple of 32: whole warps only.
+  constexpr int STRIDE = RS_THREADS / PPT;
+  const uint32_t i0 = a.p0 + blockIdx.x * RS_THREADS + threadIdx.x;
+  if (i0 >= a.p_end) return;
   const WT* __restrict__ w = reinterpret_cast<const WT*>(a.w);
-  const uint32_t lane = threadIdx.x & 31u, i_al = i - lane, n = a.n;
-  uint32_t k = a.first ? i : (uint32_t)a.kstate[i];
-  WT wk = wfetch<WT, TEX>(w, a.tex, k);
-  int bstar = -1;
+  const uint32_t lane = threadIdx.x & 31u, n = a.n;
+  uint32_t ii[PPT], ial[PPT];
+  bool live[PPT];
+  WT wk[PPT];
+  int bstar[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    ii[p] = i0 + p * STRIDE;
+    live[p] = ii[p] < a.p_end;
+    ial[p] = ii[p] - lane;
+    const uint32_t k0 = live[p] ? (a.first ? ii[p] : (uint32_t)a.kstate[ii[p]]) : 0u;
+    wk[p] = wfetch<WT, TEX>(w, a.tex, k0);
+    bstar[p] = -1;
+  }
   if constexpr (RNG == RNG_MEGORES) {
-    // counter t's key x0 + t*M_CTR is formed with IMAD.WIDE (FMA pipe): the ALU pipe
-    // is the binding one (the splitmix xorshifts)
-    const uint64_t x0 = megores_key(a.base, i, (uint64_t)a.b0);
-#pragma unroll 4
+    uint64_t x[PPT];
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) x[p] = megores_key(a.base, ii[p], (uint64_t)a.b0);
+#pragma unroll(4 / PPT)
     for (int t = 0; t < a.cnt; ++t) {
       const uint2 o = oc.o[t];
-      const WT wj = wfetch<WT, TEX>(w, a.tex, mego_j<POW2>(i_al, lane, o, n));
-      const uint64_t x = x0 + (uint64_t)(uint32_t)t * M_CTR;
-      const double u = (double)mix64_m53(x) * 0x1p-53;  // exact: u01 (M/rng.py:105-108)
-      if (accept_w<NOZERO>(u, wk, wj)) { wk = wj; bstar = t; }
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) {
+        const WT wj = wfetch<WT, TEX>(w, a.tex, mego_j<POW2>(ial[p], lane, o, n));
+        const double u = (double)mix64_m53(x[p]) * 0x1p-53;  // exact: u01 (M/rng.py:105-108)
+        x[p] += M_CTR;
+        if (accept_w<NOZERO>(u, wk[p], wj)) { wk[p] = wj; bstar[p] = t; }
+      }
     }
   } else {
     // philox: draw t = b0 + t; block (t >> 2), word (t & 3); b0 % 4 == 0.  Full groups of
     // four draws run unguarded; the state weight is kept in float64 (the conversion pipe,
     // not the ALU, is this variant's scarce resource).
-    double wkd = (double)wk;
+    double wkd[PPT];
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) wkd[p] = (double)wk[p];
     const int full = a.cnt & ~3;
     auto group = [&](int t0, int lim) {
-      uint32_t c0 = i, c1 = 0, c2 = (uint32_t)((a.b0 + t0) >> 2), c3 = 0;
+      uint32_t c0[PPT], c1[PPT], c2[PPT], c3[PPT];
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) {
+        c0[p] = ii[p]; c1[p] = 0; c2[p] = (uint32_t)((a.b0 + t0) >> 2); c3[p] = 0;
+      }
 #pragma unroll
       for (int r = 0; r < 10; ++r) {
-        const uint64_t q0 = (uint64_t)PHILOX_M0 * c0, q1 = (uint64_t)PHILOX_M1 * c2;
-        const uint32_t n0 = (uint32_t)(q1 >> 32) ^ c1 ^ a.pk0[r], n2 = (uint32_t)(q0 >> 32) ^ c3 ^ a.pk1[r];
-        c1 = (uint32_t)q1;
-        c3 = (uint32_t)q0;
-        c0 = n0;
-        c2 = n2;
+#pragma unroll
+        for (int p = 0; p < PPT; ++p) {
+          const uint64_t q0 = (uint64_t)PHILOX_M0 * c0[p], q1 = (uint64_t)PHILOX_M1 * c2[p];
+          const uint32_t n0 = (uint32_t)(q1 >> 32) ^ c1[p] ^ a.pk0[r], n2 = (uint32_t)(q0 >> 32) ^ c3[p] ^ a.pk1[r];
+          c1[p] = (uint32_t)q1;
+          c3[p] = (uint32_t)q0;
+          c0[p] = n0;
+          c2[p] = n2;
+        }
       }
-      const uint32_t wd[4] = {c0, c1, c2, c3};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         if (q < lim) {
           const int t = t0 + q;
-          const WT wj = wfetch<WT, TEX>(w, a.tex, mego_j<POW2>(i_al, lane, oc.o[t], n));
-          const double wjd = (double)wj;
-          const bool le = ((double)wd[q] * 0x1p-32) * wkd <= wjd;  // I2F (conversion pipe) + exact DMUL
-          const bool acc = NOZERO ? le : (le && !(wj == (WT)0 && wkd == 0.0));
-          if (acc) { wkd = wjd; bstar = t; }
+          const uint2 o = oc.o[t];
+#pragma unroll
+          for (int p = 0; p < PPT; ++p) {
+            const uint32_t wd = q == 0 ? c0[p] : q == 1 ? c1[p] : q == 2 ? c2[p] : c3[p];
+            const WT wj = wfetch<WT, TEX>(w, a.tex, mego_j<POW2>(ial[p], lane, o, n));
+            const double wjd = (double)wj;
+            const bool le = ((double)wd * 0x1p-32) * wkd[p] <= wjd;  // I2F + exact DMUL
+            const bool acc = NOZERO ? le : (le && !(wj == (WT)0 && wkd[p] == 0.0));
+            if (acc) { wkd[p] = wjd; bstar[p] = t; }
+          }
         }
       }
     };
     for (int t0 = 0; t0 < full; t0 += 4) group(t0, 4);
     if (full < a.cnt) group(full, a.cnt - full);
   }
-  if (bstar >= 0) k = mego_j<POW2>(i_al, lane, oc.o[bstar], n);
-  if (a.last) a.anc[i] = (int64_t)k;
-  else a.kstate[i] = (int32_t)k;
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    if (!live[p]) continue;
+    uint32_t k = a.first ? ii[p] : (uint32_t)a.kstate[ii[p]];
+    if (bstar[p] >= 0) k = mego_j<POW2>(ial[p], lane, oc.o[bstar[p]], n);
+    if (a.last) a.anc[ii[p]] = (int64_t)k;
+    else a.kstate[ii[p]] = (int32_t)k;
+  }
 }
 
 // ---------------------------------------------------------------------------
