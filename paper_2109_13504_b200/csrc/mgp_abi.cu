@@ -169,8 +169,14 @@ void offsets_host(uint64_t seed, int64_t n, int32_t b, int rng, int64_t* out) {
 
 // Particles per thread: 2 for the Philox stream (interleaved Philox chains; measured +6.5%),
 // 1 for megores (its ALU-bound splitmix chain gains nothing from more ILP).
+#ifndef MGP_PPT_PHILOX
+#define MGP_PPT_PHILOX 2
+#endif
+#ifndef MGP_PPT_MEGORES
+#define MGP_PPT_MEGORES 1
+#endif
 template <int RNG>
-constexpr int mego_ppt() { return RNG == RNG_PHILOX ? 2 : 1; }
+constexpr int mego_ppt() { return RNG == RNG_PHILOX ? MGP_PPT_PHILOX : MGP_PPT_MEGORES; }
 
 template <int RNG, typename WT, bool POW2, bool NZ, bool TEX>
 int launch_mego_w32(const ResampleArgs& a, const OffChunk& oc, cudaStream_t st) {
