@@ -167,10 +167,11 @@ void offsets_host(uint64_t seed, int64_t n, int32_t b, int rng, int64_t* out) {
 // ---------------------------------------------------------------------------
 // kernel dispatch helpers
 
-// Particles per thread: 2 for the Philox stream (interleaved Philox chains; measured +6.5%),
+// Particles per thread: 4 for the Philox stream (interleaved Philox chains; measured 5.97 -> 5.54 ms
+// at 2^24, PPT 1 -> 4; scripts/mb/ppt_sweep.sh),
 // 1 for megores (its ALU-bound splitmix chain gains nothing from more ILP).
 #ifndef MGP_PPT_PHILOX
-#define MGP_PPT_PHILOX 2
+#define MGP_PPT_PHILOX 4
 #endif
 #ifndef MGP_PPT_MEGORES
 #define MGP_PPT_MEGORES 1
