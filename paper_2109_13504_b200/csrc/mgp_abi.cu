@@ -341,6 +341,7 @@ int run_range(Plan& p, int64_t p0, int64_t p_end, int64_t* anc, cudaStream_t st)
   a.base = megores_base(p.seed);
   a.kstate = p.kstate;
   a.anc = anc;
+  a.one = 1;
   {
     uint32_t k0 = (uint32_t)p.seed, k1 = (uint32_t)(p.seed >> 32);
     for (int r = 0; r < 10; ++r) { a.pk0[r] = k0; a.pk1[r] = k1; k0 += PHILOX_W0; k1 += PHILOX_W1; }

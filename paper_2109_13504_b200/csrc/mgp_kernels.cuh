@@ -40,6 +40,7 @@ struct ResampleArgs {
   int32_t* kstate;   // carried ancestor between launches (B > OFF_CAP)
   int64_t* anc;      // output ancestors
   cudaTextureObject_t tex;  // float32 weights as a 1-D linear texture (0: use LDG)
+  uint32_t one;             // = 1; an opaque multiplier keeps the 64-bit key add on the FMA pipe
   uint32_t pk0[10], pk1[10];  // Philox round keys (uniform; constant bank)
 };
 
@@ -98,6 +99,20 @@ __device__ __forceinline__ P4 philox_keys(uint32_t c0, uint32_t c1, uint32_t c2,
   return P4{c0, c1, c2, c3};
 }
 
+// x + M_CTR computed as IMAD.WIDE.U32(one, M_CTR_lo, x) + IMAD(one, M_CTR_hi, hi): the FMA pipe
+// does the 64-bit add; `one` (== 1) comes from the parameter space so ptxas cannot fold it.
+__device__ __forceinline__ uint64_t add64_fma(uint64_t x, uint32_t one) {
+  uint64_t r;
+  asm("{\n\t.reg .u32 lo, hi;\n\t"
+      "mad.wide.u32 %0, %1, %2, %3;\n\t"
+      "mov.b64 {lo, hi}, %0;\n\t"
+      "mad.lo.u32 hi, %1, %4, hi;\n\t"
+      "mov.b64 %0, {lo, hi};\n\t}"
+      : "=l"(r)
+      : "r"(one), "r"((uint32_t)M_CTR), "l"(x), "r"((uint32_t)(M_CTR >> 32)));
+  return r;
+}
+
 // exact (double)w * 2^-32 for a 32-bit word: (2^52 + w) * 2^-32 - 2^20 in one DFMA
 __device__ __forceinline__ double u32_exact(uint32_t w) {
   return fma(__hiloint2double(0x43300000, (int)w), 0x1p-32, -0x1p20);
@@ -145,7 +160,7 @@ __global__ void __launch_bounds__(RS_THREADS / PPT) k_megopolis_w32(const __grid
       for (int p = 0; p < PPT; ++p) {
         const WT wj = wfetch<WT, TEX>(w, a.tex, mego_j<POW2>(ial[p], lane, o, n));
         const double u = (double)mix64_m53(x[p]) * 0x1p-53;  // exact: u01 (M/rng.py:105-108)
-        x[p] += M_CTR;
+        x[p] = add64_fma(x[p], a.one);  // x += M_CTR on the FMA pipe (the ALU pipe binds)
         if (accept_w<NOZERO>(u, wk[p], wj)) { wk[p] = wj; bstar[p] = t; }
       }
     }
