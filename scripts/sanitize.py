@@ -1,0 +1,38 @@
+"""Small invocations of every kernel family, for compute-sanitizer (memcheck / racecheck / initcheck)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2109_13504_b200 as mg  # noqa: E402
+from paper_2109_13504_b200 import pfilter as pf  # noqa: E402
+from paper_2109_13504_b200.distributed import gather_from_peers  # noqa: E402
+
+rr = np.random.default_rng(0)
+for n, prec in [(4096, "single"), (3 * 1024, "double"), (96, "single"), (33, "single")]:
+    w = rr.random(n).astype(np.float32 if prec == "single" else np.float64)
+    w[::7] = 0
+    wd = mg.WeightVector(torch.from_numpy(w).cuda(), prec)
+    for rng in ("megores", "philox"):
+        if n % 32 == 0:
+            mg.megopolis(wd, 1030, seed=3, rng=rng)
+            mg.metropolis_c1(wd, 9, mg.PartitionConfig(128), seed=3, rng=rng)
+            mg.metropolis_c2(wd, 40, mg.PartitionConfig(256), seed=3, rng=rng)
+        mg.megopolis(wd, 9, mg.WarpConfig(7), seed=3, strict=False, rng=rng)
+        anc = mg.metropolis(wd, 9, 3, rng=rng)
+        mg.ancestors_to_offspring(anc, n)
+        mg.apply_ancestors(torch.arange(n * 3, dtype=torch.float32, device="cuda").reshape(n, 3), anc)
+    mg.iterations_for(wd)
+    acc = mg.QualityAccumulator(n)
+    for k in range(2):
+        acc.add(mg.ancestors_to_offspring(mg.megopolis(wd, 5, mg.WarpConfig(1), seed=k), n), wd)
+    acc.finalize()
+    mg.megopolis(w, 5, mg.WarpConfig(1), seed=1)  # host-buffer path
+shards = [torch.rand(100, 2, device="cuda") for _ in range(4)]
+gather_from_peers(shards, 100, torch.from_numpy(rr.integers(0, 400, 300)))
+traj = pf.generate_trajectory(3, 0.0, 1)
+pf.run_filter(pf.FilterConfig(n_particles=8192, b_fixed=None), traj, 2)
+torch.cuda.synchronize()
+print("sanitize workload done")
