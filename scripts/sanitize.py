@@ -19,7 +19,7 @@ for n, prec in [(4096, "single"), (3 * 1024, "double"), (96, "single"), (33, "si
         if n % 32 == 0:
             mg.megopolis(wd, 1030, seed=3, rng=rng)
             mg.metropolis_c1(wd, 9, mg.PartitionConfig(128), seed=3, rng=rng)
-            mg.metropolis_c2(wd, 40, mg.PartitionConfig(256), seed=3, rng=rng)
+            mg.metropolis_c2(wd, 40, mg.PartitionConfig(256 if n % 64 == 0 else 128), seed=3, rng=rng)
         mg.megopolis(wd, 9, mg.WarpConfig(7), seed=3, strict=False, rng=rng)
         anc = mg.metropolis(wd, 9, 3, rng=rng)
         mg.ancestors_to_offspring(anc, n)
