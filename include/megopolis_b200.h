@@ -49,6 +49,9 @@ enum { MGP_OK = 0, MGP_EINVAL = -1, MGP_EUNSUPPORTED = -2 };
  * (M/resample.py:118-122) can never fire and is compiled out.  Results are
  * identical with or without the flag when it holds. */
 enum { MGP_FLAG_NONZERO = 1 };
+/* MGP_FLAG_NO_STAGE: C1 reads its partition from global memory instead of staging it in shared
+ * memory (a benchmarking knob for SURVEY config 3; results are identical). */
+enum { MGP_FLAG_NO_STAGE = 2 };
 
 /* Weight statistics (device-resident result).  sum/mean are bit-identical to
  * numpy's np.asarray(w, float64).sum()/.mean() (pairwise summation), which feeds

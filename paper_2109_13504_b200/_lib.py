@@ -19,6 +19,7 @@ RNG = {"megores": 0, "philox": 1}
 KIND = {"metropolis": 0, "c1": 1, "c2": 2, "megopolis": 3}
 MGP_EINVAL, MGP_EUNSUPPORTED = -1, -2
 FLAG_NONZERO = 1
+FLAG_NO_STAGE = 2
 
 _lib = None
 _lock = threading.Lock()

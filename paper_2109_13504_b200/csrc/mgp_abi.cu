@@ -234,8 +234,8 @@ int launch_c12(const ResampleArgs& a, cudaStream_t st) {
 }
 
 template <int RNG, typename WT, bool C2>
-int dispatch_c12(const ResampleArgs& a, bool pow2, bool nz, cudaStream_t st) {
-  const bool stage = !C2 && (size_t)(RS_THREADS / 32) * a.n_w * sizeof(WT) <= (size_t)C1_SMEM_MAX;
+int dispatch_c12(const ResampleArgs& a, bool pow2, bool nz, bool no_stage, cudaStream_t st) {
+  const bool stage = !C2 && !no_stage && (size_t)(RS_THREADS / 32) * a.n_w * sizeof(WT) <= (size_t)C1_SMEM_MAX;
 #define C12_CASE(P, Z)                                                        \
   if (pow2 == P && nz == Z) {                                                 \
     if (stage) return launch_c12<RNG, WT, P, Z, C2, !C2>(a, st);              \
@@ -305,6 +305,7 @@ int launch_generic(int kind, GenericArgs ga, cudaStream_t st) {
 struct Plan {
   int kind, dtype, rng;
   bool nz;  // no zero weights (caller asserted MGP_FLAG_NONZERO)
+  bool no_stage = false;  // MGP_FLAG_NO_STAGE
   const void* w;
   int64_t n, n_w, n_part;
   int32_t b, warp;
@@ -380,7 +381,7 @@ int run_range(Plan& p, int64_t p0, int64_t p_end, int64_t* anc, cudaStream_t st)
       const bool pow2 = is_pow2(p.n_w) && p.n_w >= 2;
       a.log2 = ilog2((uint64_t)p.n_w);
       const bool c2 = p.kind == MGP_KIND_C2;
-#define C12_GO(R, T) (c2 ? dispatch_c12<R, T, true>(a, pow2, p.nz, st) : dispatch_c12<R, T, false>(a, pow2, p.nz, st))
+#define C12_GO(R, T) (c2 ? dispatch_c12<R, T, true>(a, pow2, p.nz, p.no_stage, st) : dispatch_c12<R, T, false>(a, pow2, p.nz, p.no_stage, st))
       if (p.rng == MGP_RNG_MEGORES)
         rc = p.dtype == MGP_F32 ? C12_GO(RNG_MEGORES, float) : C12_GO(RNG_MEGORES, double);
       else
@@ -408,6 +409,7 @@ int make_plan(Plan& p, int kind, const void* w, int dtype, int64_t n, int32_t b,
   p.n_w = 0;
   p.n_part = 0;
   p.nz = (flags & MGP_FLAG_NONZERO) != 0;
+  p.no_stage = (flags & MGP_FLAG_NO_STAGE) != 0;
   if (kind == MGP_KIND_MEGOPOLIS) {
     if ((rc = check_warp(n, warp, strict, "megopolis"))) return rc;
     p.off.resize((size_t)b);
