@@ -162,3 +162,45 @@ def test_cpu_only_compute_fails_loudly():
         mg.megopolis(mg.WeightVector(np.ones(64)), 4, seed=0)
     with pytest.raises(RuntimeError, match="CUDA device"):
         mg.ancestors_to_offspring(np.zeros(4, dtype=np.int64))
+
+
+def test_shim_patches_both_namespaces(tmp_path, monkeypatch):
+    """shim.install patches megores.<fn> and megores.resample.<fn> (M/__init__.py:12-28 binds at
+    import; make_resampler resolves resample globals at call time, M/resample.py:441-454).
+    Uses a stand-in package with the reference's layout; the GPU run of the real reference
+    through the shim is tests/test_parity_gpu.py::test_shim_routes_reference_api."""
+    import importlib
+    import sys
+
+    from paper_2109_13504_b200 import resample as R
+    from paper_2109_13504_b200 import shim
+
+    pkg = tmp_path / "fake_megores"
+    pkg.mkdir()
+    (pkg / "resample.py").write_text(
+        "def metropolis(*a, **k): return 'cpu'\n"
+        "def metropolis_c1(*a, **k): return 'cpu'\n"
+        "def metropolis_c2(*a, **k): return 'cpu'\n"
+        "def megopolis(*a, **k): return 'cpu'\n"
+        "def ancestors_to_offspring(*a, **k): return 'cpu'\n"
+        "def apply_ancestors(*a, **k): return 'cpu'\n"
+        "def make_resampler(kind):\n"
+        "    if kind == 'megopolis':\n"
+        "        return lambda w, b, seed: megopolis(w, b, seed)\n"
+        "    return lambda w, b, seed: metropolis(w, b, seed)\n")
+    (pkg / "__init__.py").write_text("from .resample import (metropolis, metropolis_c1, metropolis_c2, megopolis,\n"
+                                     "    ancestors_to_offspring, apply_ancestors, make_resampler)\n")
+    monkeypatch.syspath_prepend(str(tmp_path))
+    fm = importlib.import_module("fake_megores")
+    saved = shim.install(fm, offspring=True)
+    try:
+        assert fm.megopolis is R.megopolis and fm.resample.megopolis is R.megopolis
+        assert fm.metropolis_c2 is R.metropolis_c2 and fm.resample.apply_ancestors is R.apply_ancestors
+        # make_resampler (resolved at call time) now reaches the B200 function
+        fn = fm.make_resampler("megopolis")
+        assert fn.__code__.co_names[0] == "megopolis" and fm.resample.megopolis is R.megopolis
+    finally:
+        shim.uninstall(fm, saved)
+    assert fm.megopolis(1) == "cpu" and fm.resample.megopolis(1) == "cpu"
+    sys.modules.pop("fake_megores", None)
+    sys.modules.pop("fake_megores.resample", None)
