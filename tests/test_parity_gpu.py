@@ -432,3 +432,15 @@ def test_config5_2p28_single_gpu(mg, oracle, rng):
     assert int(off.sum()) == n
     del anc, off, wv
     torch.cuda.empty_cache()
+
+
+def test_storage_device_upload(mg, tmp_path, oracle):
+    from paper_2109_13504_b200 import storage
+
+    w = oracle.gen_gaussian_weights(2.0, 4096, 9, "single")
+    storage.save_weights(tmp_path / "w.bin", mg.WeightVector(w, "single"))
+    wd = storage.load_weights(tmp_path / "w.bin", device="cuda")
+    assert wd.on_device and np.array_equal(wd.values.cpu().numpy(), w)
+    anc = mg.megopolis(wd, 7, seed=1)
+    storage.save_indices(tmp_path / "a.bin", anc)
+    assert np.array_equal(storage.load_indices(tmp_path / "a.bin"), oracle.megopolis(w, 7, seed=1))
