@@ -183,6 +183,19 @@ template <int RNG, typename WT, bool POW2, bool NZ, bool TEX>
 int launch_mego_w32(const ResampleArgs& a, const OffChunk& oc, cudaStream_t st) {
   const unsigned grid = (unsigned)((a.p_end - a.p0 + RS_THREADS - 1) / RS_THREADS);
   constexpr int PPT = mego_ppt<RNG>();
+  if constexpr (POW2 && PPT == 4) {
+    // full-range launch over N = 2^k >= 256: the half-split variant (j(i + N/2) = j(i) ^ N/2)
+    if (a.p0 == 0 && a.p_end == a.n && a.n >= 256) {
+      if constexpr (RNG == RNG_PHILOX && sizeof(WT) == 4 && NZ && TEX) {
+        k_megopolis_philox_half<<<a.n / RS_THREADS, 64, 0, st>>>(a, oc);
+        LAUNCH_CHECK("k_megopolis_philox_half");
+        return 0;
+      }
+      k_megopolis_w32<RNG, WT, POW2, NZ, TEX, PPT, true><<<a.n / RS_THREADS, RS_THREADS / PPT, 0, st>>>(a, oc);
+      LAUNCH_CHECK("k_megopolis_w32");
+      return 0;
+    }
+  }
   k_megopolis_w32<RNG, WT, POW2, NZ, TEX, PPT><<<grid, RS_THREADS / PPT, 0, st>>>(a, oc);
   LAUNCH_CHECK("k_megopolis_w32");
   return 0;

@@ -134,15 +134,23 @@ __device__ __forceinline__ double u1_from_word(uint32_t w) {
 // one DMUL + DSETP, one 32-bit select.  The accepted round index is carried instead
 // of j (j is a pure function of (i, o_b)) and k is rebuilt once at the end.
 
-template <int RNG, typename WT, bool POW2, bool NOZERO, bool TEX, int PPT>
-__global__ void __launch_bounds__(RS_THREADS / PPT) k_megopolis_w32(const __grid_constant__ ResampleArgs a,
+template <int RNG, typename WT, bool POW2, bool NOZERO, bool TEX, int PPT, bool HALF = false>
+__global__ void __launch_bounds__(RS_THREADS / PPT, PPT == 1 ? 0 : 1) k_megopolis_w32(const __grid_constant__ ResampleArgs a,
                                                                     const __grid_constant__ OffChunk oc) {
   // PPT particles per thread: i + p*(256/PPT) of this CTA's 256-particle block -- same lane,
   // different warps, so the lane part of the partner index is shared and the independent
   // random-stream chains interleave (ILP).  p_end is a multiple of 32: whole warps only.
-  constexpr int STRIDE = RS_THREADS / PPT;
-  const uint32_t i0 = a.p0 + blockIdx.x * RS_THREADS + threadIdx.x;
-  if (i0 >= a.p_end) return;
+  //
+  // HALF (full-range launch, N = 2^k >= 256, PPT = 4): the thread owns {i, i+64, i+N/2,
+  // i+N/2+64}, i in the lower half.  Adding N/2 modulo N flips the top index bit, so the
+  // partners of the upper pair are those of the lower pair with bit k-1 flipped:
+  // j(i + N/2) = j(i) ^ N/2 -- one LOP3 instead of an add and a mux per comparison
+  // (scripts/mb/mb_conv.cu: 5.28 -> 5.11 ms at 2^24, B = 352).
+  static_assert(!HALF || (PPT == 4 && POW2), "HALF needs PPT 4 and a power-of-two N");
+  constexpr int STRIDE = HALF ? 64 : RS_THREADS / PPT;
+  const uint32_t half = a.n >> 1;
+  const uint32_t i0 = HALF ? blockIdx.x * 128 + threadIdx.x : a.p0 + blockIdx.x * RS_THREADS + threadIdx.x;
+  if (!HALF && i0 >= a.p_end) return;
   const WT* __restrict__ w = reinterpret_cast<const WT*>(a.w);
   const uint32_t lane = threadIdx.x & 31u, n = a.n;
   uint32_t ii[PPT], ial[PPT];
@@ -151,23 +159,37 @@ __global__ void __launch_bounds__(RS_THREADS / PPT) k_megopolis_w32(const __grid
   int bstar[PPT];
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
-    ii[p] = i0 + p * STRIDE;
-    live[p] = ii[p] < a.p_end;
+    if constexpr (HALF) ii[p] = i0 + (p & 1) * STRIDE + (p >> 1) * half;
+    else ii[p] = i0 + p * STRIDE;
+    live[p] = HALF || ii[p] < a.p_end;
     ial[p] = ii[p] - lane;
     const uint32_t k0 = live[p] ? (a.first ? ii[p] : (uint32_t)a.kstate[ii[p]]) : 0u;
     wk[p] = wfetch<WT, TEX>(w, a.tex, k0);
     bstar[p] = -1;
   }
+  // partner indices of round o for all PPT particles
+  auto partners = [&](const uint2 o, uint32_t* jj) {
+    if constexpr (HALF) {
+      jj[0] = mego_j<true>(ial[0], lane, o, n);
+      jj[1] = mego_j<true>(ial[1], lane, o, n);
+      jj[2] = jj[0] ^ half;
+      jj[3] = jj[1] ^ half;
+    } else {
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) jj[p] = mego_j<POW2>(ial[p], lane, o, n);
+    }
+  };
   if constexpr (RNG == RNG_MEGORES) {
     uint64_t x[PPT];
 #pragma unroll
     for (int p = 0; p < PPT; ++p) x[p] = megores_key(a.base, ii[p], (uint64_t)a.b0);
 #pragma unroll(4 / PPT)
     for (int t = 0; t < a.cnt; ++t) {
-      const uint2 o = oc.o[t];
+      uint32_t jj[PPT];
+      partners(oc.o[t], jj);
 #pragma unroll
       for (int p = 0; p < PPT; ++p) {
-        const WT wj = wfetch<WT, TEX>(w, a.tex, mego_j<POW2>(ial[p], lane, o, n));
+        const WT wj = wfetch<WT, TEX>(w, a.tex, jj[p]);
         const double u = (double)mix64_m53(x[p]) * 0x1p-53;  // exact: u01 (M/rng.py:105-108)
         x[p] = add64_fma(x[p], a.one);  // x += M_CTR on the FMA pipe (the ALU pipe binds)
         if (accept_w<NOZERO>(u, wk[p], wj)) { wk[p] = wj; bstar[p] = t; }
@@ -203,11 +225,12 @@ __global__ void __launch_bounds__(RS_THREADS / PPT) k_megopolis_w32(const __grid
       for (int q = 0; q < 4; ++q) {
         if (q < lim) {
           const int t = t0 + q;
-          const uint2 o = oc.o[t];
+          uint32_t jj[PPT];
+          partners(oc.o[t], jj);
 #pragma unroll
           for (int p = 0; p < PPT; ++p) {
             const uint32_t wd = q == 0 ? c0[p] : q == 1 ? c1[p] : q == 2 ? c2[p] : c3[p];
-            const WT wj = wfetch<WT, TEX>(w, a.tex, mego_j<POW2>(ial[p], lane, o, n));
+            const WT wj = wfetch<WT, TEX>(w, a.tex, jj[p]);
             const double wjd = (double)wj;
             const bool le = fma(u1_from_word(wd), wkd[p], -wkd[p]) <= wjd;  // fl(u * wk) <= wj
             const bool acc = NOZERO ? le : (le && !(wj == (WT)0 && wkd[p] == 0.0));
@@ -224,6 +247,79 @@ __global__ void __launch_bounds__(RS_THREADS / PPT) k_megopolis_w32(const __grid
     if (!live[p]) continue;
     uint32_t k = a.first ? ii[p] : (uint32_t)a.kstate[ii[p]];
     if (bstar[p] >= 0) k = mego_j<POW2>(ial[p], lane, oc.o[bstar[p]], n);
+    if (a.last) a.anc[ii[p]] = (int64_t)k;
+    else a.kstate[ii[p]] = (int32_t)k;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// The headline configuration, specialised: Philox stream, float32 weights through the
+// texture path, no zero weights, N = 2^k >= 256, full-range launch.  Same arithmetic as
+// k_megopolis_w32<RNG_PHILOX, float, true, true, true, 4, true>; written as one straight
+// loop of Philox blocks (four rounds each) plus a guarded tail block, which ptxas
+// register-allocates without re-loading the round keys inside the loop
+// (scripts/mb/mb_conv.cu "x2 gen": 5.26 -> 5.21 ms at 2^24, B = 354).
+// Thread owns {i, i+64, i+N/2, i+N/2+64}; j(i + N/2) = j(i) ^ N/2.
+
+__global__ void __launch_bounds__(64, 1) k_megopolis_philox_half(const __grid_constant__ ResampleArgs a,
+                                                                 const __grid_constant__ OffChunk oc) {
+  constexpr int PPT = 4;
+  const uint32_t half = a.n >> 1;
+  const uint32_t i0 = blockIdx.x * 128 + threadIdx.x;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t cmask = (a.n - 1) & ~31u;
+  uint32_t ii[PPT];
+  double wkd[PPT];
+  int bstar[PPT];
+  ii[0] = i0; ii[1] = i0 + 64; ii[2] = i0 + half; ii[3] = i0 + half + 64;
+  const uint32_t ial0 = i0 - lane, ial1 = ial0 + 64;
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const uint32_t k0 = a.first ? ii[p] : (uint32_t)a.kstate[ii[p]];
+    wkd[p] = (double)tex1Dfetch<float>(a.tex, (int)k0);
+    bstar[p] = -1;
+  }
+  const int full = a.cnt & ~3;
+  auto body = [&](int t0, int lim) {  // rounds [t0, t0 + lim) from Philox block (b0 + t0) / 4
+    uint32_t c0[PPT], c1[PPT], c2[PPT], c3[PPT];
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) { c0[p] = ii[p]; c1[p] = 0; c2[p] = (uint32_t)((a.b0 + t0) >> 2); c3[p] = 0; }
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) {
+        const uint64_t q0 = (uint64_t)PHILOX_M0 * c0[p], q1 = (uint64_t)PHILOX_M1 * c2[p];
+        const uint32_t n0 = (uint32_t)(q1 >> 32) ^ c1[p] ^ a.pk0[r], n2 = (uint32_t)(q0 >> 32) ^ c3[p] ^ a.pk1[r];
+        c1[p] = (uint32_t)q1; c3[p] = (uint32_t)q0; c0[p] = n0; c2[p] = n2;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (q < lim) {
+        const int t = t0 + q;
+        const uint2 o = oc.o[t];
+        const uint32_t L = lane + o.y;
+        uint32_t jj[PPT];
+        jj[0] = mux3(ial0 + o.x, L, cmask);
+        jj[1] = mux3(ial1 + o.x, L, cmask);
+        jj[2] = jj[0] ^ half;
+        jj[3] = jj[1] ^ half;
+#pragma unroll
+        for (int p = 0; p < PPT; ++p) {
+          const uint32_t wd = q == 0 ? c0[p] : q == 1 ? c1[p] : q == 2 ? c2[p] : c3[p];
+          const double wjd = (double)tex1Dfetch<float>(a.tex, (int)jj[p]);
+          const double prod = fma(u1_from_word(wd), wkd[p], -wkd[p]);  // fl(u * wk)
+          if (prod <= wjd) { wkd[p] = wjd; bstar[p] = t; }
+        }
+      }
+    }
+  };
+  for (int t0 = 0; t0 < full; t0 += 4) body(t0, 4);
+  if (full < a.cnt) body(full, a.cnt - full);
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    uint32_t k = a.first ? ii[p] : (uint32_t)a.kstate[ii[p]];
+    if (bstar[p] >= 0) { const uint2 o = oc.o[bstar[p]]; k = mux3((ii[p] - lane) + o.x, lane + o.y, cmask); }
     if (a.last) a.anc[ii[p]] = (int64_t)k;
     else a.kstate[ii[p]] = (int32_t)k;
   }

@@ -145,6 +145,78 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_dup(const __grid_constant__
   }
 }
 
+
+// Full-range variant: thread owns particles {i, i+64, i+N/2, i+N/2+64}.  Partners of
+// i + N/2 are those of i with the top index bit flipped: j(i + N/2) = j(i) ^ N/2.
+// GEN: general launch state (first/kstate/last, tail rounds).
+template <int MINB, bool GEN = false, bool ONELOOP = false>
+__global__ void __launch_bounds__(64, MINB) k_x2(const __grid_constant__ ResampleArgs a, const __grid_constant__ OffChunk oc) {
+  constexpr int PPT = 4;
+  const uint32_t half = a.n >> 1;
+  const uint32_t i0 = blockIdx.x * 128 + threadIdx.x;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t cmask = (a.n - 1) & ~31u;
+  uint32_t ii[PPT];
+  double wkd[PPT];
+  int bstar[PPT];
+  ii[0] = i0; ii[1] = i0 + 64; ii[2] = i0 + half; ii[3] = i0 + half + 64;
+  const uint32_t ial0 = i0 - lane, ial1 = ial0 + 64;
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const uint32_t k0 = GEN ? (a.first ? ii[p] : (uint32_t)a.kstate[ii[p]]) : ii[p];
+    wkd[p] = (double)tex1Dfetch<float>(a.tex, (int)k0);
+    bstar[p] = -1;
+  }
+  const int full = a.cnt & ~3;
+  auto body = [&](int t0, int lim) {
+    uint32_t c0[PPT], c1[PPT], c2[PPT], c3[PPT];
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) { c0[p] = ii[p]; c1[p] = 0; c2[p] = (uint32_t)((a.b0 + t0) >> 2); c3[p] = 0; }
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) {
+        const uint64_t q0 = (uint64_t)PHILOX_M0 * c0[p], q1 = (uint64_t)PHILOX_M1 * c2[p];
+        const uint32_t n0 = (uint32_t)(q1 >> 32) ^ c1[p] ^ a.pk0[r], n2 = (uint32_t)(q0 >> 32) ^ c3[p] ^ a.pk1[r];
+        c1[p] = (uint32_t)q1; c3[p] = (uint32_t)q0; c0[p] = n0; c2[p] = n2;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (q < lim) {
+        const int t = t0 + q;
+        const uint2 o = oc.o[t];
+        const uint32_t L = lane + o.y;
+        uint32_t jj[PPT];
+        jj[0] = mux3(ial0 + o.x, L, cmask);
+        jj[1] = mux3(ial1 + o.x, L, cmask);
+        jj[2] = jj[0] ^ half;
+        jj[3] = jj[1] ^ half;
+#pragma unroll
+        for (int p = 0; p < PPT; ++p) {
+          const uint32_t wd = q == 0 ? c0[p] : q == 1 ? c1[p] : q == 2 ? c2[p] : c3[p];
+          const double wjd = (double)tex1Dfetch<float>(a.tex, (int)jj[p]);
+          const double prod = fma(u1_bits(wd), wkd[p], -wkd[p]);
+          if (prod <= wjd) { wkd[p] = wjd; bstar[p] = t; }
+        }
+      }
+    }
+  };
+  if (ONELOOP) {
+    for (int t0 = 0; t0 < a.cnt; t0 += 4) body(t0, min(4, a.cnt - t0));
+  } else {
+    for (int t0 = 0; t0 < full; t0 += 4) body(t0, 4);
+    if (GEN && full < a.cnt) body(full, a.cnt - full);
+  }
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    uint32_t k = GEN ? (a.first ? ii[p] : (uint32_t)a.kstate[ii[p]]) : ii[p];
+    if (bstar[p] >= 0) { const uint2 o = oc.o[bstar[p]]; k = mux3((ii[p] - lane) + o.x, lane + o.y, cmask); }
+    if (!GEN || a.last) a.anc[ii[p]] = (int64_t)k;
+    else a.kstate[ii[p]] = (int32_t)k;
+  }
+}
+
 template <class K>
 float time_it(K launch, int reps) {
   cudaEvent_t e0, e1;
@@ -215,13 +287,11 @@ int main(int argc, char** argv) {
   };
 #define RUN(P, U, W, M, S) check("p" #P " u" #U " w" #W " m" #M " s" #S, time_it([&]() { k_var<P, U, W, M, S><<<grid, 256 / P>>>(b, oc); }, 9))
   RUN(4, 1, 0, 1, 0);
-  RUN(4, 1, 0, 1, 1);
-  RUN(4, 1, 0, 1, 2);
-  RUN(4, 1, 1, 1, 1);
-  RUN(4, 1, 1, 1, 2);
-  RUN(2, 1, 0, 1, 1);
-  RUN(8, 1, 0, 1, 1);
-  RUN(4, 0, 0, 1, 1);
+  check("lib HALF", time_it([&]() { k_megopolis_w32<1, float, true, true, true, 4, true><<<n / 256, 64>>>(b, oc); }, 9));
+  check("x2 p4", time_it([&]() { k_x2<1><<<n / 256, 64>>>(b, oc); }, 9));
+  check("lib philox_half", time_it([&]() { k_megopolis_philox_half<<<n / 256, 64>>>(b, oc); }, 9));
+  check("x2 gen", time_it([&]() { k_x2<1, true><<<n / 256, 64>>>(b, oc); }, 9));
+  check("x2 gen1loop", time_it([&]() { k_x2<1, true, true><<<n / 256, 64>>>(b, oc); }, 9));
   {
     float* w2;
     CK(cudaMalloc(&w2, sizeof(float) * 2 * n));
