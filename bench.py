@@ -110,7 +110,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.1)
+            time.sleep(0.01)
 
     def __enter__(self):
         if self.nv:
@@ -315,6 +315,12 @@ def main():
         return ach, kavg
 
     achieved, kern_avg = roof(head)
+    # full-range Philox launches take the specialised half-split kernel; rank slices (N > 1)
+    # and the megores stream take k_megopolis_w32
+    if args.rng == "philox":
+        mego_kernel = "k_megopolis_philox_half" if world == 1 else "k_megopolis_w32<philox, 4 particles/thread>"
+    else:
+        mego_kernel = "k_megopolis_w32<megores, 1 particle/thread>"
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "megopolis_traffic.json")) as f:
@@ -394,7 +400,7 @@ def main():
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "k_megopolis_w32", "kernel_ms": kern_avg * 1e3,
+                         "kernel": mego_kernel, "kernel_ms": kern_avg * 1e3,
                          "alg_bytes_per_launch": alg_bytes},
             "cpu_baseline": cpu,
             "e2e": e2e,
