@@ -339,3 +339,62 @@ void mgo_gather(const void *states, int64_t row_bytes, const int64_t *anc, int64
         memcpy((char *)out + i * row_bytes, (const char *)states + anc[i] * row_bytes, (size_t)row_bytes);
 }
 
+
+/* ------------------------------------------------------------------------ */
+/* Prefix-sum resamplers (M/resample.py:288-354)                            */
+
+/* np.cumsum(values) (M/resample.py:288-291): a sequential left-to-right scan in the
+ * array's own dtype (float32 for "single").  Built with -ffp-contract=off and without
+ * fast-math, so every add is one IEEE binary32/binary64 round-to-nearest-even. */
+void mgo_cumsum(const void *w, int dtype, int64_t n, void *out) {
+    if (n <= 0) return;
+    if (dtype == 0) {
+        const float *a = (const float *)w;
+        float *o = (float *)out, s = a[0];
+        o[0] = s;
+        for (int64_t k = 1; k < n; ++k) { s = s + a[k]; o[k] = s; }
+    } else {
+        const double *a = (const double *)w;
+        double *o = (double *)out, s = a[0];
+        o[0] = s;
+        for (int64_t k = 1; k < n; ++k) { s = s + a[k]; o[k] = s; }
+    }
+}
+
+/* multinomial (M/resample.py:295-304): u_i = uniform01_at(seed, i, 0) * total cast to the
+ * weight dtype, ancestor = searchsorted(inclusive, u_i, side="right") clamped to n-1.
+ * `cum` is the inclusive prefix (mgo_cumsum). */
+void mgo_multinomial(const void *cum, int dtype, int64_t n, uint64_t seed, int64_t *anc) {
+    const uint64_t base = mgo_mix(seed + M_LANE);
+    const double total = dtype == 0 ? (double)((const float *)cum)[n - 1] : ((const double *)cum)[n - 1];
+    for (int64_t i = 0; i < n; ++i) {
+        const double ud = (double)(mgo_mix(base + (uint64_t)i * M_LANE) >> 11) * INV_2_53 * total;
+        int64_t lo = 0, hi = n; /* first index with cum > u */
+        if (dtype == 0) {
+            const float u = (float)ud, *c = (const float *)cum;
+            while (lo < hi) { int64_t mid = lo + (hi - lo) / 2; if (c[mid] <= u) lo = mid + 1; else hi = mid; }
+        } else {
+            const double *c = (const double *)cum;
+            while (lo < hi) { int64_t mid = lo + (hi - lo) / 2; if (c[mid] <= ud) lo = mid + 1; else hi = mid; }
+        }
+        anc[i] = lo < n - 1 ? lo : n - 1;
+    }
+}
+
+/* systematic_improved (M/resample.py:307-336): one shared u0 = uniform01_at(seed,
+ * GLOBAL_OFFSET_LANE, 0); target_i = (i + u0) / n * total in float64; the forward/backward
+ * scans settle on the first index a with float64(cum[a]) >= target_i, or n-1. */
+void mgo_systematic(const void *cum, int dtype, int64_t n, uint64_t seed, int64_t *anc) {
+    const double u0 = mgo_u01(seed, GLOBAL_OFFSET_LANE, 0);
+    const double total = dtype == 0 ? (double)((const float *)cum)[n - 1] : ((const double *)cum)[n - 1];
+    for (int64_t i = 0; i < n; ++i) {
+        const double target = ((double)i + u0) / (double)n * total;
+        int64_t lo = 0, hi = n; /* first index with cum >= target */
+        while (lo < hi) {
+            int64_t mid = lo + (hi - lo) / 2;
+            const double c = dtype == 0 ? (double)((const float *)cum)[mid] : ((const double *)cum)[mid];
+            if (c < target) lo = mid + 1; else hi = mid;
+        }
+        anc[i] = lo < n - 1 ? lo : n - 1;
+    }
+}

@@ -72,6 +72,9 @@ def lib():
         L.mgo_offspring.argtypes = [vp, i64, i64, vp]
         L.mgo_gather.argtypes = [vp, i64, vp, i64, vp]
         L.mgo_num_threads.restype = i32
+        L.mgo_cumsum.argtypes = [vp, i32, i64, vp]
+        L.mgo_multinomial.argtypes = [vp, i32, i64, u64, vp]
+        L.mgo_systematic.argtypes = [vp, i32, i64, u64, vp]
         _lib = L
     return _lib
 
@@ -312,6 +315,38 @@ class QualityAccumulator:
         return {"mse": mse, "variance": variance, "bias_sq": bias_sq,
                 "bias_contribution": bias_sq / mse if mse > 0 else 0.0,
                 "mse_per_particle": mse / self.n}
+
+
+# ---------------------------------------------------------------------------
+# Prefix-sum resamplers (M/resample.py:288-336)
+
+
+def cumsum(w) -> np.ndarray:
+    """np.cumsum in the weights' dtype, sequential left to right (M/resample.py:288-291)."""
+    values, dt = _weights(w)
+    out = np.empty_like(values)
+    lib().mgo_cumsum(_ptr(values), dt, len(values), _ptr(out))
+    return out
+
+
+def multinomial(w, seed) -> np.ndarray:
+    """M/resample.py:295-304."""
+    values, dt = _weights(w)
+    _check(values, 1)
+    cum = cumsum(values)
+    out = np.empty(len(values), dtype=np.int64)
+    lib().mgo_multinomial(_ptr(cum), dt, len(values), int(seed) & (2**64 - 1), _ptr(out))
+    return out
+
+
+def systematic(w, seed) -> np.ndarray:
+    """systematic_improved, M/resample.py:307-336."""
+    values, dt = _weights(w)
+    _check(values, 1)
+    cum = cumsum(values)
+    out = np.empty(len(values), dtype=np.int64)
+    lib().mgo_systematic(_ptr(cum), dt, len(values), int(seed) & (2**64 - 1), _ptr(out))
+    return out
 
 
 def num_threads() -> int:
