@@ -42,6 +42,8 @@ extern "C" {
 enum { MGP_F32 = 0, MGP_F64 = 1 };
 enum { MGP_RNG_MEGORES = 0, MGP_RNG_PHILOX = 1 };
 enum { MGP_KIND_METROPOLIS = 0, MGP_KIND_C1 = 1, MGP_KIND_C2 = 2, MGP_KIND_MEGOPOLIS = 3 };
+/* prefix-sum resamplers (M/resample.py:285-336): b is ignored, rng must be MGP_RNG_MEGORES */
+enum { MGP_KIND_MULTINOMIAL = 4, MGP_KIND_SYSTEMATIC = 5 };
 enum { MGP_OK = 0, MGP_EINVAL = -1, MGP_EUNSUPPORTED = -2 };
 
 /* flags: MGP_FLAG_NONZERO asserts that no weight is zero (mgp_weight_stats:
@@ -164,6 +166,17 @@ int mgp_estimate_ratio_stats(const void *d_w, int dtype, int64_t n, int64_t subs
 
 /* gen_gaussian_weights (M/weights.py:100-104) on the device (synthetic inputs) */
 int mgp_gen_gaussian(double y, int64_t n, uint64_t seed, int dtype, void *d_out, void *stream);
+
+/* Prefix-sum resamplers (M/resample.py:285-336).  mgp_cumsum is np.cumsum(values) in the
+ * weights' dtype (M/resample.py:288-291) -- numpy's sequential left-to-right rounding,
+ * reproduced bit for bit by a parallel exact scan.
+ *   multinomial(w, seed)          M/resample.py:295-304
+ *   systematic_improved(w, seed)  M/resample.py:307-336
+ * Also reachable as kinds MGP_KIND_MULTINOMIAL / MGP_KIND_SYSTEMATIC of mgp_resample_range
+ * and mgp_resample_host (b ignored). */
+int mgp_cumsum(const void *d_w, int dtype, int64_t n, void *d_out, void *stream);
+int mgp_multinomial(const void *d_w, int dtype, int64_t n, uint64_t seed, int64_t *d_anc, void *stream);
+int mgp_systematic(const void *d_w, int dtype, int64_t n, uint64_t seed, int64_t *d_anc, void *stream);
 
 /* Self-check: our Philox4x32-10 vs curand_Philox4x32_10 for counters {i, c1, c2, c3}.
  * Writes 4*n words each; returns the number of mismatching words in *h_mismatch. */

@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(HERE, "libmgp.so")
 
 MGP_F32, MGP_F64 = 0, 1
 RNG = {"megores": 0, "philox": 1}
-KIND = {"metropolis": 0, "c1": 1, "c2": 2, "megopolis": 3}
+KIND = {"metropolis": 0, "c1": 1, "c2": 2, "megopolis": 3, "multinomial": 4, "systematic": 5}
 MGP_EINVAL, MGP_EUNSUPPORTED = -1, -2
 FLAG_NONZERO = 1
 FLAG_NO_STAGE = 2
@@ -53,6 +53,9 @@ SIGNATURES = {
     "mgp_pf_predict_update": (_i32, [_vp, _i64, _dbl, _dbl, _u64, _dbl, _dbl, _i32, _vp, _vp, _vp]),
     "mgp_estimate_ratio_stats": (_i32, [_vp, _i32, _i64, _i64, _u64, _vp, _vp]),
     "mgp_gen_gaussian": (_i32, [_dbl, _i64, _u64, _i32, _vp, _vp]),
+    "mgp_cumsum": (_i32, [_vp, _i32, _i64, _vp, _vp]),
+    "mgp_multinomial": (_i32, [_vp, _i32, _i64, _u64, _vp, _vp]),
+    "mgp_systematic": (_i32, [_vp, _i32, _i64, _u64, _vp, _vp]),
     "mgp_philox_selftest": (_i32, [_u64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, _i64, _vp]),
 }
 

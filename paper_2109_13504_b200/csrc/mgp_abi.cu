@@ -15,10 +15,12 @@
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <curand_philox4x32_x.h>
 
 #include "megopolis_b200.h"
 #include "mgp_kernels.cuh"
+#include "mgp_prefix.cuh"
 
 using namespace mgp;
 
@@ -326,15 +328,80 @@ struct Plan {
   std::vector<int64_t> off;  // Megopolis offsets (host)
   int64_t* d_off = nullptr;  // device copy for the generic path
   int32_t* kstate = nullptr;
+  void* cum = nullptr;       // inclusive prefix sum (multinomial / systematic)
 };
 
+bool is_prefix_kind(int kind) { return kind == MGP_KIND_MULTINOMIAL || kind == MGP_KIND_SYSTEMATIC; }
+
+// np.cumsum(values) in the weights' dtype, bit-exact (mgp_prefix.cuh)
+template <typename WT>
+int px_cumsum(const WT* w, int64_t n, WT* cum, cudaStream_t st) {
+  ensure_pool();
+  const int64_t nch = (n + PX_CHUNK - 1) / PX_CHUNK;
+  double *csum = nullptr, *est = nullptr;
+  int32_t *e0 = nullptr, *mode = nullptr;
+  Tx* agg = nullptr;
+  WT* carry = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (const double*)nullptr, (double*)nullptr, (int)nch, st));
+  CUDA_TRY(cudaMallocAsync(&csum, sizeof(double) * nch, st));
+  CUDA_TRY(cudaMallocAsync(&est, sizeof(double) * nch, st));
+  CUDA_TRY(cudaMallocAsync(&e0, sizeof(int32_t) * nch, st));
+  CUDA_TRY(cudaMallocAsync(&mode, sizeof(int32_t) * nch, st));
+  CUDA_TRY(cudaMallocAsync(&agg, sizeof(Tx) * PX_CAND * nch, st));
+  CUDA_TRY(cudaMallocAsync(&carry, sizeof(WT) * nch, st));
+  CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes + 16, st));
+  k_px_chunk_sum<WT><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, csum);
+  LAUNCH_CHECK("k_px_chunk_sum");
+  CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, csum, est, (int)nch, st));
+  k_px_aggregate<WT><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, est, e0, agg);
+  LAUNCH_CHECK("k_px_aggregate");
+  k_px_resolve<WT><<<1, 32, 0, st>>>(w, n, nch, e0, agg, carry, mode);
+  LAUNCH_CHECK("k_px_resolve");
+  k_px_materialize<WT><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, carry, mode, cum);
+  LAUNCH_CHECK("k_px_materialize");
+  for (void* q : {(void*)csum, (void*)est, (void*)e0, (void*)mode, (void*)agg, (void*)carry, tmp})
+    CUDA_TRY(cudaFreeAsync(q, st));
+  return 0;
+}
+
+int px_cumsum_any(const void* w, int dtype, int64_t n, void* cum, cudaStream_t st) {
+  return dtype == MGP_F32 ? px_cumsum<float>((const float*)w, n, (float*)cum, st)
+                          : px_cumsum<double>((const double*)w, n, (double*)cum, st);
+}
+
+// searches over particles [p0, p_end) of a prefix-sum resampler (cum already built)
+int px_search(int kind, const void* cum, int dtype, int64_t n, uint64_t seed, int64_t p0, int64_t p_end,
+              int64_t* anc, cudaStream_t st) {
+  const int64_t cnt = p_end - p0;
+  if (cnt <= 0) return 0;
+  const unsigned grid = (unsigned)std::min<int64_t>((cnt + 255) / 256, 148 * 64);
+  // the kernels index particles from 0: shift the particle range through the output pointer
+  // and a re-based launch (i = p0 + t)
+  if (kind == MGP_KIND_MULTINOMIAL) {
+    const uint64_t base = megores_base(seed);
+    if (dtype == MGP_F32) k_multinomial<float><<<grid, 256, 0, st>>>((const float*)cum, n, base, p0, p_end, anc);
+    else k_multinomial<double><<<grid, 256, 0, st>>>((const double*)cum, n, base, p0, p_end, anc);
+    LAUNCH_CHECK("k_multinomial");
+  } else {
+    const double u0 = (double)(mix64(megores_key(megores_base(seed), GLOBAL_OFFSET_LANE, 0)) >> 11) * 0x1p-53;
+    if (dtype == MGP_F32) k_systematic<float><<<grid, 256, 0, st>>>((const float*)cum, n, u0, p0, p_end, anc);
+    else k_systematic<double><<<grid, 256, 0, st>>>((const double*)cum, n, u0, p0, p_end, anc);
+    LAUNCH_CHECK("k_systematic");
+  }
+  return 0;
+}
+
 bool plan_uses_w32(const Plan& p) {
+  if (is_prefix_kind(p.kind)) return false;
   if (p.kind == MGP_KIND_METROPOLIS) return true;
   return p.warp == 32 && p.n % 32 == 0;
 }
 
 int run_range(Plan& p, int64_t p0, int64_t p_end, int64_t* anc, cudaStream_t st) {
   if (p0 >= p_end) return 0;
+  if (is_prefix_kind(p.kind)) return px_search(p.kind, p.cum, p.dtype, p.n, p.seed, p0, p_end, anc, st);
   if (!plan_uses_w32(p)) {
     GenericArgs ga{p.w, p.n, (int64_t)p.warp, p.n_w, p.n_part, (int64_t)p.b, p0, p_end, p.seed, megores_base(p.seed),
                    p.d_off, anc};
@@ -409,7 +476,10 @@ int run_range(Plan& p, int64_t p0, int64_t p_end, int64_t* anc, cudaStream_t st)
 // Validate + build a plan (no data access).
 int make_plan(Plan& p, int kind, const void* w, int dtype, int64_t n, int32_t b, uint64_t seed, int32_t warp,
               int32_t part_bytes, int strict, int rng, int flags) {
-  int rc = check_common(dtype, n, b, rng);
+  // the prefix-sum methods take no iteration budget (make_resampler ignores b, M/resample.py:450-454)
+  if (is_prefix_kind(kind) && rng != MGP_RNG_MEGORES)
+    return set_err(MGP_EUNSUPPORTED, "the prefix-sum resamplers draw from the megores stream only");
+  int rc = check_common(dtype, n, is_prefix_kind(kind) ? 1 : b, rng);
   if (rc) return rc;
   p.kind = kind;
   p.w = w;
@@ -430,7 +500,7 @@ int make_plan(Plan& p, int kind, const void* w, int dtype, int64_t n, int32_t b,
   } else if (kind == MGP_KIND_C1 || kind == MGP_KIND_C2) {
     if ((rc = check_warp(n, warp, strict, kind == MGP_KIND_C1 ? "metropolis_c1" : "metropolis_c2"))) return rc;
     if ((rc = check_partition(n, part_bytes, &p.n_w, &p.n_part))) return rc;
-  } else if (kind != MGP_KIND_METROPOLIS) {
+  } else if (kind != MGP_KIND_METROPOLIS && !is_prefix_kind(kind)) {
     return set_err(MGP_EINVAL, "unknown resampler kind %d", kind);
   }
   return 0;
@@ -438,6 +508,10 @@ int make_plan(Plan& p, int kind, const void* w, int dtype, int64_t n, int32_t b,
 
 int plan_alloc(Plan& p, cudaStream_t st) {
   ensure_pool();
+  if (is_prefix_kind(p.kind)) {  // the prefix sum is shared by every particle range
+    CUDA_TRY(cudaMallocAsync(&p.cum, (size_t)p.n * (p.dtype == MGP_F32 ? 4 : 8), st));
+    return px_cumsum_any(p.w, p.dtype, p.n, p.cum, st);
+  }
   if (!plan_uses_w32(p) && p.kind == MGP_KIND_MEGOPOLIS) {
     CUDA_TRY(cudaMallocAsync(&p.d_off, sizeof(int64_t) * p.b, st));
     CUDA_TRY(cudaMemcpyAsync(p.d_off, p.off.data(), sizeof(int64_t) * p.b, cudaMemcpyHostToDevice, st));
@@ -450,8 +524,10 @@ int plan_alloc(Plan& p, cudaStream_t st) {
 int plan_free(Plan& p, cudaStream_t st) {
   if (p.d_off) CUDA_TRY(cudaFreeAsync(p.d_off, st));
   if (p.kstate) CUDA_TRY(cudaFreeAsync(p.kstate, st));
+  if (p.cum) CUDA_TRY(cudaFreeAsync(p.cum, st));
   p.d_off = nullptr;
   p.kstate = nullptr;
+  p.cum = nullptr;
   return 0;
 }
 
@@ -871,6 +947,22 @@ __global__ void k_philox_selftest(uint64_t key, uint32_t c1, uint32_t c2, uint32
   }
 }
 }  // namespace
+
+extern "C" int mgp_cumsum(const void* d_w, int dtype, int64_t n, void* d_out, void* stream) {
+  if (dtype != MGP_F32 && dtype != MGP_F64) return set_err(MGP_EINVAL, "dtype must be MGP_F32 or MGP_F64, got %d", dtype);
+  if (n < 1) return set_err(MGP_EINVAL, "weights must be a non-empty 1-d sequence");
+  if (n > MAX_N) return set_err(MGP_EUNSUPPORTED, "N=%lld exceeds this build's limit of 2^31-1 particles", (long long)n);
+  if (!d_w || !d_out) return set_err(MGP_EINVAL, "null pointer");
+  return px_cumsum_any(d_w, dtype, n, d_out, S(stream));
+}
+
+extern "C" int mgp_multinomial(const void* d_w, int dtype, int64_t n, uint64_t seed, int64_t* d_anc, void* stream) {
+  return resample_device(MGP_KIND_MULTINOMIAL, d_w, dtype, n, 1, seed, 32, 0, 0, MGP_RNG_MEGORES, 0, d_anc, stream);
+}
+
+extern "C" int mgp_systematic(const void* d_w, int dtype, int64_t n, uint64_t seed, int64_t* d_anc, void* stream) {
+  return resample_device(MGP_KIND_SYSTEMATIC, d_w, dtype, n, 1, seed, 32, 0, 0, MGP_RNG_MEGORES, 0, d_anc, stream);
+}
 
 extern "C" int mgp_philox_selftest(uint64_t key, uint32_t c1, uint32_t c2, uint32_t c3, int64_t n,
                                    int64_t* h_mismatch) {

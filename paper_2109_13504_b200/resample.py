@@ -6,6 +6,7 @@ Same names, signatures, defaults, return types and errors as the reference
   metropolis_c2   :228-244                  megopolis      :268-282
   make_resampler  :431-455                  megopolis_offsets :263-265
   ancestors_to_offspring :361-368           apply_ancestors   :371-377
+  multinomial     :295-304                  systematic_improved :307-336
   WarpConfig :59-75, PartitionConfig :78-93, METROPOLIS_FAMILY / ALGORITHMS :55-56
 
 Inputs: a WeightVector (this package's or the reference's), a numpy array, or a
@@ -31,7 +32,7 @@ from . import _lib
 from .weights import WeightVector, _as_weight_vector
 
 METROPOLIS_FAMILY = ("metropolis", "c1", "c2", "megopolis")
-ALGORITHMS = METROPOLIS_FAMILY  # prefix-sum resamplers are not on the B200 hot path
+ALGORITHMS = METROPOLIS_FAMILY + ("multinomial", "systematic")
 
 
 @dataclass(frozen=True)
@@ -110,6 +111,8 @@ def _validate(w: WeightVector, b, warp, strict, part, name):
 def _resample(kind, w, b, seed, warp, part, strict, rng, name):
     w = _as_weight_vector(w)
     b = int(b)
+    if kind in ("multinomial", "systematic"):
+        b = 1  # the prefix-sum methods take no iteration budget (M/resample.py:450-454)
     _validate(w, b, warp, strict, part, name)
     L = _lib.lib()
     ws = warp.warp_size if warp is not None else 32
@@ -129,6 +132,10 @@ def _resample(kind, w, b, seed, warp, part, strict, rng, name):
                 rc = L.mgp_megopolis(*args, ws, int(bool(strict)), _rng(rng), flags, D.ptr(out), s)
             elif kind == "metropolis":
                 rc = L.mgp_metropolis(*args, _rng(rng), flags, D.ptr(out), s)
+            elif kind == "multinomial":
+                rc = L.mgp_multinomial(D.ptr(vals), D.wdtype(vals), len(w), _seed(seed), D.ptr(out), s)
+            elif kind == "systematic":
+                rc = L.mgp_systematic(D.ptr(vals), D.wdtype(vals), len(w), _seed(seed), D.ptr(out), s)
             elif kind == "c1":
                 rc = L.mgp_metropolis_c1(*args, ws, pb, int(bool(strict)), _rng(rng), flags, D.ptr(out), s)
             else:
@@ -167,6 +174,35 @@ def megopolis(w, b: int, warp: WarpConfig = WarpConfig(), seed=0, strict: bool =
     return _resample("megopolis", w, b, seed, warp, None, strict, rng, "megopolis")
 
 
+def multinomial(w, seed):
+    """Per-particle uniform draw located in the prefix sum by binary search (M/resample.py:295-304).
+
+    The prefix sum is numpy's sequential float32/float64 ``np.cumsum`` order, reproduced
+    bit for bit on the device (``inclusive_prefix``)."""
+    return _resample("multinomial", w, 1, seed, None, None, False, "megores", "multinomial")
+
+
+def systematic_improved(w, seed, warp: WarpConfig = WarpConfig()):
+    """Stratified selection with one shared u (M/resample.py:307-336); each particle's
+    bracket is found by a binary search of the exact prefix sum (same result as the
+    reference's lockstep forward/backward scans)."""
+    return _resample("systematic", w, 1, seed, None, None, False, "megores", "systematic_improved")
+
+
+def inclusive_prefix(w):
+    """``np.cumsum(values)`` in the weights' dtype, bit-identical to numpy's sequential
+    scan (M/resample.py:288-291).  numpy in -> numpy out; CUDA tensor in -> CUDA tensor out."""
+    D.require_cuda()
+    t = D.torch()
+    w = _as_weight_vector(w)
+    host = not w.on_device
+    vals = t.from_numpy(np.ascontiguousarray(w.values)).cuda() if host else w.values.contiguous()
+    out = t.empty_like(vals)
+    with t.cuda.device(vals.device):
+        _lib.check(_lib.lib().mgp_cumsum(D.ptr(vals), D.wdtype(vals), vals.numel(), D.ptr(out), D.stream_ptr()))
+    return out.cpu().numpy() if host else out
+
+
 def megopolis_index(i: int, o_b: int, warp: WarpConfig, n: int) -> int:
     """Wrapped-sequential comparison index (M/resample.py:247-260); host helper."""
     if not (0 <= i < n) or not (0 <= o_b < n):
@@ -195,8 +231,10 @@ def make_resampler(kind: str, warp: WarpConfig = WarpConfig(), partition_bytes: 
         return lambda w, b, seed: fn(w, b, part, warp, seed, strict, rng=rng)
     if kind == "megopolis":
         return lambda w, b, seed: megopolis(w, b, warp, seed, strict, rng=rng)
-    if kind in ("multinomial", "systematic"):
-        raise NotImplementedError(f"{kind!r} is a prefix-sum resampler outside the B200 hot path (SURVEY 8f)")
+    if kind == "multinomial":  # the prefix-sum methods ignore b (M/resample.py:450-454)
+        return lambda w, b, seed: multinomial(w, seed)
+    if kind == "systematic":
+        return lambda w, b, seed: systematic_improved(w, seed, warp)
     raise ValueError(f"unknown resampler {kind!r}")
 
 

@@ -20,6 +20,8 @@ PATCHED = {
     "metropolis_c1": _r.metropolis_c1,
     "metropolis_c2": _r.metropolis_c2,
     "megopolis": _r.megopolis,
+    "multinomial": _r.multinomial,
+    "systematic_improved": _r.systematic_improved,
 }
 
 
