@@ -337,11 +337,11 @@ bool is_prefix_kind(int kind) { return kind == MGP_KIND_MULTINOMIAL || kind == M
 template <typename WT>
 int px_cumsum(const WT* w, int64_t n, WT* cum, cudaStream_t st) {
   ensure_pool();
-  const int64_t nch = (n + PX_CHUNK - 1) / PX_CHUNK;
+  const int64_t nch = (n + PX_CHUNK - 1) / PX_CHUNK, nsup = (nch + PX_SUPER - 1) / PX_SUPER;
   double *csum = nullptr, *est = nullptr;
-  int32_t *e0 = nullptr, *mode = nullptr;
-  Tx* agg = nullptr;
-  WT* carry = nullptr;
+  int32_t *e0 = nullptr, *mode = nullptr, *exc = nullptr, *se0 = nullptr, *smode = nullptr;
+  Tx *agg = nullptr, *sagg = nullptr;
+  WT *carry = nullptr, *scarry = nullptr;
   void* tmp = nullptr;
   size_t tmp_bytes = 0;
   CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (const double*)nullptr, (double*)nullptr, (int)nch, st));
@@ -349,19 +349,31 @@ int px_cumsum(const WT* w, int64_t n, WT* cum, cudaStream_t st) {
   CUDA_TRY(cudaMallocAsync(&est, sizeof(double) * nch, st));
   CUDA_TRY(cudaMallocAsync(&e0, sizeof(int32_t) * nch, st));
   CUDA_TRY(cudaMallocAsync(&mode, sizeof(int32_t) * nch, st));
+  CUDA_TRY(cudaMallocAsync(&exc, sizeof(int32_t) * (nch + 1), st));
   CUDA_TRY(cudaMallocAsync(&agg, sizeof(Tx) * PX_CAND * nch, st));
   CUDA_TRY(cudaMallocAsync(&carry, sizeof(WT) * nch, st));
+  CUDA_TRY(cudaMallocAsync(&se0, sizeof(int32_t) * nsup, st));
+  CUDA_TRY(cudaMallocAsync(&smode, sizeof(int32_t) * nsup, st));
+  CUDA_TRY(cudaMallocAsync(&sagg, sizeof(Tx) * PX_CAND * nsup, st));
+  CUDA_TRY(cudaMallocAsync(&scarry, sizeof(WT) * nsup, st));
   CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes + 16, st));
   k_px_chunk_sum<WT><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, csum);
   LAUNCH_CHECK("k_px_chunk_sum");
   CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, csum, est, (int)nch, st));
   k_px_aggregate<WT><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, est, e0, agg);
   LAUNCH_CHECK("k_px_aggregate");
-  k_px_resolve<WT><<<1, 32, 0, st>>>(w, n, nch, e0, agg, carry, mode);
+  k_px_super<<<(unsigned)nsup, 32, 0, st>>>(nch, e0, agg, se0, sagg);
+  LAUNCH_CHECK("k_px_super");
+  k_px_resolve<WT><<<1, 32, 0, st>>>(w, n, nch, nsup, e0, agg, se0, sagg, carry, mode, scarry, smode, exc);
   LAUNCH_CHECK("k_px_resolve");
+  k_px_expand<WT><<<(unsigned)nsup, 32, 0, st>>>(nch, e0, agg, scarry, smode, carry, mode);
+  LAUNCH_CHECK("k_px_expand");
   k_px_materialize<WT><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, carry, mode, cum);
   LAUNCH_CHECK("k_px_materialize");
-  for (void* q : {(void*)csum, (void*)est, (void*)e0, (void*)mode, (void*)agg, (void*)carry, tmp})
+  k_px_materialize_exc<WT><<<(unsigned)std::min<int64_t>(nch, 2 * 148), 32, 0, st>>>(w, n, carry, exc, cum);
+  LAUNCH_CHECK("k_px_materialize_exc");
+  for (void* q : {(void*)csum, (void*)est, (void*)e0, (void*)mode, (void*)exc, (void*)agg, (void*)carry, (void*)se0,
+                  (void*)smode, (void*)sagg, (void*)scarry, tmp})
     CUDA_TRY(cudaFreeAsync(q, st));
   return 0;
 }
@@ -377,8 +389,6 @@ int px_search(int kind, const void* cum, int dtype, int64_t n, uint64_t seed, in
   const int64_t cnt = p_end - p0;
   if (cnt <= 0) return 0;
   const unsigned grid = (unsigned)std::min<int64_t>((cnt + 255) / 256, 148 * 64);
-  // the kernels index particles from 0: shift the particle range through the output pointer
-  // and a re-based launch (i = p0 + t)
   if (kind == MGP_KIND_MULTINOMIAL) {
     const uint64_t base = megores_base(seed);
     if (dtype == MGP_F32) k_multinomial<float><<<grid, 256, 0, st>>>((const float*)cum, n, base, p0, p_end, anc);

@@ -21,15 +21,17 @@
 //   k_px_chunk_sum    float64 chunk sums -> (CUB) exclusive prefix = carry-in estimates
 //   k_px_aggregate    per chunk, the composed transducer for the 3 binades around the
 //                     estimate (e0-1, e0, e0+1)
-//   k_px_resolve      one warp walks the chunks 32 at a time: from the true carry-in s
-//                     (binade e, parity p) it scans the lanes' aggregates for e; every
-//                     chunk whose end stays inside binade e is resolved in O(1); the
-//                     first chunk that leaves the binade (or lacks an aggregate for e)
-//                     is scanned sequentially by one lane (a handful per array: the
-//                     running sum crosses each binade once)
+//   k_px_super        the same for super-chunks of 32 chunks (composition of theirs)
+//   k_px_resolve      one warp walks the super-chunks 32 at a time: from the true carry-in
+//                     s (binade e, parity p) it scans the lanes' aggregates for e; every
+//                     super-chunk whose end stays inside binade e is resolved in O(1); the
+//                     first that leaves it is descended into (chunk windows), and the chunk
+//                     the sum leaves its binade in is summed sequentially, as numpy does
+//                     (a handful per array: the running sum crosses each binade once)
+//   k_px_expand       chunk carry-ins inside the super-chunks resolved whole
 //   k_px_materialize  per chunk, an ordered block scan of the transducers from the true
-//                     carry-in writes s_k = carry + units * u_e (sequential re-scan for
-//                     the chunks the resolver scanned)
+//                     carry-in writes s_k = carry + units * u_e (the warp routine again
+//                     for the binade-crossing chunks)
 // All arithmetic is integer or exact power-of-two scaling; the result equals np.cumsum.
 #pragma once
 #include <cstdint>
@@ -80,19 +82,45 @@ __device__ __forceinline__ Tx px_compose(Tx A, Tx B) {
 
 __device__ __forceinline__ int64_t px_apply(Tx T, int64_t parity) { return parity ? T.a1 : T.a0; }
 
-// Element transducer of weight w in binade e.  Weights >= 2^(e+1) leave the binade in one
-// step: saturate.  ldexp scaling is exact (w / u_e has at most MANT+1 significant bits).
+// Element transducer of weight w in binade e: w / u_e = M * 2^(ew - e) with M the integer
+// significand (implicit bit included for normal w) -- an integer shift with an exact
+// remainder, no floating point.  Weights >= 2^(e+1) leave the binade in one step: saturate.
 template <typename WT>
 __device__ __forceinline__ Tx px_elem(WT w, int e) {
-  constexpr int MANT = PxFp<WT>::MANT;
-  if (!((double)w < ldexp(1.0, e + 1))) return Tx{PX_SAT, PX_SAT};
-  const double x = ldexp((double)w, MANT - e);
-  const double m = floor(x);
-  const double f = x - m;
-  const int64_t mi = (int64_t)m;
-  if (f < 0.5) return Tx{mi, mi};
-  if (f > 0.5) return Tx{mi + 1, mi + 1};
-  return Tx{mi + (mi & 1), mi + ((mi + 1) & 1)};  // tie: the result s + inc is even
+  if constexpr (sizeof(WT) == 4) {  // 32-bit integer path: M < 2^24, k <= 25
+    const uint32_t bits = __float_as_uint(w);
+    const int ef = (int)(bits >> 23) & 0xFF;
+    const uint32_t M = ef ? ((bits & 0x7FFFFFu) | 0x800000u) : (bits & 0x7FFFFFu);
+    const int ew = ef ? ef - 127 : -126;
+    if (ew > e) return Tx{PX_SAT, PX_SAT};
+    const int k = e - ew;
+    if (k == 0) return Tx{(int64_t)M, (int64_t)M};
+    if (k > 25) return Tx{0, 0};  // w < u_e / 2
+    const uint32_t q = M >> k, r = M & ((1u << k) - 1u), half = 1u << (k - 1);
+    const int64_t qq = (int64_t)q;
+    if (r != half) {
+      const int64_t v = qq + (r > half);
+      return Tx{v, v};
+    }
+    return Tx{qq + (qq & 1), qq + ((qq + 1) & 1)};  // tie: round half to even makes s + inc even
+  } else {
+    const uint64_t bits = (uint64_t)__double_as_longlong(w);
+    const int ef = (int)(bits >> 52) & 0x7FF;
+    uint64_t M = bits & 0xFFFFFFFFFFFFFull;
+    int ew = -1022;
+    if (ef) { M |= 1ull << 52; ew = ef - 1023; }
+    if (ew > e) return Tx{PX_SAT, PX_SAT};
+    const int k = e - ew;
+    if (k == 0) return Tx{(int64_t)M, (int64_t)M};
+    if (k > 54) return Tx{0, 0};
+    const int64_t q = (int64_t)(M >> k);
+    const uint64_t r = M & ((1ull << k) - 1), half = 1ull << (k - 1);
+    if (r != half) {
+      const int64_t v = q + (r > half);
+      return Tx{v, v};
+    }
+    return Tx{q + (q & 1), q + ((q + 1) & 1)};
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -171,56 +199,200 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_aggregate(const WT* __restric
   if (threadIdx.x == 0) e0_out[c] = e0;
 }
 
-// One warp.  carry[c] / mode[c] receive every chunk's true carry-in and its binade (or
-// PX_EXC when the chunk was scanned sequentially here).
+// The running sum s in units of its binade's spacing (S = the integer significand) and
+// that spacing u_e as a double, by bit manipulation (no division / ldexp on the resolver's
+// critical path).
 template <typename WT>
-__global__ void __launch_bounds__(32) k_px_resolve(const WT* __restrict__ w, int64_t n, int64_t nch,
-                                                   const int32_t* __restrict__ e0, const Tx* __restrict__ agg,
-                                                   WT* carry, int32_t* mode) {
-  constexpr int MANT = PxFp<WT>::MANT;
+__device__ __forceinline__ int64_t px_units(WT s) {
+  if constexpr (sizeof(WT) == 4) {
+    const uint32_t b = __float_as_uint(s);
+    return (int64_t)((b & 0x7FFFFFu) | ((b >> 23) & 0xFFu ? 0x800000u : 0u));
+  } else {
+    const uint64_t b = (uint64_t)__double_as_longlong(s);
+    return (int64_t)((b & 0xFFFFFFFFFFFFFull) | ((b >> 52) & 0x7FFull ? (1ull << 52) : 0ull));
+  }
+}
+__device__ __forceinline__ double px_ulp(int e, int mant) {  // 2^(e - mant), exact
+  const int x = e - mant;
+  return x >= -1022 ? __longlong_as_double((long long)(x + 1023) << 52) : __longlong_as_double(1ll << (x + 1074));
+}
+
+// A chunk the running sum leaves its binade in: numpy's sequential loop, by one warp.  Each
+// lane stages 32 elements in registers; lane 0 adds them in order (IEEE WT adds, the values
+// arriving by shuffle), optionally storing every prefix value.  ~1024 dependent adds: a
+// handful of such chunks per array (the sum crosses each binade once).
+constexpr int PXR_SEG = PX_CHUNK / 32;  // elements per lane
+
+template <typename WT, bool WRITE>
+__device__ WT px_chunk_seq(const WT* __restrict__ w, int64_t n, int64_t c, WT s, WT* __restrict__ cum) {
+  const int lane = threadIdx.x & 31;
+  const int64_t c0 = c * (int64_t)PX_CHUNK;
+  const int len = (int)((n - c0) < PX_CHUNK ? (n - c0) : (int64_t)PX_CHUNK);
+  WT v[PXR_SEG];
+#pragma unroll
+  for (int j = 0; j < PXR_SEG; ++j) v[j] = lane * PXR_SEG + j < len ? w[c0 + lane * PXR_SEG + j] : (WT)0;
+  WT mine[PXR_SEG];
+  for (int l = 0; l < 32; ++l) {
+    if (l * PXR_SEG >= len) break;
+#pragma unroll
+    for (int j = 0; j < PXR_SEG; ++j) {
+      const WT x = __shfl_sync(0xffffffffu, v[j], l);
+      if (l * PXR_SEG + j < len) s = s + x;  // every lane runs the same chain (uniform values)
+      if (lane == l) mine[j] = s;
+    }
+  }
+  if (WRITE) {
+#pragma unroll
+    for (int j = 0; j < PXR_SEG; ++j)
+      if (lane * PXR_SEG + j < len) cum[c0 + lane * PXR_SEG + j] = mine[j];
+  }
+  return s;
+}
+
+// Super-chunks: PX_SUPER consecutive chunks.  Their aggregate for a binade e is the ordered
+// composition of the chunks' aggregates for e (when every chunk carries e among its three
+// candidates).  One warp per super-chunk; candidates E-1, E, E+1 with E the first chunk's e0.
+constexpr int PX_SUPER = 32;
+
+__global__ void __launch_bounds__(32) k_px_super(int64_t nch, const int32_t* __restrict__ e0, const Tx* __restrict__ agg,
+                                                 int32_t* se0, Tx* sagg) {
   const int lane = threadIdx.x;
-  const int64_t lim = ((int64_t)1 << (MANT + 1)) - 1;  // last unit of the binade
+  const int64_t c = (int64_t)blockIdx.x * PX_SUPER + lane;
+  const bool valid = c < nch;
+  const int ec = valid ? e0[c] : 0;
+  const int E = __shfl_sync(0xffffffffu, ec, 0);
+#pragma unroll
+  for (int k = 0; k < PX_CAND; ++k) {
+    const int e = E - 1 + k, kk = e - (ec - 1);
+    Tx t{0, 0};  // chunks past the end: identity
+    if (valid) t = (kk >= 0 && kk < PX_CAND) ? agg[c * PX_CAND + kk] : Tx{PX_SAT, PX_SAT};
+    t = px_warp_reduce(t);
+    if (lane == 0) sagg[(int64_t)blockIdx.x * PX_CAND + k] = t;
+  }
+  if (lane == 0) se0[blockIdx.x] = E;
+}
+
+// One window of up to 32 consecutive units (super-chunks or chunks) from carry-in s: lane l
+// takes unit u0 + l (if u0 + l < uend) with its e0 / aggregates; returns the number f of
+// leading units whose composed sum stays inside s's binade, the carry-in of lane l's unit
+// (units of u_e, valid for l < f) and the carry-out after unit f-1.
+struct PxWin {
+  int f;
+  int e;
+  double ue;
+  int64_t carry_units;  // this lane's carry-in, in units of u_e
+  int64_t out_units;    // carry-out of unit f-1 (all lanes)
+};
+
+template <typename WT>
+__device__ __forceinline__ PxWin px_window(WT s, int64_t u0, int64_t uend, const int32_t* __restrict__ e0s,
+                                           const Tx* __restrict__ aggs) {
+  constexpr int MANT = PxFp<WT>::MANT;
+  const int lane = threadIdx.x & 31;
+  const int64_t lim = ((int64_t)1 << (MANT + 1)) - 1;
+  PxWin r;
+  const bool fin = isfinite((double)s);
+  r.e = PxFp<WT>::expo(s);
+  r.ue = px_ulp(r.e, MANT);
+  const int64_t S = fin ? px_units<WT>(s) : 0, p = S & 1;
+  const int64_t u = u0 + lane;
+  const bool valid = u < uend;
+  const int k = valid ? r.e - (e0s[u] - 1) : -1;
+  const bool has = fin && valid && k >= 0 && k < PX_CAND;
+  const Tx t = has ? aggs[u * PX_CAND + k] : Tx{PX_SAT, PX_SAT};
+  const Tx P = px_warp_scan(t);
+  Tx Q;
+  Q.a0 = __shfl_up_sync(0xffffffffu, P.a0, 1);
+  Q.a1 = __shfl_up_sync(0xffffffffu, P.a1, 1);
+  if (lane == 0) Q = Tx{0, 0};
+  const int64_t out = S + px_apply(P, p);
+  const unsigned bad = __ballot_sync(0xffffffffu, !(has && out <= lim));
+  r.f = bad ? __ffs(bad) - 1 : 32;
+  r.carry_units = S + px_apply(Q, p);
+  r.out_units = r.f > 0 ? __shfl_sync(0xffffffffu, out, r.f - 1) : S;
+  return r;
+}
+
+// One warp.  Walks super-chunks 32 at a time; a super-chunk the sum leaves its binade in is
+// descended into (chunk windows); a chunk the sum leaves its binade in is summed
+// sequentially (px_chunk_seq).  Writes smode[sp] = binade e and scarry[sp] for every
+// super-chunk resolved whole (its chunks' carry-ins are expanded by k_px_expand), and
+// carry[c] / mode[c] for the chunks of descended super-chunks (PX_EXC for the sequential
+// ones, also listed in exc_list[1..exc_list[0]]).
+constexpr int32_t PX_DESC = -200000;  // smode: descended into
+
+template <typename WT>
+__global__ void __launch_bounds__(32) k_px_resolve(const WT* __restrict__ w, int64_t n, int64_t nch, int64_t nsup,
+                                                   const int32_t* __restrict__ e0, const Tx* __restrict__ agg,
+                                                   const int32_t* __restrict__ se0, const Tx* __restrict__ sagg,
+                                                   WT* carry, int32_t* mode, WT* scarry, int32_t* smode,
+                                                   int32_t* exc_list) {
+  const int lane = threadIdx.x;
   WT s = (WT)0;
-  int64_t c = 0;
-  while (c < nch) {
-    const int e = PxFp<WT>::expo(s);
-    const double ue = ldexp(1.0, e - MANT);
-    const int64_t S = isfinite((double)s) ? (int64_t)((double)s / ue) : 0;  // exact: s is a whole number of u_e
-    const int64_t p = S & 1;
-    const int64_t cc = c + lane;
-    const bool valid = cc < nch;
-    const int k = valid ? e - (e0[cc] - 1) : -1;
-    const bool has = valid && k >= 0 && k < PX_CAND && isfinite((double)s);
-    Tx t = has ? agg[cc * PX_CAND + k] : Tx{PX_SAT, PX_SAT};
-    const Tx P = px_warp_scan(t);
-    Tx Q;
-    Q.a0 = __shfl_up_sync(0xffffffffu, P.a0, 1);
-    Q.a1 = __shfl_up_sync(0xffffffffu, P.a1, 1);
-    if (lane == 0) Q = Tx{0, 0};
-    const int64_t out = S + px_apply(P, p);
-    const bool safe = has && out <= lim;
-    const unsigned bad = __ballot_sync(0xffffffffu, !safe);
-    const int f = bad ? __ffs(bad) - 1 : 32;  // chunks c .. c+f-1 stay inside binade e
-    if (lane < f) {
-      carry[cc] = (WT)((double)(S + px_apply(Q, p)) * ue);
-      mode[cc] = e;
+  int64_t sp = 0;
+  int32_t nexc = 0;
+  while (sp < nsup) {
+    const PxWin r = px_window<WT>(s, sp, nsup, se0, sagg);
+    if (lane < r.f) {
+      scarry[sp + lane] = (WT)((double)r.carry_units * r.ue);
+      smode[sp + lane] = r.e;
     }
-    if (f > 0) {
-      const int64_t last = __shfl_sync(0xffffffffu, out, f - 1);
-      s = (WT)((double)last * ue);
-    }
-    c += f;
-    if (f < 32 && c < nch) {  // chunk c leaves binade e (or lacks its aggregate): sequential
-      WT t2 = s;
-      if (lane == 0) {
-        carry[c] = s;
-        mode[c] = PX_EXC;
-        const int64_t end = min(n, (c + 1) * (int64_t)PX_CHUNK);
-        for (int64_t q = c * (int64_t)PX_CHUNK; q < end; ++q) t2 = t2 + w[q];
+    if (r.f > 0) s = (WT)((double)r.out_units * r.ue);
+    sp += r.f;
+    if (r.f == 32 || sp >= nsup) continue;
+    // descend into super-chunk sp
+    if (lane == 0) smode[sp] = PX_DESC;
+    int64_t c = sp * PX_SUPER;
+    const int64_t cend = min(nch, c + PX_SUPER);
+    while (c < cend) {
+      const PxWin q = px_window<WT>(s, c, cend, e0, agg);
+      if (lane < q.f) {
+        carry[c + lane] = (WT)((double)q.carry_units * q.ue);
+        mode[c + lane] = q.e;
       }
-      s = __shfl_sync(0xffffffffu, t2, 0);
-      c += 1;
+      if (q.f > 0) s = (WT)((double)q.out_units * q.ue);
+      c += q.f;
+      if (c < cend) {  // chunk c leaves its binade: sequential
+        if (lane == 0) {
+          carry[c] = s;
+          mode[c] = PX_EXC;
+          exc_list[1 + nexc] = (int32_t)c;
+        }
+        ++nexc;
+        s = px_chunk_seq<WT, false>(w, n, c, s, nullptr);
+        ++c;
+      }
     }
+    ++sp;
+  }
+  if (lane == 0) exc_list[0] = nexc;
+}
+
+// carry-ins of the chunks of every super-chunk resolved whole: ordered scan of the chunk
+// aggregates in the super-chunk's binade from its carry-in (one warp per super-chunk)
+template <typename WT>
+__global__ void __launch_bounds__(32) k_px_expand(int64_t nch, const int32_t* __restrict__ e0,
+                                                  const Tx* __restrict__ agg, const WT* __restrict__ scarry,
+                                                  const int32_t* __restrict__ smode, WT* carry, int32_t* mode) {
+  constexpr int MANT = PxFp<WT>::MANT;
+  const int e = smode[blockIdx.x];
+  if (e == PX_DESC) return;
+  const int lane = threadIdx.x;
+  const WT s = scarry[blockIdx.x];
+  const int64_t S = px_units<WT>(s), p = S & 1;
+  const double ue = px_ulp(e, MANT);
+  const int64_t c = (int64_t)blockIdx.x * PX_SUPER + lane;
+  const bool valid = c < nch;
+  Tx t{0, 0};
+  if (valid) t = agg[c * PX_CAND + (e - (e0[c] - 1))];  // present: the super-chunk aggregate was
+  const Tx P = px_warp_scan(t);
+  Tx Q;
+  Q.a0 = __shfl_up_sync(0xffffffffu, P.a0, 1);
+  Q.a1 = __shfl_up_sync(0xffffffffu, P.a1, 1);
+  if (lane == 0) Q = Tx{0, 0};
+  if (valid) {
+    carry[c] = (WT)((double)(S + px_apply(Q, p)) * ue);
+    mode[c] = e;
   }
 }
 
@@ -234,20 +406,10 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_materialize(const WT* __restr
   const int md = mode[c];
   const WT s0 = carry[c];
   const int64_t base = c * PX_CHUNK + threadIdx.x * PX_PER_THREAD;
-  if (md == PX_EXC) {  // sequential (one thread), as numpy
-    if (threadIdx.x == 0) {
-      WT s = s0;
-      const int64_t end = min(n, (c + 1) * (int64_t)PX_CHUNK);
-      for (int64_t q = c * (int64_t)PX_CHUNK; q < end; ++q) {
-        s = s + w[q];
-        cum[q] = s;
-      }
-    }
-    return;
-  }
+  if (md == PX_EXC) return;  // binade crossings: k_px_materialize_exc
   const int e = md;
-  const double ue = ldexp(1.0, e - MANT);
-  const int64_t S = (int64_t)((double)s0 / ue);
+  const double ue = px_ulp(e, MANT);
+  const int64_t S = px_units<WT>(s0);
   WT v[PX_PER_THREAD];
   Tx te[PX_PER_THREAD];
   Tx t{0, 0};
@@ -277,12 +439,28 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_materialize(const WT* __restr
   }
 }
 
+// the binade-crossing chunks: one warp each, writing every value (separate launch, so the
+// warp routine's registers do not limit the block scan's occupancy)
+template <typename WT>
+__global__ void __launch_bounds__(32) k_px_materialize_exc(const WT* __restrict__ w, int64_t n,
+                                                          const WT* __restrict__ carry,
+                                                          const int32_t* __restrict__ exc_list, WT* __restrict__ cum) {
+  const int cnt = exc_list[0];
+  for (int q = blockIdx.x; q < cnt; q += gridDim.x) {
+    const int64_t c = exc_list[1 + q];
+    px_chunk_seq<WT, true>(w, n, c, carry[c], cum);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Searches.  multinomial (M/resample.py:295-304): key_i = WT(uniform01_at(seed, i, 0) *
 // total), ancestor = searchsorted(cum, key_i, "right") clamped to n-1.
 // systematic_improved (M/resample.py:307-336): target_i = (i + u0) / n * total (float64),
 // ancestor = first a with float64(cum[a]) >= target_i, else n-1.
 
+// Plain per-particle binary searches over the prefix sum (L2-resident at 2^24 float32):
+// latency is hidden by occupancy.  A shared-memory top-level table was tried and lost
+// (random smem probes bank-conflict; fewer resident warps).
 template <typename WT>
 __global__ void k_multinomial(const WT* __restrict__ cum, int64_t n, uint64_t base, int64_t p0, int64_t p_end,
                               int64_t* __restrict__ anc) {

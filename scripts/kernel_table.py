@@ -87,4 +87,16 @@ for row_bytes in (8, 32):
     out = torch.empty_like(states)
     add(f"gather rows of {row_bytes} B", timeit(lambda: _lib.check(L.mgp_gather(D.ptr(states), row_bytes, D.ptr(anc), n, D.ptr(out), sp))),
         8 * n + 2 * row_bytes * n)
+# prefix-sum resamplers (M/resample.py:285-336): exact sequential-order np.cumsum + searches
+cum = torch.empty(n, dtype=torch.float32, device="cuda")
+add("cumsum f32 (np.cumsum order, exact)", timeit(lambda: _lib.check(L.mgp_cumsum(D.ptr(w), 0, n, D.ptr(cum), sp))),
+    8 * n, "read w + write prefix (the pipeline reads w three times)")
+w64 = w.double()
+cum64 = torch.empty(n, dtype=torch.float64, device="cuda")
+add("cumsum f64 (np.cumsum order, exact)", timeit(lambda: _lib.check(L.mgp_cumsum(D.ptr(w64), 1, n, D.ptr(cum64), sp))),
+    16 * n)
+for kind in ("multinomial", "systematic"):
+    fn = L.mgp_multinomial if kind == "multinomial" else L.mgp_systematic
+    ms = timeit(lambda fn=fn: _lib.check(fn(D.ptr(w), 0, n, 7, D.ptr(anc), sp)))
+    add(f"{kind} f32 (cumsum + binary search)", ms, 8 * n + 8 * n, f"{n / (ms * 1e-3):.3e} particles/s")
 print(json.dumps({"n": n, "y": a.y, "B": b, "peak_hbm_gbs": peak, "rows": rows}, indent=1))
