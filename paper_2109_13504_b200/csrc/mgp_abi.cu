@@ -186,14 +186,19 @@ int launch_mego_w32(const ResampleArgs& a, const OffChunk& oc, cudaStream_t st) 
   const unsigned grid = (unsigned)((a.p_end - a.p0 + RS_THREADS - 1) / RS_THREADS);
   constexpr int PPT = mego_ppt<RNG>();
   if constexpr (POW2 && PPT == 4) {
-    // full-range launch over N = 2^k >= 256: the half-split variant (j(i + N/2) = j(i) ^ N/2)
-    if (a.p0 == 0 && a.p_end == a.n && a.n >= 256) {
+    // N = 2^k >= 256, full range or an explicit lower-half range (a.half): the half-split
+    // variant (j(i + N/2) = j(i) ^ N/2); particles i and i + N/2 for i in [p0, p_end)
+    if (a.half || (a.p0 == 0 && a.p_end == a.n && a.n >= 256)) {
+      ResampleArgs h = a;
+      if (!a.half) { h.p0 = 0; h.p_end = a.n / 2; }
+      const unsigned hgrid = (unsigned)((h.p_end - h.p0) / 128);
+      if (hgrid == 0) return 0;
       if constexpr (RNG == RNG_PHILOX && sizeof(WT) == 4 && NZ && TEX) {
-        k_megopolis_philox_half<<<a.n / RS_THREADS, 64, 0, st>>>(a, oc);
+        k_megopolis_philox_half<<<hgrid, 64, 0, st>>>(h, oc);
         LAUNCH_CHECK("k_megopolis_philox_half");
         return 0;
       }
-      k_megopolis_w32<RNG, WT, POW2, NZ, TEX, PPT, true><<<a.n / RS_THREADS, RS_THREADS / PPT, 0, st>>>(a, oc);
+      k_megopolis_w32<RNG, WT, POW2, NZ, TEX, PPT, true><<<hgrid, RS_THREADS / PPT, 0, st>>>(h, oc);
       LAUNCH_CHECK("k_megopolis_w32");
       return 0;
     }
@@ -329,7 +334,15 @@ struct Plan {
   int64_t* d_off = nullptr;  // device copy for the generic path
   int32_t* kstate = nullptr;
   void* cum = nullptr;       // inclusive prefix sum (multinomial / systematic)
+  bool half = false;         // run_range ranges are lower-half ranges of the half-split kernel
 };
+
+// The half-split Megopolis kernel applies: W = 32, N = 2^k >= 256, 4 particles per thread
+// (the Philox stream), offsets in one launch.
+bool plan_half_ok(const Plan& p) {
+  return p.kind == MGP_KIND_MEGOPOLIS && p.warp == 32 && p.rng == MGP_RNG_PHILOX && p.n >= 256 &&
+         (p.n & (p.n - 1)) == 0 && p.b <= OFF_CAP;
+}
 
 bool is_prefix_kind(int kind) { return kind == MGP_KIND_MULTINOMIAL || kind == MGP_KIND_SYSTEMATIC; }
 
@@ -433,6 +446,7 @@ int run_range(Plan& p, int64_t p0, int64_t p_end, int64_t* anc, cudaStream_t st)
   a.kstate = p.kstate;
   a.anc = anc;
   a.one = 1;
+  a.half = p.half ? 1 : 0;
   {
     uint32_t k0 = (uint32_t)p.seed, k1 = (uint32_t)(p.seed >> 32);
     for (int r = 0; r < 10; ++r) { a.pk0[r] = k0; a.pk1[r] = k1; k0 += PHILOX_W0; k1 += PHILOX_W1; }
@@ -538,6 +552,31 @@ int plan_free(Plan& p, cudaStream_t st) {
   p.d_off = nullptr;
   p.kstate = nullptr;
   p.cum = nullptr;
+  return 0;
+}
+
+// Per-thread, per-device streams and events of the host-buffer path, created once (stream
+// and event creation would otherwise cost tens of microseconds per call).
+struct HostCtx {
+  int dev;
+  cudaStream_t st, st2, cp;
+  std::vector<cudaEvent_t> ev;
+};
+thread_local std::vector<HostCtx*> g_host_ctx;
+
+int host_ctx(HostCtx** out) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  for (HostCtx* c : g_host_ctx)
+    if (c->dev == dev) { *out = c; return 0; }
+  HostCtx* c = new HostCtx{dev, nullptr, nullptr, nullptr, {}};
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->cp, cudaStreamNonBlocking));
+  c->ev.resize(40);  // > 2 * 16 chunk events + 1: an event is never re-recorded while awaited
+  for (auto& e : c->ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  g_host_ctx.push_back(c);
+  *out = c;
   return 0;
 }
 
@@ -653,9 +692,10 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
   if (n > MAX_N) return set_err(MGP_EUNSUPPORTED, "N exceeds 2^31-1");
   if (device >= 0) CUDA_TRY(cudaSetDevice(device));
   ensure_pool();
-  cudaStream_t st, cp;
-  CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  CUDA_TRY(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
+  HostCtx* hc = nullptr;
+  if (int rc0 = host_ctx(&hc)) return rc0;
+  cudaStream_t st = hc->st, st2 = hc->st2, cp = hc->cp;
+  size_t next_ev = 0;
   const size_t wbytes = (size_t)n * (dtype == MGP_F32 ? 4 : 8);
   void* d_w = nullptr;
   int64_t* d_anc = nullptr;
@@ -663,19 +703,17 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
   mgp_weight_stats_t hs{};
   int rc = 0;
   Plan p;
-  std::vector<cudaEvent_t> evs;
   auto cleanup = [&]() {
     cudaStreamSynchronize(cp);
+    cudaStreamSynchronize(st2);
     cudaStreamSynchronize(st);
     if (d_w) cudaFreeAsync(d_w, st);
     if (d_anc) cudaFreeAsync(d_anc, st);
     if (d_stats) cudaFreeAsync(d_stats, st);
     plan_free(p, st);
     cudaStreamSynchronize(st);
-    for (auto e : evs) cudaEventDestroy(e);
-    cudaStreamDestroy(cp);
-    cudaStreamDestroy(st);
   };
+  auto new_event = [&]() { return hc->ev[next_ev++ % hc->ev.size()]; };
 #define HTRY(x)                 \
   do {                          \
     rc = (x);                   \
@@ -704,6 +742,35 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
   HTRY(plan_alloc(p, st));
   // Overlap the ancestor download with the remaining compute: particle chunks are
   // independent given (w, offsets, seed); each chunk's D2H waits only on its kernel.
+  if (plan_half_ok(p)) {  // half-split kernel: chunk c = lower-half range [c0, c1) + its mirror
+    p.half = true;
+    const int64_t half = n / 2;
+    const int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(16, n >> 20));
+    int64_t step = (half + nchunk - 1) / nchunk;
+    step = (step + 127) / 128 * 128;
+    // chunk kernels alternate between two streams so each one's drain overlaps the next
+    // one's start (they are independent given the weights and offsets)
+    cudaEvent_t ready = new_event();
+    HCUDA(cudaEventRecord(ready, st));
+    HCUDA(cudaStreamWaitEvent(st2, ready, 0));
+    int k = 0;
+    for (int64_t c0 = 0; c0 < half; c0 += step, ++k) {
+      const int64_t c1 = std::min(half, c0 + step);
+      cudaStream_t ks = (k & 1) ? st2 : st;
+      HTRY(run_range(p, c0, c1, d_anc, ks));
+      cudaEvent_t ev = new_event();
+      HCUDA(cudaEventRecord(ev, ks));
+      HCUDA(cudaStreamWaitEvent(cp, ev, 0));
+      HCUDA(cudaMemcpyAsync(h_anc + c0, d_anc + c0, sizeof(int64_t) * (c1 - c0), cudaMemcpyDeviceToHost, cp));
+      HCUDA(cudaMemcpyAsync(h_anc + half + c0, d_anc + half + c0, sizeof(int64_t) * (c1 - c0),
+                            cudaMemcpyDeviceToHost, cp));
+    }
+    HCUDA(cudaStreamSynchronize(cp));
+    HCUDA(cudaStreamSynchronize(st2));
+    HCUDA(cudaStreamSynchronize(st));
+    cleanup();
+    return 0;
+  }
   const bool chunkable = !(plan_uses_w32(p) && p.kind == MGP_KIND_MEGOPOLIS && p.b > OFF_CAP);
   // ~16 chunks of >= 2^20 particles: the D2H tail after the last kernel is ~1/16 of the download
   const int64_t nchunk = chunkable ? std::max<int64_t>(1, std::min<int64_t>(16, n >> 20)) : 1;
@@ -712,9 +779,7 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
   for (int64_t c0 = 0; c0 < n; c0 += step) {
     const int64_t c1 = std::min(n, c0 + step);
     HTRY(run_range(p, c0, c1, d_anc, st));
-    cudaEvent_t ev;
-    HCUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    evs.push_back(ev);
+    cudaEvent_t ev = new_event();
     HCUDA(cudaEventRecord(ev, st));
     HCUDA(cudaStreamWaitEvent(cp, ev, 0));
     HCUDA(cudaMemcpyAsync(h_anc + c0, d_anc + c0, sizeof(int64_t) * (c1 - c0), cudaMemcpyDeviceToHost, cp));

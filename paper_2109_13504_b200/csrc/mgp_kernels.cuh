@@ -41,6 +41,7 @@ struct ResampleArgs {
   int64_t* anc;      // output ancestors
   cudaTextureObject_t tex;  // float32 weights as a 1-D linear texture (0: use LDG)
   uint32_t one;             // = 1; an opaque multiplier keeps the 64-bit key add on the FMA pipe
+  int half;                 // half-split launch: [p0, p_end) is a range of LOWER-half particles
   uint32_t pk0[10], pk1[10];  // Philox round keys (uniform; constant bank)
 };
 
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(RS_THREADS / PPT, PPT == 1 ? 0 : 1) k_megopoli
   static_assert(!HALF || (PPT == 4 && POW2), "HALF needs PPT 4 and a power-of-two N");
   constexpr int STRIDE = HALF ? 64 : RS_THREADS / PPT;
   const uint32_t half = a.n >> 1;
-  const uint32_t i0 = HALF ? blockIdx.x * 128 + threadIdx.x : a.p0 + blockIdx.x * RS_THREADS + threadIdx.x;
+  const uint32_t i0 = HALF ? a.p0 + blockIdx.x * 128 + threadIdx.x : a.p0 + blockIdx.x * RS_THREADS + threadIdx.x;
   if (!HALF && i0 >= a.p_end) return;
   const WT* __restrict__ w = reinterpret_cast<const WT*>(a.w);
   const uint32_t lane = threadIdx.x & 31u, n = a.n;
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(64, 1) k_megopolis_philox_half(const __grid_co
                                                                  const __grid_constant__ OffChunk oc) {
   constexpr int PPT = 4;
   const uint32_t half = a.n >> 1;
-  const uint32_t i0 = blockIdx.x * 128 + threadIdx.x;
+  const uint32_t i0 = a.p0 + blockIdx.x * 128 + threadIdx.x;  // p0: lower-half start (multiple of 128)
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t cmask = (a.n - 1) & ~31u;
   uint32_t ii[PPT];
