@@ -318,7 +318,7 @@ def main():
     # full-range Philox launches take the specialised half-split kernel; rank slices (N > 1)
     # and the megores stream take k_megopolis_w32
     if args.rng == "philox":
-        mego_kernel = "k_megopolis_philox_half" if world == 1 else "k_megopolis_w32<philox, 4 particles/thread>"
+        mego_kernel = "k_megopolis_w32<philox, half-split, 4 particles/thread>" if world == 1 else "k_megopolis_w32<philox, 4 particles/thread>"
     else:
         mego_kernel = "k_megopolis_w32<megores, 1 particle/thread>"
     traffic = None

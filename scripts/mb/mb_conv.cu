@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_dup(const __grid_constant__
 // Full-range variant: thread owns particles {i, i+64, i+N/2, i+N/2+64}.  Partners of
 // i + N/2 are those of i with the top index bit flipped: j(i + N/2) = j(i) ^ N/2.
 // GEN: general launch state (first/kstate/last, tail rounds).
-template <int MINB, bool GEN = false, bool ONELOOP = false>
+template <int MINB, bool GEN = false, bool ONELOOP = false, bool KST = true>
 __global__ void __launch_bounds__(64, MINB) k_x2(const __grid_constant__ ResampleArgs a, const __grid_constant__ OffChunk oc) {
   constexpr int PPT = 4;
   const uint32_t half = a.n >> 1;
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(64, MINB) k_x2(const __grid_constant__ Resampl
   const uint32_t ial0 = i0 - lane, ial1 = ial0 + 64;
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
-    const uint32_t k0 = GEN ? (a.first ? ii[p] : (uint32_t)a.kstate[ii[p]]) : ii[p];
+    const uint32_t k0 = (GEN && KST) ? (a.first ? ii[p] : (uint32_t)a.kstate[ii[p]]) : ii[p];
     wkd[p] = (double)tex1Dfetch<float>(a.tex, (int)k0);
     bstar[p] = -1;
   }
@@ -210,9 +210,9 @@ __global__ void __launch_bounds__(64, MINB) k_x2(const __grid_constant__ Resampl
   }
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
-    uint32_t k = GEN ? (a.first ? ii[p] : (uint32_t)a.kstate[ii[p]]) : ii[p];
+    uint32_t k = (GEN && KST) ? (a.first ? ii[p] : (uint32_t)a.kstate[ii[p]]) : ii[p];
     if (bstar[p] >= 0) { const uint2 o = oc.o[bstar[p]]; k = mux3((ii[p] - lane) + o.x, lane + o.y, cmask); }
-    if (!GEN || a.last) a.anc[ii[p]] = (int64_t)k;
+    if (!GEN || !KST || a.last) a.anc[ii[p]] = (int64_t)k;
     else a.kstate[ii[p]] = (int32_t)k;
   }
 }
@@ -289,9 +289,9 @@ int main(int argc, char** argv) {
   RUN(4, 1, 0, 1, 0);
   check("lib HALF", time_it([&]() { k_megopolis_w32<1, float, true, true, true, 4, true><<<n / 256, 64>>>(b, oc); }, 9));
   check("x2 p4", time_it([&]() { k_x2<1><<<n / 256, 64>>>(b, oc); }, 9));
-  check("lib philox_half", time_it([&]() { k_megopolis_philox_half<<<n / 256, 64>>>(b, oc); }, 9));
   check("x2 gen", time_it([&]() { k_x2<1, true><<<n / 256, 64>>>(b, oc); }, 9));
-  check("x2 gen1loop", time_it([&]() { k_x2<1, true, true><<<n / 256, 64>>>(b, oc); }, 9));
+  check("x2 gen nokst", time_it([&]() { k_x2<1, true, false, false><<<n / 256, 64>>>(b, oc); }, 9));
+  check("x2 gen", time_it([&]() { k_x2<1, true><<<n / 256, 64>>>(b, oc); }, 9));
   {
     float* w2;
     CK(cudaMalloc(&w2, sizeof(float) * 2 * n));
