@@ -10,3 +10,4 @@ ncu --set full --clock-control none --import-source on -k regex:k_megopolis -s 1
 ncu --set full --clock-control none --import-source on -k regex:k_megopolis -s 1 -c 1 -o gpurun_out/prof_megores \
     python scripts/prof_step.py --steps 2 --rng megores > gpurun_out/ncu_megores.log 2>&1
 ls gpurun_out
+timeout 600 python scripts/kernel_table.py > gpurun_out/kernel_table.json 2> gpurun_out/kernel_table.err
