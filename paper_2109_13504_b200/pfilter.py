@@ -164,8 +164,9 @@ def _resample_device(cfg: FilterConfig, w, b: int, seed):
     n = w.numel()
     anc = t.empty(n, dtype=t.int64, device=w.device)
     kind = cfg.resampler
-    if kind not in METROPOLIS_FAMILY:
-        raise NotImplementedError(f"{kind!r} is not a Metropolis-family resampler (SURVEY 8f)")
+    if kind not in _lib.KIND:
+        raise ValueError(f"unknown resampler {kind!r}")
+    prefix = kind not in METROPOLIS_FAMILY  # multinomial / systematic ignore b (M/resample.py:450-454)
     flags = _lib.FLAG_NONZERO if cfg.precision == "double" else 0  # float32 cast can underflow to 0
     if cfg.precision == "single":  # _check_weights (M/resample.py:96-100) inside the resampler
         from .weights import device_stats
@@ -173,8 +174,9 @@ def _resample_device(cfg: FilterConfig, w, b: int, seed):
         if device_stats(w).n_pos == 0:
             raise ValueError("all weights are zero")
     _lib.check(_lib.lib().mgp_resample_range(
-        _lib.KIND[kind], D.ptr(w), D.wdtype(w), n, int(b), int(seed) & (2**64 - 1), cfg.warp.warp_size,
-        int(cfg.partition_bytes or 0), 1, _lib.RNG[cfg.rng], flags, 0, n, D.ptr(anc), D.stream_ptr()))
+        _lib.KIND[kind], D.ptr(w), D.wdtype(w), n, 1 if prefix else int(b), int(seed) & (2**64 - 1),
+        cfg.warp.warp_size, int(cfg.partition_bytes or 0), 1, _lib.RNG["megores" if prefix else cfg.rng], flags, 0, n,
+        D.ptr(anc), D.stream_ptr()))
     return anc
 
 
@@ -243,9 +245,8 @@ def run_benchmark(base_cfg: FilterConfig, trajectories, runs_per_trajectory: int
     """RMSE and mean resample ratio per (algorithm, B) (M/pfilter.py:182-226)."""
     rows = []
     for name, part_bytes in algorithms:
-        if name not in METROPOLIS_FAMILY:
-            raise NotImplementedError(f"{name!r} is not a Metropolis-family resampler (SURVEY 8f)")
-        for b in list(b_values):
+        # prefix-sum resamplers ignore B and report b = 0 (M/pfilter.py:191-196)
+        for b in (list(b_values) if name in METROPOLIS_FAMILY else [0]):
             cfg = replace(base_cfg, resampler=name, partition_bytes=part_bytes, b_fixed=b if b > 0 else None)
             per_traj, ratios = [], []
             for ti, traj in enumerate(trajectories):

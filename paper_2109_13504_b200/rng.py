@@ -64,3 +64,17 @@ def gaussian_at(seed, lane, counter, mean=0.0, stddev=1.0):  # M/rng.py:152-161
     u2 = (h2 >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
     z = np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * np.pi * u2)
     return mean + stddev * z
+
+
+def uniform01_at(seed, lane, counter):  # M/rng.py:128-131
+    import numpy as np
+
+    h = _hash_np(seed, lane, counter)
+    return (h >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+
+
+def uniform_open01_at(seed, lane, counter):  # M/rng.py:134-137
+    import numpy as np
+
+    h = _hash_np(seed, lane, counter)
+    return ((h >> np.uint64(11)).astype(np.float64) + 0.5) * (1.0 / 9007199254740992.0)

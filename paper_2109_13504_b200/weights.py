@@ -189,3 +189,40 @@ def gen_gaussian_weights(params: GaussianWeightParams, seed, precision="single",
         _lib.check(_lib.lib().mgp_gen_gaussian(float(params.y), params.n, int(seed) & (2**64 - 1),
                                                D.wdtype(out), D.ptr(out), D.stream_ptr()))
     return WeightVector(out, precision)
+
+
+# ---------------------------------------------------------------------------
+# Host generators: the reference's own formulas in numpy (input synthesis for the CLI's
+# experiment grids, so the weights -- and every downstream result -- match the reference
+# bit for bit).  The hot path never calls these.
+
+
+@dataclass(frozen=True)
+class GammaWeightParams:  # M/weights.py:77-86
+    alpha: float
+    beta: float
+    n: int
+
+    def __post_init__(self):
+        if self.alpha <= 0 or self.beta <= 0:
+            raise ValueError(f"alpha and beta must be > 0, got {self.alpha}, {self.beta}")
+        if self.n < 1:
+            raise ValueError(f"n must be >= 1, got {self.n}")
+
+
+def gen_gaussian_weights_host(params: GaussianWeightParams, seed, precision="single") -> WeightVector:
+    """M/weights.py:100-104 in numpy: w = exp(-(x - y)^2 / 2) / sqrt(2 pi), x = gaussian_at(seed, i, 0)."""
+    from .rng import gaussian_at
+
+    x = gaussian_at(seed, np.arange(params.n), 0)
+    return WeightVector(np.exp(-0.5 * (x - params.y) ** 2) * GAUSSIAN_PEAK, precision)
+
+
+def gen_gamma_weights(params: GammaWeightParams, seed, precision="single") -> WeightVector:
+    """I.i.d. gamma(alpha, rate=beta) weights by inverse-CDF sampling (M/weights.py:107-111)."""
+    from scipy import stats
+
+    from .rng import uniform_open01_at
+
+    u = uniform_open01_at(seed, np.arange(params.n), 0)
+    return WeightVector(stats.gamma.ppf(u, a=params.alpha, scale=1.0 / params.beta), precision)
