@@ -64,6 +64,17 @@ __device__ __forceinline__ bool accept_w(double u, WT wk, WT wj) {
   else return le && !(wj == (WT)0 && wk == (WT)0);
 }
 
+// accept j for a Philox word (u = word * 2^-32): fl(u * wk) as one DFMA on 1 + u (exact),
+// see u1_from_word below; same binary64 value as accept_w((double)word * 2^-32, wk, wj).
+__device__ __forceinline__ double u1_from_word(uint32_t w);
+template <bool NOZERO, typename WT>
+__device__ __forceinline__ bool accept_word(uint32_t word, WT wk, WT wj) {
+  const double wkd = (double)wk;
+  const bool le = fma(u1_from_word(word), wkd, -wkd) <= (double)wj;
+  if constexpr (NOZERO) return le;
+  else return le && !(wj == (WT)0 && wk == (WT)0);
+}
+
 // (a & c) | (b & ~c) in one LOP3
 __device__ __forceinline__ uint32_t mux3(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
@@ -290,7 +301,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_metropolis(const __grid_constant
           const uint32_t wu = h == 0 ? blk.x : blk.z, wjw = h == 0 ? blk.y : blk.w;
           const uint32_t j = __umulhi(wjw, n);
           const WT wj = __ldg(w + j);
-          if (accept_w<NOZERO>((double)wu * 0x1p-32, wk, wj)) { wk = wj; k = j; }
+          if (accept_word<NOZERO>(wu, wk, wj)) { wk = wj; k = j; }
           ++t;
         }
       }
@@ -370,7 +381,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_c12_w32(const __grid_constant__ 
           const uint32_t wu = h == 0 ? blk.x : blk.z, wjw = h == 0 ? blk.y : blk.w;
           const uint32_t jl = __umulhi(wjw, n_w);
           const WT wj = (STAGE && !C2) ? part[jl] : __ldg(w + lo + jl);
-          if (accept_w<NOZERO>((double)wu * 0x1p-32, wk, wj)) { wk = wj; k = lo + jl; }
+          if (accept_word<NOZERO>(wu, wk, wj)) { wk = wj; k = lo + jl; }
           ++t;
         }
       }

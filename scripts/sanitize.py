@@ -30,6 +30,16 @@ for n, prec in [(4096, "single"), (3 * 1024, "double"), (96, "single"), (33, "si
         acc.add(mg.ancestors_to_offspring(mg.megopolis(wd, 5, mg.WarpConfig(1), seed=k), n), wd)
     acc.finalize()
     mg.megopolis(w, 5, mg.WarpConfig(1), seed=1)  # host-buffer path
+# prefix sums: binade crossings (ones), rounding ties (dyadic), f64, partial chunks
+for w in (np.ones(40000, np.float32), (rr.integers(1, 8, 70001) / 4.0).astype(np.float32), rr.random(5000),
+          rr.random(1025).astype(np.float32)):
+    wd = torch.from_numpy(w).cuda()
+    mg.inclusive_prefix(wd)
+    mg.multinomial(wd, 3)
+    mg.systematic_improved(wd, 3)
+mg.multinomial(np.ones(3000, np.float32), 1)  # host path
+# half-split Megopolis through the chunked host path (Philox, N = 2^k)
+mg.megopolis(rr.random(1 << 12).astype(np.float32), 7, seed=5, rng="philox")
 shards = [torch.rand(100, 2, device="cuda") for _ in range(4)]
 gather_from_peers(shards, 100, torch.from_numpy(rr.integers(0, 400, 300)))
 traj = pf.generate_trajectory(3, 0.0, 1)
