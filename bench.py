@@ -232,6 +232,11 @@ def main():
     else:
         local_w = full
     stats = torch.empty(8, dtype=torch.float64, device=dev)
+    from paper_2109_13504_b200.distributed import combine_slice_stats, slice_tree_aligned
+    from paper_2109_13504_b200.weights import WeightStats
+
+    aligned = slice_tree_aligned(world, n_loc)
+    stats_all = torch.empty(world * 8, dtype=torch.int64, device=dev)
     anc = torch.empty(n_loc, dtype=torch.int64, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -247,12 +252,27 @@ def main():
 
         def step(ev=None):
             """One hot-path pass: (all-gather) -> stats -> B -> megopolis(slice)."""
-            gather_weights()
-            _lib.check(L.mgp_weight_stats(D.ptr(full), 0, n_glob, D.ptr(stats), sp))
-            host = stats.cpu().numpy()  # 64 B; the reference also derives B on the host
-            mean, mx = float(host[1]), float(host[2])
-            b = mg.compute_iterations(EPS, mean, mx).b
-            flags = _lib.FLAG_NONZERO if host.view(np.int64)[4] == 0 else 0
+            if world > 1 and aligned:
+                # slice statistics + an 8-word all-gather give the global B bit for bit
+                # (distributed.combine_slice_stats); the host derives B while the weight
+                # all-gather is still in flight
+                _lib.check(L.mgp_weight_stats(D.ptr(local_w), 0, n_loc, D.ptr(stats), sp))
+                ws = dist.all_gather_into_tensor(stats_all, stats.view(torch.int64), async_op=True)
+                ww = dist.all_gather_into_tensor(full, local_w, async_op=True)
+                ws.wait()
+                rows = stats_all.view(world, 8).cpu().numpy()
+                g = combine_slice_stats([WeightStats(n_loc, *r.view(np.float64)[:3], *r[3:])
+                                         for r in rows])
+                b = mg.compute_iterations(EPS, g.mean, g.max).b
+                flags = _lib.FLAG_NONZERO if g.n_zero == 0 else 0
+                ww.wait()
+            else:
+                gather_weights()
+                _lib.check(L.mgp_weight_stats(D.ptr(full), 0, n_glob, D.ptr(stats), sp))
+                host = stats.cpu().numpy()  # 64 B; the reference also derives B on the host
+                mean, mx = float(host[1]), float(host[2])
+                b = mg.compute_iterations(EPS, mean, mx).b
+                flags = _lib.FLAG_NONZERO if host.view(np.int64)[4] == 0 else 0
             if ev is not None:
                 ev[0].record(stream)
             _lib.check(L.mgp_resample_range(_lib.KIND["megopolis"], D.ptr(full), 0, n_glob, b, RUN_SEED, 32, 0, 1,

@@ -6,8 +6,13 @@ weight vector, the shared offsets and the seed only (M/resample.py:185-197), so:
 
   1. weights: the per-rank slices are all-gathered into a replicated f32[N]
      (the one real exchange of the path; 4N bytes over NVLink),
-  2. B rule: every rank reduces the replicated array with the same numpy-exact
-     pairwise tree, so every rank derives the identical B without a collective,
+  2. B rule: numpy's pairwise tree (np.asarray(w, f64).mean(), M/bench.py:119) splits an
+     array of N = 2^g * n_local elements exactly at the rank boundaries when world = 2^g
+     and n_local % 8 == 0, n_local > 64 (each split is n2 = len/2 - (len/2) % 8); every
+     rank's slice sum is then a node of the global tree, so each rank reduces only its
+     own slice and the world slice sums are combined in the tree's order after a tiny
+     all-gather -- bit-identical to the single-GPU B, and overlapped with the weight
+     all-gather.  Other shapes reduce the replicated array with the same tree,
   3. offsets: derived from the seed on every rank (no collective),
   4. resample: each rank runs the kernel on its particle slice (global indices),
   5. states: apply_ancestors needs rows owned by other ranks -- exchanged with
@@ -31,7 +36,37 @@ from dataclasses import dataclass
 from . import _device as D
 from . import _lib
 from .resample import PartitionConfig, WarpConfig
-from .weights import compute_iterations, device_stats
+from .weights import WeightStats, compute_iterations, device_stats
+
+
+def slice_tree_aligned(world: int, n_local: int) -> bool:
+    """True when numpy's pairwise summation tree over world * n_local elements has every
+    rank slice as a subtree (see module docstring)."""
+    return world >= 1 and (world & (world - 1)) == 0 and n_local % 8 == 0 and n_local > 64
+
+
+def combine_slice_stats(parts) -> WeightStats:
+    """Global WeightStats from per-rank slice stats in rank order, combining the slice sums
+    pairwise exactly like numpy's tree above the slices (requires a power-of-two count)."""
+    sums = [p.sum for p in parts]
+    while len(sums) > 1:
+        sums = [sums[2 * i] + sums[2 * i + 1] for i in range(len(sums) // 2)]
+    n = sum(p.n for p in parts)
+    total = sums[0]
+    return WeightStats(n, total, total / n, max(p.max for p in parts), sum(p.n_pos for p in parts),
+                       sum(p.n_zero for p in parts), sum(p.n_neg for p in parts),
+                       sum(p.n_nonfinite for p in parts), sum(p.n_notnormal for p in parts))
+
+
+def _pack(st):
+    return [float(st.n), float(st.sum), float(st.max), float(st.n_pos), float(st.n_zero), float(st.n_neg),
+            float(st.n_nonfinite), float(st.n_notnormal)]
+
+
+def _unpack(row):
+    v = [float(x) for x in row]
+    return WeightStats(int(v[0]), v[1], v[1] / v[0] if v[0] else 0.0, v[2], int(v[3]), int(v[4]), int(v[5]),
+                       int(v[6]), int(v[7]))
 
 
 class CudaOps:
@@ -99,13 +134,33 @@ class ShardedResampler:
             self._dist.all_gather(parts, w_local.contiguous(), group=self.group)
         return full
 
+    # -- 2. weight statistics ---------------------------------------------------
+    def global_stats(self, w_local, full=None):
+        """Statistics of the global weight vector, bit-identical to one device's pass over it.
+        Slice-aligned shapes reduce only the local slice plus a world-sized all-gather of
+        8 numbers (float64 carries the counts exactly up to 2^53)."""
+        t = D.torch()
+        n_local = w_local.numel()
+        if not slice_tree_aligned(self.world, n_local):
+            return self.ops.stats(full if full is not None else self.replicate_weights(w_local))
+        mine = t.tensor(_pack(self.ops.stats(w_local)), dtype=t.float64, device=w_local.device)
+        rows = t.empty(self.world * 8, dtype=t.float64, device=w_local.device)
+        if self.world == 1:
+            rows.copy_(mine)
+        else:
+            try:
+                self._dist.all_gather_into_tensor(rows, mine, group=self.group)
+            except (RuntimeError, AttributeError, NotImplementedError):
+                self._dist.all_gather(list(rows.chunk(self.world)), mine, group=self.group)
+        return combine_slice_stats([_unpack(r) for r in rows.view(self.world, 8).cpu().tolist()])
+
     # -- 2-4. B rule + per-slice resample --------------------------------------
     def resample(self, w_local, b: int | None = None, seed=0, epsilon: float = 0.01):
         """Ancestors (global indices) for this rank's particle slice, and the B used."""
         n_local = w_local.numel()
         full = self.replicate_weights(w_local)
         n = full.numel()
-        st = self.ops.stats(full)
+        st = self.global_stats(w_local, full)
         if st.n_nonfinite:
             raise ValueError("weights must be finite")
         if st.n_neg:

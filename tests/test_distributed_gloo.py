@@ -37,7 +37,10 @@ class _Stats:
         self.n_neg = int((v < 0).sum())
         self.n_pos = int((v > 0).sum())
         self.n_zero = int((v == 0).sum())
+        self.n_notnormal = int((~np.isfinite(v) | (v <= 0) | (np.abs(v) < np.finfo(v.dtype).tiny)).sum())
+        self.n = len(v)
         self.mean, self.max = oracle.weight_mean_max(v)
+        self.sum = oracle.pairwise_sum(np.asarray(v, dtype=np.float64))
 
 
 class OracleOps:
@@ -126,3 +129,22 @@ def test_sharded_equals_single_process(oracle, world, case):
     assert np.array_equal(anc, ref)
     states_full = np.stack([np.arange(n) * 1.5, np.arange(n)], axis=1)
     assert np.array_equal(states, states_full[ref])
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+@pytest.mark.parametrize("n_local", [72, 1000, 4096, 3 * 1024 + 8])
+def test_slice_stats_combine_bit_exact(oracle, world, n_local):
+    """Per-rank slice sums combined in numpy's tree order == the pairwise sum of the whole
+    array, bit for bit (the B rule of the sharded path without reducing the replicated array)."""
+    from paper_2109_13504_b200.distributed import combine_slice_stats, slice_tree_aligned
+
+    assert slice_tree_aligned(world, n_local)
+    w = oracle.gen_gaussian_weights(2.5, world * n_local, 77 + n_local, "single")
+    parts = [_Stats(torch.from_numpy(w[r * n_local:(r + 1) * n_local])) for r in range(world)]
+    for p in parts:
+        p.n_neg, p.n_nonfinite = 0, 0
+    g = combine_slice_stats(parts)
+    total = oracle.pairwise_sum(np.asarray(w, dtype=np.float64))
+    mean, mx = oracle.weight_mean_max(w)
+    assert g.sum == total and g.mean == mean and g.max == mx and g.n == world * n_local
+    assert not slice_tree_aligned(3, 1024) and not slice_tree_aligned(2, 60) and not slice_tree_aligned(2, 1001)

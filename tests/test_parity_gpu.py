@@ -444,3 +444,24 @@ def test_storage_device_upload(mg, tmp_path, oracle):
     anc = mg.megopolis(wd, 7, seed=1)
     storage.save_indices(tmp_path / "a.bin", anc)
     assert np.array_equal(storage.load_indices(tmp_path / "a.bin"), oracle.megopolis(w, 7, seed=1))
+
+
+@pytest.mark.parametrize("zeros", [False, True])
+def test_half_split_host_chunks(mg, oracle, zeros):
+    """The half-split kernel through the host-buffer path's lower/upper chunk pairs on two
+    streams (N = 2^21: two pairs) and through a rank-style particle range (not split)."""
+    from paper_2109_13504_b200 import _lib
+
+    n, b = 1 << 21, 9
+    w = oracle.gen_gaussian_weights(3.0, n, 4242, "single")
+    if zeros:
+        w[np.random.default_rng(1).random(n) < 0.2] = 0
+    ref = oracle.megopolis(w, b, seed=99, rng="philox")
+    assert np.array_equal(mg.megopolis(w, b, seed=99, rng="philox"), ref)
+    wd = torch.from_numpy(w).cuda()
+    out = torch.empty(n // 4, dtype=torch.int64, device="cuda")
+    p0 = 3 * n // 8
+    _lib.check(_lib.lib().mgp_resample_range(_lib.KIND["megopolis"], wd.data_ptr(), 0, n, b, 99, 32, 0, 1,
+                                             _lib.RNG["philox"], 0, p0, p0 + n // 4, out.data_ptr(),
+                                             torch.cuda.current_stream().cuda_stream))
+    assert np.array_equal(out.cpu().numpy(), ref[p0:p0 + n // 4])
