@@ -217,6 +217,71 @@ __global__ void __launch_bounds__(64, MINB) k_x2(const __grid_constant__ Resampl
   }
 }
 
+
+// Software-pipelined half-split: the Philox block of the next group is computed in the same
+// basic block as the compares of the current one.  PPT 4 ({i, i+64, i+N/2, i+N/2+64}) or
+// PPT 2 ({i, i+N/2}).  No tail (B % 4 == 0 harness).
+template <int PPT, int MINB>
+__global__ void __launch_bounds__(PPT == 4 ? 64 : 128, MINB) k_sp(const __grid_constant__ ResampleArgs a, const __grid_constant__ OffChunk oc) {
+  const uint32_t half = a.n >> 1;
+  constexpr int LOWC = PPT == 4 ? 128 : 128;  // lower-half particles per CTA
+  const uint32_t i0 = blockIdx.x * LOWC + threadIdx.x;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t cmask = (a.n - 1) & ~31u;
+  uint32_t ii[PPT];
+  if (PPT == 4) { ii[0] = i0; ii[1] = i0 + 64; ii[2] = i0 + half; ii[3] = i0 + half + 64; }
+  else { ii[0] = i0; ii[1] = i0 + half; }
+  const uint32_t ial0 = i0 - lane, ial1 = ial0 + 64;
+  double wkd[PPT];
+  int bstar[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) { wkd[p] = (double)tex1Dfetch<float>(a.tex, (int)ii[p]); bstar[p] = -1; }
+  auto philox = [&](int t0, uint32_t (&c0)[PPT], uint32_t (&c1)[PPT], uint32_t (&c2)[PPT], uint32_t (&c3)[PPT]) {
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) { c0[p] = ii[p]; c1[p] = 0; c2[p] = (uint32_t)((a.b0 + t0) >> 2); c3[p] = 0; }
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) {
+        const uint64_t q0 = (uint64_t)PHILOX_M0 * c0[p], q1 = (uint64_t)PHILOX_M1 * c2[p];
+        const uint32_t n0 = (uint32_t)(q1 >> 32) ^ c1[p] ^ a.pk0[r], n2 = (uint32_t)(q0 >> 32) ^ c3[p] ^ a.pk1[r];
+        c1[p] = (uint32_t)q1; c3[p] = (uint32_t)q0; c0[p] = n0; c2[p] = n2;
+      }
+    }
+  };
+  uint32_t c0[PPT], c1[PPT], c2[PPT], c3[PPT];
+  philox(0, c0, c1, c2, c3);
+  const int full = a.cnt & ~3;
+  for (int t0 = 0; t0 < full; t0 += 4) {
+    uint32_t d0[PPT], d1[PPT], d2[PPT], d3[PPT];
+    philox(t0 + 4, d0, d1, d2, d3);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int t = t0 + q;
+      const uint2 o = oc.o[t];
+      const uint32_t L = lane + o.y;
+      uint32_t jj[PPT];
+      jj[0] = mux3(ial0 + o.x, L, cmask);
+      if (PPT == 4) { jj[1] = mux3(ial1 + o.x, L, cmask); jj[2] = jj[0] ^ half; jj[3] = jj[1] ^ half; }
+      else jj[1] = jj[0] ^ half;
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) {
+        const uint32_t wd = q == 0 ? c0[p] : q == 1 ? c1[p] : q == 2 ? c2[p] : c3[p];
+        const double wjd = (double)tex1Dfetch<float>(a.tex, (int)jj[p]);
+        if (fma(u1_bits(wd), wkd[p], -wkd[p]) <= wjd) { wkd[p] = wjd; bstar[p] = t; }
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) { c0[p] = d0[p]; c1[p] = d1[p]; c2[p] = d2[p]; c3[p] = d3[p]; }
+  }
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    uint32_t k = ii[p];
+    if (bstar[p] >= 0) { const uint2 o = oc.o[bstar[p]]; k = mux3((ii[p] - lane) + o.x, lane + o.y, cmask); }
+    a.anc[ii[p]] = (int64_t)k;
+  }
+}
+
 template <class K>
 float time_it(K launch, int reps) {
   cudaEvent_t e0, e1;
@@ -290,6 +355,8 @@ int main(int argc, char** argv) {
   check("lib HALF", time_it([&]() { k_megopolis_w32<1, float, true, true, true, 4, true><<<n / 256, 64>>>(b, oc); }, 9));
   check("x2 p4", time_it([&]() { k_x2<1><<<n / 256, 64>>>(b, oc); }, 9));
   check("x2 gen", time_it([&]() { k_x2<1, true><<<n / 256, 64>>>(b, oc); }, 9));
+  check("sp p4", time_it([&]() { k_sp<4, 1><<<n / 256, 64>>>(b, oc); }, 9));
+  check("sp p2", time_it([&]() { k_sp<2, 1><<<n / 256, 128>>>(b, oc); }, 9));
   check("x2 gen nokst", time_it([&]() { k_x2<1, true, false, false><<<n / 256, 64>>>(b, oc); }, 9));
   check("x2 gen", time_it([&]() { k_x2<1, true><<<n / 256, 64>>>(b, oc); }, 9));
   {

@@ -1,9 +1,10 @@
 """The reference's own resampler tests and quality acceptance criteria, run against
 the B200 implementation through its public API.
 
-Mirrors pkg/tests/test_resample.py (T/test_resample.py) and the path-relevant
-criteria of pkg/tests/test_acceptance.py (1-4, 7, 9) with the same fixtures
-(T/conftest.py:15-44), thresholds and seeds.
+Mirrors pkg/tests/test_resample.py (T/test_resample.py) and the acceptance criteria of
+pkg/tests/test_acceptance.py (1-7 and 9-12; 8 is the analytical traffic model, which the
+B200 build replaces with ncu counters) with the same fixtures (T/conftest.py:15-44),
+thresholds and seeds.
 """
 
 import numpy as np
@@ -256,3 +257,118 @@ def test_criterion_09_megopolis_structural_invariants(m):
         n = 32 * int(rnd.integers(1, 9))
         anc = m.megopolis(m.WeightVector(np.ones(n), "double"), int(rnd.integers(1, 9)), seed=m.derive_seed(902, trial))
         assert sorted(anc) == list(range(n))
+
+
+def test_criterion_05_unbiased_baselines_and_ordering(m):  # T/test_acceptance.py:84-106
+    n, k = 2**12, 64
+    w = gaussian_w(m, 1.0, n, m.derive_seed(500), "double")
+    wd = np.asarray(w.values)
+    b = m.compute_iterations(0.01, float(wd.mean()), float(wd.max())).b
+    wdev = m.WeightVector(torch.from_numpy(wd).cuda(), "double")
+    expect = n * wd / wd.sum()
+    mse, unbiased_ok = {}, True
+    for kind in ("multinomial", "systematic", "megopolis"):
+        fn = m.make_resampler(kind)
+        runs = np.stack([m.ancestors_to_offspring(fn(wdev, b, m.derive_seed(501, i)), n).cpu().numpy()
+                         for i in range(k)]).astype(np.float64)
+        mse[kind] = m.quality_stats(runs, wdev).mse
+        if kind != "megopolis":
+            mean, std = runs.mean(axis=0), runs.std(axis=0, ddof=1)
+            live = std > 0
+            z = (mean[live] - expect[live]) / (std[live] / np.sqrt(k))
+            unbiased_ok = unbiased_ok and (np.abs(z) > 3).mean() <= 0.01
+            unbiased_ok = unbiased_ok and np.all(np.abs(mean[~live] - expect[~live]) <= 1.0)
+    assert unbiased_ok and mse["systematic"] < mse["megopolis"] < mse["multinomial"], mse
+
+
+def test_criterion_06_prefix_sum_instability(m):  # T/test_acceptance.py:109-176
+    ns, k_mse, k_meg, sequences = (2**12, 2**16, 2**20), 8, 32, 2
+
+    def exact_bias_sq(values):  # the kernels' float32 prefix vs the float64 reference
+        c = np.asarray(m.inclusive_prefix(values), dtype=np.float64)
+        e32 = len(c) * np.diff(np.concatenate(([0.0], c))) / c[-1]
+        v64 = np.asarray(values, dtype=np.float64)
+        return float(np.sum((e32 - n64(v64)) ** 2))
+
+    def n64(v):
+        return len(v) * v / v.sum()
+
+    bc = {}
+    for n in ns:
+        per = {kind: [] for kind in ("multinomial", "systematic")}
+        for s in range(sequences):
+            w = gaussian_w(m, 1.0, n, m.derive_seed(600, n, s), "single")
+            wdev = m.WeightVector(torch.from_numpy(w.values).cuda(), "single")
+            bias_sq = exact_bias_sq(w.values)
+            for kind in per:
+                fn = m.make_resampler(kind)
+                acc = m.QualityAccumulator(n)
+                for i in range(k_mse):
+                    acc.add(m.ancestors_to_offspring(fn(wdev, 1, m.derive_seed(601, n, s, i)), n), wdev)
+                per[kind].append(bias_sq / acc.finalize().mse)
+        for kind in per:
+            bc[(kind, n)] = float(np.mean(per[kind]))
+    for kind in ("multinomial", "systematic"):
+        seq = [bc[(kind, n)] for n in ns]
+        assert seq[0] < seq[1] < seq[2], (kind, seq)
+    fn = m.make_resampler("megopolis")
+    meg = {}
+    for n in (ns[0], ns[-1]):
+        per = []
+        for s in range(sequences):
+            w = gaussian_w(m, 1.0, n, m.derive_seed(600, n, s), "single")
+            wdev = m.WeightVector(torch.from_numpy(w.values).cuda(), "single")
+            b = m.iterations_for(wdev, 0.01).b
+            acc = m.QualityAccumulator(n)
+            for i in range(k_meg):
+                acc.add(m.ancestors_to_offspring(fn(wdev, b, m.derive_seed(601, n, s, i)), n), wdev)
+            per.append(acc.finalize().bias_contribution)
+        meg[n] = float(np.mean(per))
+    floor = 1.0 / k_meg
+    assert abs(meg[ns[-1]] - meg[ns[0]]) <= 0.1 * floor
+    assert all(0.8 * floor <= v <= 1.2 * floor for v in meg.values()), meg
+
+
+def test_criterion_10_systematic_oracle_equivalence(m):  # T/test_acceptance.py:253-262
+    from oracle import oracle  # the sequential stratified restatement (M/resample.py:339-354)
+
+    rnd = np.random.default_rng(100)
+    for trial in range(500):
+        n = int(rnd.integers(1, 257))
+        w = rnd.uniform(0, 1, n) ** 3 + 1e-9
+        seed = m.derive_seed(1000, trial)
+        assert np.array_equal(m.systematic_improved(m.WeightVector(w, "double"), seed), oracle.systematic(w, seed))
+
+
+def test_criterion_11_end_to_end_orderings(m):  # T/test_acceptance.py:265-287
+    from paper_2109_13504_b200 import pfilter as pf
+
+    trajectories = [pf.generate_trajectory(100, 0.0, m.derive_seed(1100, i)) for i in range(4)]
+    cfg = pf.FilterConfig(n_particles=2**16, precision="single")
+    rows = pf.run_benchmark(cfg, trajectories, 10, [16, 32, 64],
+                            [("megopolis", None), ("c1", 128), ("systematic", None)], m.derive_seed(1101))
+    rmse = {(r["algorithm"], r["b"]): r["rmse"] for r in rows}
+    meg = [rmse[("megopolis", b)] for b in (16, 32, 64)]
+    c1 = [rmse[("c1", b)] for b in (16, 32, 64)]
+    sys_r = rmse[("systematic", 0)]
+    assert all(a <= c - 0.05 for a, c in zip(meg, c1)), (meg, c1)
+    assert abs(meg[2] - sys_r) <= 0.03 * sys_r and meg[2] <= meg[0] + 0.05 and meg[2] <= meg[1] + 0.05, (meg, sys_r)
+
+
+def test_criterion_12_cli_determinism(m, tmp_path):  # T/test_acceptance.py:290-308 (quality, pf)
+    from paper_2109_13504_b200.cli import main
+
+    commands = {
+        "quality": ["quality", "--algorithms", "megopolis,c2:128", "--n-grid", "1024", "--params", "0,1",
+                    "--k-runs", "4", "--sequences", "2", "--seed", "12"],
+        "pf": ["pf", "--algorithms", "megopolis", "--n", "1024", "--b-grid", "4", "--trajectories", "1",
+               "--runs", "2", "--t-steps", "5", "--seed", "12"],
+    }
+    for name, args in commands.items():
+        payloads = []
+        for rep in range(2):
+            out = tmp_path / f"{name}-{rep}.csv"
+            assert main(args + ["--out", str(out)]) == 0
+            payloads.append(out.read_bytes())
+        assert payloads[0] == payloads[1], name
+
