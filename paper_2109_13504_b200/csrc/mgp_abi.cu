@@ -399,13 +399,25 @@ int px_search(int kind, const void* cum, int dtype, int64_t n, uint64_t seed, in
   const unsigned grid = (unsigned)std::min<int64_t>((cnt + 255) / 256, 148 * 64);
   if (kind == MGP_KIND_MULTINOMIAL) {
     const uint64_t base = megores_base(seed);
-    if (dtype == MGP_F32) k_multinomial<float><<<grid, 256, 0, st>>>((const float*)cum, n, base, p0, p_end, anc);
-    else k_multinomial<double><<<grid, 256, 0, st>>>((const double*)cum, n, base, p0, p_end, anc);
+    int64_t K = 1;
+    while (K * 2 * PXM_PER_BUCKET <= n) K *= 2;
+    int32_t* start = nullptr;
+    CUDA_TRY(cudaMallocAsync(&start, sizeof(int32_t) * (K + 1), st));
+    const unsigned kg = (unsigned)std::min<int64_t>((K + 256) / 256, 148 * 16);
+    if (dtype == MGP_F32) {
+      k_multinomial_buckets<float><<<kg, 256, 0, st>>>((const float*)cum, n, K, start);
+      k_multinomial<float><<<grid, 256, 0, st>>>((const float*)cum, n, base, p0, p_end, K, start, anc);
+    } else {
+      k_multinomial_buckets<double><<<kg, 256, 0, st>>>((const double*)cum, n, K, start);
+      k_multinomial<double><<<grid, 256, 0, st>>>((const double*)cum, n, base, p0, p_end, K, start, anc);
+    }
     LAUNCH_CHECK("k_multinomial");
+    CUDA_TRY(cudaFreeAsync(start, st));
   } else {
     const double u0 = (double)(mix64(megores_key(megores_base(seed), GLOBAL_OFFSET_LANE, 0)) >> 11) * 0x1p-53;
-    if (dtype == MGP_F32) k_systematic<float><<<grid, 256, 0, st>>>((const float*)cum, n, u0, p0, p_end, anc);
-    else k_systematic<double><<<grid, 256, 0, st>>>((const double*)cum, n, u0, p0, p_end, anc);
+    const unsigned sg = (unsigned)std::min<int64_t>((cnt / PXS_RUN + 256) / 256, 148 * 64);
+    if (dtype == MGP_F32) k_systematic<float><<<sg, 256, 0, st>>>((const float*)cum, n, u0, p0, p_end, anc);
+    else k_systematic<double><<<sg, 256, 0, st>>>((const double*)cum, n, u0, p0, p_end, anc);
     LAUNCH_CHECK("k_systematic");
   }
   return 0;

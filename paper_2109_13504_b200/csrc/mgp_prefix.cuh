@@ -123,6 +123,18 @@ __device__ __forceinline__ Tx px_elem(WT w, int e) {
   }
 }
 
+// Same increment as a plain integer plus a tie flag (tie: inc = q, the transducer is
+// {q + (q & 1), q + ((q + 1) & 1)}).  The fast paths below sum plain increments while no
+// element of the warp / block is a tie -- the common case for real weights.
+template <typename WT>
+__device__ __forceinline__ int64_t px_inc(WT w, int e, bool& tie) {
+  const Tx t = px_elem<WT>(w, e);
+  tie = t.a0 != t.a1;
+  return t.a0;  // the increment when !tie
+}
+
+__device__ __forceinline__ int64_t px_sat_add(int64_t a, int64_t b) { return px_sat(a + b); }
+
 // ---------------------------------------------------------------------------
 
 template <typename WT>
@@ -184,10 +196,25 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_aggregate(const WT* __restric
 #pragma unroll
   for (int k = 0; k < PX_CAND; ++k) {
     const int e = e0 - 1 + k;
-    Tx t{0, 0};
+    bool tie = false;
+    int64_t sum = 0;
 #pragma unroll
-    for (int j = 0; j < PX_PER_THREAD; ++j) t = px_compose(t, px_elem<WT>(v[j], e));
-    t = px_warp_reduce(t);
+    for (int j = 0; j < PX_PER_THREAD; ++j) {
+      bool tj;
+      sum = px_sat_add(sum, px_inc<WT>(v[j], e, tj));
+      tie |= tj;
+    }
+    Tx t;
+    if (__any_sync(0xffffffffu, tie)) {  // rounding ties in this warp: parity transducers
+      t = Tx{0, 0};
+#pragma unroll
+      for (int j = 0; j < PX_PER_THREAD; ++j) t = px_compose(t, px_elem<WT>(v[j], e));
+      t = px_warp_reduce(t);
+    } else {  // plain saturating integer sum
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum = px_sat_add(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+      t = Tx{sum, sum};
+    }
     if ((threadIdx.x & 31) == 0) red[k][threadIdx.x >> 5] = t;
   }
   __syncthreads();
@@ -410,25 +437,54 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_materialize(const WT* __restr
   const int e = md;
   const double ue = px_ulp(e, MANT);
   const int64_t S = px_units<WT>(s0);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WT v[PX_PER_THREAD];
+  int64_t inc[PX_PER_THREAD];
+  int64_t tsum = 0;
+  bool tie = false;
+#pragma unroll
+  for (int j = 0; j < PX_PER_THREAD; ++j) {
+    v[j] = base + j < n ? w[base + j] : (WT)0;
+    bool tj;
+    inc[j] = px_inc<WT>(v[j], e, tj);
+    tie |= tj;
+    tsum += inc[j];  // a resolved chunk stays inside its binade: no saturation here
+  }
+  if (!__syncthreads_or(tie)) {  // no rounding ties in the chunk: plain exclusive integer scan
+    __shared__ int64_t wtot[PX_THREADS / 32];
+    int64_t x = tsum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x += y;
+    }
+    if (lane == 31) wtot[wid] = x;
+    __syncthreads();
+    int64_t U = S + x - tsum;
+    for (int q = 0; q < wid; ++q) U += wtot[q];
+#pragma unroll
+    for (int j = 0; j < PX_PER_THREAD; ++j) {
+      U += inc[j];
+      if (base + j < n) cum[base + j] = (WT)((double)U * ue);
+    }
+    return;
+  }
+  // exclusive ordered block scan of the per-thread transducers
   Tx te[PX_PER_THREAD];
   Tx t{0, 0};
 #pragma unroll
   for (int j = 0; j < PX_PER_THREAD; ++j) {
-    v[j] = base + j < n ? w[base + j] : (WT)0;
     te[j] = px_elem<WT>(v[j], e);
     t = px_compose(t, te[j]);
   }
-  // exclusive ordered block scan of the per-thread transducers
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  Tx inc = px_warp_scan(t);
-  if (lane == 31) wsum[wid] = inc;
+  Tx incw = px_warp_scan(t);
+  if (lane == 31) wsum[wid] = incw;
   __syncthreads();
   Tx pre{0, 0};
   for (int q = 0; q < wid; ++q) pre = px_compose(pre, wsum[q]);
   Tx ex;
-  ex.a0 = __shfl_up_sync(0xffffffffu, inc.a0, 1);
-  ex.a1 = __shfl_up_sync(0xffffffffu, inc.a1, 1);
+  ex.a0 = __shfl_up_sync(0xffffffffu, incw.a0, 1);
+  ex.a1 = __shfl_up_sync(0xffffffffu, incw.a1, 1);
   if (lane == 0) ex = Tx{0, 0};
   ex = px_compose(pre, ex);
   int64_t U = S + px_apply(ex, S & 1);
@@ -438,6 +494,7 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_materialize(const WT* __restr
     if (base + j < n) cum[base + j] = (WT)((double)U * ue);
   }
 }
+
 
 // the binade-crossing chunks: one warp each, writing every value (separate launch, so the
 // warp routine's registers do not limit the block scan's occupancy)
@@ -458,40 +515,90 @@ __global__ void __launch_bounds__(32) k_px_materialize_exc(const WT* __restrict_
 // systematic_improved (M/resample.py:307-336): target_i = (i + u0) / n * total (float64),
 // ancestor = first a with float64(cum[a]) >= target_i, else n-1.
 
-// Plain per-particle binary searches over the prefix sum (L2-resident at 2^24 float32):
-// latency is hidden by occupancy.  A shared-memory top-level table was tried and lost
-// (random smem probes bank-conflict; fewer resident warps).
+// Searches of the prefix sum.
+//
+// multinomial (M/resample.py:295-304): key_i = WT(uniform01_at(seed, i, 0) * total) is
+// uniform in [0, total), so a bucket index narrows every search: K buckets with boundary
+// values bnd[b] = WT(total * b / K) (non-decreasing) and start[b] = upper_bound(cum, bnd[b]);
+// a key in [bnd[b], bnd[b+1]) has its answer in [start[b], start[b+1]] (upper_bound is
+// monotone).  The bucket is guessed from the key and corrected by exact comparisons against
+// the stored boundaries, then ~log2(N/K) probes finish the search (vs log2 N).
+constexpr int PXM_PER_BUCKET = 16;
+
+template <typename WT>
+__device__ __forceinline__ int64_t pxs_upper(const WT* __restrict__ cum, int64_t lo, int64_t hi, WT key) {
+  while (lo < hi) {  // first index in [lo, hi) with cum > key (hi if none)
+    const int64_t mid = (lo + hi) >> 1;
+    if (__ldg(cum + mid) <= key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+template <typename WT>
+__device__ __forceinline__ WT pxm_bound(double total, int64_t b, int64_t K) {
+  return b >= K ? (WT)INFINITY : (WT)(total * (double)b / (double)K);
+}
+
+template <typename WT>
+__global__ void k_multinomial_buckets(const WT* __restrict__ cum, int64_t n, int64_t K, int32_t* __restrict__ start) {
+  const double total = (double)cum[n - 1];
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= K; b += (int64_t)gridDim.x * blockDim.x)
+    start[b] = (int32_t)(b == 0 ? pxs_upper(cum, 0, n, (WT)0) - 0 : pxs_upper(cum, 0, n, pxm_bound<WT>(total, b, K)));
+}
+
 template <typename WT>
 __global__ void k_multinomial(const WT* __restrict__ cum, int64_t n, uint64_t base, int64_t p0, int64_t p_end,
-                              int64_t* __restrict__ anc) {
+                              int64_t K, const int32_t* __restrict__ start, int64_t* __restrict__ anc) {
   const double total = (double)cum[n - 1];
   for (int64_t i = p0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p_end; i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t h = mix64(megores_key(base, (uint64_t)i, 0));
     const double ud = __dmul_rn((double)(h >> 11) * 0x1p-53, total);
     const WT key = (WT)ud;
-    int64_t lo = 0, hi = n;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (__ldg(cum + mid) <= key) lo = mid + 1;
-      else hi = mid;
-    }
-    anc[i] = lo < n - 1 ? lo : n - 1;
+    int64_t bk = (int64_t)((double)key / total * (double)K);
+    bk = bk < 0 ? 0 : (bk >= K ? K - 1 : bk);
+    while (bk > 0 && key < pxm_bound<WT>(total, bk, K)) --bk;          // exact corrections
+    while (bk < K - 1 && !(key < pxm_bound<WT>(total, bk + 1, K))) ++bk;
+    // key >= bnd[bk] (bnd[0] = 0 <= key) and key < bnd[bk+1]: answer in [start[bk], start[bk+1]]
+    const int64_t lo = bk == 0 ? 0 : start[bk];
+    const int64_t hi = start[bk + 1];
+    const int64_t a = pxs_upper(cum, lo, hi, key);
+    anc[i] = a < n - 1 ? a : n - 1;
   }
 }
+
+// systematic_improved (M/resample.py:307-336): target_i = (i + u0) / n * total (float64) is
+// monotone in i, so each thread takes a run of PXS_RUN consecutive particles: one binary
+// search, then a galloping search from the previous answer for each next particle.  (A
+// warp-interleaved run with coalesced stores was tried: the 32-strata gallops cost more.)
+constexpr int PXS_RUN = 16;
 
 template <typename WT>
 __global__ void k_systematic(const WT* __restrict__ cum, int64_t n, double u0, int64_t p0, int64_t p_end,
                              int64_t* __restrict__ anc) {
   const double total = (double)cum[n - 1];
-  for (int64_t i = p0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p_end; i += (int64_t)gridDim.x * blockDim.x) {
-    const double target = __dmul_rn(__ddiv_rn(__dadd_rn((double)i, u0), (double)n), total);
-    int64_t lo = 0, hi = n;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if ((double)__ldg(cum + mid) < target) lo = mid + 1;
-      else hi = mid;
+  const int64_t nrun = (p_end - p0 + PXS_RUN - 1) / PXS_RUN;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrun; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i0 = p0 + r * PXS_RUN, i1 = min(p_end, i0 + PXS_RUN);
+    int64_t a = 0;
+    for (int64_t i = i0; i < i1; ++i) {
+      const double target = __dmul_rn(__ddiv_rn(__dadd_rn((double)i, u0), (double)n), total);
+      // first index >= a with float64(cum) >= target (targets are non-decreasing in i)
+      int64_t lo = a, step = 1, hi = a;
+      if (i == i0) {
+        hi = n;
+      } else {  // gallop: a, a+1, a+3, a+7, ... until cum >= target
+        while (hi < n && (double)__ldg(cum + hi) < target) { lo = hi + 1; hi += step; step <<= 1; }
+        if (hi > n) hi = n;
+      }
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((double)__ldg(cum + mid) < target) lo = mid + 1;
+        else hi = mid;
+      }
+      a = lo;
+      anc[i] = a < n - 1 ? a : n - 1;
     }
-    anc[i] = lo < n - 1 ? lo : n - 1;
   }
 }
 
