@@ -12,10 +12,12 @@ batch: weight statistics -> B (host, like the reference) -> Megopolis kernel.
 Inputs are resident in HBM for ``value``; ``e2e`` runs the same step through the
 host-buffer C-ABI entry (pinned host weights in, pinned host ancestors out).
 
-Multi-GPU (weak scaling): rank r owns particles [r*2^24, (r+1)*2^24) of a global
-population of N*G; each step all-gathers the weight slices over NCCL (the
-replicated-weights exchange of SURVEY 8e), computes B on the replicated array and
-resamples its own slice.
+Multi-GPU (weak scaling): a global population of 2^24 * G particles; rank r owns stripe r
+of each half ([r*h, (r+1)*h) and N/2 + [r*h, (r+1)*h), h = 2^23: the "stripes" layout of
+distributed.ShardedResampler, under which every rank runs the half-split kernel).  Each
+step all-gathers the weight stripes over NCCL (the replicated-weights exchange of SURVEY
+8e), derives the global B bit-exactly from per-stripe statistics (an all-gather of 16
+words, overlapped with the weight all-gather) and resamples the rank's stripes.
 
 The L2 (126 MB) would hold the 64 MiB weight array across steps, so a 256 MiB
 buffer is written between timed steps (outside the CUDA-event windows).
@@ -53,7 +55,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=N_PER_GPU, help="particles per GPU")
+    ap.add_argument("--n", "--particles", dest="n", type=int, default=N_PER_GPU, help="particles per GPU")
     ap.add_argument("--rng", default="philox", choices=["megores", "philox"],
                     help="headline stream; the other one is measured too and reported under 'streams'")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -213,38 +215,54 @@ def main():
     from paper_2109_13504_b200 import _device as D
 
     rank, world, local = dist_env()
+    # MGP_BENCH_LOOPBACK=1 (test plumbing only): every rank on cuda:0 with gloo collectives, to
+    # exercise the sharded step's logic on a one-GPU machine; never used for a reported number
+    loopback = os.environ.get("MGP_BENCH_LOOPBACK") == "1"
+    if loopback:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if loopback:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     L = _lib.lib()
     n_loc = args.n
     n_glob = n_loc * world
 
-    # weights: each rank generates its slice of the global population (device generator,
-    # same per-particle stream as the reference generator) then all-gathers.
+    # weights: rank r owns stripe r of each half of the global population ("stripes" layout of
+    # distributed.ShardedResampler: particles [r*h, (r+1)*h) and N/2 + [r*h, (r+1)*h), h = n/2),
+    # so every rank runs the half-split Megopolis kernel.  Each rank produces its stripes
+    # (device generator, same per-particle stream as the reference generator) and the two
+    # halves are all-gathered.
     full = host_weights(n_glob) if world == 1 else None
+    h, half = n_loc // 2, n_glob // 2
+    lo0, lo1 = rank * h, (rank + 1) * h
     if world > 1:
-        gen_full = host_weights(n_glob)  # deterministic; slice it to emulate per-rank production
-        local_w = gen_full[rank * n_loc:(rank + 1) * n_loc].clone()
+        gen_full = host_weights(n_glob)  # deterministic; sliced to emulate per-rank production
+        local_w = torch.cat([gen_full[lo0:lo1], gen_full[half + lo0:half + lo1]])
         del gen_full
         full = torch.empty(n_glob, dtype=torch.float32, device=dev)
     else:
         local_w = full
-    stats = torch.empty(8, dtype=torch.float64, device=dev)
+    stats = torch.empty(16, dtype=torch.float64, device=dev)
     from paper_2109_13504_b200.distributed import combine_slice_stats, slice_tree_aligned
     from paper_2109_13504_b200.weights import WeightStats
 
-    aligned = slice_tree_aligned(world, n_loc)
-    stats_all = torch.empty(world * 8, dtype=torch.int64, device=dev)
+    aligned = n_loc % 2 == 0 and slice_tree_aligned(world, h)
+    stats_all = torch.empty(world * 16, dtype=torch.int64, device=dev)
     anc = torch.empty(n_loc, dtype=torch.int64, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
     sp = ctypes.c_void_p(stream.cuda_stream)
 
-    def gather_weights():
+    def gather_weights(async_op=False):
         if world > 1:
-            dist.all_gather_into_tensor(full, local_w)
+            w1 = dist.all_gather_into_tensor(full[:half], local_w[:h], async_op=async_op)
+            w2 = dist.all_gather_into_tensor(full[half:], local_w[h:], async_op=async_op)
+            return (w1, w2)
+        return ()
 
     def measure(rng_id):
         """W warm-up + K timed steps of the hot path for one random stream."""
@@ -253,19 +271,22 @@ def main():
         def step(ev=None):
             """One hot-path pass: (all-gather) -> stats -> B -> megopolis(slice)."""
             if world > 1 and aligned:
-                # slice statistics + an 8-word all-gather give the global B bit for bit
-                # (distributed.combine_slice_stats); the host derives B while the weight
-                # all-gather is still in flight
-                _lib.check(L.mgp_weight_stats(D.ptr(local_w), 0, n_loc, D.ptr(stats), sp))
+                # stripe statistics + a 16-word all-gather give the global B bit for bit
+                # (numpy's tree: lower half + upper half, each the rank stripes in order;
+                # distributed.combine_slice_stats); the host derives B while the weight
+                # all-gathers are still in flight
+                _lib.check(L.mgp_weight_stats(D.ptr(local_w), 0, h, D.ptr(stats), sp))
+                _lib.check(L.mgp_weight_stats(D.ptr(local_w[h:]), 0, h, D.ptr(stats[8:]), sp))
                 ws = dist.all_gather_into_tensor(stats_all, stats.view(torch.int64), async_op=True)
-                ww = dist.all_gather_into_tensor(full, local_w, async_op=True)
+                wws = gather_weights(async_op=True)
                 ws.wait()
-                rows = stats_all.view(world, 8).cpu().numpy()
-                g = combine_slice_stats([WeightStats(n_loc, *r.view(np.float64)[:3], *r[3:])
-                                         for r in rows])
+                rows = stats_all.view(world * 2, 8).cpu().numpy()
+                per = [WeightStats(h, *r.view(np.float64)[:3], *r[3:]) for r in rows]
+                g = combine_slice_stats([combine_slice_stats(per[0::2]), combine_slice_stats(per[1::2])])
                 b = mg.compute_iterations(EPS, g.mean, g.max).b
                 flags = _lib.FLAG_NONZERO if g.n_zero == 0 else 0
-                ww.wait()
+                for wk in wws:
+                    wk.wait()
             else:
                 gather_weights()
                 _lib.check(L.mgp_weight_stats(D.ptr(full), 0, n_glob, D.ptr(stats), sp))
@@ -275,8 +296,12 @@ def main():
                 flags = _lib.FLAG_NONZERO if host.view(np.int64)[4] == 0 else 0
             if ev is not None:
                 ev[0].record(stream)
-            _lib.check(L.mgp_resample_range(_lib.KIND["megopolis"], D.ptr(full), 0, n_glob, b, RUN_SEED, 32, 0, 1,
-                                             rng_id, flags, rank * n_loc, (rank + 1) * n_loc, D.ptr(anc), sp))
+            if world > 1:
+                _lib.check(L.mgp_resample_stripes(_lib.KIND["megopolis"], D.ptr(full), 0, n_glob, b, RUN_SEED, 32, 0,
+                                                  1, rng_id, flags, lo0, lo1, D.ptr(anc), sp))
+            else:
+                _lib.check(L.mgp_resample_range(_lib.KIND["megopolis"], D.ptr(full), 0, n_glob, b, RUN_SEED, 32, 0,
+                                                 1, rng_id, flags, 0, n_loc, D.ptr(anc), sp))
             if ev is not None:
                 ev[1].record(stream)
             nonlocal_b[0] = b
@@ -323,7 +348,8 @@ def main():
     b = head["b"]
     ms_per_step = head["ms_per_step"]
     value = n_glob / (ms_per_step / 1e3)  # all ranks' particles per second
-    launches = args.steps * (2 + math.ceil(b / 1024))  # stats (2 kernels) + megopolis launches
+    # stats (2 kernels, per stripe when sharded) + megopolis launches
+    launches = args.steps * ((4 if world > 1 and aligned else 2) + math.ceil(b / 1024))
 
     # roofline: algorithmic bytes of one Megopolis launch: N*B*4 + N*4 + N*8 + 8*B
     alg_bytes = n_loc * b * 4 + n_loc * 4 + n_loc * 8 + 8 * b
@@ -335,10 +361,9 @@ def main():
         return ach, kavg
 
     achieved, kern_avg = roof(head)
-    # full-range Philox launches take the specialised half-split kernel; rank slices (N > 1)
-    # and the megores stream take k_megopolis_w32
+    # Philox launches (full range, or a rank's stripes) take the half-split kernel
     if args.rng == "philox":
-        mego_kernel = "k_megopolis_w32<philox, half-split, 4 particles/thread>" if world == 1 else "k_megopolis_w32<philox, 4 particles/thread>"
+        mego_kernel = "k_megopolis_w32<philox, half-split, 4 particles/thread>"
     else:
         mego_kernel = "k_megopolis_w32<megores, 1 particle/thread>"
     traffic = None

@@ -111,6 +111,14 @@ int mgp_resample_range(int kind, const void *d_w, int dtype, int64_t n, int32_t 
                        int32_t partition_bytes, int strict, int rng, int flags, int64_t p0, int64_t p1,
                        int64_t *d_anc_slice, void *stream);
 
+/* Two-stripe particle range: particles [lo0, lo1) and [N/2 + lo0, N/2 + lo1) (0 <= lo0 <= lo1
+ * <= N/2, N even) into d_anc_local[0, L) and d_anc_local[L, 2L), L = lo1 - lo0.  This is the
+ * sharded "stripes" layout (rank r owns stripe r of each half), under which every rank can run
+ * the half-split Megopolis kernel. */
+int mgp_resample_stripes(int kind, const void *d_w, int dtype, int64_t n, int32_t b, uint64_t seed, int32_t warp,
+                         int32_t partition_bytes, int strict, int rng, int flags, int64_t lo0, int64_t lo1,
+                         int64_t *d_anc_local, void *stream);
+
 /* Host-buffer drop-in for make_resampler(kind, ...)(w, b, seed) (M/resample.py:431-455):
  * copies h_w to the device, validates (WeightVector + _check_weights), derives B
  * from epsilon when b <= 0 (reporting it in *b_used), resamples, and streams the

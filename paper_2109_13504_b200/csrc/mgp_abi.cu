@@ -330,6 +330,7 @@ struct Plan {
   int32_t* kstate = nullptr;
   void* cum = nullptr;       // inclusive prefix sum (multinomial / systematic)
   bool half = false;         // run_range ranges are lower-half ranges of the half-split kernel
+  int64_t hi_shift = 0;      // half-split: upper-half ancestors land at anc[i - hi_shift]
 };
 
 // The half-split Megopolis kernel applies: W = 32, N = 2^k >= 256, 4 particles per thread
@@ -454,6 +455,7 @@ int run_range(Plan& p, int64_t p0, int64_t p_end, int64_t* anc, cudaStream_t st)
   a.anc = anc;
   a.one = 1;
   a.half = p.half ? 1 : 0;
+  a.hi_shift = p.hi_shift;
   {
     uint32_t k0 = (uint32_t)p.seed, k1 = (uint32_t)(p.seed >> 32);
     for (int r = 0; r < 10; ++r) { a.pk0[r] = k0; a.pk1[r] = k1; k0 += PHILOX_W0; k1 += PHILOX_W1; }
@@ -1029,6 +1031,36 @@ __global__ void k_philox_selftest(uint64_t key, uint32_t c1, uint32_t c2, uint32
   }
 }
 }  // namespace
+
+// Particles [lo0, lo1) and their mirrors [n/2 + lo0, n/2 + lo1) -- the two-stripe ownership
+// of the sharded layout (distributed.py, layout="stripes"), which lets every rank run the
+// half-split Megopolis kernel.  d_anc_local[0, L) receives the lower stripe, [L, 2L) the upper.
+extern "C" int mgp_resample_stripes(int kind, const void* d_w, int dtype, int64_t n, int32_t b, uint64_t seed,
+                                    int32_t warp, int32_t partition_bytes, int strict, int rng, int flags,
+                                    int64_t lo0, int64_t lo1, int64_t* d_anc_local, void* stream) {
+  Plan p;
+  int rc = make_plan(p, kind, d_w, dtype, n, b, seed, warp, partition_bytes, strict, rng, flags);
+  if (rc) return rc;
+  if (!d_w || !d_anc_local) return set_err(MGP_EINVAL, "null pointer");
+  if (n % 2) return set_err(MGP_EINVAL, "the stripe layout needs an even N, got %lld", (long long)n);
+  const int64_t half = n / 2, L = lo1 - lo0;
+  if (lo0 < 0 || lo1 > half || L < 0)
+    return set_err(MGP_EINVAL, "stripe [%lld, %lld) outside [0, %lld)", (long long)lo0, (long long)lo1, (long long)half);
+  if (plan_uses_w32(p) && (lo0 % 32 || half % 32))
+    return set_err(MGP_EINVAL, "lo0 and N/2 must be multiples of 32 for this resampler");
+  cudaStream_t st = S(stream);
+  if ((rc = plan_alloc(p, st))) return rc;
+  if (plan_half_ok(p) && lo0 % 128 == 0 && L % 128 == 0) {
+    p.half = true;
+    p.hi_shift = half - L;
+    rc = run_range(p, lo0, lo1, d_anc_local - lo0, st);
+  } else {
+    rc = run_range(p, lo0, lo1, d_anc_local - lo0, st);
+    if (!rc) rc = run_range(p, half + lo0, half + lo1, d_anc_local + L - (half + lo0), st);
+  }
+  int rc2 = plan_free(p, st);
+  return rc ? rc : rc2;
+}
 
 extern "C" int mgp_cumsum(const void* d_w, int dtype, int64_t n, void* d_out, void* stream) {
   if (dtype != MGP_F32 && dtype != MGP_F64) return set_err(MGP_EINVAL, "dtype must be MGP_F32 or MGP_F64, got %d", dtype);

@@ -42,6 +42,7 @@ struct ResampleArgs {
   cudaTextureObject_t tex;  // float32 weights as a 1-D linear texture (0: use LDG)
   uint32_t one;             // = 1; an opaque multiplier keeps the 64-bit key add on the FMA pipe
   int half;                 // half-split launch: [p0, p_end) is a range of LOWER-half particles
+  int64_t hi_shift;         // half-split: upper-half particle i stores its ancestor at anc[i - hi_shift]
   uint32_t pk0[10], pk1[10];  // Philox round keys (uniform; constant bank)
 };
 
@@ -259,7 +260,7 @@ __global__ void __launch_bounds__(RS_THREADS / PPT, PPT == 1 ? 0 : 1) k_megopoli
     if (!live[p]) continue;
     uint32_t k = a.first ? ii[p] : (uint32_t)a.kstate[ii[p]];
     if (bstar[p] >= 0) k = mego_j<POW2>(ial[p], lane, oc.o[bstar[p]], n);
-    if (a.last) a.anc[ii[p]] = (int64_t)k;
+    if (a.last) a.anc[(int64_t)ii[p] - (HALF && p >= 2 ? a.hi_shift : 0)] = (int64_t)k;
     else a.kstate[ii[p]] = (int32_t)k;
   }
 }

@@ -85,6 +85,16 @@ class CudaOps:
             D.ptr(out), D.stream_ptr()))
         return out
 
+    def resample_stripes(self, kind, w_full, b, seed, warp, partition_bytes, strict, rng, nonzero, lo0, lo1):
+        t = D.torch()
+        out = t.empty(2 * (lo1 - lo0), dtype=t.int64, device=w_full.device)
+        flags = _lib.FLAG_NONZERO if nonzero else 0
+        _lib.check(_lib.lib().mgp_resample_stripes(
+            _lib.KIND[kind], D.ptr(w_full), D.wdtype(w_full), w_full.numel(), int(b), int(seed) & (2**64 - 1),
+            int(warp), int(partition_bytes or 0), int(bool(strict)), _lib.RNG[rng], flags, int(lo0), int(lo1),
+            D.ptr(out), D.stream_ptr()))
+        return out
+
     def gather_rows(self, states, idx):
         t = D.torch()
         src = states.contiguous()
@@ -106,6 +116,7 @@ class ShardedResampler:
     rng: str = "megores"
     group: object = None
     ops: object = None
+    layout: str = "contiguous"  # or "stripes": rank r owns stripe r of each half of the population
 
     def __post_init__(self):
         import torch.distributed as dist
@@ -117,21 +128,52 @@ class ShardedResampler:
             self.ops = CudaOps()
         if self.kind in ("c1", "c2") and self.partition_bytes is None:
             raise ValueError(f"{self.kind} requires a partition size")
+        if self.layout not in ("contiguous", "stripes"):
+            raise ValueError(f"unknown layout {self.layout!r}")
+
+    # -- ownership --------------------------------------------------------------
+    def owned(self, n_local: int):
+        """Global particle ranges of this rank's local rows, in local order."""
+        r = self.rank
+        if self.layout == "contiguous":
+            return [(r * n_local, (r + 1) * n_local)]
+        h, half = n_local // 2, n_local // 2 * self.world
+        return [(r * h, (r + 1) * h), (half + r * h, half + (r + 1) * h)]
+
+    def _owner_local(self, g, n_local):
+        """(owner rank, local row) of global particle indices g (tensor)."""
+        t = D.torch()
+        if self.layout == "contiguous":
+            owner = t.div(g, n_local, rounding_mode="floor")
+            return owner, g - owner * n_local
+        h = n_local // 2
+        half = h * self.world
+        upper = g >= half
+        gl = t.where(upper, g - half, g)
+        owner = t.div(gl, h, rounding_mode="floor")
+        return owner, gl - owner * h + upper.to(g.dtype) * h
 
     # -- 1. replicated weights ---------------------------------------------
+    def _gather_into(self, out, part):
+        if self.world == 1:
+            out.copy_(part)
+            return
+        try:
+            self._dist.all_gather_into_tensor(out, part.contiguous(), group=self.group)
+        except (RuntimeError, AttributeError, NotImplementedError):
+            self._dist.all_gather(list(out.chunk(self.world)), part.contiguous(), group=self.group)
+
     def replicate_weights(self, w_local):
-        """All-gather the per-rank weight slices into the full replicated vector."""
+        """All-gather the per-rank weight slices (or stripes) into the full replicated vector."""
         t = D.torch()
         n_local = w_local.numel()
         full = t.empty(n_local * self.world, dtype=w_local.dtype, device=w_local.device)
-        if self.world == 1:
-            full.copy_(w_local)
-            return full
-        try:
-            self._dist.all_gather_into_tensor(full, w_local.contiguous(), group=self.group)
-        except (RuntimeError, AttributeError, NotImplementedError):
-            parts = list(full.chunk(self.world))
-            self._dist.all_gather(parts, w_local.contiguous(), group=self.group)
+        if self.layout == "contiguous":
+            self._gather_into(full, w_local)
+        else:
+            h, half = n_local // 2, n_local // 2 * self.world
+            self._gather_into(full[:half], w_local[:h])
+            self._gather_into(full[half:], w_local[h:])
         return full
 
     # -- 2. weight statistics ---------------------------------------------------
@@ -141,18 +183,21 @@ class ShardedResampler:
         8 numbers (float64 carries the counts exactly up to 2^53)."""
         t = D.torch()
         n_local = w_local.numel()
-        if not slice_tree_aligned(self.world, n_local):
+        stripes = self.layout == "stripes"
+        unit = n_local // 2 if stripes else n_local  # the tree-aligned piece each rank reduces
+        if not slice_tree_aligned(self.world, unit) or (stripes and n_local % 2):
             return self.ops.stats(full if full is not None else self.replicate_weights(w_local))
-        mine = t.tensor(_pack(self.ops.stats(w_local)), dtype=t.float64, device=w_local.device)
-        rows = t.empty(self.world * 8, dtype=t.float64, device=w_local.device)
-        if self.world == 1:
-            rows.copy_(mine)
-        else:
-            try:
-                self._dist.all_gather_into_tensor(rows, mine, group=self.group)
-            except (RuntimeError, AttributeError, NotImplementedError):
-                self._dist.all_gather(list(rows.chunk(self.world)), mine, group=self.group)
-        return combine_slice_stats([_unpack(r) for r in rows.view(self.world, 8).cpu().tolist()])
+        pieces = [w_local[:unit], w_local[unit:]] if stripes else [w_local]
+        mine = t.tensor(sum((_pack(self.ops.stats(pc)) for pc in pieces), []), dtype=t.float64,
+                        device=w_local.device)
+        rows = t.empty(self.world * mine.numel(), dtype=t.float64, device=w_local.device)
+        self._gather_into(rows, mine)
+        per = [_unpack(r) for r in rows.view(self.world * len(pieces), 8).cpu().tolist()]
+        if not stripes:
+            return combine_slice_stats(per)
+        lower = combine_slice_stats(per[0::2])  # root of numpy's tree: lower half + upper half
+        upper = combine_slice_stats(per[1::2])
+        return combine_slice_stats([lower, upper])
 
     # -- 2-4. B rule + per-slice resample --------------------------------------
     def resample(self, w_local, b: int | None = None, seed=0, epsilon: float = 0.01):
@@ -176,10 +221,13 @@ class ShardedResampler:
                              f"({self.warp.warp_size}) in strict mode")
         if self.kind in ("c1", "c2"):
             PartitionConfig(self.partition_bytes).n_partitions(n, self.warp)
+        args = (self.kind, full, b, seed, self.warp.warp_size, self.partition_bytes, self.strict, self.rng,
+                st.n_zero == 0)
+        if self.layout == "stripes":
+            (lo0, lo1), _ = self.owned(n_local)
+            return self.ops.resample_stripes(*args, lo0, lo1), b
         p0 = self.rank * n_local
-        anc = self.ops.resample_range(self.kind, full, b, seed, self.warp.warp_size, self.partition_bytes,
-                                      self.strict, self.rng, st.n_zero == 0, p0, p0 + n_local)
-        return anc, b
+        return self.ops.resample_range(*args, p0, p0 + n_local), b
 
     # -- 5. particle states ---------------------------------------------------
     def exchange(self, states_local, anc_local):
@@ -193,10 +241,10 @@ class ShardedResampler:
         dev = states_local.device
         anc = anc_local.to(device=dev, dtype=t.int64)
         if self.world == 1:
-            return self.ops.gather_rows(states_local, anc)
-        owner = t.div(anc, n_local, rounding_mode="floor")
+            return self.ops.gather_rows(states_local, self._owner_local(anc, n_local)[1])
+        owner, local = self._owner_local(anc, n_local)
         order = t.argsort(owner, stable=True)
-        send_idx = (anc - owner * n_local)[order].contiguous()
+        send_idx = local[order].contiguous()
         send_counts = t.bincount(owner, minlength=self.world).to(t.int64)
         recv_counts = t.empty_like(send_counts)
         dist.all_to_all_single(recv_counts, send_counts, group=self.group)

@@ -55,8 +55,47 @@ class OracleOps:
         anc = oracle.resample(kind, w_full.numpy(), b, seed, warp, partition_bytes, strict, rng, p0=p0, p1=p1)
         return torch.from_numpy(anc[p0:p1].copy())
 
+    def resample_stripes(self, kind, w_full, b, seed, warp, partition_bytes, strict, rng, nonzero, lo0, lo1):
+        from oracle import oracle
+
+        half = w_full.numel() // 2
+        anc = oracle.resample(kind, w_full.numpy(), b, seed, warp, partition_bytes, strict, rng)
+        return torch.from_numpy(np.concatenate([anc[lo0:lo1], anc[half + lo0:half + lo1]]))
+
     def gather_rows(self, states, idx):
         return states[idx]
+
+
+def _worker_stripes(rank, world, port, case, q):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle
+        from paper_2109_13504_b200.distributed import ShardedResampler
+
+        kind, n_local, y, prec, rng, b = case
+        n, h = n_local * world, n_local // 2
+        w_full = oracle.gen_gaussian_weights(y, n, 4343, prec)
+        sr = ShardedResampler(kind=kind, partition_bytes=128 if kind in ("c1", "c2") else None, rng=rng,
+                              ops=OracleOps(), layout="stripes")
+        (a0, a1), (b0, b1) = sr.owned(n_local)
+        w_local = torch.from_numpy(np.concatenate([w_full[a0:a1], w_full[b0:b1]]))
+        anc_local, b_used = sr.resample(w_local, b=b, seed=77)
+        states_full = np.stack([np.arange(n, dtype=np.float64) * 1.5, np.arange(n, dtype=np.float64)], axis=1)
+        s_local = torch.from_numpy(np.concatenate([states_full[a0:a1], states_full[b0:b1]]))
+        new_local = sr.exchange(s_local, anc_local)
+        parts = [torch.zeros(n_local, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(parts, anc_local)
+        news = [torch.zeros_like(new_local) for _ in range(world)]
+        dist.all_gather(news, new_local)
+        if rank == 0:  # back to global particle order
+            anc = np.concatenate([p[:h].numpy() for p in parts] + [p[h:].numpy() for p in parts])
+            st = np.concatenate([x[:h].numpy() for x in news] + [x[h:].numpy() for x in news])
+            q.put((int(b_used), anc, st))
+    finally:
+        dist.destroy_process_group()
 
 
 def _worker(rank, world, port, case, q):
@@ -94,11 +133,11 @@ def _worker(rank, world, port, case, q):
         dist.destroy_process_group()
 
 
-def _run(world, case):
+def _run(world, case, target=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    procs = [ctx.Process(target=target or _worker, args=(r, world, port, case, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = q.get(timeout=300)
@@ -148,3 +187,26 @@ def test_slice_stats_combine_bit_exact(oracle, world, n_local):
     mean, mx = oracle.weight_mean_max(w)
     assert g.sum == total and g.mean == mean and g.max == mx and g.n == world * n_local
     assert not slice_tree_aligned(3, 1024) and not slice_tree_aligned(2, 60) and not slice_tree_aligned(2, 1001)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("case", [
+    ("megopolis", 512, 4.0, "single", "philox", None),
+    ("megopolis", 192, 2.0, "double", "megores", 5),
+    ("c2", 256, 1.0, "single", "megores", 4),
+])
+def test_stripes_layout_equals_single_process(oracle, world, case):
+    """layout="stripes": rank r owns stripe r of each half (the half-split kernel's pairing);
+    ancestors, the slice-statistics B and the exchanged states equal the single process's."""
+    kind, n_local, y, prec, rng, b = case
+    b_used, anc, states = _run(world, case, _worker_stripes)
+    n = n_local * world
+    w_full = oracle.gen_gaussian_weights(y, n, 4343, prec)
+    if b is None:
+        mean, mx = oracle.weight_mean_max(w_full)
+        assert b_used == oracle.compute_iterations(0.01, mean, mx)
+    ref = oracle.resample(kind, w_full, b_used, 77, 32, 128 if kind in ("c1", "c2") else None, True, rng)
+    assert np.array_equal(anc, ref)
+    states_full = np.stack([np.arange(n) * 1.5, np.arange(n)], axis=1)
+    assert np.array_equal(states, states_full[ref])
+

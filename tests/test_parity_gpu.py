@@ -465,3 +465,23 @@ def test_half_split_host_chunks(mg, oracle, zeros):
                                              _lib.RNG["philox"], 0, p0, p0 + n // 4, out.data_ptr(),
                                              torch.cuda.current_stream().cuda_stream))
     assert np.array_equal(out.cpu().numpy(), ref[p0:p0 + n // 4])
+
+
+@pytest.mark.parametrize("rng,n,b,prec", [("philox", 1 << 16, 7, "single"), ("philox", 1 << 15, 1030, "single"),
+                                          ("megores", 1 << 14, 9, "single"), ("philox", 3 * 4096, 5, "double")])
+def test_resample_stripes(mg, oracle, rng, n, b, prec):
+    """mgp_resample_stripes (the sharded 'stripes' layout): lower stripe then upper stripe,
+    half-split kernel when it applies, two range launches otherwise."""
+    from paper_2109_13504_b200 import _lib
+
+    w = oracle.gen_gaussian_weights(2.0, n, 515, prec)
+    ref = oracle.megopolis(w, b, seed=3, rng=rng)
+    wd = torch.from_numpy(w).cuda()
+    half = n // 2
+    for lo0, lo1 in ((0, half), (256, half // 2 + 128), (half // 4, half // 4 + 32), (128, 128)):
+        out = torch.empty(max(1, 2 * (lo1 - lo0)), dtype=torch.int64, device="cuda")
+        _lib.check(_lib.lib().mgp_resample_stripes(_lib.KIND["megopolis"], wd.data_ptr(), 0 if prec == "single" else 1,
+                                                   n, b, 3, 32, 0, 1, _lib.RNG[rng], 0, lo0, lo1, out.data_ptr(),
+                                                   torch.cuda.current_stream().cuda_stream))
+        got = out.cpu().numpy()[:2 * (lo1 - lo0)]
+        assert np.array_equal(got, np.concatenate([ref[lo0:lo1], ref[half + lo0:half + lo1]])), (lo0, lo1)
