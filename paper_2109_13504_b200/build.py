@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libmgp.so")
 SOURCES = [os.path.join(CSRC, "mgp_abi.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("mgp_kernels.cuh", "mgp_device.cuh")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("mgp_kernels.cuh", "mgp_device.cuh", "mgp_prefix.cuh")] + [
     os.path.join(ROOT, "include", "megopolis_b200.h")]
 
 NVCC_FLAGS = [
