@@ -186,6 +186,11 @@ int mgp_cumsum(const void *d_w, int dtype, int64_t n, void *d_out, void *stream)
 int mgp_multinomial(const void *d_w, int dtype, int64_t n, uint64_t seed, int64_t *d_anc, void *stream);
 int mgp_systematic(const void *d_w, int dtype, int64_t n, uint64_t seed, int64_t *d_anc, void *stream);
 
+/* systematic_oracle(w, u) (M/resample.py:339-354) for an explicit u in [0, 1): the reference's
+ * sequential stratified selection, with its comparison semantics (float32 weights compare in
+ * float32 against float32(target), NumPy 2 weak-scalar promotion). */
+int mgp_systematic_oracle(const void *d_w, int dtype, int64_t n, double u, int64_t *d_anc, void *stream);
+
 /* Self-check: our Philox4x32-10 vs curand_Philox4x32_10 for counters {i, c1, c2, c3}.
  * Writes 4*n words each; returns the number of mismatching words in *h_mismatch. */
 int mgp_philox_selftest(uint64_t key, uint32_t c1, uint32_t c2, uint32_t c3, int64_t n, int64_t *h_mismatch);

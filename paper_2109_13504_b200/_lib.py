@@ -58,6 +58,7 @@ SIGNATURES = {
     "mgp_cumsum": (_i32, [_vp, _i32, _i64, _vp, _vp]),
     "mgp_multinomial": (_i32, [_vp, _i32, _i64, _u64, _vp, _vp]),
     "mgp_systematic": (_i32, [_vp, _i32, _i64, _u64, _vp, _vp]),
+    "mgp_systematic_oracle": (_i32, [_vp, _i32, _i64, _dbl, _vp, _vp]),
     "mgp_philox_selftest": (_i32, [_u64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, _i64, _vp]),
 }
 

@@ -1078,6 +1078,27 @@ extern "C" int mgp_systematic(const void* d_w, int dtype, int64_t n, uint64_t se
   return resample_device(MGP_KIND_SYSTEMATIC, d_w, dtype, n, 1, seed, 32, 0, 0, MGP_RNG_MEGORES, 0, d_anc, stream);
 }
 
+extern "C" int mgp_systematic_oracle(const void* d_w, int dtype, int64_t n, double u, int64_t* d_anc, void* stream) {
+  if (!(u >= 0.0 && u < 1.0)) return set_err(MGP_EINVAL, "u must be in [0, 1), got %.17g", u);
+  if (dtype != MGP_F32 && dtype != MGP_F64) return set_err(MGP_EINVAL, "dtype must be MGP_F32 or MGP_F64, got %d", dtype);
+  if (n < 1) return set_err(MGP_EINVAL, "weights must be a non-empty 1-d sequence");
+  if (n > MAX_N) return set_err(MGP_EUNSUPPORTED, "N=%lld exceeds this build's limit of 2^31-1 particles", (long long)n);
+  if (!d_w || !d_anc) return set_err(MGP_EINVAL, "null pointer");
+  cudaStream_t st = S(stream);
+  ensure_pool();
+  void* cum = nullptr;
+  CUDA_TRY(cudaMallocAsync(&cum, (size_t)n * (dtype == MGP_F32 ? 4 : 8), st));
+  int rc = px_cumsum_any(d_w, dtype, n, cum, st);
+  if (!rc) {
+    const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 64);
+    if (dtype == MGP_F32) k_systematic_oracle<float><<<grid, 256, 0, st>>>((const float*)cum, n, u, d_anc);
+    else k_systematic_oracle<double><<<grid, 256, 0, st>>>((const double*)cum, n, u, d_anc);
+    LAUNCH_CHECK("k_systematic_oracle");
+  }
+  CUDA_TRY(cudaFreeAsync(cum, st));
+  return rc;
+}
+
 extern "C" int mgp_philox_selftest(uint64_t key, uint32_t c1, uint32_t c2, uint32_t c3, int64_t n,
                                    int64_t* h_mismatch) {
   unsigned long long* d = nullptr;

@@ -602,4 +602,25 @@ __global__ void k_systematic(const WT* __restrict__ cum, int64_t n, double u0, i
   }
 }
 
+// systematic_oracle(w, u) (M/resample.py:339-354): the reference's sequential stratified loop
+// for an explicit u.  Its comparison `cum[j] < target` has a float32 array element on the left
+// and a Python float on the right; under NumPy 2 (NEP 50) the Python float is a weak scalar
+// converted to float32, so for float32 weights the comparison is made in float32 against
+// float32(target) -- the only difference from systematic_improved (float64 comparison).
+template <typename WT>
+__global__ void k_systematic_oracle(const WT* __restrict__ cum, int64_t n, double u, int64_t* __restrict__ anc) {
+  const double total = (double)cum[n - 1];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double target = __dmul_rn(__ddiv_rn(__dadd_rn((double)i, u), (double)n), total);
+    const WT key = (WT)target;  // float32 weights: the weak-scalar conversion; float64: exact
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(cum + mid) < key) lo = mid + 1;
+      else hi = mid;
+    }
+    anc[i] = lo < n - 1 ? lo : n - 1;
+  }
+}
+
 }  // namespace mgp

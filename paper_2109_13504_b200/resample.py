@@ -189,6 +189,27 @@ def systematic_improved(w, seed, warp: WarpConfig = WarpConfig()):
     return _resample("systematic", w, 1, seed, None, None, False, "megores", "systematic_improved")
 
 
+def systematic_oracle(w, u: float):
+    """Sequential single-pass stratified reference for a given u in [0, 1) (M/resample.py:339-354),
+    with the reference's comparison semantics (float32 weights: float32 comparison against
+    float32(target), NumPy 2 weak-scalar promotion).  numpy in -> numpy out."""
+    u = float(u)
+    if not (0.0 <= u < 1.0):
+        raise ValueError(f"u must be in [0, 1), got {u}")
+    D.require_cuda()
+    t = D.torch()
+    w = _as_weight_vector(w)
+    host = not w.on_device
+    vals = t.from_numpy(np.ascontiguousarray(w.values)).cuda() if host else w.values.contiguous()
+    if (w.stats().n_pos if not host else int(np.any(w.values > 0))) == 0:
+        raise ValueError("all weights are zero")
+    out = t.empty(vals.numel(), dtype=t.int64, device=vals.device)
+    with t.cuda.device(vals.device):
+        _lib.check(_lib.lib().mgp_systematic_oracle(D.ptr(vals), D.wdtype(vals), vals.numel(), u, D.ptr(out),
+                                                    D.stream_ptr()))
+    return out.cpu().numpy() if host else out
+
+
 def inclusive_prefix(w):
     """``np.cumsum(values)`` in the weights' dtype, bit-identical to numpy's sequential
     scan (M/resample.py:288-291).  numpy in -> numpy out; CUDA tensor in -> CUDA tensor out."""

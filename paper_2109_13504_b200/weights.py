@@ -226,3 +226,35 @@ def gen_gamma_weights(params: GammaWeightParams, seed, precision="single") -> We
 
     u = uniform_open01_at(seed, np.arange(params.n), 0)
     return WeightVector(stats.gamma.ppf(u, a=params.alpha, scale=1.0 / params.beta), precision)
+
+
+def estimate_ratio(w, subset_size: int, seed) -> float:
+    """mean(w) / max(w) over the first ``subset_size`` entries of the seed's stable permutation
+    (M/weights.py:134-154), on the device (radix sort of the 53-bit keys, numpy-exact mean)."""
+    t = D.torch()
+    wv = _as_weight_vector(w)
+    n = len(wv)
+    if not (1 <= subset_size <= n):
+        raise ValueError(f"subset_size must be in [1, {n}], got {subset_size}")
+    vals = wv.values if wv.on_device else t.from_numpy(np.ascontiguousarray(wv.values)).cuda()
+    out = t.empty(2, dtype=t.float64, device=vals.device)
+    with t.cuda.device(vals.device):
+        _lib.check(_lib.lib().mgp_estimate_ratio_stats(D.ptr(vals), D.wdtype(vals), n, int(subset_size),
+                                                       int(seed) & (2**64 - 1), D.ptr(out), D.stream_ptr()))
+    mean, mx = (float(v) for v in out.cpu().numpy())
+    if mx == 0.0:
+        raise ValueError("subset contains only zero weights")
+    return mean / mx
+
+
+def proposition_recurrence(mean_w: float, max_w: float, n: int, b: int) -> float:
+    """P_k = 1/N + P_{k-1} (1 - mean/max), P_0 = 0, after b steps (M/weights.py:157-172)."""
+    if b < 0:
+        raise ValueError(f"B must be >= 0, got {b}")
+    if mean_w <= 0 or max_w <= 0 or mean_w > max_w:
+        raise ValueError("need 0 < mean_w <= max_w")
+    ratio = mean_w / max_w
+    p = 0.0
+    for _ in range(b):
+        p = 1.0 / n + p * (1.0 - ratio)
+    return p

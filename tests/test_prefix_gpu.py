@@ -182,3 +182,34 @@ def test_prefix_errors():
         mg.multinomial(np.zeros(8, np.float32), 1)
     with pytest.raises(ValueError, match="all weights are zero"):
         mg.systematic_improved(torch.zeros(8, device="cuda"), 1)
+
+
+def test_systematic_oracle_and_estimate_ratio_golden():
+    """systematic_oracle(w, u) with the reference's comparison semantics, and estimate_ratio,
+    against the unmodified reference (tests/golden/make_golden_sysoracle.py)."""
+    gold = json.load(open(os.path.join(HERE, "golden", "golden_sysoracle.json")))
+    for c in gold["cases"]:
+        dt = np.float32 if c["precision"] == "single" else np.float64
+        w = np.asarray(c["w"], dtype=dt)
+        wv = mg.WeightVector(w, c["precision"])
+        got = mg.systematic_oracle(wv, c["u"])
+        assert got.tolist() == c["anc"]
+        assert mg.estimate_ratio(wv, c["ratio_subset"], c["ratio_seed"]) == c["ratio"]
+    with pytest.raises(ValueError, match="u must be in"):
+        mg.systematic_oracle(np.ones(4), 1.0)  # T/test_resample.py:268-271
+
+
+def test_systematic_oracle_reference_cases():  # T/test_resample.py:222-253
+    w = mg.WeightVector(np.ones(64), "double")
+    for u in (0.25, 0.5, 0.999):
+        assert list(mg.systematic_oracle(w, u)) == list(range(64))
+    assert list(mg.systematic_oracle(w, 0.0)) == [0] + list(range(63))  # ties resolve to the lower bracket
+    assert np.all(mg.systematic_oracle(mg.WeightVector(np.array([0.0, 0.0, 5.0, 0.0]), "double"), 0.3) == 2)
+    off = mg.ancestors_to_offspring(mg.systematic_oracle(mg.WeightVector(np.array([0.5, 0.5, 0.0, 0.0]), "double"),
+                                                         0.1), 4)
+    assert list(off) == [2, 2, 0, 0]
+    w4 = mg.WeightVector(np.array([1.0, 2.0, 3.0, 2.0]), "double")
+    counts = np.zeros(4)
+    for k in range(10**4):
+        counts += np.bincount(mg.systematic_oracle(w4, float(ora.u01(1234, k, 0))), minlength=4)
+    assert np.all(np.abs(counts / 10**4 - np.array([0.5, 1.0, 1.5, 1.0])) < 0.05)
