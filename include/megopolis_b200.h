@@ -141,6 +141,13 @@ int mgp_quality_add(const int64_t *d_counts, const double *d_e, int64_t n, doubl
                     double *d_se_total, double *d_se_run, void *stream);
 int mgp_quality_finalize(const double *d_sum, const double *d_sumsq, const double *d_e, int64_t n, int64_t k,
                          double *d_variance, double *d_bias_sq, void *stream);
+/* K runs of a resampler accumulated on the device (the inner loop of the quality grids,
+ * M/bench.py:121-126): for each h_seeds[r]: ancestors = kind(w, b, seed) -> offspring ->
+ * QualityAccumulator.add into d_sum / d_sumsq / *d_se_total (d_e from mgp_expected_offspring).
+ * Same results as K separate calls, without a host round trip per run. */
+int mgp_quality_runs(int kind, const void *d_w, int dtype, int64_t n, int32_t b, const uint64_t *h_seeds, int32_t k,
+                     int32_t warp, int32_t partition_bytes, int strict, int rng, int flags, const double *d_e,
+                     double *d_sum, double *d_sumsq, double *d_se_total, void *stream);
 /* squared_error (M/metrics.py:63-68) for one offspring vector */
 int mgp_squared_error(const int64_t *d_counts, const double *d_e, int64_t n, double *d_out, void *stream);
 

@@ -47,6 +47,8 @@ SIGNATURES = {
     "mgp_expected_offspring": (_i32, [_vp, _i32, _i64, _vp, _vp, _vp]),
     "mgp_quality_add": (_i32, [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
     "mgp_quality_finalize": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
+    "mgp_quality_runs": (_i32, [_i32, _vp, _i32, _i64, _i32, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp,
+                                 _vp, _vp]),
     "mgp_squared_error": (_i32, [_vp, _vp, _i64, _vp, _vp]),
     "mgp_gather": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp]),
     "mgp_gather_peers": (_i32, [_vp, _i32, _i64, _i64, _vp, _i64, _vp, _vp]),

@@ -107,13 +107,13 @@ def quality_grid(spec: ExperimentSpec, rng_stream: str = "megores"):
     import torch
 
     from .metrics import QualityAccumulator
-    from .resample import ancestors_to_offspring, make_resampler
+    from .resample import make_resampler
     from .weights import WeightVector, iterations_for
 
     rows = []
     for token in spec.algorithms:
         name, part_bytes = algorithm_token(token)
-        fn = make_resampler(name, partition_bytes=part_bytes, rng=rng_stream)
+        make_resampler(name, partition_bytes=part_bytes, rng=rng_stream)  # argument validation
         for n in spec.n_grid:
             for param in spec.params:
                 stats, bs = [], []
@@ -123,9 +123,8 @@ def quality_grid(spec: ExperimentSpec, rng_stream: str = "megores"):
                     b = iterations_for(w, spec.epsilon).b
                     bs.append(b)
                     acc = QualityAccumulator(n)
-                    for k in range(spec.k_runs):
-                        anc = fn(w, b, _rng.derive_seed(spec.seed, token_id(token), n, seq, k))
-                        acc.add(ancestors_to_offspring(anc, n), w)
+                    seeds = [_rng.derive_seed(spec.seed, token_id(token), n, seq, k) for k in range(spec.k_runs)]
+                    acc.add_runs(name, w, b, seeds, partition_bytes=part_bytes, rng=rng_stream)
                     stats.append(acc.finalize())
 
                 def avg(attr):

@@ -1062,6 +1062,50 @@ extern "C" int mgp_resample_stripes(int kind, const void* d_w, int dtype, int64_
   return rc ? rc : rc2;
 }
 
+// K resampling runs accumulated into a QualityAccumulator on the device: per seed, the
+// resampler, the offspring histogram and QualityAccumulator.add (M/metrics.py:86-93), with no
+// host round trip between runs -- the inner loop of the quality grids (M/bench.py:121-126).
+extern "C" int mgp_quality_runs(int kind, const void* d_w, int dtype, int64_t n, int32_t b, const uint64_t* h_seeds,
+                                int32_t k, int32_t warp, int32_t partition_bytes, int strict, int rng, int flags,
+                                const double* d_e, double* d_sum, double* d_sumsq, double* d_se_total, void* stream) {
+  if (k < 0 || (k > 0 && !h_seeds)) return set_err(MGP_EINVAL, "invalid seed list");
+  if (!d_w || !d_e || !d_sum || !d_sumsq || !d_se_total) return set_err(MGP_EINVAL, "null pointer");
+  cudaStream_t st = S(stream);
+  ensure_pool();
+  int64_t *anc = nullptr, *counts = nullptr;
+  double* se_run = nullptr;
+  CUDA_TRY(cudaMallocAsync(&anc, sizeof(int64_t) * n, st));
+  CUDA_TRY(cudaMallocAsync(&counts, sizeof(int64_t) * n, st));
+  CUDA_TRY(cudaMallocAsync(&se_run, sizeof(double), st));
+  int rc = 0;
+  Plan shared;  // prefix-sum kinds: one prefix sum serves every seed
+  const bool prefix = is_prefix_kind(kind);
+  if (prefix) {
+    rc = make_plan(shared, kind, d_w, dtype, n, b, 0, warp, partition_bytes, strict, rng, flags);
+    if (!rc) rc = plan_alloc(shared, st);
+  }
+  for (int32_t r = 0; r < k && !rc; ++r) {
+    if (prefix) {
+      shared.seed = h_seeds[r];
+      rc = run_range(shared, 0, n, anc, st);
+    } else {
+      Plan p;
+      rc = make_plan(p, kind, d_w, dtype, n, b, h_seeds[r], warp, partition_bytes, strict, rng, flags);
+      if (!rc) rc = plan_alloc(p, st);
+      if (!rc) rc = run_range(p, 0, n, anc, st);
+      int rc2 = plan_free(p, st);
+      if (!rc) rc = rc2;
+    }
+    if (!rc) rc = mgp_offspring(anc, n, n, counts, nullptr, st);
+    if (!rc) rc = mgp_quality_add(counts, d_e, n, d_sum, d_sumsq, d_se_total, se_run, st);
+  }
+  if (prefix) plan_free(shared, st);
+  cudaFreeAsync(anc, st);
+  cudaFreeAsync(counts, st);
+  cudaFreeAsync(se_run, st);
+  return rc;
+}
+
 extern "C" int mgp_cumsum(const void* d_w, int dtype, int64_t n, void* d_out, void* stream) {
   if (dtype != MGP_F32 && dtype != MGP_F64) return set_err(MGP_EINVAL, "dtype must be MGP_F32 or MGP_F64, got %d", dtype);
   if (n < 1) return set_err(MGP_EINVAL, "weights must be a non-empty 1-d sequence");

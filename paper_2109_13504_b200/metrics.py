@@ -93,6 +93,32 @@ class QualityAccumulator:
                                                   D.ptr(self._sum_sq), D.ptr(self._se),
                                                   D.ptr(self._se[1:]), D.stream_ptr()))
 
+    def add_runs(self, kind: str, w, b: int, seeds, warp_size: int = 32, partition_bytes: int | None = None,
+                 strict: bool = True, rng: str = "megores") -> None:
+        """K runs of resampler ``kind`` (one per seed) added in one device pass -- the same as
+        ``for s in seeds: self.add(ancestors_to_offspring(make_resampler(kind, ...)(w, b, s)), w)``
+        (M/bench.py:121-126) without a host round trip per run."""
+        import ctypes
+
+        t = D.torch()
+        wd = _dev_weights(w).to(self.device)
+        if self._expected is None:
+            self._expected = _expected(wd)
+        from .weights import device_stats
+
+        st = device_stats(wd)
+        if st.n_pos == 0:
+            raise ValueError("all weights are zero")
+        seeds = [int(s) & (2**64 - 1) for s in seeds]
+        arr = (ctypes.c_uint64 * max(1, len(seeds)))(*seeds)
+        flags = _lib.FLAG_NONZERO if st.n_zero == 0 else 0
+        with t.cuda.device(self.device):
+            _lib.check(_lib.lib().mgp_quality_runs(
+                _lib.KIND[kind], D.ptr(wd), D.wdtype(wd), self.n, int(b), ctypes.cast(arr, ctypes.c_void_p),
+                len(seeds), int(warp_size), int(partition_bytes or 0), int(bool(strict)), _lib.RNG[rng], flags,
+                D.ptr(self._expected), D.ptr(self._sum), D.ptr(self._sum_sq), D.ptr(self._se), D.stream_ptr()))
+        self.k += len(seeds)
+
     @property
     def _se_total(self) -> float:
         return float(self._se[0].item())

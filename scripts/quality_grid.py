@@ -41,7 +41,7 @@ rows = []
 t0 = time.time()
 for token in a.algs.split(","):
     name, _, part = token.partition(":")
-    fn = mg.make_resampler(name, partition_bytes=int(part) if part else None, rng=a.rng)
+    pb = int(part) if part else None
     for lg in (int(x) for x in a.ns.split(",")):
         n = 1 << lg
         for y in (float(x) for x in a.ys.split(",")):
@@ -52,8 +52,9 @@ for token in a.algs.split(","):
                 b = mg.iterations_for(w, 0.01).b
                 bs.append(b)
                 acc = mg.QualityAccumulator(n)
-                for k in range(a.k):
-                    acc.add(mg.ancestors_to_offspring(fn(w, b, mg.derive_seed(a.seed, 7, lg, s, k)), n), w)
+                # the K runs in one device pass (mgp_quality_runs): identical to K add() calls
+                acc.add_runs(name, w, b, [mg.derive_seed(a.seed, 7, lg, s, k) for k in range(a.k)],
+                             partition_bytes=pb, rng=a.rng)
                 per_seq.append(acc.finalize())
             row = {"algorithm": token, "n": n, "y": y, "b_mean": float(np.mean(bs)), "k": a.k, "sequences": a.seq,
                    "mse_per_particle": float(np.mean([q.mse_per_particle for q in per_seq])),
