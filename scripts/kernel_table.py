@@ -68,6 +68,16 @@ for kind, part in [("megopolis", 0), ("metropolis", 0), ("c1", 128), ("c1", 2048
         add(f"{kind}{':' + str(part) if part else ''} {rng}", ms, resample_bytes,
             f"{n * b / (ms * 1e-3):.3e} comparisons/s, {n / (ms * 1e-3):.3e} particles/s")
 
+# float64 weights (the reference's "double"): 128 MiB of weights, beyond L2's reach
+w64 = w.double()
+for rng in ("megores", "philox"):
+    def go64(rng=rng):
+        _lib.check(L.mgp_resample_range(_lib.KIND["megopolis"], D.ptr(w64), 1, n, b, 7, 32, 0, 1, _lib.RNG[rng],
+                                        _lib.FLAG_NONZERO, 0, n, D.ptr(anc), sp))
+    ms = timeit(go64)
+    add(f"megopolis f64 {rng}", ms, n * b * 8 + n * 8 + n * 8 + 8 * b,
+        f"{n * b / (ms * 1e-3):.3e} comparisons/s, {n / (ms * 1e-3):.3e} particles/s (8 B per comparison)")
+
 stats = torch.empty(8, dtype=torch.float64, device="cuda")
 add("weight_stats (pairwise sum+max+flags)", timeit(lambda: _lib.check(L.mgp_weight_stats(D.ptr(w), 0, n, D.ptr(stats), sp))), 4 * n)
 counts = torch.empty(n, dtype=torch.int64, device="cuda")
