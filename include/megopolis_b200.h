@@ -168,10 +168,13 @@ int mgp_mean(const void *d_x, int dtype, int64_t n, double *d_out, void *stream)
  *   mgp_pf_init: x_i = gaussian_at(seed, i, 0) * sqrt(process_var)          (init_state)
  *   mgp_pf_predict_update: noise = gaussian_at(seed, i, 0) * sqrt(process_var);
  *     x' = transition(x, t, noise) with cos_term = 8 cos(1.2 t) (M/pfilter.py:86-89);
- *     w = max(likelihood(z, x', obs_var), tiny) cast to dtype (M/pfilter.py:92-103). */
+ *     w = max(likelihood(z, x', obs_var), tiny) cast to dtype (M/pfilter.py:92-103);
+ *     *d_any_pos |= 1 if any weight is > 0 (nullable; the resampler's all-zero check,
+ *     M/resample.py:96-100, without a host round trip). */
 int mgp_pf_init(int64_t n, uint64_t seed, double sqrt_process_var, double *d_x, void *stream);
 int mgp_pf_predict_update(const double *d_x, int64_t n, double cos_term, double sqrt_process_var, uint64_t seed,
-                          double z, double obs_var, int dtype, double *d_xpred, void *d_w, void *stream);
+                          double z, double obs_var, int dtype, double *d_xpred, void *d_w, int32_t *d_any_pos,
+                          void *stream);
 
 /* estimate_ratio (M/weights.py:134-154) statistics: d_out = {mean, max} (float64) of the
  * subset formed by the first `subset` entries of the stable argsort of uniform01_at(seed, i, 0)

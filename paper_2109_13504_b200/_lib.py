@@ -54,7 +54,7 @@ SIGNATURES = {
     "mgp_gather_peers": (_i32, [_vp, _i32, _i64, _i64, _vp, _i64, _vp, _vp]),
     "mgp_mean": (_i32, [_vp, _i32, _i64, _vp, _vp]),
     "mgp_pf_init": (_i32, [_i64, _u64, _dbl, _vp, _vp]),
-    "mgp_pf_predict_update": (_i32, [_vp, _i64, _dbl, _dbl, _u64, _dbl, _dbl, _i32, _vp, _vp, _vp]),
+    "mgp_pf_predict_update": (_i32, [_vp, _i64, _dbl, _dbl, _u64, _dbl, _dbl, _i32, _vp, _vp, _vp, _vp]),
     "mgp_estimate_ratio_stats": (_i32, [_vp, _i32, _i64, _i64, _u64, _vp, _vp]),
     "mgp_gen_gaussian": (_i32, [_dbl, _i64, _u64, _i32, _vp, _vp]),
     "mgp_cumsum": (_i32, [_vp, _i32, _i64, _vp, _vp]),

@@ -936,7 +936,8 @@ int mgp_pf_init(int64_t n, uint64_t seed, double sqrt_process_var, double* d_x, 
 }
 
 int mgp_pf_predict_update(const double* d_x, int64_t n, double cos_term, double sqrt_process_var, uint64_t seed,
-                          double z, double obs_var, int dtype, double* d_xpred, void* d_w, void* stream) {
+                          double z, double obs_var, int dtype, double* d_xpred, void* d_w, int32_t* d_any_pos,
+                          void* stream) {
   if (n < 1) return set_err(MGP_EINVAL, "n_particles must be positive");
   if (!(obs_var > 0)) return set_err(MGP_EINVAL, "obs_var must be positive");
   const double norm = std::sqrt(2.0 * 3.141592653589793 * obs_var);  // math.sqrt(2.0 * math.pi * obs_var)
@@ -944,10 +945,10 @@ int mgp_pf_predict_update(const double* d_x, int64_t n, double cos_term, double 
   const uint64_t base = megores_base(seed);
   if (dtype == MGP_F32)
     k_pf_predict_update<float><<<grid, 256, 0, S(stream)>>>(d_x, n, cos_term, sqrt_process_var, base, z, obs_var, norm,
-                                                            d_xpred, (float*)d_w);
+                                                            d_xpred, (float*)d_w, d_any_pos);
   else if (dtype == MGP_F64)
     k_pf_predict_update<double><<<grid, 256, 0, S(stream)>>>(d_x, n, cos_term, sqrt_process_var, base, z, obs_var, norm,
-                                                             d_xpred, (double*)d_w);
+                                                             d_xpred, (double*)d_w, d_any_pos);
   else
     return set_err(MGP_EINVAL, "dtype must be MGP_F32 or MGP_F64");
   LAUNCH_CHECK("k_pf_predict_update");

@@ -868,7 +868,8 @@ __global__ void k_pf_init(int64_t n, uint64_t base, double sqrt_pv, double* __re
 template <typename WT>
 __global__ void k_pf_predict_update(const double* __restrict__ x, int64_t n, double cos_term, double sqrt_pv,
                                     uint64_t base, double z, double obs_var, double norm,
-                                    double* __restrict__ xp, WT* __restrict__ w) {
+                                    double* __restrict__ xp, WT* __restrict__ w, int32_t* any_pos) {
+  bool pos = false;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double v = __dmul_rn(gaussian_at_dev(base, (uint64_t)i), sqrt_pv);
     const double xi = x[i];
@@ -880,8 +881,13 @@ __global__ void k_pf_predict_update(const double* __restrict__ x, int64_t n, dou
     const double r = __dsub_rn(z, __ddiv_rn(__dmul_rn(xn, xn), 20.0));
     double dens = __ddiv_rn(exp(__ddiv_rn(__dmul_rn(__dmul_rn(-0.5, r), r), obs_var)), norm);
     dens = dens > 2.2250738585072014e-308 ? dens : 2.2250738585072014e-308;
-    w[i] = (WT)dens;
+    const WT wv = (WT)dens;
+    w[i] = wv;
+    pos |= wv > (WT)0;
   }
+  // _check_weights' "any w > 0" (M/resample.py:96-100), without a host round trip: float32
+  // weights can underflow to 0 (the float64 floor becomes 0.0f)
+  if (any_pos && __any_sync(0xffffffffu, pos) && (threadIdx.x & 31) == 0) atomicOr(any_pos, 1);
 }
 
 // estimate_ratio subset (M/weights.py:134-154): keys = the 53-bit draw of uniform01_at(seed, i, 0)

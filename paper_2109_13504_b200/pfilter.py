@@ -158,8 +158,8 @@ def _iteration_budget(cfg: FilterConfig, w, step_seed) -> int:  # M/pfilter.py:1
 
 
 def _resample_device(cfg: FilterConfig, w, b: int, seed):
-    """Device resample with the weights' validity known by construction (likelihood floor:
-    positive and finite), so no host round trip is needed."""
+    """Device resample of the step's weights (finite and non-negative by construction; the
+    all-zero check is the predict/update kernel's any-positive flag, checked by the caller)."""
     t = D.torch()
     n = w.numel()
     anc = t.empty(n, dtype=t.int64, device=w.device)
@@ -168,11 +168,6 @@ def _resample_device(cfg: FilterConfig, w, b: int, seed):
         raise ValueError(f"unknown resampler {kind!r}")
     prefix = kind not in METROPOLIS_FAMILY  # multinomial / systematic ignore b (M/resample.py:450-454)
     flags = _lib.FLAG_NONZERO if cfg.precision == "double" else 0  # float32 cast can underflow to 0
-    if cfg.precision == "single":  # _check_weights (M/resample.py:96-100) inside the resampler
-        from .weights import device_stats
-
-        if device_stats(w).n_pos == 0:
-            raise ValueError("all weights are zero")
     _lib.check(_lib.lib().mgp_resample_range(
         _lib.KIND[kind], D.ptr(w), D.wdtype(w), n, 1 if prefix else int(b), int(seed) & (2**64 - 1),
         cfg.warp.warp_size, int(cfg.partition_bytes or 0), 1, _lib.RNG["megores" if prefix else cfg.rng], flags, 0, n,
@@ -180,48 +175,74 @@ def _resample_device(cfg: FilterConfig, w, b: int, seed):
     return anc
 
 
+def _step(x, t: int, z: float, cfg: FilterConfig, seed, est_out, any_pos, ev):
+    """One SIR step (M/pfilter.py:143-165) queued on the current stream without host round trips
+    (except the estimate_ratio B rule when ``b_fixed`` is None, which the reference also derives
+    on the host): the estimate lands in ``est_out`` (device float64), the any-positive flag of the
+    step's weights in ``any_pos`` (device int32, zeroed by the caller), stage events in ``ev``."""
+    tch = D.torch()
+    n = cfg.n_particles
+    dev = x.device
+    stream = tch.cuda.current_stream(dev)
+    s = D.stream_ptr(dev)
+    ev.record(0, stream)
+    xp = tch.empty_like(x)
+    w = tch.empty(n, dtype=tch.float32 if cfg.precision == "single" else tch.float64, device=dev)
+    _lib.check(_lib.lib().mgp_pf_predict_update(
+        D.ptr(x), n, 8.0 * math.cos(1.2 * t), math.sqrt(cfg.process_var), derive_seed(seed, _TAG_PROCESS, t),
+        float(z), cfg.obs_var, D.wdtype(w), D.ptr(xp), D.ptr(w), D.ptr(any_pos), s))
+    ev.record(1, stream)
+    step_seed = derive_seed(seed, _TAG_RESAMPLE, t)
+    b = _iteration_budget(cfg, w, step_seed)
+    if b < 1:
+        raise ValueError(f"B must be >= 1, got {b}")
+    anc = _resample_device(cfg, w, b, step_seed)
+    resampled = tch.empty_like(xp)
+    _lib.check(_lib.lib().mgp_gather(D.ptr(xp), 8, D.ptr(anc), n, D.ptr(resampled), s))
+    ev.record(2, stream)
+    _lib.check(_lib.lib().mgp_mean(D.ptr(resampled), _lib.MGP_F64, n, D.ptr(est_out), s))
+    ev.record(3, stream)
+    return resampled
+
+
 def sir_step(state: FilterState, z: float, cfg: FilterConfig, seed) -> FilterState:  # M/pfilter.py:143-165
     """Predict/update, resample, estimate on the device; per-stage CUDA-event times."""
     tch = D.torch()
     t = state.t + 1
-    x = state.particles
-    n = cfg.n_particles
-    dev = x.device
+    dev = state.particles.device
     with tch.cuda.device(dev):
-        stream = tch.cuda.current_stream(dev)
-        s = D.stream_ptr(dev)
-        ev = _Events(tch)
-        ev.record(0, stream)
-        xp = tch.empty_like(x)
-        w = tch.empty(n, dtype=tch.float32 if cfg.precision == "single" else tch.float64, device=dev)
-        _lib.check(_lib.lib().mgp_pf_predict_update(
-            D.ptr(x), n, 8.0 * math.cos(1.2 * t), math.sqrt(cfg.process_var), derive_seed(seed, _TAG_PROCESS, t),
-            float(z), cfg.obs_var, D.wdtype(w), D.ptr(xp), D.ptr(w), s))
-        ev.record(1, stream)
-        step_seed = derive_seed(seed, _TAG_RESAMPLE, t)
-        b = _iteration_budget(cfg, w, step_seed)
-        if b < 1:
-            raise ValueError(f"B must be >= 1, got {b}")
-        anc = _resample_device(cfg, w, b, step_seed)
-        resampled = tch.empty_like(xp)
-        _lib.check(_lib.lib().mgp_gather(D.ptr(xp), 8, D.ptr(anc), n, D.ptr(resampled), s))
-        ev.record(2, stream)
         est = tch.empty(1, dtype=tch.float64, device=dev)
-        _lib.check(_lib.lib().mgp_mean(D.ptr(resampled), _lib.MGP_F64, n, D.ptr(est), s))
-        ev.record(3, stream)
+        any_pos = tch.zeros(1, dtype=tch.int32, device=dev)
+        ev = _Events(tch)
+        resampled = _step(state.particles, t, z, cfg, seed, est, any_pos, ev)
         timings = ev.timings()
+        if int(any_pos.item()) == 0:
+            raise ValueError("all weights are zero")  # _check_weights (M/resample.py:96-100)
     return FilterState(resampled, float(est.item()), t, timings)
 
 
 def run_filter(cfg: FilterConfig, trajectory: Trajectory, seed):  # M/pfilter.py:168-179
+    """All T steps queued back to back on the device; estimates, the any-positive flags and the
+    stage events are read once at the end."""
+    tch = D.torch()
     state = init_state(cfg, seed)
     t_steps = len(trajectory.truth)
-    estimates = np.empty(t_steps, dtype=np.float64)
-    stages = np.zeros(3, dtype=np.float64)
-    for k in range(t_steps):
-        state = sir_step(state, float(trajectory.observations[k]), cfg, seed)
-        estimates[k] = state.estimate
-        stages += (state.timings.stage1, state.timings.stage2, state.timings.stage3)
+    dev = state.particles.device
+    with tch.cuda.device(dev):
+        ests = tch.empty(t_steps, dtype=tch.float64, device=dev)
+        any_pos = tch.zeros(t_steps, dtype=tch.int32, device=dev)
+        evs = [_Events(tch) for _ in range(t_steps)]
+        x = state.particles
+        for k in range(t_steps):
+            x = _step(x, k + 1, float(trajectory.observations[k]), cfg, seed, ests[k:k + 1], any_pos[k:k + 1], evs[k])
+        flags = any_pos.cpu().numpy()
+        if not flags.all():
+            raise ValueError("all weights are zero")  # _check_weights (M/resample.py:96-100)
+        estimates = ests.cpu().numpy()
+        stages = np.zeros(3, dtype=np.float64)
+        for ev in evs:
+            tm = ev.timings()
+            stages += (tm.stage1, tm.stage2, tm.stage3)
     stages /= t_steps
     return estimates, RunTimings(*stages)
 

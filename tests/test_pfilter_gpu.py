@@ -64,7 +64,7 @@ def test_init_and_predict_update(pf, g):
 
     _lib.check(_lib.lib().mgp_pf_predict_update(D.ptr(x), x.numel(), 8.0 * np.cos(1.2 * 1), np.sqrt(10.0),
                                                 derive_seed(5, 2, 1), float(z["traj_obs"][0]), 1.0, 0, D.ptr(xp),
-                                                D.ptr(w), D.stream_ptr()))
+                                                D.ptr(w), None, D.stream_ptr()))
     assert np.allclose(xp.cpu().numpy(), z["step1_pred"], rtol=1e-12, atol=1e-12)
     assert (w.cpu().numpy() == z["step1_w"]).mean() > 0.999
 
