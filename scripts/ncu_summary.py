@@ -21,7 +21,9 @@ KEYS = [
     ("sm__inst_executed_pipe_tex.avg.pct_of_peak_sustained_active", "%"),
     ("dram__bytes_read.sum", "byte"),
     ("dram__bytes_write.sum", "byte"),
-    ("lts__t_bytes.sum", "byte"),
+    ("lts__t_sectors.sum", "sector"),
+    ("lts__t_sectors.sum.per_second", "sector/ns"),
+    ("lts__t_sectors_srcunit_tex.sum", "sector"),
     ("lts__t_sector_hit_rate.pct", "%"),
     ("l1tex__t_sectors_pipe_tex_mem_texture.sum", "sector"),
     ("l1tex__t_requests_pipe_tex_mem_texture.sum", ""),
@@ -49,6 +51,10 @@ def main():
         if k in h:
             i = h.index(k)
             print(f"{k} [{units[i]}] = {v[i]}")
+    if "lts__t_sectors.sum.per_second" in h:  # derived: L2 throughput in GB/s (32-byte sectors)
+        i = h.index("lts__t_sectors.sum.per_second")
+        scale = {"sector/ns": 1e9, "sector/us": 1e6, "sector/ms": 1e3, "sector/s": 1.0}.get(units[i], float("nan"))
+        print(f"derived: L2 sector throughput [GB/s] = {float(v[i]) * scale * 32 / 1e9:.1f}")
 
 
 if __name__ == "__main__":
