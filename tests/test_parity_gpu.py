@@ -485,3 +485,18 @@ def test_resample_stripes(mg, oracle, rng, n, b, prec):
                                                    torch.cuda.current_stream().cuda_stream))
         got = out.cpu().numpy()[:2 * (lo1 - lo0)]
         assert np.array_equal(got, np.concatenate([ref[lo0:lo1], ref[half + lo0:half + lo1]])), (lo0, lo1)
+
+
+@pytest.mark.parametrize("n", [64, 128, 256, 512])
+def test_megopolis_philox_edges(mg, oracle, n):
+    """The half-split threshold (N >= 256), tail groups of every length (B % 4), and the
+    multi-launch carry (B > 1024) through the device and host paths, Philox stream."""
+    rr = np.random.default_rng(n)
+    w = (rr.random(n) ** 3).astype(np.float32)
+    w[rr.random(n) < 0.1] = 0
+    for b in (1, 2, 3, 4, 5, 1023, 1024, 1025, 2049):
+        seed = int(rr.integers(1 << 62))
+        ref = oracle.megopolis(w, b, seed=seed, rng="philox")
+        assert np.array_equal(mg.megopolis(w, b, seed=seed, rng="philox"), ref), (n, b, "host")
+        got = mg.megopolis(mg.WeightVector(torch.from_numpy(w).cuda(), "single"), b, seed=seed, rng="philox")
+        assert np.array_equal(got.cpu().numpy(), ref), (n, b, "device")
