@@ -564,6 +564,10 @@ int plan_free(Plan& p, cudaStream_t st) {
   return 0;
 }
 
+#ifndef MGP_HOST_CHUNKS
+#define MGP_HOST_CHUNKS 16  // lower/upper chunk pairs of the half-split host path
+#endif
+
 // Per-thread, per-device streams and events of the host-buffer path, created once (stream
 // and event creation would otherwise cost tens of microseconds per call).
 struct HostCtx {
@@ -582,7 +586,7 @@ int host_ctx(HostCtx** out) {
   CUDA_TRY(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&c->cp, cudaStreamNonBlocking));
-  c->ev.resize(40);  // > 2 * 16 chunk events + 1: an event is never re-recorded while awaited
+  c->ev.resize(2 * MGP_HOST_CHUNKS + 8);  // > chunk events + 1: never re-recorded while awaited
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   g_host_ctx.push_back(c);
   *out = c;
@@ -754,7 +758,7 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
   if (plan_half_ok(p)) {  // half-split kernel: chunk c = lower-half range [c0, c1) + its mirror
     p.half = true;
     const int64_t half = n / 2;
-    const int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(16, n >> 20));
+    const int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(MGP_HOST_CHUNKS, n >> 20));
     int64_t step = (half + nchunk - 1) / nchunk;
     step = (step + 127) / 128 * 128;
     // chunk kernels alternate between two streams so each one's drain overlaps the next
