@@ -20,7 +20,11 @@
 // Pipeline (chunks of PX_CHUNK elements):
 //   k_px_chunk_sum    float64 chunk sums -> (CUB) exclusive prefix = carry-in estimates
 //   k_px_aggregate    per chunk, the composed transducer for the 3 binades around the
-//                     estimate (e0-1, e0, e0+1)
+//                     estimate (e0-1, e0, e0+1).  All three are needed: for skewed weights
+//                     float32 drops whole addends below half an ulp, so the sequential sum
+//                     drifts from the float64 estimate systematically (tens of percent at
+//                     2^24 Gaussian y=4 weights), not by a random-walk sqrt(n) ulps; computing
+//                     only the estimate's binade sent most chunks down the sequential path
 //   k_px_super        the same for super-chunks of 32 chunks (composition of theirs)
 //   k_px_resolve      one warp walks the super-chunks 32 at a time: from the true carry-in
 //                     s (binade e, parity p) it scans the lanes' aggregates for e; every
