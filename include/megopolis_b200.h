@@ -111,6 +111,17 @@ int mgp_resample_range(int kind, const void *d_w, int dtype, int64_t n, int32_t 
                        int32_t partition_bytes, int strict, int rng, int flags, int64_t p0, int64_t p1,
                        int64_t *d_anc_slice, void *stream);
 
+/* Resample particles [p0, p1) AND apply the ancestors in one kernel (apply_ancestors,
+ * M/resample.py:371-377, fused): d_rows_out[i - p0] = row d_anc[i] of the owner
+ * h_peer_rows[d_anc / rows_local] -- local memory or NVLink-mapped peer memory of the rank that
+ * owns the row (sharded particle states).  h_peer_rows is a host array of npeers device
+ * pointers; rows of row_bytes.  W = 32 resamplers copy the row in the kernel's final store; other
+ * shapes run mgp_gather_peers after the resampler. */
+int mgp_resample_gather(int kind, const void *d_w, int dtype, int64_t n, int32_t b, uint64_t seed, int32_t warp,
+                        int32_t partition_bytes, int strict, int rng, int flags, int64_t p0, int64_t p1,
+                        const void *const *h_peer_rows, int npeers, int64_t rows_local, int64_t row_bytes,
+                        int64_t *d_anc_slice, void *d_rows_out, void *stream);
+
 /* Two-stripe particle range: particles [lo0, lo1) and [N/2 + lo0, N/2 + lo1) (0 <= lo0 <= lo1
  * <= N/2, N even) into d_anc_local[0, L) and d_anc_local[L, 2L), L = lo1 - lo0.  This is the
  * sharded "stripes" layout (rank r owns stripe r of each half), under which every rank can run

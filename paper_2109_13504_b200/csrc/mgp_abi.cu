@@ -193,12 +193,14 @@ int launch_mego_w32(const ResampleArgs& a, const OffChunk& oc, cudaStream_t st) 
       if (!a.half) { h.p0 = 0; h.p_end = a.n / 2; }
       const unsigned hgrid = (unsigned)((h.p_end - h.p0) / 128);
       if (hgrid == 0) return 0;
-      k_megopolis_w32<RNG, WT, POW2, NZ, TEX, PPT, true><<<hgrid, RS_THREADS / PPT, 0, st>>>(h, oc);
+      if (a.rows_out) k_megopolis_w32<RNG, WT, POW2, NZ, TEX, PPT, true, true><<<hgrid, RS_THREADS / PPT, 0, st>>>(h, oc);
+      else k_megopolis_w32<RNG, WT, POW2, NZ, TEX, PPT, true><<<hgrid, RS_THREADS / PPT, 0, st>>>(h, oc);
       LAUNCH_CHECK("k_megopolis_w32");
       return 0;
     }
   }
-  k_megopolis_w32<RNG, WT, POW2, NZ, TEX, PPT><<<grid, RS_THREADS / PPT, 0, st>>>(a, oc);
+  if (a.rows_out) k_megopolis_w32<RNG, WT, POW2, NZ, TEX, PPT, false, true><<<grid, RS_THREADS / PPT, 0, st>>>(a, oc);
+  else k_megopolis_w32<RNG, WT, POW2, NZ, TEX, PPT><<<grid, RS_THREADS / PPT, 0, st>>>(a, oc);
   LAUNCH_CHECK("k_megopolis_w32");
   return 0;
 }
@@ -331,6 +333,11 @@ struct Plan {
   void* cum = nullptr;       // inclusive prefix sum (multinomial / systematic)
   bool half = false;         // run_range ranges are lower-half ranges of the half-split kernel
   int64_t hi_shift = 0;      // half-split: upper-half ancestors land at anc[i - hi_shift]
+  // fused apply_ancestors (ResampleArgs::rows_*); rows_out already shifted like the anc pointer
+  const void* const* rows_peers = nullptr;
+  int64_t rows_local = 0;
+  uint32_t row_words = 0;
+  uint32_t* rows_out = nullptr;
 };
 
 // The half-split Megopolis kernel applies: W = 32, N = 2^k >= 256, 4 particles per thread
@@ -456,6 +463,10 @@ int run_range(Plan& p, int64_t p0, int64_t p_end, int64_t* anc, cudaStream_t st)
   a.one = 1;
   a.half = p.half ? 1 : 0;
   a.hi_shift = p.hi_shift;
+  a.rows_peers = p.rows_peers;
+  a.rows_local = p.rows_local;
+  a.row_words = p.row_words;
+  a.rows_out = p.rows_out;
   {
     uint32_t k0 = (uint32_t)p.seed, k1 = (uint32_t)(p.seed >> 32);
     for (int r = 0; r < 10; ++r) { a.pk0[r] = k0; a.pk1[r] = k1; k0 += PHILOX_W0; k1 += PHILOX_W1; }
@@ -1036,6 +1047,49 @@ __global__ void k_philox_selftest(uint64_t key, uint32_t c1, uint32_t c2, uint32
   }
 }
 }  // namespace
+
+// Resample particles [p0, p1) and apply the ancestors in the same kernel: out_rows[i - p0] =
+// row anc[i], read directly from its owner (peer_rows[anc / rows_local]: local memory or
+// NVLink-mapped peer memory).  Fused into the W = 32 resampler kernels' final store; other
+// shapes run the resampler and mgp_gather_peers back to back.
+extern "C" int mgp_resample_gather(int kind, const void* d_w, int dtype, int64_t n, int32_t b, uint64_t seed,
+                                   int32_t warp, int32_t partition_bytes, int strict, int rng, int flags, int64_t p0,
+                                   int64_t p1, const void* const* h_peer_rows, int npeers, int64_t rows_local,
+                                   int64_t row_bytes, int64_t* d_anc_slice, void* d_rows_out, void* stream) {
+  Plan p;
+  int rc = make_plan(p, kind, d_w, dtype, n, b, seed, warp, partition_bytes, strict, rng, flags);
+  if (rc) return rc;
+  if (!d_w || !d_anc_slice || !h_peer_rows || (!d_rows_out && row_bytes)) return set_err(MGP_EINVAL, "null pointer");
+  if (p0 < 0 || p1 > n || p0 > p1) return set_err(MGP_EINVAL, "particle range [%lld, %lld) outside [0, %lld)",
+                                                  (long long)p0, (long long)p1, (long long)n);
+  if (npeers < 1 || npeers > 64 || rows_local < 1 || row_bytes < 0 || rows_local * npeers < n)
+    return set_err(MGP_EINVAL, "invalid peer table (npeers=%d, rows_local=%lld, N=%lld)", npeers,
+                   (long long)rows_local, (long long)n);
+  if (plan_uses_w32(p) && p0 % 32) return set_err(MGP_EINVAL, "p0 must be a multiple of 32, got %lld", (long long)p0);
+  cudaStream_t st = S(stream);
+  uintptr_t al = (uintptr_t)d_rows_out | (uintptr_t)row_bytes;
+  for (int r = 0; r < npeers; ++r) {
+    if (!h_peer_rows[r]) return set_err(MGP_EINVAL, "null peer pointer %d", r);
+    al |= (uintptr_t)h_peer_rows[r];
+  }
+  const bool fused = plan_uses_w32(p) && row_bytes > 0 && (al & 3) == 0;
+  if ((rc = plan_alloc(p, st))) return rc;
+  void** d_table = nullptr;
+  if (fused) {
+    CUDA_TRY(cudaMallocAsync((void**)&d_table, sizeof(void*) * npeers, st));
+    CUDA_TRY(cudaMemcpyAsync(d_table, h_peer_rows, sizeof(void*) * npeers, cudaMemcpyHostToDevice, st));
+    p.rows_peers = (const void* const*)d_table;
+    p.rows_local = rows_local;
+    p.row_words = (uint32_t)(row_bytes / 4);
+    p.rows_out = (uint32_t*)d_rows_out - p0 * (row_bytes / 4);
+  }
+  rc = run_range(p, p0, p1, d_anc_slice - p0, st);
+  if (!rc && !fused && row_bytes > 0)
+    rc = mgp_gather_peers(h_peer_rows, npeers, rows_local, row_bytes, d_anc_slice, p1 - p0, d_rows_out, st);
+  int rc2 = plan_free(p, st);
+  if (d_table) cudaFreeAsync(d_table, st);
+  return rc ? rc : rc2;
+}
 
 // Particles [lo0, lo1) and their mirrors [n/2 + lo0, n/2 + lo1) -- the two-stripe ownership
 // of the sharded layout (distributed.py, layout="stripes"), which lets every rank run the

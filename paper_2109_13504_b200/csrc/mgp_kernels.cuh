@@ -44,7 +44,32 @@ struct ResampleArgs {
   int half;                 // half-split launch: [p0, p_end) is a range of LOWER-half particles
   int64_t hi_shift;         // half-split: upper-half particle i stores its ancestor at anc[i - hi_shift]
   uint32_t pk0[10], pk1[10];  // Philox round keys (uniform; constant bank)
+  // fused apply_ancestors (null rows_out: off): the resampled particle's state row is copied
+  // from its owner's memory -- a local array or NVLink-mapped peer memory, owner = k / rows_local
+  const void* const* rows_peers;  // device array of per-owner row pointers
+  int64_t rows_local;             // rows per owner
+  uint32_t row_words;             // 4-byte words per row
+  uint32_t* rows_out;             // output rows, indexed like anc (same shifts)
 };
+
+// Final store of one particle: the ancestor (last launch) or the carried state, and with the
+// fused gather the ancestor's state row, read directly from its owner (M/resample.py:371-377).
+// ROWS: compiled only into the fused-gather instantiations, so the plain kernels' code (and
+// ptxas's scheduling of their main loop) is unchanged (the runtime branch alone cost 1.8%).
+template <bool ROWS = true>
+__device__ __forceinline__ void store_result(const ResampleArgs& a, int64_t out_idx, uint32_t i, uint32_t k) {
+  if (!a.last) {
+    a.kstate[i] = (int32_t)k;
+    return;
+  }
+  a.anc[out_idx] = (int64_t)k;
+  if (ROWS && a.rows_out) {
+    const int64_t owner = (int64_t)k / a.rows_local, local = (int64_t)k - owner * a.rows_local;
+    const uint32_t* __restrict__ src = reinterpret_cast<const uint32_t*>(a.rows_peers[owner]) + local * a.row_words;
+    uint32_t* __restrict__ dst = a.rows_out + out_idx * a.row_words;
+    for (uint32_t q = 0; q < a.row_words; ++q) dst[q] = src[q];
+  }
+}
 
 // ---------------------------------------------------------------------------
 // weight loads.  float32 -> float64 conversion is F2F (exact for every float32,
@@ -147,7 +172,7 @@ __device__ __forceinline__ double u1_from_word(uint32_t w) {
 // one DMUL + DSETP, one 32-bit select.  The accepted round index is carried instead
 // of j (j is a pure function of (i, o_b)) and k is rebuilt once at the end.
 
-template <int RNG, typename WT, bool POW2, bool NOZERO, bool TEX, int PPT, bool HALF = false>
+template <int RNG, typename WT, bool POW2, bool NOZERO, bool TEX, int PPT, bool HALF = false, bool ROWS = false>
 __global__ void __launch_bounds__(RS_THREADS / PPT, PPT == 1 ? 0 : 1) k_megopolis_w32(const __grid_constant__ ResampleArgs a,
                                                                     const __grid_constant__ OffChunk oc) {
   // PPT particles per thread: i + p*(256/PPT) of this CTA's 256-particle block -- same lane,
@@ -260,8 +285,7 @@ __global__ void __launch_bounds__(RS_THREADS / PPT, PPT == 1 ? 0 : 1) k_megopoli
     if (!live[p]) continue;
     uint32_t k = a.first ? ii[p] : (uint32_t)a.kstate[ii[p]];
     if (bstar[p] >= 0) k = mego_j<POW2>(ial[p], lane, oc.o[bstar[p]], n);
-    if (a.last) a.anc[(int64_t)ii[p] - (HALF && p >= 2 ? a.hi_shift : 0)] = (int64_t)k;
-    else a.kstate[ii[p]] = (int32_t)k;
+    store_result<ROWS>(a, (int64_t)ii[p] - (HALF && p >= 2 ? a.hi_shift : 0), ii[p], k);
   }
 }
 
@@ -308,8 +332,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_metropolis(const __grid_constant
       }
     }
   }
-  if (a.last) a.anc[i] = (int64_t)k;
-  else a.kstate[i] = (int32_t)k;
+  store_result(a, i, i, k);
 }
 
 // ---------------------------------------------------------------------------
@@ -388,8 +411,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_c12_w32(const __grid_constant__ 
       }
     }
   }
-  if (a.last) a.anc[i] = (int64_t)k;
-  else a.kstate[i] = (int32_t)k;
+  store_result(a, i, i, k);
 }
 
 // ---------------------------------------------------------------------------

@@ -500,3 +500,36 @@ def test_megopolis_philox_edges(mg, oracle, n):
         assert np.array_equal(mg.megopolis(w, b, seed=seed, rng="philox"), ref), (n, b, "host")
         got = mg.megopolis(mg.WeightVector(torch.from_numpy(w).cuda(), "single"), b, seed=seed, rng="philox")
         assert np.array_equal(got.cpu().numpy(), ref), (n, b, "device")
+
+
+@pytest.mark.parametrize("rng,kind,warp,n,cols", [("philox", "megopolis", 32, 1 << 14, 1), ("megores", "megopolis", 32, 4096, 3),
+                                                  ("philox", "c1", 32, 4096, 2), ("megores", "megopolis", 7, 700, 1)])
+def test_resample_gather_fused(mg, oracle, rng, kind, warp, n, cols):
+    """mgp_resample_gather: resample + apply_ancestors in one kernel, the ancestor rows read from
+    a 4-owner pointer table (the NVLink peer-memory layout, emulated with 4 shards on one
+    device); the generic (W = 7) shape takes the two-kernel fallback."""
+    import ctypes
+
+    from paper_2109_13504_b200 import _lib
+
+    w = oracle.gen_gaussian_weights(3.0, n, 99, "single")
+    b = 9
+    part = 128 if kind == "c1" else 0
+    if kind == "megopolis":
+        ref = oracle.megopolis(w, b, warp, seed=4, strict=(n % warp == 0), rng=rng)
+    else:
+        ref = oracle.metropolis_c1(w, b, part, warp, seed=4, rng=rng)
+    rows_local = (n + 3) // 4
+    states = torch.arange(4 * rows_local * cols, dtype=torch.float64, device="cuda").reshape(4 * rows_local, cols) * 0.5
+    shards = [states[r * rows_local:(r + 1) * rows_local].contiguous() for r in range(4)]
+    table = (ctypes.c_void_p * 4)(*[s.data_ptr() for s in shards])
+    wd = torch.from_numpy(w).cuda()
+    for p0, p1 in ((0, n), (0, n // 2), (n // 4 - (n // 4) % 32, n)):
+        anc = torch.empty(p1 - p0, dtype=torch.int64, device="cuda")
+        out = torch.empty(p1 - p0, cols, dtype=torch.float64, device="cuda")
+        _lib.check(_lib.lib().mgp_resample_gather(
+            _lib.KIND[kind], wd.data_ptr(), 0, n, b, 4, warp, part, int(n % warp == 0), _lib.RNG[rng], 0, p0, p1,
+            ctypes.cast(table, ctypes.c_void_p), 4, rows_local, 8 * cols, anc.data_ptr(), out.data_ptr(),
+            torch.cuda.current_stream().cuda_stream))
+        assert np.array_equal(anc.cpu().numpy(), ref[p0:p1]), (p0, p1)
+        assert torch.equal(out, states[torch.from_numpy(ref[p0:p1]).cuda()]), (p0, p1)
