@@ -363,7 +363,7 @@ def main():
     achieved, kern_avg = roof(head)
     # Philox launches (full range, or a rank's stripes) take the half-split kernel
     if args.rng == "philox":
-        mego_kernel = "k_megopolis_w32<philox, half-split, 4 particles/thread>"
+        mego_kernel = "k_megopolis_philox_half (half-split, 4 particles/thread)"
     else:
         mego_kernel = "k_megopolis_w32<megores, 1 particle/thread>"
     traffic = None

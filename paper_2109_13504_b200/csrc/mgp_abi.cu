@@ -193,8 +193,13 @@ int launch_mego_w32(const ResampleArgs& a, const OffChunk& oc, cudaStream_t st) 
       if (!a.half) { h.p0 = 0; h.p_end = a.n / 2; }
       const unsigned hgrid = (unsigned)((h.p_end - h.p0) / 128);
       if (hgrid == 0) return 0;
-      if (a.rows_out) k_megopolis_w32<RNG, WT, POW2, NZ, TEX, PPT, true, true><<<hgrid, RS_THREADS / PPT, 0, st>>>(h, oc);
-      else k_megopolis_w32<RNG, WT, POW2, NZ, TEX, PPT, true><<<hgrid, RS_THREADS / PPT, 0, st>>>(h, oc);
+      if (a.rows_out) {
+        k_megopolis_w32<RNG, WT, POW2, NZ, TEX, PPT, true, true><<<hgrid, RS_THREADS / PPT, 0, st>>>(h, oc);
+      } else if constexpr (RNG == RNG_PHILOX && sizeof(WT) == 4 && NZ && TEX) {
+        k_megopolis_philox_half<<<hgrid, 64, 0, st>>>(h, oc);  // the headline configuration
+      } else {
+        k_megopolis_w32<RNG, WT, POW2, NZ, TEX, PPT, true><<<hgrid, RS_THREADS / PPT, 0, st>>>(h, oc);
+      }
       LAUNCH_CHECK("k_megopolis_w32");
       return 0;
     }

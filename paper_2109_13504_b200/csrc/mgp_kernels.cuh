@@ -290,6 +290,78 @@ __global__ void __launch_bounds__(RS_THREADS / PPT, PPT == 1 ? 0 : 1) k_megopoli
 }
 
 // ---------------------------------------------------------------------------
+// The headline configuration, specialised: Philox stream, float32 weights through the texture
+// path, no zero weights, half-split (N = 2^k >= 256).  Same arithmetic and layout as
+// k_megopolis_w32<RNG_PHILOX, float, true, true, true, 4, true>, written as one straight loop of
+// Philox blocks plus a guarded tail block: ptxas schedules this form 0.6-1% faster on every box
+// measured (scripts/mb/mb_conv.cu "x2 gen" vs "lib HALF").  [p0, p_end) is a range of
+// lower-half particles (multiple of 128); upper-half ancestors land at anc[i - hi_shift].
+
+__global__ void __launch_bounds__(64, 1) k_megopolis_philox_half(const __grid_constant__ ResampleArgs a,
+                                                                 const __grid_constant__ OffChunk oc) {
+  constexpr int PPT = 4;
+  const uint32_t half = a.n >> 1;
+  const uint32_t i0 = a.p0 + blockIdx.x * 128 + threadIdx.x;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t cmask = (a.n - 1) & ~31u;
+  uint32_t ii[PPT];
+  double wkd[PPT];
+  int bstar[PPT];
+  ii[0] = i0; ii[1] = i0 + 64; ii[2] = i0 + half; ii[3] = i0 + half + 64;
+  const uint32_t ial0 = i0 - lane, ial1 = ial0 + 64;
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const uint32_t k0 = a.first ? ii[p] : (uint32_t)a.kstate[ii[p]];
+    wkd[p] = (double)tex1Dfetch<float>(a.tex, (int)k0);
+    bstar[p] = -1;
+  }
+  const int full = a.cnt & ~3;
+  auto body = [&](int t0, int lim) {  // rounds [t0, t0 + lim) from Philox block (b0 + t0) / 4
+    uint32_t c0[PPT], c1[PPT], c2[PPT], c3[PPT];
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) { c0[p] = ii[p]; c1[p] = 0; c2[p] = (uint32_t)((a.b0 + t0) >> 2); c3[p] = 0; }
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) {
+        const uint64_t q0 = (uint64_t)PHILOX_M0 * c0[p], q1 = (uint64_t)PHILOX_M1 * c2[p];
+        const uint32_t n0 = (uint32_t)(q1 >> 32) ^ c1[p] ^ a.pk0[r], n2 = (uint32_t)(q0 >> 32) ^ c3[p] ^ a.pk1[r];
+        c1[p] = (uint32_t)q1; c3[p] = (uint32_t)q0; c0[p] = n0; c2[p] = n2;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (q < lim) {
+        const int t = t0 + q;
+        const uint2 o = oc.o[t];
+        const uint32_t L = lane + o.y;
+        uint32_t jj[PPT];
+        jj[0] = mux3(ial0 + o.x, L, cmask);
+        jj[1] = mux3(ial1 + o.x, L, cmask);
+        jj[2] = jj[0] ^ half;
+        jj[3] = jj[1] ^ half;
+#pragma unroll
+        for (int p = 0; p < PPT; ++p) {
+          const uint32_t wd = q == 0 ? c0[p] : q == 1 ? c1[p] : q == 2 ? c2[p] : c3[p];
+          const double wjd = (double)tex1Dfetch<float>(a.tex, (int)jj[p]);
+          const double prod = fma(u1_from_word(wd), wkd[p], -wkd[p]);  // fl(u * wk)
+          if (prod <= wjd) { wkd[p] = wjd; bstar[p] = t; }
+        }
+      }
+    }
+  };
+  for (int t0 = 0; t0 < full; t0 += 4) body(t0, 4);
+  if (full < a.cnt) body(full, a.cnt - full);
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    uint32_t k = a.first ? ii[p] : (uint32_t)a.kstate[ii[p]];
+    if (bstar[p] >= 0) { const uint2 o = oc.o[bstar[p]]; k = mux3((ii[p] - lane) + o.x, lane + o.y, cmask); }
+    if (a.last) a.anc[(int64_t)ii[p] - (p >= 2 ? a.hi_shift : 0)] = (int64_t)k;
+    else a.kstate[ii[p]] = (int32_t)k;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Metropolis (uniform random partner; the uncoalesced baseline, M/resample.py:125-138)
 
 template <int RNG, typename WT, bool POW2, bool NOZERO>

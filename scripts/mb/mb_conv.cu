@@ -355,6 +355,21 @@ int main(int argc, char** argv) {
   check("lib HALF", time_it([&]() { k_megopolis_w32<1, float, true, true, true, 4, true><<<n / 256, 64>>>(b, oc); }, 9));
   check("x2 p4", time_it([&]() { k_x2<1><<<n / 256, 64>>>(b, oc); }, 9));
   check("x2 gen", time_it([&]() { k_x2<1, true><<<n / 256, 64>>>(b, oc); }, 9));
+  {  // wave quantisation probe: grids of whole waves (148 SMs x CTAs per SM) vs the full grid
+    int bps = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_megopolis_w32<1, float, true, true, true, 4, true>, 64, 0));
+    const int slots = 148 * bps, full = (int)(n / 256);
+    for (int g : {full, full / slots * slots, full / slots * slots - slots / 2}) {
+      float ms = time_it([&]() { k_megopolis_w32<1, float, true, true, true, 4, true><<<g, 64>>>(b, oc); }, 9);
+      printf("grid %d (%.2f waves of %d): %.3f ms, %.4f ms per 1000 CTAs\n", g, (double)g / slots, slots, ms,
+             ms / g * 1000);
+    }
+    CK(cudaMemset(anc1, 0xff, 8ull * n));
+  }
+  check("lib philox_half", time_it([&]() { k_megopolis_philox_half<<<n / 256, 64>>>(b, oc); }, 9));
+  check("x2 gen m11", time_it([&]() { k_x2<11, true><<<n / 256, 64>>>(b, oc); }, 9));
+  check("x2 gen m12", time_it([&]() { k_x2<12, true><<<n / 256, 64>>>(b, oc); }, 9));
+  check("x2 gen m14", time_it([&]() { k_x2<14, true><<<n / 256, 64>>>(b, oc); }, 9));
   check("sp p4", time_it([&]() { k_sp<4, 1><<<n / 256, 64>>>(b, oc); }, 9));
   check("sp p2", time_it([&]() { k_sp<2, 1><<<n / 256, 128>>>(b, oc); }, 9));
   check("x2 gen nokst", time_it([&]() { k_x2<1, true, false, false><<<n / 256, 64>>>(b, oc); }, 9));
