@@ -167,6 +167,8 @@ class ShardedResampler:
         """All-gather the per-rank weight slices (or stripes) into the full replicated vector."""
         t = D.torch()
         n_local = w_local.numel()
+        if self.layout == "stripes" and n_local % 2:
+            raise ValueError(f"the stripes layout needs an even number of particles per rank, got {n_local}")
         full = t.empty(n_local * self.world, dtype=w_local.dtype, device=w_local.device)
         if self.layout == "contiguous":
             self._gather_into(full, w_local)
