@@ -171,7 +171,8 @@ void offsets_host(uint64_t seed, int64_t n, int32_t b, int rng, int64_t* out) {
 
 // Particles per thread: 4 for the Philox stream (interleaved Philox chains; measured 5.97 -> 5.54 ms
 // at 2^24, PPT 1 -> 4; scripts/mb/ppt_sweep.sh),
-// 1 for megores (its ALU-bound splitmix chain gains nothing from more ILP).
+// 1 for megores (its issue-bound splitmix chain gains nothing from more ILP: 2 or 4 particles
+// per thread, with or without the half split, measured 0.6-0.8% slower; scripts/mb/ppt_megores.sh).
 #ifndef MGP_PPT_PHILOX
 #define MGP_PPT_PHILOX 4
 #endif
