@@ -111,16 +111,20 @@ int mgp_resample_range(int kind, const void *d_w, int dtype, int64_t n, int32_t 
                        int32_t partition_bytes, int strict, int rng, int flags, int64_t p0, int64_t p1,
                        int64_t *d_anc_slice, void *stream);
 
-/* Resample particles [p0, p1) AND apply the ancestors in one kernel (apply_ancestors,
- * M/resample.py:371-377, fused): d_rows_out[i - p0] = row d_anc[i] of the owner
- * h_peer_rows[d_anc / rows_local] -- local memory or NVLink-mapped peer memory of the rank that
- * owns the row (sharded particle states).  h_peer_rows is a host array of npeers device
- * pointers; rows of row_bytes.  W = 32 resamplers copy the row in the kernel's final store; other
- * shapes run mgp_gather_peers after the resampler. */
+/* Resample AND apply the ancestors in one kernel (apply_ancestors, M/resample.py:371-377, fused):
+ * each resampled particle's state row is read directly from its owner h_peer_rows[owner] -- local
+ * memory or NVLink-mapped peer memory of the rank that owns the row (sharded particle states).
+ * layout 0 (contiguous): particles [p0, p1) into d_anc_out / d_rows_out[i - p0];
+ *   owner = anc / rows_local.
+ * layout 1 (stripes): particles [p0, p1) and N/2 + [p0, p1) into [L lower | L upper] (as
+ *   mgp_resample_stripes); owner r holds [r*h, (r+1)*h) then N/2 + [r*h, (r+1)*h), h = rows_local/2.
+ * h_peer_rows: host array of npeers device pointers; rows of row_bytes.  W = 32 resamplers with
+ * 4-byte-aligned rows copy the row in the kernel's final store; other shapes run a peer-gather
+ * kernel with the same owner mapping afterwards. */
 int mgp_resample_gather(int kind, const void *d_w, int dtype, int64_t n, int32_t b, uint64_t seed, int32_t warp,
-                        int32_t partition_bytes, int strict, int rng, int flags, int64_t p0, int64_t p1,
+                        int32_t partition_bytes, int strict, int rng, int flags, int layout, int64_t p0, int64_t p1,
                         const void *const *h_peer_rows, int npeers, int64_t rows_local, int64_t row_bytes,
-                        int64_t *d_anc_slice, void *d_rows_out, void *stream);
+                        int64_t *d_anc_out, void *d_rows_out, void *stream);
 
 /* Two-stripe particle range: particles [lo0, lo1) and [N/2 + lo0, N/2 + lo1) (0 <= lo0 <= lo1
  * <= N/2, N even) into d_anc_local[0, L) and d_anc_local[L, 2L), L = lo1 - lo0.  This is the

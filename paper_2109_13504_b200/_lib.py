@@ -40,8 +40,8 @@ SIGNATURES = {
     "mgp_metropolis_c2": (_i32, [_vp, _i32, _i64, _i32, _u64, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
     "mgp_resample_range": (_i32, [_i32, _vp, _i32, _i64, _i32, _u64, _i32, _i32, _i32, _i32, _i32, _i64, _i64, _vp,
                                    _vp]),
-    "mgp_resample_gather": (_i32, [_i32, _vp, _i32, _i64, _i32, _u64, _i32, _i32, _i32, _i32, _i32, _i64, _i64, _vp,
-                                    _i32, _i64, _i64, _vp, _vp, _vp]),
+    "mgp_resample_gather": (_i32, [_i32, _vp, _i32, _i64, _i32, _u64, _i32, _i32, _i32, _i32, _i32, _i32, _i64, _i64,
+                                    _vp, _i32, _i64, _i64, _vp, _vp, _vp]),
     "mgp_resample_stripes": (_i32, [_i32, _vp, _i32, _i64, _i32, _u64, _i32, _i32, _i32, _i32, _i32, _i64, _i64,
                                      _vp, _vp]),
     "mgp_resample_host": (_i32, [_i32, _vp, _i32, _i64, _i32, _dbl, _u64, _i32, _i32, _i32, _i32, _vp, _vp, _i32]),

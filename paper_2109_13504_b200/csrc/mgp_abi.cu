@@ -342,6 +342,7 @@ struct Plan {
   // fused apply_ancestors (ResampleArgs::rows_*); rows_out already shifted like the anc pointer
   const void* const* rows_peers = nullptr;
   int64_t rows_local = 0;
+  int64_t rows_half = 0;
   uint32_t row_words = 0;
   uint32_t* rows_out = nullptr;
 };
@@ -471,6 +472,7 @@ int run_range(Plan& p, int64_t p0, int64_t p_end, int64_t* anc, cudaStream_t st)
   a.hi_shift = p.hi_shift;
   a.rows_peers = p.rows_peers;
   a.rows_local = p.rows_local;
+  a.rows_half = p.rows_half;
   a.row_words = p.row_words;
   a.rows_out = p.rows_out;
   {
@@ -908,8 +910,8 @@ int mgp_gather(const void* d_states, int64_t row_bytes, const int64_t* d_anc, in
   return 0;
 }
 
-int mgp_gather_peers(const void* const* peer_states, int npeers, int64_t n_local, int64_t row_bytes,
-                     const int64_t* d_anc, int64_t n, void* d_out, void* stream) {
+static int gather_peers(const void* const* peer_states, int npeers, int64_t n_local, int64_t row_bytes,
+                        const int64_t* d_anc, int64_t n, void* d_out, void* stream, int64_t rows_half) {
   if (npeers < 1 || npeers > 64) return set_err(MGP_EINVAL, "npeers must be in [1, 64], got %d", npeers);
   if (n_local < 1 || row_bytes < 0 || n < 0) return set_err(MGP_EINVAL, "invalid sizes");
   if (n == 0 || row_bytes == 0) return 0;
@@ -923,15 +925,24 @@ int mgp_gather_peers(const void* const* peer_states, int npeers, int64_t n_local
   cudaStream_t st = S(stream);
   const unsigned grid = (unsigned)std::min<int64_t>((n * row_bytes / 4 + 255) / 256 + 1, 148 * 32);
   if ((al & 15) == 0)
-    k_gather_peers<uint4><<<grid, 256, 0, st>>>(pt, npeers, n_local, d_anc, n, row_bytes / 16, (uint4*)d_out);
+    k_gather_peers<uint4><<<grid, 256, 0, st>>>(pt, npeers, n_local, d_anc, n, row_bytes / 16, (uint4*)d_out,
+                                                  rows_half);
   else if ((al & 7) == 0)
-    k_gather_peers<uint2><<<grid, 256, 0, st>>>(pt, npeers, n_local, d_anc, n, row_bytes / 8, (uint2*)d_out);
+    k_gather_peers<uint2><<<grid, 256, 0, st>>>(pt, npeers, n_local, d_anc, n, row_bytes / 8, (uint2*)d_out,
+                                                  rows_half);
   else if ((al & 3) == 0)
-    k_gather_peers<uint32_t><<<grid, 256, 0, st>>>(pt, npeers, n_local, d_anc, n, row_bytes / 4, (uint32_t*)d_out);
+    k_gather_peers<uint32_t><<<grid, 256, 0, st>>>(pt, npeers, n_local, d_anc, n, row_bytes / 4, (uint32_t*)d_out,
+                                                  rows_half);
   else
-    k_gather_peers<uint8_t><<<grid, 256, 0, st>>>(pt, npeers, n_local, d_anc, n, row_bytes, (uint8_t*)d_out);
+    k_gather_peers<uint8_t><<<grid, 256, 0, st>>>(pt, npeers, n_local, d_anc, n, row_bytes, (uint8_t*)d_out,
+                                                  rows_half);
   LAUNCH_CHECK("k_gather_peers");
   return 0;
+}
+
+int mgp_gather_peers(const void* const* peer_states, int npeers, int64_t n_local, int64_t row_bytes,
+                     const int64_t* d_anc, int64_t n, void* d_out, void* stream) {
+  return gather_peers(peer_states, npeers, n_local, row_bytes, d_anc, n, d_out, stream, 0);
 }
 
 int mgp_mean(const void* d_x, int dtype, int64_t n, double* d_out, void* stream) {
@@ -1054,24 +1065,32 @@ __global__ void k_philox_selftest(uint64_t key, uint32_t c1, uint32_t c2, uint32
 }
 }  // namespace
 
-// Resample particles [p0, p1) and apply the ancestors in the same kernel: out_rows[i - p0] =
-// row anc[i], read directly from its owner (peer_rows[anc / rows_local]: local memory or
-// NVLink-mapped peer memory).  Fused into the W = 32 resampler kernels' final store; other
-// shapes run the resampler and mgp_gather_peers back to back.
+// Resample and apply the ancestors in the same kernel: the resampled particles' state rows
+// are read directly from their owners (peer_rows[owner]: local memory or NVLink-mapped peer
+// memory).  layout 0: particles [p0, p1), out_rows[i - p0], owner = anc / rows_local.
+// layout 1 (stripes): particles [p0, p1) and N/2 + [p0, p1), outputs [L lower | L upper] like
+// mgp_resample_stripes, owner r holding [r*h, (r+1)*h) and N/2 + [r*h, (r+1)*h), h = rows_local/2.
+// Fused into the W = 32 kernels' final store; other shapes run mgp_gather_peers afterwards.
 extern "C" int mgp_resample_gather(int kind, const void* d_w, int dtype, int64_t n, int32_t b, uint64_t seed,
-                                   int32_t warp, int32_t partition_bytes, int strict, int rng, int flags, int64_t p0,
-                                   int64_t p1, const void* const* h_peer_rows, int npeers, int64_t rows_local,
-                                   int64_t row_bytes, int64_t* d_anc_slice, void* d_rows_out, void* stream) {
+                                   int32_t warp, int32_t partition_bytes, int strict, int rng, int flags, int layout,
+                                   int64_t p0, int64_t p1, const void* const* h_peer_rows, int npeers,
+                                   int64_t rows_local, int64_t row_bytes, int64_t* d_anc_out, void* d_rows_out,
+                                   void* stream) {
   Plan p;
   int rc = make_plan(p, kind, d_w, dtype, n, b, seed, warp, partition_bytes, strict, rng, flags);
   if (rc) return rc;
-  if (!d_w || !d_anc_slice || !h_peer_rows || (!d_rows_out && row_bytes)) return set_err(MGP_EINVAL, "null pointer");
-  if (p0 < 0 || p1 > n || p0 > p1) return set_err(MGP_EINVAL, "particle range [%lld, %lld) outside [0, %lld)",
-                                                  (long long)p0, (long long)p1, (long long)n);
+  if (!d_w || !d_anc_out || !h_peer_rows || (!d_rows_out && row_bytes)) return set_err(MGP_EINVAL, "null pointer");
+  if (layout != 0 && layout != 1) return set_err(MGP_EINVAL, "layout must be 0 (contiguous) or 1 (stripes)");
+  const int64_t half = n / 2, lim = layout ? half : n, L = p1 - p0;
+  if (p0 < 0 || p1 > lim || L < 0)
+    return set_err(MGP_EINVAL, "particle range [%lld, %lld) outside [0, %lld)", (long long)p0, (long long)p1,
+                   (long long)lim);
+  if (layout == 1 && (n % 2 || rows_local % 2)) return set_err(MGP_EINVAL, "the stripes layout needs even sizes");
   if (npeers < 1 || npeers > 64 || rows_local < 1 || row_bytes < 0 || rows_local * npeers < n)
     return set_err(MGP_EINVAL, "invalid peer table (npeers=%d, rows_local=%lld, N=%lld)", npeers,
                    (long long)rows_local, (long long)n);
-  if (plan_uses_w32(p) && p0 % 32) return set_err(MGP_EINVAL, "p0 must be a multiple of 32, got %lld", (long long)p0);
+  if (plan_uses_w32(p) && (p0 % 32 || (layout == 1 && half % 32)))
+    return set_err(MGP_EINVAL, "p0 (and N/2) must be multiples of 32 for this resampler");
   cudaStream_t st = S(stream);
   uintptr_t al = (uintptr_t)d_rows_out | (uintptr_t)row_bytes;
   for (int r = 0; r < npeers; ++r) {
@@ -1081,17 +1100,33 @@ extern "C" int mgp_resample_gather(int kind, const void* d_w, int dtype, int64_t
   const bool fused = plan_uses_w32(p) && row_bytes > 0 && (al & 3) == 0;
   if ((rc = plan_alloc(p, st))) return rc;
   void** d_table = nullptr;
+  const int64_t words = row_bytes / 4;
   if (fused) {
     CUDA_TRY(cudaMallocAsync((void**)&d_table, sizeof(void*) * npeers, st));
     CUDA_TRY(cudaMemcpyAsync(d_table, h_peer_rows, sizeof(void*) * npeers, cudaMemcpyHostToDevice, st));
     p.rows_peers = (const void* const*)d_table;
     p.rows_local = rows_local;
-    p.row_words = (uint32_t)(row_bytes / 4);
-    p.rows_out = (uint32_t*)d_rows_out - p0 * (row_bytes / 4);
+    p.rows_half = layout ? half : 0;
+    p.row_words = (uint32_t)words;
   }
-  rc = run_range(p, p0, p1, d_anc_slice - p0, st);
-  if (!rc && !fused && row_bytes > 0)
-    rc = mgp_gather_peers(h_peer_rows, npeers, rows_local, row_bytes, d_anc_slice, p1 - p0, d_rows_out, st);
+  if (layout == 0) {
+    if (fused) p.rows_out = (uint32_t*)d_rows_out - p0 * words;
+    rc = run_range(p, p0, p1, d_anc_out - p0, st);
+  } else if (plan_half_ok(p) && p0 % 128 == 0 && L % 128 == 0) {
+    p.half = true;
+    p.hi_shift = half - L;
+    if (fused) p.rows_out = (uint32_t*)d_rows_out - p0 * words;
+    rc = run_range(p, p0, p1, d_anc_out - p0, st);
+  } else {
+    if (fused) p.rows_out = (uint32_t*)d_rows_out - p0 * words;
+    rc = run_range(p, p0, p1, d_anc_out - p0, st);
+    if (fused) p.rows_out = (uint32_t*)d_rows_out + L * words - (half + p0) * words;
+    if (!rc) rc = run_range(p, half + p0, half + p1, d_anc_out + L - (half + p0), st);
+  }
+  if (!rc && !fused && row_bytes > 0) {  // two-kernel fallback (owner mapping on the host side)
+    rc = gather_peers(h_peer_rows, npeers, rows_local, row_bytes, d_anc_out, layout ? 2 * L : L, d_rows_out, st,
+                      layout ? half : 0);
+  }
   int rc2 = plan_free(p, st);
   if (d_table) cudaFreeAsync(d_table, st);
   return rc ? rc : rc2;

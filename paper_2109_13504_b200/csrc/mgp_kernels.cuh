@@ -45,9 +45,12 @@ struct ResampleArgs {
   int64_t hi_shift;         // half-split: upper-half particle i stores its ancestor at anc[i - hi_shift]
   uint32_t pk0[10], pk1[10];  // Philox round keys (uniform; constant bank)
   // fused apply_ancestors (null rows_out: off): the resampled particle's state row is copied
-  // from its owner's memory -- a local array or NVLink-mapped peer memory, owner = k / rows_local
+  // from its owner's memory -- a local array or NVLink-mapped peer memory.  Contiguous layout
+  // (rows_half == 0): owner = k / rows_local.  Stripes layout (rows_half = N/2): owner r holds
+  // [r*h, (r+1)*h) then N/2 + [r*h, (r+1)*h), h = rows_local / 2.
   const void* const* rows_peers;  // device array of per-owner row pointers
   int64_t rows_local;             // rows per owner
+  int64_t rows_half;              // 0, or N/2 for the stripes layout
   uint32_t row_words;             // 4-byte words per row
   uint32_t* rows_out;             // output rows, indexed like anc (same shifts)
 };
@@ -64,7 +67,15 @@ __device__ __forceinline__ void store_result(const ResampleArgs& a, int64_t out_
   }
   a.anc[out_idx] = (int64_t)k;
   if (ROWS && a.rows_out) {
-    const int64_t owner = (int64_t)k / a.rows_local, local = (int64_t)k - owner * a.rows_local;
+    int64_t owner, local;
+    if (a.rows_half) {
+      const int64_t h = a.rows_local >> 1, up = (int64_t)k >= a.rows_half, kk = (int64_t)k - up * a.rows_half;
+      owner = kk / h;
+      local = kk - owner * h + up * h;
+    } else {
+      owner = (int64_t)k / a.rows_local;
+      local = (int64_t)k - owner * a.rows_local;
+    }
     const uint32_t* __restrict__ src = reinterpret_cast<const uint32_t*>(a.rows_peers[owner]) + local * a.row_words;
     uint32_t* __restrict__ dst = a.rows_out + out_idx * a.row_words;
     for (uint32_t q = 0; q < a.row_words; ++q) dst[q] = src[q];
@@ -911,12 +922,21 @@ struct PeerTable {
 
 template <typename V>
 __global__ void k_gather_peers(const __grid_constant__ PeerTable peers, int npeers, int64_t n_local,
-                               const int64_t* __restrict__ anc, int64_t n, int64_t row_v, V* __restrict__ dst) {
+                               const int64_t* __restrict__ anc, int64_t n, int64_t row_v, V* __restrict__ dst,
+                               int64_t rows_half) {
   const int64_t total = n * row_v;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = t / row_v, c = t - i * row_v;
     const int64_t a = anc[i];
-    const int64_t owner = a / n_local, local = a - owner * n_local;
+    int64_t owner, local;
+    if (rows_half) {  // stripes: owner r holds stripe r of each half, low stripe first
+      const int64_t h = n_local >> 1, up = a >= rows_half, k = a - up * rows_half;
+      owner = k / h;
+      local = k - owner * h + up * h;
+    } else {
+      owner = a / n_local;
+      local = a - owner * n_local;
+    }
     const V* src = reinterpret_cast<const V*>(peers.p[owner]);
     dst[t] = src[local * row_v + c];
   }

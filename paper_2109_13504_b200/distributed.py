@@ -95,6 +95,24 @@ class CudaOps:
             D.ptr(out), D.stream_ptr()))
         return out
 
+    def resample_gather(self, kind, w_full, b, seed, warp, partition_bytes, strict, rng, nonzero, layout, p0, p1,
+                        peer_states):
+        """mgp_resample_gather: ancestors plus the resampled state rows in one kernel."""
+        t = D.torch()
+        ref = peer_states[0]
+        count = (p1 - p0) * (2 if layout == "stripes" else 1)
+        anc = t.empty(count, dtype=t.int64, device=w_full.device)
+        out = t.empty((count,) + tuple(ref.shape[1:]), dtype=ref.dtype, device=w_full.device)
+        ptrs = (ctypes.c_void_p * len(peer_states))(*[p.data_ptr() for p in peer_states])
+        row_bytes = ref[0].numel() * ref.element_size() if ref.shape[0] else 0
+        flags = _lib.FLAG_NONZERO if nonzero else 0
+        _lib.check(_lib.lib().mgp_resample_gather(
+            _lib.KIND[kind], D.ptr(w_full), D.wdtype(w_full), w_full.numel(), int(b), int(seed) & (2**64 - 1),
+            int(warp), int(partition_bytes or 0), int(bool(strict)), _lib.RNG[rng], flags,
+            1 if layout == "stripes" else 0, int(p0), int(p1), ctypes.cast(ptrs, ctypes.c_void_p), len(peer_states),
+            int(ref.shape[0]), row_bytes, D.ptr(anc), D.ptr(out), D.stream_ptr()))
+        return anc, out
+
     def gather_rows(self, states, idx):
         t = D.torch()
         src = states.contiguous()
@@ -201,13 +219,11 @@ class ShardedResampler:
         upper = combine_slice_stats(per[1::2])
         return combine_slice_stats([lower, upper])
 
-    # -- 2-4. B rule + per-slice resample --------------------------------------
-    def resample(self, w_local, b: int | None = None, seed=0, epsilon: float = 0.01):
-        """Ancestors (global indices) for this rank's particle slice, and the B used."""
-        n_local = w_local.numel()
-        full = self.replicate_weights(w_local)
+    def _checked_b(self, full, w_local, b, epsilon):
+        """The reference's validation (M/weights.py:49-59, M/resample.py:96-108, 84-93) and B."""
         n = full.numel()
         st = self.global_stats(w_local, full)
+        self._last_stats = st
         if st.n_nonfinite:
             raise ValueError("weights must be finite")
         if st.n_neg:
@@ -223,6 +239,15 @@ class ShardedResampler:
                              f"({self.warp.warp_size}) in strict mode")
         if self.kind in ("c1", "c2"):
             PartitionConfig(self.partition_bytes).n_partitions(n, self.warp)
+        return b
+
+    # -- 2-4. B rule + per-slice resample --------------------------------------
+    def resample(self, w_local, b: int | None = None, seed=0, epsilon: float = 0.01):
+        """Ancestors (global indices) for this rank's particle slice, and the B used."""
+        n_local = w_local.numel()
+        full = self.replicate_weights(w_local)
+        b = self._checked_b(full, w_local, b, epsilon)
+        st = self._last_stats
         args = (self.kind, full, b, seed, self.warp.warp_size, self.partition_bytes, self.strict, self.rng,
                 st.n_zero == 0)
         if self.layout == "stripes":
@@ -230,6 +255,20 @@ class ShardedResampler:
             return self.ops.resample_stripes(*args, lo0, lo1), b
         p0 = self.rank * n_local
         return self.ops.resample_range(*args, p0, p0 + n_local), b
+
+    def resample_gather(self, w_local, peer_states, b: int | None = None, seed=0, epsilon: float = 0.01):
+        """resample + apply_ancestors in one kernel: ``peer_states[r]`` is rank r's local state
+        array as addressable from this device (NVLink P2P / symmetric-memory mappings; rank order,
+        this rank's own array included).  Returns (ancestors, resampled local states, B)."""
+        n_local = w_local.numel()
+        full = self.replicate_weights(w_local)
+        b = self._checked_b(full, w_local, b, epsilon)
+        st = self._last_stats
+        (p0, p1) = self.owned(n_local)[0]
+        anc, rows = self.ops.resample_gather(self.kind, full, b, seed, self.warp.warp_size, self.partition_bytes,
+                                             self.strict, self.rng, st.n_zero == 0, self.layout, p0, p1,
+                                             peer_states)
+        return anc, rows, b
 
     # -- 5. particle states ---------------------------------------------------
     def exchange(self, states_local, anc_local):

@@ -62,6 +62,24 @@ class OracleOps:
         anc = oracle.resample(kind, w_full.numpy(), b, seed, warp, partition_bytes, strict, rng)
         return torch.from_numpy(np.concatenate([anc[lo0:lo1], anc[half + lo0:half + lo1]]))
 
+    def resample_gather(self, kind, w_full, b, seed, warp, partition_bytes, strict, rng, nonzero, layout, p0, p1,
+                        peer_states):
+        """ancestors as above, then each row read from its owner's array (the fused kernel's
+        owner mapping, mgp_kernels.cuh store_result / k_gather_peers)."""
+        args = (kind, w_full, b, seed, warp, partition_bytes, strict, rng, nonzero, p0, p1)
+        anc = (self.resample_stripes if layout == "stripes" else self.resample_range)(*args)
+        n_local, half = peer_states[0].shape[0], w_full.numel() // 2
+        rows = []
+        for a in anc.tolist():
+            if layout == "stripes":
+                up = a >= half
+                k = a - up * half
+                owner, local = k // (n_local // 2), k % (n_local // 2) + up * (n_local // 2)
+            else:
+                owner, local = divmod(a, n_local)
+            rows.append(peer_states[owner][local])
+        return anc, torch.stack(rows)
+
     def gather_rows(self, states, idx):
         return states[idx]
 
@@ -86,6 +104,11 @@ def _worker_stripes(rank, world, port, case, q):
         states_full = np.stack([np.arange(n, dtype=np.float64) * 1.5, np.arange(n, dtype=np.float64)], axis=1)
         s_local = torch.from_numpy(np.concatenate([states_full[a0:a1], states_full[b0:b1]]))
         new_local = sr.exchange(s_local, anc_local)
+        # the fused path: every rank's state array addressable here (peer mappings, emulated)
+        peers = [torch.zeros_like(s_local) for _ in range(world)]
+        dist.all_gather(peers, s_local)
+        anc_f, rows_f, b_f = sr.resample_gather(w_local, peers, b=b, seed=77)
+        assert b_f == b_used and torch.equal(anc_f, anc_local) and torch.equal(rows_f, new_local)
         parts = [torch.zeros(n_local, dtype=torch.int64) for _ in range(world)]
         dist.all_gather(parts, anc_local)
         news = [torch.zeros_like(new_local) for _ in range(world)]
@@ -125,6 +148,10 @@ def _worker(rank, world, port, case, q):
         states_full = np.stack([np.arange(n, dtype=np.float64) * 1.5, np.arange(n, dtype=np.float64)], axis=1)
         s_local = torch.from_numpy(states_full[rank * n_local:(rank + 1) * n_local].copy())
         new_local = sr.exchange(s_local, anc_local)
+        peers = [torch.zeros_like(s_local) for _ in range(world)]
+        dist.all_gather(peers, s_local)
+        anc_f, rows_f, b_f = sr.resample_gather(w_local, peers, b=b, seed=99)
+        assert b_f == b_used and torch.equal(anc_f, anc_local) and torch.equal(rows_f, new_local)
         news = [torch.zeros_like(new_local) for _ in range(world)]
         dist.all_gather(news, new_local)
         if rank == 0:

@@ -405,6 +405,11 @@ def test_sharded_resampler_cuda_ops_single_rank(mg, oracle):
         assert np.array_equal(anc.cpu().numpy(), oracle.megopolis(w, b, seed=31))
         st = torch.arange(1 << 16, dtype=torch.float64, device="cuda")
         assert torch.equal(sr.exchange(st, anc), st[anc])
+        for layout in ("contiguous", "stripes"):  # the fused resample + row gather
+            sr = ShardedResampler(layout=layout)
+            st2 = torch.stack([st, -st], 1)
+            anc2, rows, b2 = sr.resample_gather(torch.from_numpy(w).cuda(), [st2], seed=31)
+            assert b2 == b and torch.equal(anc2, anc) and torch.equal(rows, st2[anc])
     finally:
         dist.destroy_process_group()
 
@@ -528,8 +533,51 @@ def test_resample_gather_fused(mg, oracle, rng, kind, warp, n, cols):
         anc = torch.empty(p1 - p0, dtype=torch.int64, device="cuda")
         out = torch.empty(p1 - p0, cols, dtype=torch.float64, device="cuda")
         _lib.check(_lib.lib().mgp_resample_gather(
-            _lib.KIND[kind], wd.data_ptr(), 0, n, b, 4, warp, part, int(n % warp == 0), _lib.RNG[rng], 0, p0, p1,
+            _lib.KIND[kind], wd.data_ptr(), 0, n, b, 4, warp, part, int(n % warp == 0), _lib.RNG[rng], 0, 0, p0, p1,
             ctypes.cast(table, ctypes.c_void_p), 4, rows_local, 8 * cols, anc.data_ptr(), out.data_ptr(),
             torch.cuda.current_stream().cuda_stream))
         assert np.array_equal(anc.cpu().numpy(), ref[p0:p1]), (p0, p1)
         assert torch.equal(out, states[torch.from_numpy(ref[p0:p1]).cuda()]), (p0, p1)
+
+
+@pytest.mark.parametrize("kind,rng,n,b,cols", [("megopolis", "philox", 1 << 14, 9, 2), ("megopolis", "megores", 4096, 6, 2),
+                                                ("megopolis", "philox", 4096, 1030, 2),
+                                                ("megopolis", "philox", 4096, 7, 3),  # 3-byte rows: unfused
+                                                ("metropolis", "megores", 4096, 5, 2),  # W != 32: unfused
+                                                ("c2", "philox", 8192, 5, 2)])
+def test_resample_gather_stripes(mg, oracle, kind, rng, n, b, cols):
+    """mgp_resample_gather, stripes layout: 4 owners each holding stripe r of each half; the
+    fused kernel (or the two-kernel route for other shapes) reads each ancestor's row from its
+    owner (pointer table on one device)."""
+    import ctypes
+
+    from paper_2109_13504_b200 import _lib
+
+    w = oracle.gen_gaussian_weights(2.5, n, 123, "single")
+    part = 512 if kind == "c2" else 0
+    fn = {"megopolis": lambda: oracle.megopolis(w, b, seed=8, rng=rng),
+          "metropolis": lambda: oracle.metropolis(w, b, seed=8, rng=rng),
+          "c2": lambda: oracle.metropolis_c2(w, b, part, seed=8, rng=rng)}[kind]
+    ref = fn()
+    world, half = 4, n // 2
+    h = half // world
+    dt = torch.uint8 if cols == 3 else torch.float32
+    rows_full = (torch.arange(n * cols, device="cuda") % 251).to(dt).reshape(n, cols)
+    if dt == torch.float32:
+        rows_full = rows_full * 0.25
+    shards = [torch.cat([rows_full[r * h:(r + 1) * h], rows_full[half + r * h:half + (r + 1) * h]]).contiguous()
+              for r in range(world)]
+    table = (ctypes.c_void_p * world)(*[s.data_ptr() for s in shards])
+    row_bytes = cols * rows_full.element_size()
+    wd = torch.from_numpy(w).cuda()
+    for r in range(world):
+        lo0, lo1 = r * h, (r + 1) * h
+        anc = torch.empty(2 * h, dtype=torch.int64, device="cuda")
+        out = torch.empty(2 * h, cols, dtype=dt, device="cuda")
+        _lib.check(_lib.lib().mgp_resample_gather(
+            _lib.KIND[kind], wd.data_ptr(), 0, n, b, 8, 32, part, 1, _lib.RNG[rng], 0, 1, lo0, lo1,
+            ctypes.cast(table, ctypes.c_void_p), world, 2 * h, row_bytes, anc.data_ptr(), out.data_ptr(),
+            torch.cuda.current_stream().cuda_stream))
+        want = np.concatenate([ref[lo0:lo1], ref[half + lo0:half + lo1]])
+        assert np.array_equal(anc.cpu().numpy(), want), r
+        assert torch.equal(out, rows_full[torch.from_numpy(want).cuda()]), r
