@@ -175,6 +175,16 @@ int mgp_gather(const void *d_states, int64_t row_bytes, const int64_t *d_anc, in
 int mgp_gather_peers(const void *const *peer_states, int npeers, int64_t n_local, int64_t row_bytes,
                      const int64_t *d_anc, int64_t n, void *d_out, void *stream);
 
+/* Peer mappings for the two entry points above (CUDA IPC; no reference counterpart -- the
+ * reference is single-process).  mgp_ipc_export: the 64-byte cudaIpcMemHandle_t of the
+ * allocation holding d_ptr and d_ptr's offset in it.  mgp_ipc_open (in another process,
+ * any device with peer access): the mapped pointer to the same bytes, peer access enabled
+ * lazily.  mgp_ipc_close(mapped pointer, offset) unmaps.  The exporting process keeps
+ * the allocation alive while it is mapped. */
+int mgp_ipc_export(const void *d_ptr, void *handle_out, int64_t *offset_out);
+int mgp_ipc_open(const void *handle, int64_t offset, void **d_ptr_out);
+int mgp_ipc_close(void *d_ptr, int64_t offset);
+
 /* np.mean of a float64 / float32 vector (numpy pairwise order), e.g. the filter estimate
  * (M/pfilter.py:162). */
 int mgp_mean(const void *d_x, int dtype, int64_t n, double *d_out, void *stream);

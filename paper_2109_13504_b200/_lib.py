@@ -54,6 +54,9 @@ SIGNATURES = {
     "mgp_squared_error": (_i32, [_vp, _vp, _i64, _vp, _vp]),
     "mgp_gather": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp]),
     "mgp_gather_peers": (_i32, [_vp, _i32, _i64, _i64, _vp, _i64, _vp, _vp]),
+    "mgp_ipc_export": (_i32, [_vp, _vp, _vp]),
+    "mgp_ipc_open": (_i32, [_vp, _i64, _vp]),
+    "mgp_ipc_close": (_i32, [_vp, _i64]),
     "mgp_mean": (_i32, [_vp, _i32, _i64, _vp, _vp]),
     "mgp_pf_init": (_i32, [_i64, _u64, _dbl, _vp, _vp]),
     "mgp_pf_predict_update": (_i32, [_vp, _i64, _dbl, _dbl, _u64, _dbl, _dbl, _i32, _vp, _vp, _vp, _vp]),

@@ -945,6 +945,53 @@ int mgp_gather_peers(const void* const* peer_states, int npeers, int64_t n_local
   return gather_peers(peer_states, npeers, n_local, row_bytes, d_anc, n, d_out, stream, 0);
 }
 
+// ---------------------------------------------------------------------------
+// Peer mappings of particle-state arrays (CUDA IPC): one process per GPU exports its
+// state array, the others map it (peer access over NVLink enabled lazily), and the
+// mapped pointers feed mgp_gather_peers / mgp_resample_gather's owner table.  The
+// driver's cuMemGetAddressRange (looked up at run time, so the library does not link
+// libcuda) finds the allocation an interior pointer -- e.g. a caching-allocator block --
+// belongs to; the handle names that allocation and the offset locates the array in it.
+
+typedef int (*PfnMemGetAddressRange)(unsigned long long*, size_t*, unsigned long long);
+
+int mgp_ipc_export(const void* d_ptr, void* handle_out, int64_t* offset_out) {
+  if (!d_ptr || !handle_out || !offset_out) return set_err(MGP_EINVAL, "null pointer");
+  static PfnMemGetAddressRange range = nullptr;
+  if (!range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CUDA_TRY(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !fn) return set_err(MGP_EUNSUPPORTED, "cuMemGetAddressRange not found");
+    range = (PfnMemGetAddressRange)fn;
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (unsigned long long)(uintptr_t)d_ptr) != 0)
+    return set_err(MGP_EINVAL, "pointer %p is not a device allocation", d_ptr);
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, (void*)(uintptr_t)base));
+  std::memcpy(handle_out, &h, sizeof(h));
+  *offset_out = (int64_t)((uintptr_t)d_ptr - (uintptr_t)base);
+  return 0;
+}
+
+int mgp_ipc_open(const void* handle, int64_t offset, void** d_ptr_out) {
+  if (!handle || !d_ptr_out || offset < 0) return set_err(MGP_EINVAL, "invalid argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  void* base = nullptr;
+  CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  *d_ptr_out = (char*)base + offset;
+  return 0;
+}
+
+int mgp_ipc_close(void* d_ptr, int64_t offset) {
+  if (!d_ptr || offset < 0) return set_err(MGP_EINVAL, "invalid argument");
+  CUDA_TRY(cudaIpcCloseMemHandle((char*)d_ptr - offset));
+  return 0;
+}
+
 int mgp_mean(const void* d_x, int dtype, int64_t n, double* d_out, void* stream) {
   if (n < 1) return set_err(MGP_EINVAL, "n must be >= 1");
   PwOut out{nullptr, d_out, nullptr, nullptr};

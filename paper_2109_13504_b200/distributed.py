@@ -17,8 +17,8 @@ weight vector, the shared offsets and the seed only (M/resample.py:185-197), so:
   4. resample: each rank runs the kernel on its particle slice (global indices),
   5. states: apply_ancestors needs rows owned by other ranks -- exchanged with
      all-to-all (bucketed by owner) or read directly from peer memory
-     (``gather_from_peers`` / mgp_gather_peers) when the rows live in
-     NVLink-mapped symmetric memory.
+     (``gather_from_peers`` / mgp_gather_peers, or fused into the resampling kernel by
+     ``ShardedResampler.resample_gather``) through CUDA IPC mappings (``PeerRows``).
 
 The concatenation of every rank's ancestors equals the single-GPU result, which
 equals the reference's, bit for bit.
@@ -99,17 +99,17 @@ class CudaOps:
                         peer_states):
         """mgp_resample_gather: ancestors plus the resampled state rows in one kernel."""
         t = D.torch()
-        ref = peer_states[0]
+        table, ref = _peer_table(peer_states)
         count = (p1 - p0) * (2 if layout == "stripes" else 1)
         anc = t.empty(count, dtype=t.int64, device=w_full.device)
         out = t.empty((count,) + tuple(ref.shape[1:]), dtype=ref.dtype, device=w_full.device)
-        ptrs = (ctypes.c_void_p * len(peer_states))(*[p.data_ptr() for p in peer_states])
+        ptrs = (ctypes.c_void_p * len(table))(*table)
         row_bytes = ref[0].numel() * ref.element_size() if ref.shape[0] else 0
         flags = _lib.FLAG_NONZERO if nonzero else 0
         _lib.check(_lib.lib().mgp_resample_gather(
             _lib.KIND[kind], D.ptr(w_full), D.wdtype(w_full), w_full.numel(), int(b), int(seed) & (2**64 - 1),
             int(warp), int(partition_bytes or 0), int(bool(strict)), _lib.RNG[rng], flags,
-            1 if layout == "stripes" else 0, int(p0), int(p1), ctypes.cast(ptrs, ctypes.c_void_p), len(peer_states),
+            1 if layout == "stripes" else 0, int(p0), int(p1), ctypes.cast(ptrs, ctypes.c_void_p), len(table),
             int(ref.shape[0]), row_bytes, D.ptr(anc), D.ptr(out), D.stream_ptr()))
         return anc, out
 
@@ -257,9 +257,10 @@ class ShardedResampler:
         return self.ops.resample_range(*args, p0, p0 + n_local), b
 
     def resample_gather(self, w_local, peer_states, b: int | None = None, seed=0, epsilon: float = 0.01):
-        """resample + apply_ancestors in one kernel: ``peer_states[r]`` is rank r's local state
-        array as addressable from this device (NVLink P2P / symmetric-memory mappings; rank order,
-        this rank's own array included).  Returns (ancestors, resampled local states, B)."""
+        """resample + apply_ancestors in one kernel.  ``peer_states``: a PeerRows (every rank's
+        state array mapped here by CUDA IPC), or a list whose entry r is rank r's local state
+        array as addressable from this device (rank order, this rank's own array included).
+        Returns (ancestors, resampled local states, B)."""
         n_local = w_local.numel()
         full = self.replicate_weights(w_local)
         b = self._checked_b(full, w_local, b, epsilon)
@@ -301,15 +302,60 @@ class ShardedResampler:
         return out
 
 
-def gather_from_peers(peer_states, n_local: int, anc, out=None):
-    """out[i] = row anc[i] read directly from its owner's memory (mgp_gather_peers).
+class PeerRows:
+    """Every rank's particle-state array, addressable from this device (CUDA IPC mappings).
 
-    ``peer_states``: one CUDA tensor (or raw device pointer) per rank, each holding
-    that rank's n_local rows and addressable from this device (NVLink P2P /
-    symmetric memory).  Single-kernel sharded gather: no staging, no all-to-all."""
-    t = D.torch()
-    ptrs = []
-    ref = None
+    Collective: each rank passes its own ``states_local`` (same row shape and dtype on every
+    rank, allocated on its GPU); the handles travel by one all_gather_object and each rank
+    maps its peers' arrays (mgp_ipc_open; peer access over NVLink is enabled lazily).
+    ``ptrs[r]`` is rank r's array as seen here (this rank's own pointer unmapped).  The
+    arrays must stay alive and in place while mapped; ``close()`` unmaps.  Pass the
+    object to ``ShardedResampler.resample_gather`` or ``gather_from_peers``."""
+
+    def __init__(self, states_local, group=None):
+        import torch.distributed as dist
+
+        t = D.torch()
+        if not states_local.is_cuda or not states_local.is_contiguous():
+            raise ValueError("states_local must be a contiguous CUDA tensor")
+        self.template = states_local
+        self.rows_local = states_local.shape[0]
+        L = _lib.lib()
+        h = ctypes.create_string_buffer(64)
+        off = ctypes.c_int64(0)
+        _lib.check(L.mgp_ipc_export(ctypes.c_void_p(states_local.data_ptr()), h, ctypes.byref(off)))
+        rank = dist.get_rank(group)
+        world = dist.get_world_size(group)
+        mine = (bytes(h.raw), int(off.value), tuple(states_local.shape), str(states_local.dtype),
+                t.cuda.current_device())
+        every = [None] * world
+        dist.all_gather_object(every, mine, group=group)
+        self.ptrs, self._opened = [], []
+        for r, (hr, offr, shape, dtype, _) in enumerate(every):
+            if shape != mine[2] or dtype != mine[3]:
+                raise ValueError(f"rank {r} holds states {shape} {dtype}, this rank {mine[2]} {mine[3]}")
+            if r == rank:
+                self.ptrs.append(states_local.data_ptr())
+                continue
+            p = ctypes.c_void_p(0)
+            _lib.check(L.mgp_ipc_open(ctypes.create_string_buffer(hr, 64), offr, ctypes.byref(p)))
+            self.ptrs.append(p.value)
+            self._opened.append((p.value, offr))
+
+    def __len__(self):
+        return len(self.ptrs)
+
+    def close(self):
+        for p, off in self._opened:
+            _lib.check(_lib.lib().mgp_ipc_close(ctypes.c_void_p(p), off))
+        self._opened = []
+
+
+def _peer_table(peer_states):
+    """(pointers, template tensor) from a PeerRows or a list of tensors / raw pointers."""
+    if isinstance(peer_states, PeerRows):
+        return list(peer_states.ptrs), peer_states.template
+    ptrs, ref = [], None
     for p in peer_states:
         if D.is_tensor(p):
             ref = p if ref is None else ref
@@ -318,6 +364,17 @@ def gather_from_peers(peer_states, n_local: int, anc, out=None):
             ptrs.append(int(p))
     if ref is None:
         raise ValueError("at least one peer must be given as a tensor (shape/dtype template)")
+    return ptrs, ref
+
+
+def gather_from_peers(peer_states, n_local: int, anc, out=None):
+    """out[i] = row anc[i] read directly from its owner's memory (mgp_gather_peers).
+
+    ``peer_states``: one CUDA tensor (or raw device pointer) per rank, each holding
+    that rank's n_local rows and addressable from this device (NVLink P2P /
+    symmetric memory).  Single-kernel sharded gather: no staging, no all-to-all."""
+    t = D.torch()
+    ptrs, ref = _peer_table(peer_states)
     anc = anc.to(device=ref.device, dtype=t.int64).contiguous()
     if out is None:
         out = t.empty((anc.numel(),) + tuple(ref.shape[1:]), dtype=ref.dtype, device=ref.device)
