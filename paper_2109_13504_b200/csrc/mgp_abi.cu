@@ -110,6 +110,31 @@ void ensure_pool() {
   g_pool_ready.push_back(dev);
 }
 
+// Stream-ordered scratch owned by one call: every block allocated through it is released
+// (cudaFreeAsync, ordered after the work queued so far) when it goes out of scope, so the
+// early returns of CUDA_TRY / LAUNCH_CHECK do not leak.
+class Scratch {
+ public:
+  explicit Scratch(cudaStream_t st) : st_(st) { ensure_pool(); }
+  ~Scratch() {
+    for (auto it = p_.rbegin(); it != p_.rend(); ++it) cudaFreeAsync(*it, st_);
+  }
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
+  template <typename T>
+  cudaError_t alloc(T** out, size_t bytes) {
+    void* q = nullptr;
+    const cudaError_t e = cudaMallocAsync(&q, bytes ? bytes : 1, st_);
+    if (e == cudaSuccess) p_.push_back(q);
+    *out = static_cast<T*>(q);
+    return e;
+  }
+
+ private:
+  cudaStream_t st_;
+  std::vector<void*> p_;
+};
+
 // ---------------------------------------------------------------------------
 // pairwise reduction plumbing
 
@@ -136,13 +161,13 @@ int pw_depth(int64_t n) {
 
 template <class Elem, typename WT, bool STATS>
 int pw_reduce(const Elem& e, const WT* wraw, int64_t n, PwOut out, cudaStream_t st) {
-  ensure_pool();
+  Scratch sc(st);
   const int depth = pw_depth(n);
   const int64_t nch = 1ll << depth;
   double* heap = nullptr;
   WStats* cst = nullptr;
-  CUDA_TRY(cudaMallocAsync(&heap, sizeof(double) * 2 * nch, st));
-  if (STATS) CUDA_TRY(cudaMallocAsync(&cst, sizeof(WStats) * nch, st));
+  CUDA_TRY(sc.alloc(&heap, sizeof(double) * 2 * nch));
+  if (STATS) CUDA_TRY(sc.alloc(&cst, sizeof(WStats) * nch));
   if (n == (int64_t)PW_CHUNK << depth)  // power-of-two N >= 4096: perfect 32-leaf chunk subtrees
     k_pw_chunks4096<Elem, WT, STATS><<<(unsigned)nch, PW_THREADS, 0, st>>>(e, wraw, depth, heap, cst);
   else
@@ -150,8 +175,6 @@ int pw_reduce(const Elem& e, const WT* wraw, int64_t n, PwOut out, cudaStream_t 
   LAUNCH_CHECK("k_pw_chunks");
   k_pw_final<<<1, 1024, 0, st>>>(heap, depth, n, cst, out);
   LAUNCH_CHECK("k_pw_final");
-  CUDA_TRY(cudaFreeAsync(heap, st));
-  if (cst) CUDA_TRY(cudaFreeAsync(cst, st));
   return 0;
 }
 
@@ -345,6 +368,15 @@ struct Plan {
   int64_t rows_half = 0;
   uint32_t row_words = 0;
   uint32_t* rows_out = nullptr;
+  cudaStream_t alloc_st = nullptr;  // stream of plan_alloc's buffers
+
+  Plan() = default;
+  Plan(const Plan&) = delete;
+  Plan& operator=(const Plan&) = delete;
+  ~Plan() {  // early-return paths: release whatever plan_free did not
+    for (void* q : {(void*)d_off, (void*)kstate, cum})
+      if (q) cudaFreeAsync(q, alloc_st);
+  }
 };
 
 // The half-split Megopolis kernel applies: W = 32, N = 2^k >= 256, 4 particles per thread
@@ -359,7 +391,7 @@ bool is_prefix_kind(int kind) { return kind == MGP_KIND_MULTINOMIAL || kind == M
 // np.cumsum(values) in the weights' dtype, bit-exact (mgp_prefix.cuh)
 template <typename WT>
 int px_cumsum(const WT* w, int64_t n, WT* cum, cudaStream_t st) {
-  ensure_pool();
+  Scratch sc(st);
   const int64_t nch = (n + PX_CHUNK - 1) / PX_CHUNK, nsup = (nch + PX_SUPER - 1) / PX_SUPER;
   double *csum = nullptr, *est = nullptr;
   int32_t *e0 = nullptr, *mode = nullptr, *exc = nullptr, *se0 = nullptr, *smode = nullptr;
@@ -368,18 +400,18 @@ int px_cumsum(const WT* w, int64_t n, WT* cum, cudaStream_t st) {
   void* tmp = nullptr;
   size_t tmp_bytes = 0;
   CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (const double*)nullptr, (double*)nullptr, (int)nch, st));
-  CUDA_TRY(cudaMallocAsync(&csum, sizeof(double) * nch, st));
-  CUDA_TRY(cudaMallocAsync(&est, sizeof(double) * nch, st));
-  CUDA_TRY(cudaMallocAsync(&e0, sizeof(int32_t) * nch, st));
-  CUDA_TRY(cudaMallocAsync(&mode, sizeof(int32_t) * nch, st));
-  CUDA_TRY(cudaMallocAsync(&exc, sizeof(int32_t) * (nch + 1), st));
-  CUDA_TRY(cudaMallocAsync(&agg, sizeof(Tx) * PX_CAND * nch, st));
-  CUDA_TRY(cudaMallocAsync(&carry, sizeof(WT) * nch, st));
-  CUDA_TRY(cudaMallocAsync(&se0, sizeof(int32_t) * nsup, st));
-  CUDA_TRY(cudaMallocAsync(&smode, sizeof(int32_t) * nsup, st));
-  CUDA_TRY(cudaMallocAsync(&sagg, sizeof(Tx) * PX_CAND * nsup, st));
-  CUDA_TRY(cudaMallocAsync(&scarry, sizeof(WT) * nsup, st));
-  CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes + 16, st));
+  CUDA_TRY(sc.alloc(&csum, sizeof(double) * nch));
+  CUDA_TRY(sc.alloc(&est, sizeof(double) * nch));
+  CUDA_TRY(sc.alloc(&e0, sizeof(int32_t) * nch));
+  CUDA_TRY(sc.alloc(&mode, sizeof(int32_t) * nch));
+  CUDA_TRY(sc.alloc(&exc, sizeof(int32_t) * (nch + 1)));
+  CUDA_TRY(sc.alloc(&agg, sizeof(Tx) * PX_CAND * nch));
+  CUDA_TRY(sc.alloc(&carry, sizeof(WT) * nch));
+  CUDA_TRY(sc.alloc(&se0, sizeof(int32_t) * nsup));
+  CUDA_TRY(sc.alloc(&smode, sizeof(int32_t) * nsup));
+  CUDA_TRY(sc.alloc(&sagg, sizeof(Tx) * PX_CAND * nsup));
+  CUDA_TRY(sc.alloc(&scarry, sizeof(WT) * nsup));
+  CUDA_TRY(sc.alloc(&tmp, tmp_bytes + 16));
   k_px_chunk_sum<WT><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, csum);
   LAUNCH_CHECK("k_px_chunk_sum");
   CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, csum, est, (int)nch, st));
@@ -395,9 +427,6 @@ int px_cumsum(const WT* w, int64_t n, WT* cum, cudaStream_t st) {
   LAUNCH_CHECK("k_px_materialize");
   k_px_materialize_exc<WT><<<(unsigned)std::min<int64_t>(nch, 2 * 148), 32, 0, st>>>(w, n, carry, exc, cum);
   LAUNCH_CHECK("k_px_materialize_exc");
-  for (void* q : {(void*)csum, (void*)est, (void*)e0, (void*)mode, (void*)exc, (void*)agg, (void*)carry, (void*)se0,
-                  (void*)smode, (void*)sagg, (void*)scarry, tmp})
-    CUDA_TRY(cudaFreeAsync(q, st));
   return 0;
 }
 
@@ -416,8 +445,9 @@ int px_search(int kind, const void* cum, int dtype, int64_t n, uint64_t seed, in
     const uint64_t base = megores_base(seed);
     int64_t K = 1;
     while (K * 2 * PXM_PER_BUCKET <= n) K *= 2;
+    Scratch sc(st);
     int32_t* start = nullptr;
-    CUDA_TRY(cudaMallocAsync(&start, sizeof(int32_t) * (K + 1), st));
+    CUDA_TRY(sc.alloc(&start, sizeof(int32_t) * (K + 1)));
     const unsigned kg = (unsigned)std::min<int64_t>((K + 256) / 256, 148 * 16);
     if (dtype == MGP_F32) {
       k_multinomial_buckets<float><<<kg, 256, 0, st>>>((const float*)cum, n, K, start);
@@ -427,7 +457,6 @@ int px_search(int kind, const void* cum, int dtype, int64_t n, uint64_t seed, in
       k_multinomial<double><<<grid, 256, 0, st>>>((const double*)cum, n, base, p0, p_end, K, start, anc);
     }
     LAUNCH_CHECK("k_multinomial");
-    CUDA_TRY(cudaFreeAsync(start, st));
   } else {
     const double u0 = (double)(mix64(megores_key(megores_base(seed), GLOBAL_OFFSET_LANE, 0)) >> 11) * 0x1p-53;
     const unsigned sg = (unsigned)std::min<int64_t>((cnt / PXS_RUN + 256) / 256, 148 * 64);
@@ -560,6 +589,7 @@ int make_plan(Plan& p, int kind, const void* w, int dtype, int64_t n, int32_t b,
 
 int plan_alloc(Plan& p, cudaStream_t st) {
   ensure_pool();
+  p.alloc_st = st;
   if (is_prefix_kind(p.kind)) {  // the prefix sum is shared by every particle range
     CUDA_TRY(cudaMallocAsync(&p.cum, (size_t)p.n * (p.dtype == MGP_F32 ? 4 : 8), st));
     return px_cumsum_any(p.w, p.dtype, p.n, p.cum, st);
@@ -830,13 +860,12 @@ int mgp_offspring(const int64_t* d_anc, int64_t n_anc, int64_t n, int64_t* d_cou
   if (n) CUDA_TRY(cudaMemsetAsync(d_counts, 0, sizeof(int64_t) * n, st));
   if (d_bad) CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int32_t), st));
   if (n_anc == 0) return 0;
-  ensure_pool();
+  Scratch sc(st);
   int32_t* bad = d_bad;
-  if (!bad) CUDA_TRY(cudaMallocAsync(&bad, sizeof(int32_t), st));
+  if (!bad) CUDA_TRY(sc.alloc(&bad, sizeof(int32_t)));
   const unsigned grid = (unsigned)((n_anc + 255) / 256);
   k_offspring<int64_t><<<grid, 256, 0, st>>>(d_anc, n_anc, n, d_counts, bad);
   LAUNCH_CHECK("k_offspring");
-  if (!d_bad) CUDA_TRY(cudaFreeAsync(bad, st));
   return 0;
 }
 
@@ -1040,10 +1069,10 @@ int mgp_estimate_ratio_stats(const void* d_w, int dtype, int64_t n, int64_t subs
                                                (long long)subset);
   if (dtype != MGP_F32 && dtype != MGP_F64) return set_err(MGP_EINVAL, "dtype must be MGP_F32 or MGP_F64");
   if (n > MAX_N) return set_err(MGP_EUNSUPPORTED, "N exceeds 2^31-1");
-  ensure_pool();
   cudaStream_t st = S(stream);
+  Scratch sc(st);
   mgp_weight_stats_t* ws = nullptr;
-  CUDA_TRY(cudaMallocAsync(&ws, sizeof *ws, st));
+  CUDA_TRY(sc.alloc(&ws, sizeof *ws));
   int rc = 0;
   if (subset == n) {  // the full array in natural order (M/weights.py:146-147)
     rc = mgp_weight_stats(d_w, dtype, n, ws, st);
@@ -1053,34 +1082,27 @@ int mgp_estimate_ratio_stats(const void* d_w, int dtype, int64_t n, int64_t subs
     double* sub = nullptr;
     void* tmp = nullptr;
     size_t tmp_bytes = 0;
-    CUDA_TRY(cudaMallocAsync(&k_in, 8 * n, st));
-    CUDA_TRY(cudaMallocAsync(&k_out, 8 * n, st));
-    CUDA_TRY(cudaMallocAsync(&i_in, 4 * n, st));
-    CUDA_TRY(cudaMallocAsync(&i_out, 4 * n, st));
-    CUDA_TRY(cudaMallocAsync(&sub, 8 * subset, st));
+    CUDA_TRY(sc.alloc(&k_in, 8 * n));
+    CUDA_TRY(sc.alloc(&k_out, 8 * n));
+    CUDA_TRY(sc.alloc(&i_in, 4 * n));
+    CUDA_TRY(sc.alloc(&i_out, 4 * n));
+    CUDA_TRY(sc.alloc(&sub, 8 * subset));
     const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
     k_ratio_keys<<<grid, 256, 0, st>>>(n, megores_base(seed), k_in, i_in);
     LAUNCH_CHECK("k_ratio_keys");
     CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, i_in, i_out, (int)n, 0, 53, st));
-    CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, st));
+    CUDA_TRY(sc.alloc(&tmp, tmp_bytes));
     CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k_in, k_out, i_in, i_out, (int)n, 0, 53, st));
     const unsigned g2 = (unsigned)std::min<int64_t>((subset + 255) / 256, 148 * 16);
     if (dtype == MGP_F32) k_gather_f64<float><<<g2, 256, 0, st>>>((const float*)d_w, i_out, subset, sub);
     else k_gather_f64<double><<<g2, 256, 0, st>>>((const double*)d_w, i_out, subset, sub);
     LAUNCH_CHECK("k_gather_f64");
     rc = mgp_weight_stats(sub, MGP_F64, subset, ws, st);
-    cudaFreeAsync(tmp, st);
-    cudaFreeAsync(sub, st);
-    cudaFreeAsync(i_out, st);
-    cudaFreeAsync(i_in, st);
-    cudaFreeAsync(k_out, st);
-    cudaFreeAsync(k_in, st);
   }
   if (!rc) {
     CUDA_TRY(cudaMemcpyAsync(d_out, &ws->mean, sizeof(double), cudaMemcpyDeviceToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(d_out + 1, &ws->max, sizeof(double), cudaMemcpyDeviceToDevice, st));
   }
-  cudaFreeAsync(ws, st);
   return rc;
 }
 
@@ -1146,10 +1168,11 @@ extern "C" int mgp_resample_gather(int kind, const void* d_w, int dtype, int64_t
   }
   const bool fused = plan_uses_w32(p) && row_bytes > 0 && (al & 3) == 0;
   if ((rc = plan_alloc(p, st))) return rc;
+  Scratch gsc(st);
   void** d_table = nullptr;
   const int64_t words = row_bytes / 4;
   if (fused) {
-    CUDA_TRY(cudaMallocAsync((void**)&d_table, sizeof(void*) * npeers, st));
+    CUDA_TRY(gsc.alloc(&d_table, sizeof(void*) * npeers));
     CUDA_TRY(cudaMemcpyAsync(d_table, h_peer_rows, sizeof(void*) * npeers, cudaMemcpyHostToDevice, st));
     p.rows_peers = (const void* const*)d_table;
     p.rows_local = rows_local;
@@ -1170,12 +1193,11 @@ extern "C" int mgp_resample_gather(int kind, const void* d_w, int dtype, int64_t
     if (fused) p.rows_out = (uint32_t*)d_rows_out + L * words - (half + p0) * words;
     if (!rc) rc = run_range(p, half + p0, half + p1, d_anc_out + L - (half + p0), st);
   }
-  if (!rc && !fused && row_bytes > 0) {  // two-kernel fallback (owner mapping on the host side)
+  if (!rc && !fused && row_bytes > 0) {  // two-kernel route: peer gather with the same owner mapping
     rc = gather_peers(h_peer_rows, npeers, rows_local, row_bytes, d_anc_out, layout ? 2 * L : L, d_rows_out, st,
                       layout ? half : 0);
   }
   int rc2 = plan_free(p, st);
-  if (d_table) cudaFreeAsync(d_table, st);
   return rc ? rc : rc2;
 }
 
@@ -1218,12 +1240,12 @@ extern "C" int mgp_quality_runs(int kind, const void* d_w, int dtype, int64_t n,
   if (k < 0 || (k > 0 && !h_seeds)) return set_err(MGP_EINVAL, "invalid seed list");
   if (!d_w || !d_e || !d_sum || !d_sumsq || !d_se_total) return set_err(MGP_EINVAL, "null pointer");
   cudaStream_t st = S(stream);
-  ensure_pool();
+  Scratch sc(st);
   int64_t *anc = nullptr, *counts = nullptr;
   double* se_run = nullptr;
-  CUDA_TRY(cudaMallocAsync(&anc, sizeof(int64_t) * n, st));
-  CUDA_TRY(cudaMallocAsync(&counts, sizeof(int64_t) * n, st));
-  CUDA_TRY(cudaMallocAsync(&se_run, sizeof(double), st));
+  CUDA_TRY(sc.alloc(&anc, sizeof(int64_t) * n));
+  CUDA_TRY(sc.alloc(&counts, sizeof(int64_t) * n));
+  CUDA_TRY(sc.alloc(&se_run, sizeof(double)));
   int rc = 0;
   Plan shared;  // prefix-sum kinds: one prefix sum serves every seed
   const bool prefix = is_prefix_kind(kind);
@@ -1246,10 +1268,10 @@ extern "C" int mgp_quality_runs(int kind, const void* d_w, int dtype, int64_t n,
     if (!rc) rc = mgp_offspring(anc, n, n, counts, nullptr, st);
     if (!rc) rc = mgp_quality_add(counts, d_e, n, d_sum, d_sumsq, d_se_total, se_run, st);
   }
-  if (prefix) plan_free(shared, st);
-  cudaFreeAsync(anc, st);
-  cudaFreeAsync(counts, st);
-  cudaFreeAsync(se_run, st);
+  if (prefix) {
+    const int rc2 = plan_free(shared, st);
+    if (!rc) rc = rc2;
+  }
   return rc;
 }
 
@@ -1276,9 +1298,9 @@ extern "C" int mgp_systematic_oracle(const void* d_w, int dtype, int64_t n, doub
   if (n > MAX_N) return set_err(MGP_EUNSUPPORTED, "N=%lld exceeds this build's limit of 2^31-1 particles", (long long)n);
   if (!d_w || !d_anc) return set_err(MGP_EINVAL, "null pointer");
   cudaStream_t st = S(stream);
-  ensure_pool();
+  Scratch sc(st);
   void* cum = nullptr;
-  CUDA_TRY(cudaMallocAsync(&cum, (size_t)n * (dtype == MGP_F32 ? 4 : 8), st));
+  CUDA_TRY(sc.alloc(&cum, (size_t)n * (dtype == MGP_F32 ? 4 : 8)));
   int rc = px_cumsum_any(d_w, dtype, n, cum, st);
   if (!rc) {
     const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 64);
@@ -1286,20 +1308,19 @@ extern "C" int mgp_systematic_oracle(const void* d_w, int dtype, int64_t n, doub
     else k_systematic_oracle<double><<<grid, 256, 0, st>>>((const double*)cum, n, u, d_anc);
     LAUNCH_CHECK("k_systematic_oracle");
   }
-  CUDA_TRY(cudaFreeAsync(cum, st));
   return rc;
 }
 
 extern "C" int mgp_philox_selftest(uint64_t key, uint32_t c1, uint32_t c2, uint32_t c3, int64_t n,
                                    int64_t* h_mismatch) {
+  Scratch sc(nullptr);
   unsigned long long* d = nullptr;
-  CUDA_TRY(cudaMalloc(&d, sizeof *d));
+  CUDA_TRY(sc.alloc(&d, sizeof *d));
   CUDA_TRY(cudaMemset(d, 0, sizeof *d));
   k_philox_selftest<<<148 * 4, 256>>>(key, c1, c2, c3, n, d);
   LAUNCH_CHECK("k_philox_selftest");
   unsigned long long h = 0;
   CUDA_TRY(cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost));
-  CUDA_TRY(cudaFree(d));
   *h_mismatch = (int64_t)h;
   return 0;
 }

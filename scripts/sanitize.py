@@ -42,6 +42,30 @@ mg.multinomial(np.ones(3000, np.float32), 1)  # host path
 mg.megopolis(rr.random(1 << 12).astype(np.float32), 7, seed=5, rng="philox")
 shards = [torch.rand(100, 2, device="cuda") for _ in range(4)]
 gather_from_peers(shards, 100, torch.from_numpy(rr.integers(0, 400, 300)))
+# fused resample + peer-row gather: contiguous / stripes owner mappings, fused (W = 32, 4-byte
+# rows) and two-kernel (metropolis, 3-byte rows) routes
+import ctypes  # noqa: E402
+
+from paper_2109_13504_b200 import _lib  # noqa: E402
+
+wq = torch.from_numpy(rr.random(4096).astype(np.float32)).cuda()
+for kind, layout, cols, dt in (("megopolis", 0, 2, torch.float32), ("megopolis", 1, 2, torch.float32),
+                               ("megopolis", 1, 3, torch.uint8), ("metropolis", 1, 2, torch.float32),
+                               ("metropolis", 0, 2, torch.float32)):
+    own = [torch.zeros(1024, cols, dtype=dt, device="cuda") for _ in range(4)]
+    tab = (ctypes.c_void_p * 4)(*[o.data_ptr() for o in own])
+    lo, hi = (256, 512) if layout else (1024, 2048)
+    cnt = (hi - lo) * (2 if layout else 1)
+    anc = torch.empty(cnt, dtype=torch.int64, device="cuda")
+    out = torch.empty(cnt, cols, dtype=dt, device="cuda")
+    _lib.check(_lib.lib().mgp_resample_gather(
+        _lib.KIND[kind], wq.data_ptr(), 0, 4096, 9, 3, 32, 0, 1, _lib.RNG["philox"], 0, layout, lo, hi,
+        ctypes.cast(tab, ctypes.c_void_p), 4, 1024, cols * own[0].element_size(), anc.data_ptr(), out.data_ptr(),
+        torch.cuda.current_stream().cuda_stream))
+acc = mg.QualityAccumulator(4096)
+acc.add_runs("megopolis", mg.WeightVector(wq, "single"), 5, [1, 2, 3])
+mg.estimate_ratio(mg.WeightVector(wq, "single"), 1000, 7)
+mg.systematic_oracle(mg.WeightVector(wq, "single"), 0.25)
 traj = pf.generate_trajectory(3, 0.0, 1)
 pf.run_filter(pf.FilterConfig(n_particles=8192, b_fixed=None), traj, 2)
 torch.cuda.synchronize()
