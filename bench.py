@@ -408,16 +408,27 @@ def main():
         te_o = e2e_time(_lib.RNG[other])
         res[other]["e2e"] = {"value": n_loc * world / te_o, "ms_per_step": te_o * 1e3}
 
-    # quality (offspring MSE / bias, M/metrics.py) outside the timed region, rank 0
+    # quality (offspring MSE / bias, M/metrics.py) outside the timed region.  N > 1: the sharded
+    # path (stripes-layout resample -> owner-bucketed offspring -> ShardedQuality), which equals
+    # one device's QualityAccumulator over the whole population bit for bit.
     quality = None
-    if rank == 0 and args.quality_runs >= 2 and world == 1:
+    if args.quality_runs >= 2:
         qs = {}
-        wv = mg.WeightVector(full, "single")
         for kind in ("megopolis", "metropolis"):
-            acc = mg.QualityAccumulator(n_glob)
-            fn = mg.make_resampler(kind, rng=args.rng)
-            for k in range(args.quality_runs):
-                acc.add(mg.ancestors_to_offspring(fn(wv, b, mg.derive_seed(2002, k)), n_glob), wv)
+            if world == 1:
+                wv = mg.WeightVector(full, "single")
+                acc = mg.QualityAccumulator(n_glob)
+                fn = mg.make_resampler(kind, rng=args.rng)
+                for k in range(args.quality_runs):
+                    acc.add(mg.ancestors_to_offspring(fn(wv, b, mg.derive_seed(2002, k)), n_glob), wv)
+            else:
+                from paper_2109_13504_b200.distributed import ShardedResampler
+
+                sr = ShardedResampler(kind=kind, rng=args.rng, layout="stripes")
+                acc = sr.quality(local_w)
+                for k in range(args.quality_runs):
+                    a_loc, _ = sr.resample(local_w, b=b, seed=mg.derive_seed(2002, k))
+                    acc.add(sr.offspring(a_loc))
             st = acc.finalize()
             qs[kind] = {"mse_per_particle": st.mse_per_particle, "bias_contribution": st.bias_contribution}
         quality = {"runs": args.quality_runs, **qs, "paper_megopolis_y4": 0.6508, "paper_metropolis": 1.0}

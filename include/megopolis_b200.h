@@ -152,6 +152,10 @@ int mgp_offspring(const int64_t *d_anc, int64_t n_anc, int64_t n, int64_t *d_cou
  *   add:       sum += o; sum_sq += o*o; se_total += sum((o - e)^2)      (:86-93)
  *   finalize:  variance = sum(sum_sq/k - mean^2), bias_sq = sum((mean - e)^2) (:95-110) */
 int mgp_expected_offspring(const void *d_w, int dtype, int64_t n, double *d_e, double *d_total, void *stream);
+/* _expected_offspring for a slice of a sharded population: d_e = n_all * w / total over the
+ * n_slice local weights, total = the global float64 sum (numpy order) computed elsewhere. */
+int mgp_expected_offspring_slice(const void *d_w, int dtype, int64_t n_slice, int64_t n_all, double total,
+                                 double *d_e, void *stream);
 int mgp_quality_add(const int64_t *d_counts, const double *d_e, int64_t n, double *d_sum, double *d_sumsq,
                     double *d_se_total, double *d_se_run, void *stream);
 int mgp_quality_finalize(const double *d_sum, const double *d_sumsq, const double *d_e, int64_t n, int64_t k,

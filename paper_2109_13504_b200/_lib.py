@@ -47,6 +47,7 @@ SIGNATURES = {
     "mgp_resample_host": (_i32, [_i32, _vp, _i32, _i64, _i32, _dbl, _u64, _i32, _i32, _i32, _i32, _vp, _vp, _i32]),
     "mgp_offspring": (_i32, [_vp, _i64, _i64, _vp, _vp, _vp]),
     "mgp_expected_offspring": (_i32, [_vp, _i32, _i64, _vp, _vp, _vp]),
+    "mgp_expected_offspring_slice": (_i32, [_vp, _i32, _i64, _i64, _dbl, _vp, _vp]),
     "mgp_quality_add": (_i32, [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
     "mgp_quality_finalize": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
     "mgp_quality_runs": (_i32, [_i32, _vp, _i32, _i64, _i32, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp,

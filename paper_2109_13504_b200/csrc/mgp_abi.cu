@@ -878,14 +878,29 @@ int mgp_expected_offspring(const void* d_w, int dtype, int64_t n, double* d_e, d
   if (dtype == MGP_F32) {
     const float* w = (const float*)d_w;
     if ((rc = pw_reduce<ElemWeight<float>, float, false>(ElemWeight<float>{w}, w, n, out, st))) return rc;
-    k_expected<float><<<grid, 256, 0, st>>>(w, n, d_total, d_e);
+    k_expected<float><<<grid, 256, 0, st>>>(w, n, (double)n, d_total, 0.0, d_e);
   } else if (dtype == MGP_F64) {
     const double* w = (const double*)d_w;
     if ((rc = pw_reduce<ElemWeight<double>, double, false>(ElemWeight<double>{w}, w, n, out, st))) return rc;
-    k_expected<double><<<grid, 256, 0, st>>>(w, n, d_total, d_e);
+    k_expected<double><<<grid, 256, 0, st>>>(w, n, (double)n, d_total, 0.0, d_e);
   } else {
     return set_err(MGP_EINVAL, "dtype must be MGP_F32 or MGP_F64");
   }
+  LAUNCH_CHECK("k_expected");
+  return 0;
+}
+
+int mgp_expected_offspring_slice(const void* d_w, int dtype, int64_t n_slice, int64_t n_all, double total,
+                                 double* d_e, void* stream) {
+  if (n_slice < 0 || n_all < 1) return set_err(MGP_EINVAL, "invalid sizes");
+  if (!(total > 0)) return set_err(MGP_EINVAL, "total weight must be positive");
+  if (n_slice == 0) return 0;
+  const unsigned grid = (unsigned)std::min<int64_t>((n_slice + 255) / 256, 148 * 16);
+  if (dtype == MGP_F32) k_expected<float><<<grid, 256, 0, S(stream)>>>((const float*)d_w, n_slice, (double)n_all,
+                                                                       nullptr, total, d_e);
+  else if (dtype == MGP_F64) k_expected<double><<<grid, 256, 0, S(stream)>>>((const double*)d_w, n_slice,
+                                                                             (double)n_all, nullptr, total, d_e);
+  else return set_err(MGP_EINVAL, "dtype must be MGP_F32 or MGP_F64");
   LAUNCH_CHECK("k_expected");
   return 0;
 }

@@ -893,10 +893,11 @@ __global__ void k_quality_accum(const CT* __restrict__ counts, int64_t n, double
 
 // expected offspring N * w / sum(w)  (M/metrics.py:55-60: len(values) * values / total)
 template <typename WT>
-__global__ void k_expected(const WT* __restrict__ w, int64_t n, const double* total, double* e) {
-  const double t = *total;
+__global__ void k_expected(const WT* __restrict__ w, int64_t n, double n_all, const double* total, double total_v,
+                           double* e) {
+  const double t = total ? *total : total_v;  // the total on the device, or given by value (sharded slices)
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    e[i] = __ddiv_rn(__dmul_rn((double)n, (double)w[i]), t);
+    e[i] = __ddiv_rn(__dmul_rn(n_all, (double)w[i]), t);
 }
 
 // ---------------------------------------------------------------------------

@@ -45,6 +45,17 @@ def slice_tree_aligned(world: int, n_local: int) -> bool:
     return world >= 1 and (world & (world - 1)) == 0 and n_local % 8 == 0 and n_local > 64
 
 
+def tree_sum(values):
+    """Combine float64 partial sums of consecutive, equally sized tree-aligned pieces in the
+    order of numpy's pairwise tree above them (adjacent pairs, level by level)."""
+    vals = [float(v) for v in values]
+    if len(vals) & (len(vals) - 1):
+        raise ValueError("tree_sum needs a power-of-two number of pieces")
+    while len(vals) > 1:
+        vals = [vals[2 * i] + vals[2 * i + 1] for i in range(len(vals) // 2)]
+    return vals[0]
+
+
 def combine_slice_stats(parts) -> WeightStats:
     """Global WeightStats from per-rank slice stats in rank order, combining the slice sums
     pairwise exactly like numpy's tree above the slices (requires a power-of-two count)."""
@@ -112,6 +123,38 @@ class CudaOps:
             1 if layout == "stripes" else 0, int(p0), int(p1), ctypes.cast(ptrs, ctypes.c_void_p), len(table),
             int(ref.shape[0]), row_bytes, D.ptr(anc), D.ptr(out), D.stream_ptr()))
         return anc, out
+
+    def offspring(self, local_idx, n_local):
+        """counts[r] = #{i: local_idx[i] == r} (ancestors_to_offspring over this rank's rows)."""
+        t = D.torch()
+        counts = t.empty(n_local, dtype=t.int64, device=local_idx.device)
+        idx = local_idx.to(t.int64).contiguous()
+        _lib.check(_lib.lib().mgp_offspring(D.ptr(idx), idx.numel(), n_local, D.ptr(counts), None, D.stream_ptr()))
+        return counts
+
+    def expected_slice(self, w_slice, n_all, total):
+        t = D.torch()
+        e = t.empty(w_slice.numel(), dtype=t.float64, device=w_slice.device)
+        _lib.check(_lib.lib().mgp_expected_offspring_slice(D.ptr(w_slice), D.wdtype(w_slice), w_slice.numel(),
+                                                           int(n_all), float(total), D.ptr(e), D.stream_ptr()))
+        return e
+
+    def quality_add(self, counts, e, acc_sum, acc_sumsq):
+        """sum += o, sum_sq += o*o over one segment; returns the segment's pairwise sum((o - e)^2)."""
+        t = D.torch()
+        se = t.zeros(2, dtype=t.float64, device=counts.device)
+        _lib.check(_lib.lib().mgp_quality_add(D.ptr(counts), D.ptr(e), counts.numel(), D.ptr(acc_sum),
+                                              D.ptr(acc_sumsq), D.ptr(se), D.ptr(se[1:]), D.stream_ptr()))
+        return float(se[1].item())
+
+    def quality_finalize(self, acc_sum, acc_sumsq, e, k):
+        """The segment's pairwise sum(sum_sq/k - mean^2) and sum((mean - e)^2)."""
+        t = D.torch()
+        out = t.empty(2, dtype=t.float64, device=acc_sum.device)
+        _lib.check(_lib.lib().mgp_quality_finalize(D.ptr(acc_sum), D.ptr(acc_sumsq), D.ptr(e), acc_sum.numel(), int(k),
+                                                   D.ptr(out), D.ptr(out[1:]), D.stream_ptr()))
+        v, bsq = out.cpu().tolist()
+        return v, bsq
 
     def gather_rows(self, states, idx):
         t = D.torch()
@@ -271,6 +314,44 @@ class ShardedResampler:
                                              peer_states)
         return anc, rows, b
 
+    def _send_to_owners(self, anc, n_local):
+        """Bucket global indices by owner rank and deliver each owner its local row indices
+        (one all-to-all of counts, one of indices).  Returns (order, send sizes, receive
+        sizes, received local indices)."""
+        t = D.torch()
+        owner, local = self._owner_local(anc, n_local)
+        order = t.argsort(owner, stable=True)
+        send_idx = local[order].contiguous()
+        send_counts = t.bincount(owner, minlength=self.world).to(t.int64)
+        recv_counts = t.empty_like(send_counts)
+        self._dist.all_to_all_single(recv_counts, send_counts, group=self.group)
+        sc, rc = send_counts.tolist(), recv_counts.tolist()
+        recv_idx = t.empty(sum(rc), dtype=t.int64, device=anc.device)
+        self._dist.all_to_all_single(recv_idx, send_idx, output_split_sizes=rc, input_split_sizes=sc,
+                                     group=self.group)
+        return order, sc, rc, recv_idx
+
+    # -- 6. offspring counts and quality (SURVEY 8e item 6) ----------------------
+    def offspring(self, anc_local, n_local: int | None = None):
+        """ancestors_to_offspring (M/resample.py:361-368) of the whole population, sharded: the
+        counts of this rank's own particles (local order).  Ancestors travel to their owners
+        (owner-bucketed all-to-all of local indices, 8 bytes per particle) and each owner
+        histograms what it received; the counts equal the single-device histogram's slice."""
+        t = D.torch()
+        n_local = anc_local.numel() if n_local is None else n_local
+        anc = anc_local.to(t.int64)
+        n_all = n_local * self.world
+        if anc.numel() and (int(anc.min()) < 0 or int(anc.max()) >= n_all):
+            raise ValueError("ancestor indices out of range")
+        if self.world == 1:
+            return self.ops.offspring(anc, n_local)
+        _, _, _, recv_idx = self._send_to_owners(anc, n_local)
+        return self.ops.offspring(recv_idx, n_local)
+
+    def quality(self, w_local):
+        """A QualityAccumulator over the sharded population (see ShardedQuality)."""
+        return ShardedQuality(self, w_local)
+
     # -- 5. particle states ---------------------------------------------------
     def exchange(self, states_local, anc_local):
         """apply_ancestors across ranks: rows anc_local[i] (global) into a fresh local array.
@@ -284,15 +365,7 @@ class ShardedResampler:
         anc = anc_local.to(device=dev, dtype=t.int64)
         if self.world == 1:
             return self.ops.gather_rows(states_local, self._owner_local(anc, n_local)[1])
-        owner, local = self._owner_local(anc, n_local)
-        order = t.argsort(owner, stable=True)
-        send_idx = local[order].contiguous()
-        send_counts = t.bincount(owner, minlength=self.world).to(t.int64)
-        recv_counts = t.empty_like(send_counts)
-        dist.all_to_all_single(recv_counts, send_counts, group=self.group)
-        sc, rc = send_counts.tolist(), recv_counts.tolist()
-        recv_idx = t.empty(sum(rc), dtype=t.int64, device=dev)
-        dist.all_to_all_single(recv_idx, send_idx, output_split_sizes=rc, input_split_sizes=sc, group=self.group)
+        order, sc, rc, recv_idx = self._send_to_owners(anc, n_local)
         rows = self.ops.gather_rows(states_local, recv_idx)
         reply = t.empty((sum(sc),) + tuple(states_local.shape[1:]), dtype=states_local.dtype, device=dev)
         dist.all_to_all_single(reply, rows.contiguous(), output_split_sizes=sc, input_split_sizes=rc,
@@ -300,6 +373,98 @@ class ShardedResampler:
         out = t.empty_like(reply)
         out[order] = reply
         return out
+
+
+class ShardedQuality:
+    """QualityAccumulator (M/metrics.py:71-110) over a population sharded like ``sr``.
+
+    Every rank keeps sum / sum_sq / expected offspring for its own particles only.  The
+    reductions over all N particles (the per-run squared error, the final variance and
+    squared bias) are numpy pairwise sums; when the ownership pieces are nodes of numpy's
+    tree (``slice_tree_aligned``, as for the B rule) each rank reduces its pieces and the
+    world's partial sums are combined in the tree's order -- bit-identical to one device's
+    accumulator over the whole population.  Other shapes all-gather the counts and run the
+    full accumulator on every rank."""
+
+    def __init__(self, sr: ShardedResampler, w_local):
+        t = D.torch()
+        self.sr = sr
+        self.n_local = w_local.numel()
+        self.n = self.n_local * sr.world
+        self.k = 0
+        self._se_total = 0.0
+        st = sr.global_stats(w_local)
+        if not st.sum > 0:  # M/metrics.py:57-59
+            raise ValueError("total weight must be positive")
+        stripes = sr.layout == "stripes"
+        unit = self.n_local // 2 if stripes else self.n_local
+        self.aligned = slice_tree_aligned(sr.world, unit) and not (stripes and self.n_local % 2)
+        self.segments = [(0, unit), (unit, self.n_local)] if stripes else [(0, self.n_local)]
+        if self.aligned:
+            self._e = sr.ops.expected_slice(w_local.contiguous(), self.n, st.sum)
+            self._sum = t.zeros(self.n_local, dtype=t.float64, device=w_local.device)
+            self._sum_sq = t.zeros_like(self._sum)
+        else:
+            full = sr.replicate_weights(w_local)
+            self._e = sr.ops.expected_slice(full, self.n, st.sum)
+            self._sum = t.zeros(self.n, dtype=t.float64, device=w_local.device)
+            self._sum_sq = t.zeros_like(self._sum)
+
+    def _combine(self, parts):
+        """Partial sums, one per (rank, segment), into numpy's whole-array sum."""
+        t = D.torch()
+        mine = t.tensor(parts, dtype=t.float64, device=self._sum.device).reshape(-1)
+        rows = t.empty(self.sr.world * mine.numel(), dtype=t.float64, device=mine.device)
+        self.sr._gather_into(rows, mine)
+        per = rows.view(self.sr.world, len(parts), -1).cpu().numpy()
+        if len(self.segments) == 1:
+            return [tree_sum(per[:, 0, c]) for c in range(per.shape[2])]
+        return [tree_sum([tree_sum(per[:, 0, c]), tree_sum(per[:, 1, c])]) for c in range(per.shape[2])]
+
+    def _global_counts(self, counts_local):
+        """Counts of the whole population in global particle order (unaligned shapes)."""
+        t = D.torch()
+        every = t.empty(self.n, dtype=t.int64, device=counts_local.device)
+        if self.sr.layout == "contiguous":
+            self.sr._gather_into(every, counts_local.contiguous())
+            return every
+        h, half = self.n_local // 2, self.n // 2
+        self.sr._gather_into(every[:half], counts_local[:h].contiguous())
+        self.sr._gather_into(every[half:], counts_local[h:].contiguous())
+        return every
+
+    def add(self, counts_local) -> None:
+        """One run: ``counts_local`` = this rank's slice of the offspring vector (e.g. from
+        ``ShardedResampler.offspring``)."""
+        t = D.torch()
+        o = counts_local.to(device=self._sum.device, dtype=t.int64).contiguous()
+        if o.numel() != self.n_local:
+            raise ValueError(f"length mismatch: {o.numel()} offspring vs {self.n_local} local weights")
+        ops = self.sr.ops
+        if self.aligned:
+            se = [ops.quality_add(o[a:b], self._e[a:b], self._sum[a:b], self._sum_sq[a:b]) for a, b in self.segments]
+            run = self._combine([[v] for v in se])[0]
+        else:
+            run = ops.quality_add(self._global_counts(o), self._e, self._sum, self._sum_sq)
+        self.k += 1
+        self._se_total += float(run)
+
+    def finalize(self):
+        from .metrics import QualityStats
+
+        if self.k < 2:
+            raise ValueError(f"need at least 2 runs to estimate variance, got {self.k}")
+        ops = self.sr.ops
+        if self.aligned:
+            parts = [list(ops.quality_finalize(self._sum[a:b], self._sum_sq[a:b], self._e[a:b], self.k))
+                     for a, b in self.segments]
+            variance, bias_sq = self._combine(parts)
+        else:
+            variance, bias_sq = ops.quality_finalize(self._sum, self._sum_sq, self._e, self.k)
+        mse = self._se_total / self.k
+        contribution = bias_sq / mse if mse > 0 else 0.0
+        return QualityStats(mse=mse, variance=float(variance), bias_sq=float(bias_sq),
+                            bias_contribution=contribution, mse_per_particle=mse / self.n)
 
 
 class PeerRows:

@@ -8,8 +8,10 @@ and by the peer-gather GPU test below.
 """
 
 import os
+import queue
 import socket
 import sys
+import time
 
 import numpy as np
 import pytest
@@ -79,6 +81,22 @@ class OracleOps:
                 owner, local = divmod(a, n_local)
             rows.append(peer_states[owner][local])
         return anc, torch.stack(rows)
+
+    def offspring(self, local_idx, n_local):
+        return torch.from_numpy(np.bincount(local_idx.numpy(), minlength=n_local).astype(np.int64))
+
+    def expected_slice(self, w_slice, n_all, total):  # M/metrics.py:55-60 on a slice
+        return torch.from_numpy(n_all * np.asarray(w_slice.numpy(), dtype=np.float64) / total)
+
+    def quality_add(self, counts, e, acc_sum, acc_sumsq):  # M/metrics.py:86-93 on a segment
+        o = counts.numpy().astype(np.float64)
+        acc_sum += torch.from_numpy(o)
+        acc_sumsq += torch.from_numpy(o * o)
+        return float(((o - e.numpy()) ** 2).sum())
+
+    def quality_finalize(self, acc_sum, acc_sumsq, e, k):  # M/metrics.py:95-110 on a segment
+        mean = acc_sum.numpy() / k
+        return float((acc_sumsq.numpy() / k - mean * mean).sum()), float(((mean - e.numpy()) ** 2).sum())
 
     def gather_rows(self, states, idx):
         return states[idx]
@@ -160,6 +178,35 @@ def _worker(rank, world, port, case, q):
         dist.destroy_process_group()
 
 
+def _worker_quality(rank, world, port, case, q):
+    """K runs of the sharded resampler -> sharded offspring -> ShardedQuality, against the
+    reference's own single-process QualityAccumulator arithmetic (numpy) on the same runs."""
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle
+        from paper_2109_13504_b200.distributed import ShardedResampler
+
+        layout, n_local, y, rng, runs = case
+        n = n_local * world
+        w_full = oracle.gen_gaussian_weights(y, n, 4545, "single")
+        sr = ShardedResampler(rng=rng, ops=OracleOps(), layout=layout)
+        idx = np.concatenate([np.arange(lo, hi) for lo, hi in sr.owned(n_local)])
+        w_local = torch.from_numpy(w_full[idx].copy())
+        acc = sr.quality(w_local)
+        for k in range(runs):
+            anc_local, _ = sr.resample(w_local, b=7, seed=1000 + k)
+            counts = sr.offspring(anc_local)
+            acc.add(counts)
+        st = acc.finalize()
+        if rank == 0:
+            q.put((acc.aligned, st))
+    finally:
+        dist.destroy_process_group()
+
+
 def _run(world, case, target=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -167,10 +214,20 @@ def _run(world, case, target=None):
     procs = [ctx.Process(target=target or _worker, args=(r, world, port, case, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = q.get(timeout=300)
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    res, t0 = None, time.time()
+    try:
+        while res is None and time.time() - t0 < 300:
+            try:
+                res = q.get(timeout=1)
+            except queue.Empty:
+                if any(p.exitcode not in (None, 0) for p in procs):
+                    break
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.exitcode is None:
+                p.kill()
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     return res
 
 
@@ -237,3 +294,33 @@ def test_stripes_layout_equals_single_process(oracle, world, case):
     states_full = np.stack([np.arange(n) * 1.5, np.arange(n)], axis=1)
     assert np.array_equal(states, states_full[ref])
 
+
+
+@pytest.mark.parametrize("world,case", [
+    (2, ("contiguous", 256, 2.0, "philox", 3)),
+    (4, ("stripes", 256, 3.0, "megores", 3)),
+    (2, ("stripes", 512, 1.0, "philox", 2)),
+    (2, ("contiguous", 48, 2.0, "megores", 3)),  # not tree-aligned: the all-gather route
+])
+def test_sharded_offspring_quality(oracle, world, case):
+    """ShardedResampler.offspring + ShardedQuality equal the reference's QualityAccumulator
+    (M/metrics.py:71-110, numpy) over the same K runs of the whole population, bit for bit."""
+    layout, n_local, y, rng, runs = case
+    aligned, st = _run(world, case, _worker_quality)
+    assert aligned == (n_local >= 128 or (layout == "contiguous" and n_local > 64))
+    n = n_local * world
+    w_full = oracle.gen_gaussian_weights(y, n, 4545, "single")
+    v = w_full.astype(np.float64)
+    e = len(v) * v / v.sum()
+    s1, s2, se = np.zeros(n), np.zeros(n), 0.0
+    for k in range(runs):
+        o = np.bincount(oracle.resample("megopolis", w_full, 7, 1000 + k, 32, None, True, rng),
+                        minlength=n).astype(np.float64)
+        s1 += o
+        s2 += o * o
+        se += float(((o - e) ** 2).sum())
+    mean = s1 / runs
+    assert st.mse == se / runs
+    assert st.variance == float((s2 / runs - mean * mean).sum())
+    assert st.bias_sq == float(((mean - e) ** 2).sum())
+    assert st.mse_per_particle == st.mse / n

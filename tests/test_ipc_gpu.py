@@ -9,7 +9,9 @@ maps NVLink peer memory on a multi-GPU node).  Then, per rank:
   ancestor's state row from its owner's mapped array inside the resampling kernel), both
   ownership layouts, must equal the oracle's ancestors and ``states_full[ancestors]``;
 * ``gather_from_peers`` (mgp_gather_peers) must agree with it;
-* the all-to-all ``exchange`` must agree with both.
+* the all-to-all ``exchange`` must agree with both;
+* ``ShardedResampler.offspring`` + ``ShardedQuality`` over two runs must equal the reference's
+  QualityAccumulator arithmetic on the whole population, bit for bit.
 """
 
 from __future__ import annotations
@@ -72,6 +74,12 @@ def _worker(rank, world, port, case, q):
         if layout == "contiguous":
             assert torch.equal(gather_from_peers(peers, n_local, anc), rows)
         assert torch.equal(sr.exchange(s_local, anc), rows)
+        # sharded offspring counts and quality over two runs (seeds 2021, 2022)
+        acc = sr.quality(w_local)
+        acc.add(sr.offspring(anc))
+        anc2, _ = sr.resample(w_local, b=b, seed=2022)
+        acc.add(sr.offspring(anc2))
+        qst = acc.finalize()
         torch.cuda.synchronize()
         dist.barrier()  # every rank done reading before anyone unmaps / frees
         peers.close()
@@ -87,7 +95,7 @@ def _worker(rank, world, port, case, q):
             else:
                 a = torch.cat(parts).numpy()
                 st = torch.cat(news).numpy()
-            q.put((int(b_used), a, st))
+            q.put((int(b_used), a, st, qst))
     finally:
         dist.destroy_process_group()
 
@@ -123,7 +131,7 @@ def test_peer_rows_resample_gather(oracle, world, case):
             if p.exitcode is None:
                 p.kill()
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
-    b_used, anc, st = res
+    b_used, anc, st, qst = res
     n = n_local * world
     w_full = oracle.gen_gaussian_weights(3.0, n, 777, "single")
     if b is None:
@@ -133,3 +141,12 @@ def test_peer_rows_resample_gather(oracle, world, case):
     assert np.array_equal(anc, ref)
     states_full = np.stack([np.arange(n) * 0.5, -np.arange(n, dtype=np.float64)], 1)
     assert np.array_equal(st, states_full[ref])
+    # ShardedQuality == the reference's QualityAccumulator arithmetic (M/metrics.py:71-110)
+    ref2 = oracle.resample(kind, w_full, b_used, 2022, 32, 256 if kind in ("c1", "c2") else None, True, rng)
+    v = w_full.astype(np.float64)
+    e = n * v / v.sum()
+    o1, o2 = (np.bincount(r, minlength=n).astype(np.float64) for r in (ref, ref2))
+    mean = (o1 + o2) / 2
+    assert qst.mse == (float(((o1 - e) ** 2).sum()) + float(((o2 - e) ** 2).sum())) / 2
+    assert qst.variance == float(((o1 * o1 + o2 * o2) / 2 - mean * mean).sum())
+    assert qst.bias_sq == float(((mean - e) ** 2).sum())

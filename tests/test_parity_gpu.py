@@ -410,6 +410,17 @@ def test_sharded_resampler_cuda_ops_single_rank(mg, oracle):
             st2 = torch.stack([st, -st], 1)
             anc2, rows, b2 = sr.resample_gather(torch.from_numpy(w).cuda(), [st2], seed=31)
             assert b2 == b and torch.equal(anc2, anc) and torch.equal(rows, st2[anc])
+            # sharded offspring + quality on one rank == the single-device accumulator
+            wv = torch.from_numpy(w).cuda()
+            acc, ref_acc = sr.quality(wv), mg.QualityAccumulator(1 << 16)
+            for s in (31, 32, 33):
+                a, _ = sr.resample(wv, seed=s)
+                c = sr.offspring(a)
+                if layout == "contiguous":
+                    assert torch.equal(c, mg.ancestors_to_offspring(a, 1 << 16))
+                acc.add(c)
+                ref_acc.add(mg.ancestors_to_offspring(mg.megopolis(w, b, seed=s), 1 << 16), w)
+            assert acc.aligned and acc.finalize() == ref_acc.finalize()
     finally:
         dist.destroy_process_group()
 
