@@ -106,6 +106,7 @@ def _worker(rank, world, port, case, q):
     (4, ("megopolis", "stripes", 4096, "megores", 7)),
     (2, ("c2", "contiguous", 4096, "megores", 5)),
     (2, ("metropolis", "stripes", 2048, "philox", 4)),
+    (2, ("megopolis", "stripes", 1 << 23, "philox", None)),  # N = 2^24 (config 4), B from the rule
 ])
 def test_peer_rows_resample_gather(oracle, world, case):
     import torch.multiprocessing as mp
