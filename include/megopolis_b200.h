@@ -179,6 +179,18 @@ int mgp_gather(const void *d_states, int64_t row_bytes, const int64_t *d_anc, in
 int mgp_gather_peers(const void *const *peer_states, int npeers, int64_t n_local, int64_t row_bytes,
                      const int64_t *d_anc, int64_t n, void *d_out, void *stream);
 
+/* Comparison-index replay (comparison_indices, M/resample.py:384-428): d_out[r * n + i] = the
+ * weight index particle i reads at round r, for kind 0-3, reference (megores) stream; B x N int64.
+ * word_bytes is WarpConfig.word_bytes (the C1/C2 partition width is partition_bytes / word_bytes). */
+int mgp_comparison_indices(int kind, int64_t n, int32_t b, uint64_t seed, int32_t warp, int32_t partition_bytes,
+                           int32_t word_bytes, int64_t *d_out, void *stream);
+/* The warp transaction model (traffic_report, M/warpsim.py:94-111) over a rows x width trace of
+ * word indices, groups of `warp` consecutive entries of a row: d_out[0] = total transactions
+ * (distinct aligned segments per group, summed), d_out[1] = the largest per-group count,
+ * d_out[2] = unnecessary words (segments * words_per_segment - distinct words, summed). */
+int mgp_traffic_report(const int64_t *d_idx, int64_t rows, int64_t width, int32_t warp, int32_t word_bytes,
+                       int32_t segment_bytes, int64_t *d_out, void *stream);
+
 /* Peer mappings for the two entry points above (CUDA IPC; no reference counterpart -- the
  * reference is single-process).  mgp_ipc_export: the 64-byte cudaIpcMemHandle_t of the
  * allocation holding d_ptr and d_ptr's offset in it.  mgp_ipc_open (in another process,

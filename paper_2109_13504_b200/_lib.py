@@ -55,6 +55,8 @@ SIGNATURES = {
     "mgp_squared_error": (_i32, [_vp, _vp, _i64, _vp, _vp]),
     "mgp_gather": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp]),
     "mgp_gather_peers": (_i32, [_vp, _i32, _i64, _i64, _vp, _i64, _vp, _vp]),
+    "mgp_comparison_indices": (_i32, [_i32, _i64, _i32, _u64, _i32, _i32, _i32, _vp, _vp]),
+    "mgp_traffic_report": (_i32, [_vp, _i64, _i64, _i32, _i32, _i32, _vp, _vp]),
     "mgp_ipc_export": (_i32, [_vp, _vp, _vp]),
     "mgp_ipc_open": (_i32, [_vp, _i64, _vp]),
     "mgp_ipc_close": (_i32, [_vp, _i64]),

@@ -139,6 +139,30 @@ def quality_grid(spec: ExperimentSpec, rng_stream: str = "megores"):
     return rows
 
 
+def traffic_grid(spec: ExperimentSpec):
+    """Transaction-model rows for the Metropolis-family algorithms (M/bench.py:152-178)."""
+    from .resample import WarpConfig
+    from .warpsim import rng_draws_per_iteration, trace_algorithm, traffic_report
+    from .weights import WeightVector
+
+    rows = []
+    warp = WarpConfig()
+    for token in spec.algorithms:
+        name, part_bytes = algorithm_token(token)
+        if name in ("multinomial", "systematic"):
+            continue
+        for n in spec.n_grid:
+            w = WeightVector(np.ones(n), spec.precision)
+            report = traffic_report(trace_algorithm(name, w, spec.traffic_b, warp, part_bytes, spec.seed))
+            rows.append({"algorithm": token, "n": n, "b": spec.traffic_b,
+                         "partition_bytes": part_bytes if part_bytes is not None else "", "seed": spec.seed,
+                         "mean_transactions": report.per_iteration_mean, "max_transactions": report.per_warp_max,
+                         "total_transactions": report.total_transactions,
+                         "unnecessary_words": report.unnecessary_words,
+                         "rng_draws_per_iteration": rng_draws_per_iteration(name)})
+    return rows
+
+
 def pf_grid(spec: ExperimentSpec):
     """Filter-benchmark rows (RMSE) and the timing sidecar (resample ratio), M/bench.py:181-204."""
     from .pfilter import FilterConfig, generate_trajectory, run_benchmark
@@ -293,8 +317,8 @@ def run(args) -> int:
         wd = np.asarray(w.values, dtype=np.float64)
         print(f"wrote {spec.out}: n={args.n} mean={wd.mean():.6g} max={wd.max():.6g} ratio={wd.mean() / wd.max():.6g}")
     elif cmd == "traffic":
-        raise ValueError("traffic is the reference's analytical transaction model (megores.warpsim); the B200 "
-                         "backend measures sectors per request with ncu instead (DESIGN.md section 4)")
+        write_csv(spec.out, traffic_grid(spec))
+        print(f"wrote {spec.out}")
     return 0
 
 

@@ -1121,6 +1121,57 @@ int mgp_estimate_ratio_stats(const void* d_w, int dtype, int64_t n, int64_t subs
   return rc;
 }
 
+int mgp_comparison_indices(int kind, int64_t n, int32_t b, uint64_t seed, int32_t warp, int32_t partition_bytes,
+                           int32_t word_bytes, int64_t* d_out, void* stream) {
+  if (kind < MGP_KIND_METROPOLIS || kind > MGP_KIND_MEGOPOLIS)
+    return set_err(MGP_EINVAL, "unknown Metropolis-family resampler kind %d", kind);
+  if (n < 1) return set_err(MGP_EINVAL, "n must be >= 1, got %lld", (long long)n);
+  if (b < 0) return set_err(MGP_EINVAL, "B must be >= 0, got %d", b);
+  if (warp < 1) return set_err(MGP_EINVAL, "warp_size must be positive, got %d", warp);
+  int64_t n_w = 0, n_part = 0;
+  if (kind == MGP_KIND_C1 || kind == MGP_KIND_C2) {  // PartitionConfig (M/resample.py:78-93)
+    if (partition_bytes < 1 || word_bytes < 1 || partition_bytes % word_bytes)
+      return set_err(MGP_EINVAL, "partition_bytes must be a positive multiple of word_bytes");
+    n_w = partition_bytes / word_bytes;
+    if (n % n_w) return set_err(MGP_EINVAL, "N=%lld is not divisible by the partition width %lld", (long long)n,
+                                (long long)n_w);
+    n_part = n / n_w;
+  }
+  if (b == 0) return 0;
+  cudaStream_t st = S(stream);
+  Scratch sc(st);
+  int64_t* d_off = nullptr;
+  if (kind == MGP_KIND_MEGOPOLIS) {  // megopolis_offsets (M/resample.py:263-265), host like the resampler
+    std::vector<int64_t> off((size_t)b);
+    offsets_host(seed, n, b, MGP_RNG_MEGORES, off.data());
+    CUDA_TRY(sc.alloc(&d_off, sizeof(int64_t) * b));
+    CUDA_TRY(cudaMemcpyAsync(d_off, off.data(), sizeof(int64_t) * b, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaStreamSynchronize(st));  // the host vector goes out of scope
+  }
+  const unsigned grid = (unsigned)std::min<int64_t>(((int64_t)b * n + 255) / 256, 148 * 32);
+  k_comparison_indices<<<grid, 256, 0, st>>>(kind, n, b, megores_base(seed), warp, n_w, n_part, d_off, d_out);
+  LAUNCH_CHECK("k_comparison_indices");
+  return 0;
+}
+
+int mgp_traffic_report(const int64_t* d_idx, int64_t rows, int64_t width, int32_t warp, int32_t word_bytes,
+                       int32_t segment_bytes, int64_t* d_out, void* stream) {
+  if (rows < 0 || width < 0) return set_err(MGP_EINVAL, "negative trace shape");
+  if (warp < 1 || warp > 4096) return set_err(MGP_EINVAL, "warp_size must be in [1, 4096], got %d", warp);
+  if (word_bytes < 1 || segment_bytes % word_bytes)
+    return set_err(MGP_EINVAL, "segment_bytes must be a positive multiple of word_bytes");
+  if (width % warp)
+    return set_err(MGP_EINVAL, "trace width %lld is not a multiple of the warp size %d", (long long)width, warp);
+  cudaStream_t st = S(stream);
+  CUDA_TRY(cudaMemsetAsync(d_out, 0, 3 * sizeof(int64_t), st));
+  const int64_t groups = rows * (width / warp);
+  if (groups == 0) return 0;
+  const unsigned grid = (unsigned)std::min<int64_t>((groups + 255) / 256, 148 * 8);
+  k_traffic<<<grid, 256, 0, st>>>(d_idx, groups, warp, word_bytes, segment_bytes, (unsigned long long*)d_out);
+  LAUNCH_CHECK("k_traffic");
+  return 0;
+}
+
 int mgp_gen_gaussian(double y, int64_t n, uint64_t seed, int dtype, void* d_out, void* stream) {
   if (y < 0) return set_err(MGP_EINVAL, "y must be >= 0, got %.17g", y);
   if (n < 1) return set_err(MGP_EINVAL, "n must be >= 1, got %lld", (long long)n);

@@ -944,6 +944,79 @@ __global__ void k_gather_peers(const __grid_constant__ PeerTable peers, int npee
 }
 
 // ---------------------------------------------------------------------------
+// Comparison-index replay and the warp transaction model (M/resample.py:384-428,
+// M/warpsim.py:62-111).  k_comparison_indices writes the weight index particle i reads
+// at round r (row-major [B][N]) with the resamplers' own draw conventions (reference
+// stream); k_traffic counts, for every W-wide group of one row, the distinct aligned
+// segments (transactions) and distinct words it touches.
+
+enum { TR_METROPOLIS = 0, TR_C1 = 1, TR_C2 = 2, TR_MEGOPOLIS = 3 };
+
+__global__ void k_comparison_indices(int kind, int64_t n, int32_t b, uint64_t base, int64_t warp, int64_t n_w,
+                                     int64_t n_part, const int64_t* __restrict__ off, int64_t* __restrict__ out) {
+  const int64_t total = (int64_t)b * n;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / n, i = t - r * n;
+    int64_t j;
+    if (kind == TR_MEGOPOLIS) {  // (i - i%W + o - o%W + (i + o)%W) mod N
+      const int64_t o = off[r];
+      j = (i - i % warp + o - o % warp + (i + o) % warp) % n;
+    } else {
+      const int64_t local = below_from_hash(mix64(megores_key(base, (uint64_t)i, 2ull * (uint64_t)r + 1)),
+                                            kind == TR_METROPOLIS ? n : n_w);
+      if (kind == TR_METROPOLIS) {
+        j = local;
+      } else {  // partition of the particle's logical warp: drawn once (C1) or per round (C2)
+        const uint64_t wl = WARP_LANE_BASE + (uint64_t)(i / warp);
+        const int64_t p = below_from_hash(mix64(megores_key(base, wl, kind == TR_C1 ? 0ull : (uint64_t)r)), n_part);
+        j = p * n_w + local;
+      }
+    }
+    out[t] = j;
+  }
+}
+
+__device__ __forceinline__ int64_t floor_div(int64_t a, int64_t d) {  // d > 0; numpy's //
+  const int64_t q = a / d;
+  return q - ((a % d) < 0);
+}
+
+__global__ void k_traffic(const int64_t* __restrict__ idx, int64_t groups, int32_t w, int32_t word_bytes,
+                          int32_t seg_bytes, unsigned long long* __restrict__ acc) {
+  const int64_t wps = seg_bytes / word_bytes;
+  unsigned long long tot = 0, waste = 0, mx = 0;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t* row = idx + g * w;
+    int64_t segs = 0, words = 0;
+    for (int a = 0; a < w; ++a) {  // an element is new if no earlier one of the group matches it
+      const int64_t va = row[a], sa = floor_div(va * word_bytes, seg_bytes);
+      bool new_word = true, new_seg = true;
+      for (int c = 0; c < a && (new_word || new_seg); ++c) {
+        const int64_t vc = row[c];
+        new_word &= vc != va;
+        new_seg &= floor_div(vc * word_bytes, seg_bytes) != sa;
+      }
+      segs += new_seg;
+      words += new_word;
+    }
+    tot += (unsigned long long)segs;
+    waste += (unsigned long long)(segs * wps - words);
+    mx = segs > (int64_t)mx ? (unsigned long long)segs : mx;
+  }
+  for (int s = 16; s; s >>= 1) {
+    tot += __shfl_xor_sync(0xffffffffu, tot, s);
+    waste += __shfl_xor_sync(0xffffffffu, waste, s);
+    const unsigned long long o = __shfl_xor_sync(0xffffffffu, mx, s);
+    mx = o > mx ? o : mx;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&acc[0], tot);
+    atomicMax(&acc[1], mx);
+    atomicAdd(&acc[2], waste);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Synthetic Gaussian-family weights on the device (M/weights.py:100-104 with the
 // Box-Muller draw of M/rng.py:152-161).  Same formula and stream; libm rounding of
 // exp/log/cos may differ from the host's in the last float64 bit.

@@ -311,3 +311,25 @@ def apply_ancestors(states, ancestors):
     if host:
         return out.cpu().numpy().view(s_np.dtype).reshape(s_np.shape)
     return out
+
+
+def comparison_indices(kind: str, n: int, b: int, seed, warp: WarpConfig = WarpConfig(),
+                       partition_bytes: int | None = None, device: bool = False):
+    """The (B, N) matrix of weight indices each resampler reads, per round (M/resample.py:384-428).
+
+    Entry [r, i] is the index particle i compares against at round r, from the kernels' own
+    draw conventions (reference stream), computed on the device (mgp_comparison_indices).
+    Returns ``np.int64`` like the reference, or the CUDA tensor with ``device=True``."""
+    D.require_cuda()
+    t = D.torch()
+    if kind not in METROPOLIS_FAMILY:
+        raise ValueError(f"unknown Metropolis-family resampler {kind!r}")
+    if kind in ("c1", "c2"):
+        if partition_bytes is None:
+            raise ValueError(f"{kind} requires a partition size")
+        PartitionConfig(partition_bytes).n_partitions(n, warp)
+    out = t.empty((int(b), int(n)), dtype=t.int64, device="cuda")
+    _lib.check(_lib.lib().mgp_comparison_indices(_lib.KIND[kind], int(n), int(b), int(np.uint64(seed)),
+                                                 int(warp.warp_size), int(partition_bytes or 0),
+                                                 int(warp.word_bytes), D.ptr(out), D.stream_ptr()))
+    return out if device else out.cpu().numpy()

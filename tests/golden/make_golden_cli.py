@@ -31,15 +31,24 @@ CASES = {
                   "--trajectories", "2", "--runs", "2", "--t-steps", "20", "--seed", "5", "--out", "{out}"],
                  ["{out}", "{out}.timings.csv"]),
 }
+CASES.update({
+    "traffic_desk": (["traffic", "--algorithms", "megopolis,metropolis,c1:128,c2:128,c1:2048,systematic",
+                      "--n-grid", "1024,4096,65536", "--b", "8", "--seed", "13", "--out", "{out}"], ["{out}"]),
+    "traffic_small": (["traffic", "--algorithms", "metropolis,c2:256,megopolis", "--n-grid", "64,256",
+                       "--b", "32", "--seed", "3", "--out", "{out}"], ["{out}"]),
+})
 PLOT = ("plot_mse", ["plotdata", "--results", "{dir}/quality_single", "--figure", "mse-vs-N", "--out", "{out}"])
 
 
-def main():
+def main(only=None):
+    """Regenerate every case, or only the named ones (``python make_golden_cli.py traffic_desk``)."""
     from megores import bench
 
     os.makedirs(OUT, exist_ok=True)
     with tempfile.TemporaryDirectory() as tmp:
         for name, (argv, files) in list(CASES.items()) + [(PLOT[0], (PLOT[1], ["{out}"]))]:
+            if only and name not in only:
+                continue
             out = os.path.join(tmp, name)
             rc = bench.main([a.format(out=out, dir=OUT) for a in argv])
             assert rc == 0, (name, rc)
@@ -50,4 +59,4 @@ def main():
 
 
 if __name__ == "__main__":
-    sys.exit(main())
+    sys.exit(main(sys.argv[1:]))

@@ -2,7 +2,7 @@
 files (tests/golden/cli/, made by tests/golden/make_golden_cli.py from the unmodified
 ``megores`` console script, M/bench.py).
 
-* quality grids: byte-identical CSVs (bit-exact weights, B rule, resamplers, offspring and
+* quality and traffic grids: byte-identical CSVs (bit-exact weights, B rule, resamplers, offspring and
   quality statistics, and the same float formatting);
 * gen-weights and plotdata: byte-identical files (CPU only);
 * pf: identical rows up to the filter's libm-rounded stages (rtol 1e-6, DESIGN.md §8a);
@@ -53,8 +53,8 @@ def test_plotdata_byte_identical(tmp_path):
 
 
 def test_cli_errors(tmp_path, capsys):
-    assert cli.main(["traffic", "--out", str(tmp_path / "t.csv")]) == 2
-    assert "megores: error:" in capsys.readouterr().err
+    assert cli.main(["traffic", "--algorithms", "c7", "--out", str(tmp_path / "t.csv")]) == 2
+    assert "megores: error: unknown algorithm 'c7'" in capsys.readouterr().err
     cfg = tmp_path / "c.json"
     cfg.write_text(json.dumps({"k_runs": 4, "bogus": 1}))
     assert cli.main(["quality", "--config", str(cfg), "--out", str(tmp_path / "q.csv")]) == 2
@@ -72,7 +72,7 @@ def test_module_entry_point(tmp_path):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["quality_single", "quality_double_gamma"])
+@pytest.mark.parametrize("name", ["quality_single", "quality_double_gamma", "traffic_desk", "traffic_small"])
 def test_quality_byte_identical(tmp_path, name):
     argv, _ = CASES[name]
     rc, out = run_cli(argv, tmp_path, name)

@@ -2,8 +2,7 @@
 the B200 implementation through its public API.
 
 Mirrors pkg/tests/test_resample.py (T/test_resample.py) and the acceptance criteria of
-pkg/tests/test_acceptance.py (1-7 and 9-12; 8 is the analytical traffic model, which the
-B200 build replaces with ncu counters) with the same fixtures (T/conftest.py:15-44),
+pkg/tests/test_acceptance.py (criteria 1-12) with the same fixtures (T/conftest.py:15-44),
 thresholds and seeds.
 """
 
@@ -242,6 +241,24 @@ def test_criterion_07_proposition_oracle(m):
     emp = hits.mean()
     stderr = hits.std(ddof=1) / np.sqrt(trials)
     assert abs(emp - p) <= 3 * stderr and emp >= vals[heavy] / vals.sum() - 0.05
+
+
+def test_criterion_08_traffic_model_exactness(m):  # T/test_acceptance.py:205-229
+    from paper_2109_13504_b200.warpsim import count_transactions, trace_algorithm, traffic_report
+
+    warp = m.WarpConfig()
+    trace = trace_algorithm("megopolis", m.WeightVector(np.ones(2**12), "double"), 8, warp, None, 81)
+    grouped = trace.indices.reshape(8, -1, 32)
+    rep = traffic_report(trace)  # every (round, warp) group needs exactly 4 segments
+    assert rep.per_warp_max == 4 and rep.total_transactions == 4 * 8 * (2**12 // 32)
+    worked = (count_transactions(np.arange(32), warp), count_transactions(np.arange(0, 64, 2), warp),
+              count_transactions(np.arange(1, 33), warp), count_transactions(grouped[0, 0], warp))
+    assert worked == (4, 8, 5, 4)
+    w20 = m.WeightVector(np.ones(2**20), "double")
+    means = {kind: traffic_report(trace_algorithm(kind, w20, 2, warp, part, 82)).per_iteration_mean
+             for kind, part in (("megopolis", None), ("c1", 2048), ("c2", 2048), ("metropolis", None))}
+    assert means["megopolis"] < means["c1"] < means["metropolis"]
+    assert means["megopolis"] < means["c2"] < means["metropolis"]
 
 
 def test_criterion_09_megopolis_structural_invariants(m):
