@@ -66,6 +66,13 @@ acc = mg.QualityAccumulator(4096)
 acc.add_runs("megopolis", mg.WeightVector(wq, "single"), 5, [1, 2, 3])
 mg.estimate_ratio(mg.WeightVector(wq, "single"), 1000, 7)
 mg.systematic_oracle(mg.WeightVector(wq, "single"), 0.25)
+# transaction model: comparison-index replay (all kinds, W 32 and 7) and segment counting
+from paper_2109_13504_b200.warpsim import count_transactions, trace_algorithm, traffic_report  # noqa: E402
+
+for kind, part in (("megopolis", None), ("metropolis", None), ("c1", 128), ("c2", 256)):
+    traffic_report(trace_algorithm(kind, mg.WeightVector(np.ones(2048), "double"), 5, mg.WarpConfig(), part, 3))
+mg.comparison_indices("megopolis", 700, 3, 1, mg.WarpConfig(7))
+count_transactions(np.arange(-5, 60, 3))
 traj = pf.generate_trajectory(3, 0.0, 1)
 pf.run_filter(pf.FilterConfig(n_particles=8192, b_fixed=None), traj, 2)
 torch.cuda.synchronize()
