@@ -8,6 +8,9 @@
 ``make_resampler`` resolves ``metropolis``/``megopolis``/... from
 ``megores.resample`` globals at call time (M/resample.py:441-454), so both
 namespaces are patched.  Host inputs keep returning ``np.int64`` ancestors.
+``traffic=True`` also routes the transaction model (``comparison_indices``,
+``trace_algorithm``, ``traffic_report``, ``count_transactions``) in every module that bound
+it: ``megores``, ``megores.resample``, ``megores.warpsim`` and ``megores.bench``.
 """
 
 from __future__ import annotations
@@ -25,18 +28,28 @@ PATCHED = {
 }
 
 
-def install(megores_module, offspring: bool = False):
-    """Patch ``megores`` and ``megores.resample`` in place; returns the originals."""
+def install(megores_module, offspring: bool = False, traffic: bool = False):
+    """Patch ``megores`` and its submodules in place; returns the originals."""
     import importlib
 
-    res_mod = importlib.import_module(megores_module.__name__ + ".resample")
+    mods = [megores_module, importlib.import_module(megores_module.__name__ + ".resample")]
     saved = {}
     names = dict(PATCHED)
     if offspring:
         names["ancestors_to_offspring"] = _r.ancestors_to_offspring
         names["apply_ancestors"] = _r.apply_ancestors
+    if traffic:
+        from . import warpsim as _w
+
+        names.update(comparison_indices=_r.comparison_indices, trace_algorithm=_w.trace_algorithm,
+                     traffic_report=_w.traffic_report, count_transactions=_w.count_transactions)
+        for sub in (".warpsim", ".bench"):
+            try:
+                mods.append(importlib.import_module(megores_module.__name__ + sub))
+            except ImportError:
+                pass
     for name, fn in names.items():
-        for mod in (megores_module, res_mod):
+        for mod in mods:
             if hasattr(mod, name):
                 saved[(mod.__name__, name)] = getattr(mod, name)
                 setattr(mod, name, fn)

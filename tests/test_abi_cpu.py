@@ -189,18 +189,29 @@ def test_shim_patches_both_namespaces(tmp_path, monkeypatch):
         "        return lambda w, b, seed: megopolis(w, b, seed)\n"
         "    return lambda w, b, seed: metropolis(w, b, seed)\n")
     (pkg / "__init__.py").write_text("from .resample import (metropolis, metropolis_c1, metropolis_c2, megopolis,\n"
-                                     "    ancestors_to_offspring, apply_ancestors, make_resampler)\n")
+                                     "    ancestors_to_offspring, apply_ancestors, make_resampler)\n"
+                                     "from .warpsim import traffic_report, count_transactions\n")
+    (pkg / "warpsim.py").write_text("def trace_algorithm(*a, **k): return 'cpu'\n"
+                                    "def traffic_report(*a, **k): return 'cpu'\n"
+                                    "def count_transactions(*a, **k): return 'cpu'\n")
+    (pkg / "bench.py").write_text("from .warpsim import trace_algorithm, traffic_report\n")
     monkeypatch.syspath_prepend(str(tmp_path))
     fm = importlib.import_module("fake_megores")
-    saved = shim.install(fm, offspring=True)
+    saved = shim.install(fm, offspring=True, traffic=True)
     try:
         assert fm.megopolis is R.megopolis and fm.resample.megopolis is R.megopolis
         assert fm.metropolis_c2 is R.metropolis_c2 and fm.resample.apply_ancestors is R.apply_ancestors
         # make_resampler (resolved at call time) now reaches the B200 function
         fn = fm.make_resampler("megopolis")
         assert fn.__code__.co_names[0] == "megopolis" and fm.resample.megopolis is R.megopolis
+        from paper_2109_13504_b200 import warpsim as W
+
+        bench = sys.modules["fake_megores.bench"]
+        assert fm.traffic_report is W.traffic_report and fm.warpsim.trace_algorithm is W.trace_algorithm
+        assert bench.trace_algorithm is W.trace_algorithm and bench.traffic_report is W.traffic_report
     finally:
         shim.uninstall(fm, saved)
     assert fm.megopolis(1) == "cpu" and fm.resample.megopolis(1) == "cpu"
-    sys.modules.pop("fake_megores", None)
-    sys.modules.pop("fake_megores.resample", None)
+    assert fm.traffic_report() == "cpu" and sys.modules["fake_megores.bench"].trace_algorithm() == "cpu"
+    for name in ("fake_megores", "fake_megores.resample", "fake_megores.warpsim", "fake_megores.bench"):
+        sys.modules.pop(name, None)
