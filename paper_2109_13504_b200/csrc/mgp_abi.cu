@@ -854,16 +854,35 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
   return 0;
 }
 
+#ifndef MGP_OFFSPRING_I32_MIN
+#define MGP_OFFSPRING_I32_MIN (1ll << 20)
+#endif
+
 int mgp_offspring(const int64_t* d_anc, int64_t n_anc, int64_t n, int64_t* d_counts, int32_t* d_bad, void* stream) {
   if (n < 0 || n_anc < 0) return set_err(MGP_EINVAL, "negative size");
   cudaStream_t st = S(stream);
-  if (n) CUDA_TRY(cudaMemsetAsync(d_counts, 0, sizeof(int64_t) * n, st));
   if (d_bad) CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int32_t), st));
-  if (n_anc == 0) return 0;
   Scratch sc(st);
   int32_t* bad = d_bad;
-  if (!bad) CUDA_TRY(sc.alloc(&bad, sizeof(int32_t)));
+  if (!bad && n_anc) CUDA_TRY(sc.alloc(&bad, sizeof(int32_t)));
   const unsigned grid = (unsigned)((n_anc + 255) / 256);
+  // Large histograms count in int32 (counts <= n_anc < 2^31): half the footprint of the int64
+  // array, so the random-address atomics stay in L2 instead of read-modify-writing DRAM
+  // sectors; one streaming pass widens to the ABI's int64.
+  if (n >= MGP_OFFSPRING_I32_MIN && n_anc <= MAX_N && (((uintptr_t)d_counts) & 15) == 0) {
+    int32_t* c32 = nullptr;
+    CUDA_TRY(sc.alloc(&c32, sizeof(int32_t) * n));
+    CUDA_TRY(cudaMemsetAsync(c32, 0, sizeof(int32_t) * n, st));
+    if (n_anc) {
+      k_offspring<int32_t><<<grid, 256, 0, st>>>(d_anc, n_anc, n, c32, bad);
+      LAUNCH_CHECK("k_offspring");
+    }
+    k_widen_counts<<<(unsigned)std::min<int64_t>((n / 4 + 255) / 256 + 1, 148 * 16), 256, 0, st>>>(c32, n, d_counts);
+    LAUNCH_CHECK("k_widen_counts");
+    return 0;
+  }
+  if (n) CUDA_TRY(cudaMemsetAsync(d_counts, 0, sizeof(int64_t) * n, st));
+  if (n_anc == 0) return 0;
   k_offspring<int64_t><<<grid, 256, 0, st>>>(d_anc, n_anc, n, d_counts, bad);
   LAUNCH_CHECK("k_offspring");
   return 0;

@@ -881,6 +881,19 @@ __global__ void k_offspring(const int64_t* __restrict__ anc, int64_t n_anc, int6
   }
 }
 
+// int32 histogram -> the int64 counts of the ABI (4 counts per thread, 16-byte loads)
+__global__ void k_widen_counts(const int32_t* __restrict__ c32, int64_t n, int64_t* __restrict__ c64) {
+  const int64_t n4 = n >> 2;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += (int64_t)gridDim.x * blockDim.x) {
+    const int4 v = reinterpret_cast<const int4*>(c32)[q];
+    longlong2* d = reinterpret_cast<longlong2*>(c64) + 2 * q;
+    d[0] = make_longlong2(v.x, v.y);
+    d[1] = make_longlong2(v.z, v.w);
+  }
+  for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    c64[i] = c32[i];
+}
+
 // QualityAccumulator.add element update (M/metrics.py:90-92): sum += o, sum_sq += o*o
 template <typename CT>
 __global__ void k_quality_accum(const CT* __restrict__ counts, int64_t n, double* sum, double* sumsq) {

@@ -191,6 +191,30 @@ def test_offspring_histogram(mg):
     assert list(mg.ancestors_to_offspring(np.array([2, 2, 0, 5, 5, 5]))) == [1, 0, 2, 0, 0, 3]
 
 
+def test_offspring_histogram_large(mg):
+    """n >= 2^20 counts in an L2-resident int32 histogram and widens to int64: ragged n (the
+    widen tail), n_anc != n, a single heavy ancestor, out-of-range detection, and an output
+    view that is not 16-byte aligned (the direct int64 route)."""
+    rr = np.random.default_rng(5)
+    for n, n_anc in ((1 << 20, 1 << 20), ((1 << 20) + 3, 777777), ((1 << 21) + 1, (1 << 21) + 1)):
+        a = rr.integers(0, n, n_anc)
+        a[: n_anc // 3] = n - 1  # one heavy ancestor (contended atomics)
+        gd = mg.ancestors_to_offspring(torch.from_numpy(a).cuda(), n)
+        assert np.array_equal(gd.cpu().numpy(), np.bincount(a, minlength=n))
+    bad = torch.from_numpy(rr.integers(0, 1 << 20, 1 << 20)).cuda()
+    bad[12345] = 1 << 20
+    with pytest.raises(ValueError, match="out of range"):
+        mg.ancestors_to_offspring(bad, 1 << 20)
+    from paper_2109_13504_b200 import _lib
+
+    n = 1 << 20
+    a = torch.from_numpy(rr.integers(0, n, n)).cuda()
+    buf = torch.full((n + 1,), -7, dtype=torch.int64, device="cuda")
+    _lib.check(_lib.lib().mgp_offspring(a.data_ptr(), n, n, buf[1:].data_ptr(), None,
+                                        torch.cuda.current_stream().cuda_stream))
+    assert buf[0].item() == -7 and np.array_equal(buf[1:].cpu().numpy(), np.bincount(a.cpu().numpy(), minlength=n))
+
+
 def test_gather(mg):
     rr = np.random.default_rng(4)
     for shape, dt in [((1000,), np.float64), ((1000,), np.float32), ((513, 3), np.float32), ((64, 7), np.uint8),
