@@ -89,24 +89,34 @@ __device__ __forceinline__ int64_t px_apply(Tx T, int64_t parity) { return parit
 // Element transducer of weight w in binade e: w / u_e = M * 2^(ew - e) with M the integer
 // significand (implicit bit included for normal w) -- an integer shift with an exact
 // remainder, no floating point.  Weights >= 2^(e+1) leave the binade in one step: saturate.
+// float32, branch-free and 32-bit: q = floor(M / 2^k), v = q rounded (ties flagged), for
+// k = e - ew clamped to [0, 31] (k > 25 gives q = v = 0: M < 2^24 <= half), sat for k < 0.
+struct PxInc32 {
+  uint32_t q, v;
+  bool tie, sat;
+};
+__device__ __forceinline__ PxInc32 px_inc32(float w, int e) {
+  const uint32_t bits = __float_as_uint(w);
+  const uint32_t ef = (bits >> 23) & 0xFFu;
+  const uint32_t M = (bits & 0x7FFFFFu) | (ef ? 0x800000u : 0u);
+  const int k = e - (ef ? (int)ef - 127 : -126);
+  const uint32_t kc = (uint32_t)(k < 0 ? 0 : (k > 31 ? 31 : k));
+  const uint32_t q = M >> kc, r = M & ((1u << kc) - 1u), half = (1u << kc) >> 1;
+  PxInc32 d;
+  d.q = q;
+  d.v = q + (r > half ? 1u : 0u);
+  d.tie = kc > 0 && r == half;
+  d.sat = k < 0;
+  return d;
+}
+
 template <typename WT>
 __device__ __forceinline__ Tx px_elem(WT w, int e) {
-  if constexpr (sizeof(WT) == 4) {  // 32-bit integer path: M < 2^24, k <= 25
-    const uint32_t bits = __float_as_uint(w);
-    const int ef = (int)(bits >> 23) & 0xFF;
-    const uint32_t M = ef ? ((bits & 0x7FFFFFu) | 0x800000u) : (bits & 0x7FFFFFu);
-    const int ew = ef ? ef - 127 : -126;
-    if (ew > e) return Tx{PX_SAT, PX_SAT};
-    const int k = e - ew;
-    if (k == 0) return Tx{(int64_t)M, (int64_t)M};
-    if (k > 25) return Tx{0, 0};  // w < u_e / 2
-    const uint32_t q = M >> k, r = M & ((1u << k) - 1u), half = 1u << (k - 1);
-    const int64_t qq = (int64_t)q;
-    if (r != half) {
-      const int64_t v = qq + (r > half);
-      return Tx{v, v};
-    }
-    return Tx{qq + (qq & 1), qq + ((qq + 1) & 1)};  // tie: round half to even makes s + inc even
+  if constexpr (sizeof(WT) == 4) {  // tie: round half to even makes s + inc even
+    const PxInc32 d = px_inc32(w, e);
+    const int64_t a0 = d.tie ? (int64_t)(d.q + (d.q & 1u)) : (int64_t)d.v;
+    const int64_t a1 = d.tie ? (int64_t)(d.q + ((d.q + 1u) & 1u)) : (int64_t)d.v;
+    return d.sat ? Tx{PX_SAT, PX_SAT} : Tx{a0, a1};
   } else {
     const uint64_t bits = (uint64_t)__double_as_longlong(w);
     const int ef = (int)(bits >> 52) & 0x7FF;
@@ -132,6 +142,11 @@ __device__ __forceinline__ Tx px_elem(WT w, int e) {
 // element of the warp / block is a tie -- the common case for real weights.
 template <typename WT>
 __device__ __forceinline__ int64_t px_inc(WT w, int e, bool& tie) {
+  if constexpr (sizeof(WT) == 4) {
+    const PxInc32 d = px_inc32(w, e);
+    tie = d.tie;
+    return d.sat ? PX_SAT : (int64_t)(d.tie ? d.q + (d.q & 1u) : d.v);
+  }
   const Tx t = px_elem<WT>(w, e);
   tie = t.a0 != t.a1;
   return t.a0;  // the increment when !tie
@@ -202,13 +217,34 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_aggregate(const WT* __restric
     const int e = e0 - 1 + k;
     bool tie = false;
     int64_t sum = 0;
-#pragma unroll
-    for (int j = 0; j < PX_PER_THREAD; ++j) {
-      bool tj;
-      sum = px_sat_add(sum, px_inc<WT>(v[j], e, tj));
-      tie |= tj;
-    }
     Tx t;
+    if constexpr (sizeof(WT) == 4) {
+      // float32: every increment is < 2^24, so a warp's 128 of them sum exactly in 32 bits
+      // (one REDUX); any saturating element saturates the warp's aggregate
+      uint32_t s32 = 0;
+      bool sat = false;
+#pragma unroll
+      for (int j = 0; j < PX_PER_THREAD; ++j) {
+        const PxInc32 d = px_inc32(v[j], e);
+        s32 += d.v;
+        tie |= d.tie;
+        sat |= d.sat;
+      }
+      if (!__any_sync(0xffffffffu, tie)) {
+        const bool any_sat = __any_sync(0xffffffffu, sat);
+        const int64_t tot = (int64_t)__reduce_add_sync(0xffffffffu, s32);
+        t = any_sat ? Tx{PX_SAT, PX_SAT} : Tx{tot, tot};
+        if ((threadIdx.x & 31) == 0) red[k][threadIdx.x >> 5] = t;
+        continue;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < PX_PER_THREAD; ++j) {
+        bool tj;
+        sum = px_sat_add(sum, px_inc<WT>(v[j], e, tj));
+        tie |= tj;
+      }
+    }
     if (__any_sync(0xffffffffu, tie)) {  // rounding ties in this warp: parity transducers
       t = Tx{0, 0};
 #pragma unroll
@@ -446,13 +482,51 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_materialize(const WT* __restr
   int64_t inc[PX_PER_THREAD];
   int64_t tsum = 0;
   bool tie = false;
+  if constexpr (sizeof(WT) == 4) {
+    // float32: a resolved chunk keeps the running sum inside binade e, so every prefix is
+    // U * 2^(e-23) with U < 2^24 -- 32-bit scan, and U is exact as a float (one FMUL by the
+    // power of two, subnormal spacing included)
+    uint32_t i32[PX_PER_THREAD], t32 = 0;
 #pragma unroll
-  for (int j = 0; j < PX_PER_THREAD; ++j) {
-    v[j] = base + j < n ? w[base + j] : (WT)0;
-    bool tj;
-    inc[j] = px_inc<WT>(v[j], e, tj);
-    tie |= tj;
-    tsum += inc[j];  // a resolved chunk stays inside its binade: no saturation here
+    for (int j = 0; j < PX_PER_THREAD; ++j) {
+      v[j] = base + j < n ? w[base + j] : 0.0f;
+      const PxInc32 d = px_inc32(v[j], e);
+      i32[j] = d.v;
+      tie |= d.tie;
+      t32 += d.v;
+    }
+    if (!__syncthreads_or(tie)) {
+      __shared__ uint32_t wt32[PX_THREADS / 32];
+      uint32_t x = t32;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += y;
+      }
+      if (lane == 31) wt32[wid] = x;
+      __syncthreads();
+      uint32_t U = (uint32_t)S + x - t32;
+      for (int q = 0; q < wid; ++q) U += wt32[q];
+      const int xe = e - 23;
+      const float uef = xe >= -126 ? __uint_as_float((uint32_t)(xe + 127) << 23) : __uint_as_float(1u << (xe + 149));
+#pragma unroll
+      for (int j = 0; j < PX_PER_THREAD; ++j) {
+        U += i32[j];
+        if (base + j < n) cum[base + j] = (WT)__fmul_rn((float)U, uef);
+      }
+      return;
+    }
+#pragma unroll
+    for (int j = 0; j < PX_PER_THREAD; ++j) inc[j] = i32[j];
+  } else {
+#pragma unroll
+    for (int j = 0; j < PX_PER_THREAD; ++j) {
+      v[j] = base + j < n ? w[base + j] : (WT)0;
+      bool tj;
+      inc[j] = px_inc<WT>(v[j], e, tj);
+      tie |= tj;
+      tsum += inc[j];  // a resolved chunk stays inside its binade: no saturation here
+    }
   }
   if (!__syncthreads_or(tie)) {  // no rounding ties in the chunk: plain exclusive integer scan
     __shared__ int64_t wtot[PX_THREADS / 32];
