@@ -419,7 +419,10 @@ int px_cumsum(const WT* w, int64_t n, WT* cum, cudaStream_t st) {
   LAUNCH_CHECK("k_px_aggregate");
   k_px_super<<<(unsigned)nsup, 32, 0, st>>>(nch, e0, agg, se0, sagg);
   LAUNCH_CHECK("k_px_super");
-  k_px_resolve<WT><<<1, 32, 0, st>>>(w, n, nch, nsup, e0, agg, se0, sagg, carry, mode, scarry, smode, exc);
+  const int64_t stage = px_stage_bytes(nsup);
+  if (stage > 48 * 1024)
+    CUDA_TRY(cudaFuncSetAttribute(k_px_resolve<WT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PX_STAGE_MAX));
+  k_px_resolve<WT><<<1, 32, (size_t)stage, st>>>(w, n, nch, nsup, e0, agg, se0, sagg, carry, mode, scarry, smode, exc);
   LAUNCH_CHECK("k_px_resolve");
   k_px_expand<WT><<<(unsigned)nsup, 32, 0, st>>>(nch, e0, agg, scarry, smode, carry, mode);
   LAUNCH_CHECK("k_px_expand");

@@ -316,6 +316,81 @@ __device__ WT px_chunk_seq(const WT* __restrict__ w, int64_t n, int64_t c, WT s,
   return s;
 }
 
+// float32, resolver only (no prefix writes): the same result as px_chunk_seq<float, false>
+// without 1024 dependent adds.  From the running sum s (binade e, S units), every lane sums its
+// 32 increments in binade e (32-bit, saturating: only "does it leave the binade" matters);
+// the first lane whose inclusive prefix leaves the binade is added sequentially from the
+// exact carry (S + exclusive prefix) * u_e, and the scan restarts after it in the new binade.
+// Rounding ties or a non-finite sum fall back to numpy's sequential loop.
+__device__ float px_chunk_seq_fast(const float* __restrict__ w, int64_t n, int64_t c, float s) {
+  const int lane = threadIdx.x & 31;
+  const int64_t c0 = c * (int64_t)PX_CHUNK;
+  const int len = (int)((n - c0) < PX_CHUNK ? (n - c0) : (int64_t)PX_CHUNK);
+  float v[PXR_SEG];
+#pragma unroll
+  for (int j = 0; j < PXR_SEG; ++j) v[j] = lane * PXR_SEG + j < len ? w[c0 + lane * PXR_SEG + j] : 0.0f;
+  constexpr uint32_t CAP = 1u << 25, LIM = (1u << 24) - 1u;
+  int p = 0;  // first chunk-local element not yet added
+  while (p < len) {
+    if (!isfinite(s)) break;
+    const int e = PxFp<float>::expo(s);
+    const uint32_t S = (uint32_t)px_units<float>(s);
+    uint32_t t = 0;
+    bool tie = false, sat = false;
+#pragma unroll
+    for (int j = 0; j < PXR_SEG; ++j) {
+      const int idx = lane * PXR_SEG + j;
+      if (idx >= p && idx < len) {
+        const PxInc32 d = px_inc32(v[j], e);
+        t += d.v;  // <= 32 * 2^24
+        tie |= d.tie;
+        sat |= d.sat;
+      }
+    }
+    if (__any_sync(0xffffffffu, tie)) break;
+    t = sat ? CAP : min(t, CAP);
+    uint32_t x = t;  // inclusive scan, saturating at CAP (no overflow)
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x = min(x + y, CAP);
+    }
+    const unsigned bad = __ballot_sync(0xffffffffu, S + x > LIM);
+    const int xe = e - 23;
+    const float uef = xe >= -126 ? __uint_as_float((uint32_t)(xe + 127) << 23) : __uint_as_float(1u << (xe + 149));
+    if (!bad) {  // the rest of the chunk stays in binade e
+      s = __fmul_rn((float)(S + __shfl_sync(0xffffffffu, x, 31)), uef);
+      p = len;
+      break;
+    }
+    const int L = __ffs(bad) - 1;
+    uint32_t xm1 = __shfl_up_sync(0xffffffffu, x, 1);  // exclusive prefix (exact below lane L)
+    if (lane == 0) xm1 = 0;
+    const uint32_t ex = __shfl_sync(0xffffffffu, xm1, L);
+    s = __fmul_rn((float)(S + ex), uef);  // exact: S + ex <= LIM
+    // lane L's elements, numpy's order
+#pragma unroll
+    for (int j = 0; j < PXR_SEG; ++j) {
+      const float xv = __shfl_sync(0xffffffffu, v[j], L);
+      const int idx = L * PXR_SEG + j;
+      if (idx >= p && idx < len) s = s + xv;
+    }
+    p = (L + 1) * PXR_SEG;
+  }
+  // sequential remainder (ties / non-finite): elements [p, len)
+  for (int l = 0; l < 32; ++l) {
+    if (l * PXR_SEG >= len) break;
+    if ((l + 1) * PXR_SEG <= p) continue;
+#pragma unroll
+    for (int j = 0; j < PXR_SEG; ++j) {
+      const float xv = __shfl_sync(0xffffffffu, v[j], l);
+      const int idx = l * PXR_SEG + j;
+      if (idx >= p && idx < len) s = s + xv;
+    }
+  }
+  return s;
+}
+
 // Super-chunks: PX_SUPER consecutive chunks.  Their aggregate for a binade e is the ordered
 // composition of the chunks' aggregates for e (when every chunk carries e among its three
 // candidates).  One warp per super-chunk; candidates E-1, E, E+1 with E the first chunk's e0.
@@ -364,9 +439,19 @@ __device__ __forceinline__ PxWin px_window(WT s, int64_t u0, int64_t uend, const
   const int64_t S = fin ? px_units<WT>(s) : 0, p = S & 1;
   const int64_t u = u0 + lane;
   const bool valid = u < uend;
-  const int k = valid ? r.e - (e0s[u] - 1) : -1;
+  // the unit's binade and all its candidate aggregates in one round trip (the resolver is a
+  // chain of these windows: latency, not bandwidth, is its cost)
+  const int64_t uu = valid ? u : u0;
+  const int eu = e0s[uu];
+  Tx cand[PX_CAND];
+#pragma unroll
+  for (int q = 0; q < PX_CAND; ++q) cand[q] = aggs[uu * PX_CAND + q];
+  const int k = valid ? r.e - (eu - 1) : -1;
   const bool has = fin && valid && k >= 0 && k < PX_CAND;
-  const Tx t = has ? aggs[u * PX_CAND + k] : Tx{PX_SAT, PX_SAT};
+  Tx t{PX_SAT, PX_SAT};
+#pragma unroll
+  for (int q = 0; q < PX_CAND; ++q)
+    if (has && k == q) t = cand[q];
   const Tx P = px_warp_scan(t);
   Tx Q;
   Q.a0 = __shfl_up_sync(0xffffffffu, P.a0, 1);
@@ -388,13 +473,37 @@ __device__ __forceinline__ PxWin px_window(WT s, int64_t u0, int64_t uend, const
 // ones, also listed in exc_list[1..exc_list[0]]).
 constexpr int32_t PX_DESC = -200000;  // smode: descended into
 
+constexpr int64_t PX_STAGE_MAX = 96 * 1024;  // shared-memory budget of the resolver's staging
+__host__ __device__ __forceinline__ int64_t px_stage_bytes(int64_t nsup) {
+  const int64_t b = nsup * (int64_t)(PX_CAND * sizeof(Tx) + sizeof(int32_t));
+  return b <= PX_STAGE_MAX ? b : 0;
+}
+__device__ __forceinline__ uint32_t dyn_smem_size() {
+  uint32_t r;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+  return r;
+}
+
 template <typename WT>
 __global__ void __launch_bounds__(32) k_px_resolve(const WT* __restrict__ w, int64_t n, int64_t nch, int64_t nsup,
                                                    const int32_t* __restrict__ e0, const Tx* __restrict__ agg,
-                                                   const int32_t* __restrict__ se0, const Tx* __restrict__ sagg,
+                                                   const int32_t* se0, const Tx* sagg,
                                                    WT* carry, int32_t* mode, WT* scarry, int32_t* smode,
                                                    int32_t* exc_list) {
   const int lane = threadIdx.x;
+  // super-chunk aggregates staged in shared memory when the launch provides room (one bulk
+  // copy instead of a global round trip per super window)
+  extern __shared__ __align__(16) unsigned char px_smem[];
+  const bool staged = px_stage_bytes(nsup) != 0 && dyn_smem_size() >= px_stage_bytes(nsup);
+  if (staged) {
+    Tx* ssagg = reinterpret_cast<Tx*>(px_smem);
+    int32_t* sse0 = reinterpret_cast<int32_t*>(ssagg + nsup * PX_CAND);
+    for (int64_t q = lane; q < nsup * PX_CAND; q += 32) ssagg[q] = sagg[q];
+    for (int64_t q = lane; q < nsup; q += 32) sse0[q] = se0[q];
+    __syncwarp();
+    se0 = sse0;
+    sagg = ssagg;
+  }
   WT s = (WT)0;
   int64_t sp = 0;
   int32_t nexc = 0;
@@ -426,7 +535,8 @@ __global__ void __launch_bounds__(32) k_px_resolve(const WT* __restrict__ w, int
           exc_list[1 + nexc] = (int32_t)c;
         }
         ++nexc;
-        s = px_chunk_seq<WT, false>(w, n, c, s, nullptr);
+        if constexpr (sizeof(WT) == 4) s = px_chunk_seq_fast(w, n, c, s);
+        else s = px_chunk_seq<WT, false>(w, n, c, s, nullptr);
         ++c;
       }
     }
