@@ -110,6 +110,49 @@ __device__ __forceinline__ PxInc32 px_inc32(float w, int e) {
   return d;
 }
 
+// float64: the same branch-free form in 64 bits (M < 2^53; k clamped to [0, 63], k > 54 gives
+// q = v = 0 because M < 2^53 <= half)
+struct PxInc64 {
+  uint64_t q, v;
+  bool tie, sat;
+};
+__device__ __forceinline__ PxInc64 px_inc64(double w, int e) {
+  const uint64_t bits = (uint64_t)__double_as_longlong(w);
+  const uint32_t ef = (uint32_t)(bits >> 52) & 0x7FFu;
+  const uint64_t M = (bits & 0xFFFFFFFFFFFFFull) | (ef ? (1ull << 52) : 0ull);
+  const int k = e - (ef ? (int)ef - 1023 : -1022);
+  const uint32_t kc = (uint32_t)(k < 0 ? 0 : (k > 63 ? 63 : k));
+  const uint64_t q = M >> kc, r = M & ((1ull << kc) - 1ull), half = (1ull << kc) >> 1;
+  PxInc64 d;
+  d.q = q;
+  d.v = q + (r > half ? 1ull : 0ull);
+  d.tie = kc > 0 && r == half;
+  d.sat = k < 0;
+  return d;
+}
+
+// the per-dtype unit type of the crossing scan below: increments, their caps and the binade limit
+template <typename WT>
+struct PxScanT;
+template <>
+struct PxScanT<float> {
+  using U = uint32_t;
+  static constexpr U CAP = 1u << 25, LIM = (1u << 24) - 1u;  // 32 increments < 2^24 each: no overflow
+  __device__ static PxInc32 inc(float w, int e) { return px_inc32(w, e); }
+  __device__ static float at(U units, int e) {  // units * 2^(e-23), exact (subnormal spacing too)
+    const int xe = e - 23;
+    return __fmul_rn((float)units, xe >= -126 ? __uint_as_float((uint32_t)(xe + 127) << 23)
+                                              : __uint_as_float(1u << (xe + 149)));
+  }
+};
+template <>
+struct PxScanT<double> {
+  using U = uint64_t;
+  static constexpr U CAP = 1ull << 54, LIM = (1ull << 53) - 1ull;
+  __device__ static PxInc64 inc(double w, int e) { return px_inc64(w, e); }
+  __device__ static double at(U units, int e);
+};
+
 template <typename WT>
 __device__ __forceinline__ Tx px_elem(WT w, int e) {
   if constexpr (sizeof(WT) == 4) {  // tie: round half to even makes s + inc even
@@ -118,22 +161,10 @@ __device__ __forceinline__ Tx px_elem(WT w, int e) {
     const int64_t a1 = d.tie ? (int64_t)(d.q + ((d.q + 1u) & 1u)) : (int64_t)d.v;
     return d.sat ? Tx{PX_SAT, PX_SAT} : Tx{a0, a1};
   } else {
-    const uint64_t bits = (uint64_t)__double_as_longlong(w);
-    const int ef = (int)(bits >> 52) & 0x7FF;
-    uint64_t M = bits & 0xFFFFFFFFFFFFFull;
-    int ew = -1022;
-    if (ef) { M |= 1ull << 52; ew = ef - 1023; }
-    if (ew > e) return Tx{PX_SAT, PX_SAT};
-    const int k = e - ew;
-    if (k == 0) return Tx{(int64_t)M, (int64_t)M};
-    if (k > 54) return Tx{0, 0};
-    const int64_t q = (int64_t)(M >> k);
-    const uint64_t r = M & ((1ull << k) - 1), half = 1ull << (k - 1);
-    if (r != half) {
-      const int64_t v = q + (r > half);
-      return Tx{v, v};
-    }
-    return Tx{q + (q & 1), q + ((q + 1) & 1)};
+    const PxInc64 d = px_inc64(w, e);
+    const int64_t a0 = d.tie ? (int64_t)(d.q + (d.q & 1ull)) : (int64_t)d.v;
+    const int64_t a1 = d.tie ? (int64_t)(d.q + ((d.q + 1ull) & 1ull)) : (int64_t)d.v;
+    return d.sat ? Tx{PX_SAT, PX_SAT} : Tx{a0, a1};
   }
 }
 
@@ -283,6 +314,9 @@ __device__ __forceinline__ double px_ulp(int e, int mant) {  // 2^(e - mant), ex
   const int x = e - mant;
   return x >= -1022 ? __longlong_as_double((long long)(x + 1023) << 52) : __longlong_as_double(1ll << (x + 1074));
 }
+__device__ inline double PxScanT<double>::at(uint64_t units, int e) {  // exact: units < 2^53
+  return (double)units * px_ulp(e, 52);
+}
 
 // A chunk the running sum leaves its binade in: numpy's sequential loop, by one warp.  Each
 // lane stages 32 elements in registers; lane 0 adds them in order (IEEE WT adds, the values
@@ -316,62 +350,61 @@ __device__ WT px_chunk_seq(const WT* __restrict__ w, int64_t n, int64_t c, WT s,
   return s;
 }
 
-// float32, resolver only (no prefix writes): the same result as px_chunk_seq<float, false>
-// without 1024 dependent adds.  From the running sum s (binade e, S units), every lane sums its
-// 32 increments in binade e (32-bit, saturating: only "does it leave the binade" matters);
-// the first lane whose inclusive prefix leaves the binade is added sequentially from the
-// exact carry (S + exclusive prefix) * u_e, and the scan restarts after it in the new binade.
-// Rounding ties or a non-finite sum fall back to numpy's sequential loop.
-__device__ float px_chunk_seq_fast(const float* __restrict__ w, int64_t n, int64_t c, float s) {
+// Resolver only (no prefix writes): the same result as px_chunk_seq<WT, false> without 1024
+// dependent adds.  From the running sum s (binade e, S units), every lane sums its 32
+// increments in binade e (saturating: only "does it leave the binade" matters); the first lane
+// whose inclusive prefix leaves the binade is added sequentially from the exact carry
+// (S + exclusive prefix) * u_e, and the scan restarts after it in the new binade.  Rounding
+// ties or a non-finite sum fall back to numpy's sequential loop.
+template <typename WT>
+__device__ WT px_chunk_seq_fast(const WT* __restrict__ w, int64_t n, int64_t c, WT s) {
+  using P = PxScanT<WT>;
+  using U = typename P::U;
   const int lane = threadIdx.x & 31;
   const int64_t c0 = c * (int64_t)PX_CHUNK;
   const int len = (int)((n - c0) < PX_CHUNK ? (n - c0) : (int64_t)PX_CHUNK);
-  float v[PXR_SEG];
+  WT v[PXR_SEG];
 #pragma unroll
-  for (int j = 0; j < PXR_SEG; ++j) v[j] = lane * PXR_SEG + j < len ? w[c0 + lane * PXR_SEG + j] : 0.0f;
-  constexpr uint32_t CAP = 1u << 25, LIM = (1u << 24) - 1u;
+  for (int j = 0; j < PXR_SEG; ++j) v[j] = lane * PXR_SEG + j < len ? w[c0 + lane * PXR_SEG + j] : (WT)0;
   int p = 0;  // first chunk-local element not yet added
   while (p < len) {
-    if (!isfinite(s)) break;
-    const int e = PxFp<float>::expo(s);
-    const uint32_t S = (uint32_t)px_units<float>(s);
-    uint32_t t = 0;
+    if (!isfinite((double)s)) break;
+    const int e = PxFp<WT>::expo(s);
+    const U S = (U)px_units<WT>(s);
+    U t = 0;
     bool tie = false, sat = false;
 #pragma unroll
     for (int j = 0; j < PXR_SEG; ++j) {
       const int idx = lane * PXR_SEG + j;
       if (idx >= p && idx < len) {
-        const PxInc32 d = px_inc32(v[j], e);
-        t += d.v;  // <= 32 * 2^24
+        const auto d = P::inc(v[j], e);
+        t += d.v;  // <= 32 * 2^(MANT+1): no overflow
         tie |= d.tie;
         sat |= d.sat;
       }
     }
     if (__any_sync(0xffffffffu, tie)) break;
-    t = sat ? CAP : min(t, CAP);
-    uint32_t x = t;  // inclusive scan, saturating at CAP (no overflow)
+    t = sat ? P::CAP : (t < P::CAP ? t : P::CAP);
+    U x = t;  // inclusive scan, saturating at CAP (no overflow)
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
-      if (lane >= d) x = min(x + y, CAP);
+      const U y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x = (x + y < P::CAP) ? x + y : P::CAP;
     }
-    const unsigned bad = __ballot_sync(0xffffffffu, S + x > LIM);
-    const int xe = e - 23;
-    const float uef = xe >= -126 ? __uint_as_float((uint32_t)(xe + 127) << 23) : __uint_as_float(1u << (xe + 149));
+    const unsigned bad = __ballot_sync(0xffffffffu, S + x > P::LIM);
     if (!bad) {  // the rest of the chunk stays in binade e
-      s = __fmul_rn((float)(S + __shfl_sync(0xffffffffu, x, 31)), uef);
+      s = P::at(S + __shfl_sync(0xffffffffu, x, 31), e);
       p = len;
       break;
     }
     const int L = __ffs(bad) - 1;
-    uint32_t xm1 = __shfl_up_sync(0xffffffffu, x, 1);  // exclusive prefix (exact below lane L)
+    U xm1 = __shfl_up_sync(0xffffffffu, x, 1);  // exclusive prefix (exact below lane L)
     if (lane == 0) xm1 = 0;
-    const uint32_t ex = __shfl_sync(0xffffffffu, xm1, L);
-    s = __fmul_rn((float)(S + ex), uef);  // exact: S + ex <= LIM
+    s = P::at(S + __shfl_sync(0xffffffffu, xm1, L), e);  // exact: <= LIM units
     // lane L's elements, numpy's order
 #pragma unroll
     for (int j = 0; j < PXR_SEG; ++j) {
-      const float xv = __shfl_sync(0xffffffffu, v[j], L);
+      const WT xv = __shfl_sync(0xffffffffu, v[j], L);
       const int idx = L * PXR_SEG + j;
       if (idx >= p && idx < len) s = s + xv;
     }
@@ -383,7 +416,7 @@ __device__ float px_chunk_seq_fast(const float* __restrict__ w, int64_t n, int64
     if ((l + 1) * PXR_SEG <= p) continue;
 #pragma unroll
     for (int j = 0; j < PXR_SEG; ++j) {
-      const float xv = __shfl_sync(0xffffffffu, v[j], l);
+      const WT xv = __shfl_sync(0xffffffffu, v[j], l);
       const int idx = l * PXR_SEG + j;
       if (idx >= p && idx < len) s = s + xv;
     }
@@ -535,8 +568,7 @@ __global__ void __launch_bounds__(32) k_px_resolve(const WT* __restrict__ w, int
           exc_list[1 + nexc] = (int32_t)c;
         }
         ++nexc;
-        if constexpr (sizeof(WT) == 4) s = px_chunk_seq_fast(w, n, c, s);
-        else s = px_chunk_seq<WT, false>(w, n, c, s, nullptr);
+        s = px_chunk_seq_fast<WT>(w, n, c, s);
         ++c;
       }
     }
