@@ -60,7 +60,7 @@ def parse():
                     help="headline stream; the other one is measured too and reported under 'streams'")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--quality-runs", type=int, default=8)
+    ap.add_argument("--quality-runs", type=int, default=32)  # K >= 32
     return ap.parse_args()
 
 
