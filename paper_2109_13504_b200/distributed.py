@@ -39,6 +39,9 @@ from .resample import PartitionConfig, WarpConfig
 from .weights import WeightStats, compute_iterations, device_stats
 
 
+PREFIX_KINDS = ("multinomial", "systematic")
+
+
 def slice_tree_aligned(world: int, n_local: int) -> bool:
     """True when numpy's pairwise summation tree over world * n_local elements has every
     rank slice as a subtree (see module docstring)."""
@@ -168,7 +171,9 @@ class CudaOps:
 
 @dataclass
 class ShardedResampler:
-    """A Metropolis-family resampler over particles sharded across ranks."""
+    """A resampler over particles sharded across ranks: the Metropolis family, or the prefix-sum
+    methods (every rank scans the replicated weights -- numpy's sequential cumsum, bit-exact --
+    and searches for its own particles only)."""
 
     kind: str = "megopolis"
     warp: WarpConfig = WarpConfig()
@@ -191,6 +196,8 @@ class ShardedResampler:
             raise ValueError(f"{self.kind} requires a partition size")
         if self.layout not in ("contiguous", "stripes"):
             raise ValueError(f"unknown layout {self.layout!r}")
+        if self.kind in PREFIX_KINDS and self.rng != "megores":
+            raise ValueError(f"{self.kind} draws from the reference stream only (rng='megores')")
 
     # -- ownership --------------------------------------------------------------
     def owned(self, n_local: int):
@@ -273,6 +280,8 @@ class ShardedResampler:
             raise ValueError("weights must be non-negative")
         if st.n_pos == 0:
             raise ValueError("all weights are zero")
+        if self.kind in PREFIX_KINDS:  # multinomial / systematic take no B (M/resample.py:295-336)
+            return 1
         if b is None:
             b = compute_iterations(epsilon, st.mean, st.max).b
         if b < 1:

@@ -51,17 +51,21 @@ class OracleOps:
     def stats(self, w_full):
         return _Stats(w_full)
 
-    def resample_range(self, kind, w_full, b, seed, warp, partition_bytes, strict, rng, nonzero, p0, p1):
+    @staticmethod
+    def _full(kind, w, b, seed, warp, partition_bytes, strict, rng, **kw):
         from oracle import oracle
 
-        anc = oracle.resample(kind, w_full.numpy(), b, seed, warp, partition_bytes, strict, rng, p0=p0, p1=p1)
+        if kind in ("multinomial", "systematic"):
+            return getattr(oracle, kind)(w, seed)
+        return oracle.resample(kind, w, b, seed, warp, partition_bytes, strict, rng, **kw)
+
+    def resample_range(self, kind, w_full, b, seed, warp, partition_bytes, strict, rng, nonzero, p0, p1):
+        anc = self._full(kind, w_full.numpy(), b, seed, warp, partition_bytes, strict, rng)
         return torch.from_numpy(anc[p0:p1].copy())
 
     def resample_stripes(self, kind, w_full, b, seed, warp, partition_bytes, strict, rng, nonzero, lo0, lo1):
-        from oracle import oracle
-
         half = w_full.numel() // 2
-        anc = oracle.resample(kind, w_full.numpy(), b, seed, warp, partition_bytes, strict, rng)
+        anc = self._full(kind, w_full.numpy(), b, seed, warp, partition_bytes, strict, rng)
         return torch.from_numpy(np.concatenate([anc[lo0:lo1], anc[half + lo0:half + lo1]]))
 
     def resample_gather(self, kind, w_full, b, seed, warp, partition_bytes, strict, rng, nonzero, layout, p0, p1,
@@ -324,3 +328,45 @@ def test_sharded_offspring_quality(oracle, world, case):
     assert st.variance == float((s2 / runs - mean * mean).sum())
     assert st.bias_sq == float(((mean - e) ** 2).sum())
     assert st.mse_per_particle == st.mse / n
+
+
+@pytest.mark.parametrize("world,case", [
+    (2, ("multinomial", "contiguous", 200, "double")),
+    (4, ("systematic", "stripes", 256, "single")),
+    (3, ("systematic", "contiguous", 100, "single")),
+])
+def test_sharded_prefix_resamplers(oracle, world, case):
+    """Sharded multinomial / systematic (every rank scans the replicated weights, searches its own
+    particles): the ancestors in global order equal the single-process prefix-sum resampler."""
+    kind, layout, n_local, prec = case
+    got = _run(world, case, _worker_prefix)
+    n = n_local * world
+    w_full = oracle.gen_gaussian_weights(2.0, n, 4646, prec)
+    assert np.array_equal(got, getattr(oracle, kind)(w_full, 321))
+
+
+def _worker_prefix(rank, world, port, case, q):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle
+        from paper_2109_13504_b200.distributed import ShardedResampler
+
+        kind, layout, n_local, prec = case
+        n = n_local * world
+        w_full = oracle.gen_gaussian_weights(2.0, n, 4646, prec)
+        sr = ShardedResampler(kind=kind, ops=OracleOps(), layout=layout)
+        idx = np.concatenate([np.arange(lo, hi) for lo, hi in sr.owned(n_local)])
+        anc_local, b = sr.resample(torch.from_numpy(w_full[idx].copy()), seed=321)
+        parts = [torch.zeros(n_local, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(parts, anc_local)
+        if rank == 0:
+            if layout == "stripes":
+                h = n_local // 2
+                q.put(np.concatenate([p[:h].numpy() for p in parts] + [p[h:].numpy() for p in parts]))
+            else:
+                q.put(torch.cat(parts).numpy())
+    finally:
+        dist.destroy_process_group()

@@ -107,6 +107,8 @@ def _worker(rank, world, port, case, q):
     (2, ("c2", "contiguous", 4096, "megores", 5)),
     (2, ("metropolis", "stripes", 2048, "philox", 4)),
     (2, ("megopolis", "stripes", 1 << 23, "philox", None)),  # N = 2^24 (config 4), B from the rule
+    (2, ("multinomial", "contiguous", 4096, "megores", None)),  # prefix-sum kinds: replicated scan
+    (2, ("systematic", "stripes", 1 << 16, "megores", None)),
 ])
 def test_peer_rows_resample_gather(oracle, world, case):
     import torch.multiprocessing as mp
@@ -135,15 +137,20 @@ def test_peer_rows_resample_gather(oracle, world, case):
     b_used, anc, st, qst = res
     n = n_local * world
     w_full = oracle.gen_gaussian_weights(3.0, n, 777, "single")
-    if b is None:
+    if b is None and kind not in ("multinomial", "systematic"):
         mean, mx = oracle.weight_mean_max(w_full)
         assert b_used == oracle.compute_iterations(0.01, mean, mx)
-    ref = oracle.resample(kind, w_full, b_used, 2021, 32, 256 if kind in ("c1", "c2") else None, True, rng)
+    def full_ref(seed):
+        if kind in ("multinomial", "systematic"):
+            return getattr(oracle, kind)(w_full, seed)
+        return oracle.resample(kind, w_full, b_used, seed, 32, 256 if kind in ("c1", "c2") else None, True, rng)
+
+    ref = full_ref(2021)
     assert np.array_equal(anc, ref)
     states_full = np.stack([np.arange(n) * 0.5, -np.arange(n, dtype=np.float64)], 1)
     assert np.array_equal(st, states_full[ref])
     # ShardedQuality == the reference's QualityAccumulator arithmetic (M/metrics.py:71-110)
-    ref2 = oracle.resample(kind, w_full, b_used, 2022, 32, 256 if kind in ("c1", "c2") else None, True, rng)
+    ref2 = full_ref(2022)
     v = w_full.astype(np.float64)
     e = n * v / v.sum()
     o1, o2 = (np.bincount(r, minlength=n).astype(np.float64) for r in (ref, ref2))
