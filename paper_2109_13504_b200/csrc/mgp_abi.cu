@@ -422,7 +422,8 @@ int px_cumsum(const WT* w, int64_t n, WT* cum, cudaStream_t st) {
   const int64_t stage = px_stage_bytes(nsup);
   if (stage > 48 * 1024)
     CUDA_TRY(cudaFuncSetAttribute(k_px_resolve<WT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PX_STAGE_MAX));
-  k_px_resolve<WT><<<1, 32, (size_t)stage, st>>>(w, n, nch, nsup, e0, agg, se0, sagg, carry, mode, scarry, smode, exc);
+  k_px_resolve<WT><<<1, PXR_THREADS, (size_t)stage, st>>>(w, n, nch, nsup, e0, agg, se0, sagg, carry, mode, scarry,
+                                                          smode, exc);
   LAUNCH_CHECK("k_px_resolve");
   k_px_expand<WT><<<(unsigned)nsup, 32, 0, st>>>(nch, e0, agg, scarry, smode, carry, mode);
   LAUNCH_CHECK("k_px_expand");

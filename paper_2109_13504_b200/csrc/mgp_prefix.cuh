@@ -350,23 +350,39 @@ __device__ WT px_chunk_seq(const WT* __restrict__ w, int64_t n, int64_t c, WT s,
   return s;
 }
 
-// Resolver only (no prefix writes): the same result as px_chunk_seq<WT, false> without 1024
-// dependent adds.  From the running sum s (binade e, S units), every lane sums its 32
-// increments in binade e (saturating: only "does it leave the binade" matters); the first lane
-// whose inclusive prefix leaves the binade is added sequentially from the exact carry
-// (S + exclusive prefix) * u_e, and the scan restarts after it in the new binade.  Rounding
-// ties or a non-finite sum fall back to numpy's sequential loop.
+// The resolver runs as one CTA of PXR_THREADS threads.  Every warp walks the same windows (the
+// same data, so the same results; only warp 0 writes), and the chunks the running sum leaves
+// its binade in are resolved by the whole CTA together: from the running sum s (binade e, S
+// units) every thread sums its PXR_PER increments in binade e (saturating: only "does it leave
+// the binade" matters), a block scan finds the first thread whose prefix leaves the binade, its
+// few elements are added sequentially from the exact carry (S + exclusive prefix) * u_e, and the
+// scan restarts after them in the new binade.  Rounding ties or a non-finite sum fall back to
+// numpy's sequential loop.  The result equals px_chunk_seq<WT, false>.
+constexpr int PXR_THREADS = 256;
+constexpr int PXR_WARPS = PXR_THREADS / 32;
+constexpr int PXR_PER = PX_CHUNK / PXR_THREADS;  // 4 elements per thread
+
+template <typename U>
+__device__ __forceinline__ U px_cap_add(U a, U b, U cap) { return a + b < cap ? a + b : cap; }
+
 template <typename WT>
-__device__ WT px_chunk_seq_fast(const WT* __restrict__ w, int64_t n, int64_t c, WT s) {
+struct PxBlockScratch {
+  typename PxScanT<WT>::U wsum[PXR_WARPS];
+  int first[PXR_WARPS];
+  typename PxScanT<WT>::U excl;
+};
+
+template <typename WT>
+__device__ WT px_chunk_block(const WT* __restrict__ w, int64_t n, int64_t c, WT s, PxBlockScratch<WT>& sh) {
   using P = PxScanT<WT>;
   using U = typename P::U;
-  const int lane = threadIdx.x & 31;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t c0 = c * (int64_t)PX_CHUNK;
   const int len = (int)((n - c0) < PX_CHUNK ? (n - c0) : (int64_t)PX_CHUNK);
-  WT v[PXR_SEG];
+  WT v[PXR_PER];
 #pragma unroll
-  for (int j = 0; j < PXR_SEG; ++j) v[j] = lane * PXR_SEG + j < len ? w[c0 + lane * PXR_SEG + j] : (WT)0;
-  int p = 0;  // first chunk-local element not yet added
+  for (int j = 0; j < PXR_PER; ++j) v[j] = tid * PXR_PER + j < len ? w[c0 + tid * PXR_PER + j] : (WT)0;
+  int p = 0;  // first chunk-local element not yet added (a multiple of PXR_PER)
   while (p < len) {
     if (!isfinite((double)s)) break;
     const int e = PxFp<WT>::expo(s);
@@ -374,53 +390,58 @@ __device__ WT px_chunk_seq_fast(const WT* __restrict__ w, int64_t n, int64_t c, 
     U t = 0;
     bool tie = false, sat = false;
 #pragma unroll
-    for (int j = 0; j < PXR_SEG; ++j) {
-      const int idx = lane * PXR_SEG + j;
+    for (int j = 0; j < PXR_PER; ++j) {
+      const int idx = tid * PXR_PER + j;
       if (idx >= p && idx < len) {
         const auto d = P::inc(v[j], e);
-        t += d.v;  // <= 32 * 2^(MANT+1): no overflow
+        t += d.v;
         tie |= d.tie;
         sat |= d.sat;
       }
     }
-    if (__any_sync(0xffffffffu, tie)) break;
+    if (__syncthreads_or(tie)) break;
     t = sat ? P::CAP : (t < P::CAP ? t : P::CAP);
-    U x = t;  // inclusive scan, saturating at CAP (no overflow)
+    U x = t;  // inclusive warp scan, saturating at CAP
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const U y = __shfl_up_sync(0xffffffffu, x, d);
-      if (lane >= d) x = (x + y < P::CAP) ? x + y : P::CAP;
+      if (lane >= d) x = px_cap_add(x, y, P::CAP);
     }
-    const unsigned bad = __ballot_sync(0xffffffffu, S + x > P::LIM);
-    if (!bad) {  // the rest of the chunk stays in binade e
-      s = P::at(S + __shfl_sync(0xffffffffu, x, 31), e);
+    U wex = __shfl_up_sync(0xffffffffu, x, 1);
+    if (lane == 0) wex = 0;
+    if (lane == 31) sh.wsum[wid] = x;
+    __syncthreads();
+    U base = 0, total = 0;
+#pragma unroll
+    for (int q = 0; q < PXR_WARPS; ++q) {
+      if (q < wid) base = px_cap_add(base, sh.wsum[q], P::CAP);
+      total = px_cap_add(total, sh.wsum[q], P::CAP);
+    }
+    const U incl = px_cap_add(base, x, P::CAP), excl = px_cap_add(base, wex, P::CAP);
+    const unsigned bm = __ballot_sync(0xffffffffu, S + incl > P::LIM);
+    if (lane == 0) sh.first[wid] = bm ? wid * 32 + __ffs(bm) - 1 : PXR_THREADS;
+    __syncthreads();
+    int T = PXR_THREADS;
+#pragma unroll
+    for (int q = 0; q < PXR_WARPS; ++q) T = min(T, sh.first[q]);
+    if (T == PXR_THREADS) {  // the rest of the chunk stays in binade e
+      s = P::at(S + total, e);
       p = len;
+      __syncthreads();
       break;
     }
-    const int L = __ffs(bad) - 1;
-    U xm1 = __shfl_up_sync(0xffffffffu, x, 1);  // exclusive prefix (exact below lane L)
-    if (lane == 0) xm1 = 0;
-    s = P::at(S + __shfl_sync(0xffffffffu, xm1, L), e);  // exact: <= LIM units
-    // lane L's elements, numpy's order
+    if (tid == T) sh.excl = excl;
+    __syncthreads();
+    s = P::at(S + sh.excl, e);  // exact: <= LIM units
 #pragma unroll
-    for (int j = 0; j < PXR_SEG; ++j) {
-      const WT xv = __shfl_sync(0xffffffffu, v[j], L);
-      const int idx = L * PXR_SEG + j;
-      if (idx >= p && idx < len) s = s + xv;
+    for (int j = 0; j < PXR_PER; ++j) {  // thread T's elements, numpy's order
+      const int idx = T * PXR_PER + j;
+      if (idx >= p && idx < len) s = s + w[c0 + idx];
     }
-    p = (L + 1) * PXR_SEG;
+    p = (T + 1) * PXR_PER;
+    __syncthreads();  // sh is reused by the next pass
   }
-  // sequential remainder (ties / non-finite): elements [p, len)
-  for (int l = 0; l < 32; ++l) {
-    if (l * PXR_SEG >= len) break;
-    if ((l + 1) * PXR_SEG <= p) continue;
-#pragma unroll
-    for (int j = 0; j < PXR_SEG; ++j) {
-      const WT xv = __shfl_sync(0xffffffffu, v[j], l);
-      const int idx = l * PXR_SEG + j;
-      if (idx >= p && idx < len) s = s + xv;
-    }
-  }
+  for (int idx = p; idx < len; ++idx) s = s + w[c0 + idx];  // ties / non-finite: sequential
   return s;
 }
 
@@ -518,12 +539,14 @@ __device__ __forceinline__ uint32_t dyn_smem_size() {
 }
 
 template <typename WT>
-__global__ void __launch_bounds__(32) k_px_resolve(const WT* __restrict__ w, int64_t n, int64_t nch, int64_t nsup,
-                                                   const int32_t* __restrict__ e0, const Tx* __restrict__ agg,
-                                                   const int32_t* se0, const Tx* sagg,
-                                                   WT* carry, int32_t* mode, WT* scarry, int32_t* smode,
-                                                   int32_t* exc_list) {
-  const int lane = threadIdx.x;
+__global__ void __launch_bounds__(PXR_THREADS) k_px_resolve(const WT* __restrict__ w, int64_t n, int64_t nch,
+                                                            int64_t nsup, const int32_t* __restrict__ e0,
+                                                            const Tx* __restrict__ agg, const int32_t* se0,
+                                                            const Tx* sagg, WT* carry, int32_t* mode, WT* scarry,
+                                                            int32_t* smode, int32_t* exc_list) {
+  const int tid = threadIdx.x;
+  const bool w0 = tid < 32;  // warp 0 writes; every warp computes the same windows
+  __shared__ PxBlockScratch<WT> sh;
   // super-chunk aggregates staged in shared memory when the launch provides room (one bulk
   // copy instead of a global round trip per super window)
   extern __shared__ __align__(16) unsigned char px_smem[];
@@ -531,9 +554,9 @@ __global__ void __launch_bounds__(32) k_px_resolve(const WT* __restrict__ w, int
   if (staged) {
     Tx* ssagg = reinterpret_cast<Tx*>(px_smem);
     int32_t* sse0 = reinterpret_cast<int32_t*>(ssagg + nsup * PX_CAND);
-    for (int64_t q = lane; q < nsup * PX_CAND; q += 32) ssagg[q] = sagg[q];
-    for (int64_t q = lane; q < nsup; q += 32) sse0[q] = se0[q];
-    __syncwarp();
+    for (int64_t q = tid; q < nsup * PX_CAND; q += PXR_THREADS) ssagg[q] = sagg[q];
+    for (int64_t q = tid; q < nsup; q += PXR_THREADS) sse0[q] = se0[q];
+    __syncthreads();
     se0 = sse0;
     sagg = ssagg;
   }
@@ -542,39 +565,39 @@ __global__ void __launch_bounds__(32) k_px_resolve(const WT* __restrict__ w, int
   int32_t nexc = 0;
   while (sp < nsup) {
     const PxWin r = px_window<WT>(s, sp, nsup, se0, sagg);
-    if (lane < r.f) {
-      scarry[sp + lane] = (WT)((double)r.carry_units * r.ue);
-      smode[sp + lane] = r.e;
+    if (w0 && tid < r.f) {
+      scarry[sp + tid] = (WT)((double)r.carry_units * r.ue);
+      smode[sp + tid] = r.e;
     }
     if (r.f > 0) s = (WT)((double)r.out_units * r.ue);
     sp += r.f;
     if (r.f == 32 || sp >= nsup) continue;
     // descend into super-chunk sp
-    if (lane == 0) smode[sp] = PX_DESC;
+    if (tid == 0) smode[sp] = PX_DESC;
     int64_t c = sp * PX_SUPER;
     const int64_t cend = min(nch, c + PX_SUPER);
     while (c < cend) {
       const PxWin q = px_window<WT>(s, c, cend, e0, agg);
-      if (lane < q.f) {
-        carry[c + lane] = (WT)((double)q.carry_units * q.ue);
-        mode[c + lane] = q.e;
+      if (w0 && tid < q.f) {
+        carry[c + tid] = (WT)((double)q.carry_units * q.ue);
+        mode[c + tid] = q.e;
       }
       if (q.f > 0) s = (WT)((double)q.out_units * q.ue);
       c += q.f;
-      if (c < cend) {  // chunk c leaves its binade: sequential
-        if (lane == 0) {
+      if (c < cend) {  // chunk c leaves its binade: the whole CTA resolves it
+        if (tid == 0) {
           carry[c] = s;
           mode[c] = PX_EXC;
           exc_list[1 + nexc] = (int32_t)c;
         }
         ++nexc;
-        s = px_chunk_seq_fast<WT>(w, n, c, s);
+        s = px_chunk_block<WT>(w, n, c, s, sh);
         ++c;
       }
     }
     ++sp;
   }
-  if (lane == 0) exc_list[0] = nexc;
+  if (tid == 0) exc_list[0] = nexc;
 }
 
 // carry-ins of the chunks of every super-chunk resolved whole: ordered scan of the chunk
