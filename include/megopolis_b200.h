@@ -126,7 +126,17 @@ int mgp_resample_gather(int kind, const void *d_w, int dtype, int64_t n, int32_t
                         const void *const *h_peer_rows, int npeers, int64_t rows_local, int64_t row_bytes,
                         int64_t *d_anc_out, void *d_rows_out, void *stream);
 
-/* Two-stripe particle range: particles [lo0, lo1) and [N/2 + lo0, N/2 + lo1) (0 <= lo0 <= lo1
+/* Single-process multi-device resample from host buffers (SURVEY 8b mgp_megopolis_multi; for C hosts
+ * without torch.distributed).  The weights (host, n elements) are replicated to devs[0..ndev)
+ * (device-to-device copies peer to peer), B comes from the numpy-exact stats on devs[0] (b <= 0:
+ * the epsilon rule; *b_used receives it), and device d resamples stripe d of each half (contiguous
+ * slices when N does not split into 32-aligned stripes), writing into h_anc[n].  Same results as
+ * the single-device call; a device may appear more than once in devs. */
+int mgp_resample_multi(int kind, const void *h_w, int dtype, int64_t n, int32_t b, double epsilon, uint64_t seed,
+                       int32_t warp, int32_t partition_bytes, int strict, int rng, int ndev, const int *devs,
+                       int64_t *h_anc, int32_t *b_used);
+
+/* Two-stripe particle range:/* Two-stripe particle range: particles [lo0, lo1) and [N/2 + lo0, N/2 + lo1) (0 <= lo0 <= lo1
  * <= N/2, N even) into d_anc_local[0, L) and d_anc_local[L, 2L), L = lo1 - lo0.  This is the
  * sharded "stripes" layout (rank r owns stripe r of each half), under which every rank can run
  * the half-split Megopolis kernel. */

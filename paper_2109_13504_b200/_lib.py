@@ -42,6 +42,8 @@ SIGNATURES = {
                                    _vp]),
     "mgp_resample_gather": (_i32, [_i32, _vp, _i32, _i64, _i32, _u64, _i32, _i32, _i32, _i32, _i32, _i32, _i64, _i64,
                                     _vp, _i32, _i64, _i64, _vp, _vp, _vp]),
+    "mgp_resample_multi": (_i32, [_i32, _vp, _i32, _i64, _i32, _dbl, _u64, _i32, _i32, _i32, _i32, _i32, _vp, _vp,
+                                  _vp]),
     "mgp_resample_stripes": (_i32, [_i32, _vp, _i32, _i64, _i32, _u64, _i32, _i32, _i32, _i32, _i32, _i64, _i64,
                                      _vp, _vp]),
     "mgp_resample_host": (_i32, [_i32, _vp, _i32, _i64, _i32, _dbl, _u64, _i32, _i32, _i32, _i32, _vp, _vp, _i32]),

@@ -1320,6 +1320,115 @@ extern "C" int mgp_resample_stripes(int kind, const void* d_w, int dtype, int64_
   return rc ? rc : rc2;
 }
 
+// Single-process multi-device resample from host buffers (SURVEY 8b's mgp_megopolis_multi, for C
+// hosts without torch.distributed): the weights are replicated to every device (the
+// device-to-device copies go peer to peer), device 0 derives B from the numpy-exact stats, and
+// device d resamples stripe d of each half (the half-split kernel's pairing; contiguous slices
+// when N does not split into stripes) and writes its ancestors straight into h_anc.
+extern "C" int mgp_resample_multi(int kind, const void* h_w, int dtype, int64_t n, int32_t b, double epsilon,
+                                  uint64_t seed, int32_t warp, int32_t partition_bytes, int strict, int rng,
+                                  int ndev, const int* devs, int64_t* h_anc, int32_t* b_used) {
+  if (!h_w || !h_anc || !devs) return set_err(MGP_EINVAL, "null pointer");
+  if (ndev < 1 || ndev > 64) return set_err(MGP_EINVAL, "ndev must be in [1, 64], got %d", ndev);
+  if (dtype != MGP_F32 && dtype != MGP_F64) return set_err(MGP_EINVAL, "dtype must be MGP_F32 or MGP_F64");
+  if (n < 1) return set_err(MGP_EINVAL, "weights must be a non-empty 1-d sequence");
+  if (n > MAX_N) return set_err(MGP_EUNSUPPORTED, "N exceeds 2^31-1");
+  int prev = 0;
+  CUDA_TRY(cudaGetDevice(&prev));
+  struct Dev {
+    int id = 0;
+    cudaStream_t st = nullptr;
+    void* w = nullptr;
+    int64_t* anc = nullptr;
+    mgp_weight_stats_t* stats = nullptr;
+  };
+  std::vector<Dev> dv((size_t)ndev);
+  const size_t wbytes = (size_t)n * (dtype == MGP_F32 ? 4 : 8);
+  // stripes of h particles per device and half, or contiguous slices of `chunk`
+  const int64_t half = n / 2, h = (n % 2 == 0 && half % ndev == 0) ? half / ndev : 0;
+  const bool stripes = h > 0 && h % 32 == 0;
+  const int64_t chunk = ((n + ndev - 1) / ndev + 31) / 32 * 32;
+  int rc = 0;
+  cudaEvent_t ready = nullptr;
+  auto finish = [&](int code) {
+    if (ready) cudaEventDestroy(ready);
+    for (auto& d : dv) {
+      if (!d.st) continue;
+      cudaSetDevice(d.id);
+      cudaStreamSynchronize(d.st);
+      if (d.w) cudaFreeAsync(d.w, d.st);
+      if (d.anc) cudaFreeAsync(d.anc, d.st);
+      if (d.stats) cudaFreeAsync(d.stats, d.st);
+      cudaStreamSynchronize(d.st);
+      cudaStreamDestroy(d.st);
+    }
+    cudaSetDevice(prev);
+    return code;
+  };
+#define MTRY(x)                                                            \
+  do {                                                                     \
+    cudaError_t e_ = (x);                                                  \
+    if (e_ != cudaSuccess) return finish(cuda_err(e_, #x));                \
+  } while (0)
+  for (int d = 0; d < ndev; ++d) {
+    Dev& D = dv[(size_t)d];
+    D.id = devs[d];
+    MTRY(cudaSetDevice(D.id));
+    ensure_pool();
+    MTRY(cudaStreamCreateWithFlags(&D.st, cudaStreamNonBlocking));
+    MTRY(cudaMallocAsync(&D.w, wbytes, D.st));
+    MTRY(cudaMallocAsync((void**)&D.anc, sizeof(int64_t) * (stripes ? 2 * h : chunk), D.st));
+  }
+  // weights: host -> device 0 -> every other device (peer copies)
+  MTRY(cudaSetDevice(dv[0].id));
+  MTRY(cudaMemcpyAsync(dv[0].w, h_w, wbytes, cudaMemcpyHostToDevice, dv[0].st));
+  MTRY(cudaMallocAsync((void**)&dv[0].stats, sizeof(mgp_weight_stats_t), dv[0].st));
+  if ((rc = mgp_weight_stats(dv[0].w, dtype, n, dv[0].stats, dv[0].st))) return finish(rc);
+  MTRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  MTRY(cudaEventRecord(ready, dv[0].st));
+  for (int d = 1; d < ndev; ++d) {
+    MTRY(cudaSetDevice(dv[(size_t)d].id));
+    MTRY(cudaStreamWaitEvent(dv[(size_t)d].st, ready, 0));
+    MTRY(cudaMemcpyPeerAsync(dv[(size_t)d].w, dv[(size_t)d].id, dv[0].w, dv[0].id, wbytes, dv[(size_t)d].st));
+  }
+  // B rule and validation on the host from device 0's stats (WeightVector / _check_weights)
+  mgp_weight_stats_t hs{};
+  MTRY(cudaSetDevice(dv[0].id));
+  MTRY(cudaMemcpyAsync(&hs, dv[0].stats, sizeof hs, cudaMemcpyDeviceToHost, dv[0].st));
+  MTRY(cudaStreamSynchronize(dv[0].st));
+  if (hs.n_nonfinite) return finish(set_err(MGP_EINVAL, "weights must be finite"));
+  if (hs.n_neg) return finish(set_err(MGP_EINVAL, "weights must be non-negative"));
+  if (hs.n_pos == 0) return finish(set_err(MGP_EINVAL, "all weights are zero"));
+  if (b <= 0 && (rc = mgp_compute_iterations(epsilon, hs.mean, hs.max, &b))) return finish(rc);
+  if (b_used) *b_used = b;
+  const int flags = hs.n_zero == 0 ? MGP_FLAG_NONZERO : 0;
+  for (int d = 0; d < ndev; ++d) {
+    Dev& D = dv[(size_t)d];
+    MTRY(cudaSetDevice(D.id));
+    if (stripes) {
+      const int64_t lo0 = d * h;
+      if ((rc = mgp_resample_stripes(kind, D.w, dtype, n, b, seed, warp, partition_bytes, strict, rng, flags, lo0,
+                                     lo0 + h, D.anc, D.st)))
+        return finish(rc);
+      MTRY(cudaMemcpyAsync(h_anc + lo0, D.anc, sizeof(int64_t) * h, cudaMemcpyDeviceToHost, D.st));
+      MTRY(cudaMemcpyAsync(h_anc + half + lo0, D.anc + h, sizeof(int64_t) * h, cudaMemcpyDeviceToHost, D.st));
+    } else {
+      const int64_t p0 = std::min<int64_t>(n, d * chunk), p1 = std::min<int64_t>(n, p0 + chunk);
+      if (p1 <= p0) continue;
+      if ((rc = mgp_resample_range(kind, D.w, dtype, n, b, seed, warp, partition_bytes, strict, rng, flags, p0, p1,
+                                   D.anc, D.st)))
+        return finish(rc);
+      MTRY(cudaMemcpyAsync(h_anc + p0, D.anc, sizeof(int64_t) * (p1 - p0), cudaMemcpyDeviceToHost, D.st));
+    }
+  }
+  for (auto& d : dv) {
+    MTRY(cudaSetDevice(d.id));
+    MTRY(cudaStreamSynchronize(d.st));
+  }
+#undef MTRY
+  return finish(0);
+}
+
 // K resampling runs accumulated into a QualityAccumulator on the device: per seed, the
 // resampler, the offspring histogram and QualityAccumulator.add (M/metrics.py:86-93), with no
 // host round trip between runs -- the inner loop of the quality grids (M/bench.py:121-126).

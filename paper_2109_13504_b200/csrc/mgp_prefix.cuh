@@ -539,7 +539,7 @@ __device__ __forceinline__ uint32_t dyn_smem_size() {
 }
 
 template <typename WT>
-__global__ void __launch_bounds__(PXR_THREADS) k_px_resolve(const WT* __restrict__ w, int64_t n, int64_t nch,
+__global__ void __launch_bounds__(PXR_THREADS, 1) k_px_resolve(const WT* __restrict__ w, int64_t n, int64_t nch,
                                                             int64_t nsup, const int32_t* __restrict__ e0,
                                                             const Tx* __restrict__ agg, const int32_t* se0,
                                                             const Tx* sagg, WT* carry, int32_t* mode, WT* scarry,

@@ -191,6 +191,38 @@ def test_offspring_histogram(mg):
     assert list(mg.ancestors_to_offspring(np.array([2, 2, 0, 5, 5, 5]))) == [1, 0, 2, 0, 0, 3]
 
 
+@pytest.mark.parametrize("kind,rng,n,ndev", [("megopolis", "philox", 1 << 16, 2), ("megopolis", "megores", 1 << 14, 4),
+                                             ("megopolis", "philox", 3 * 1024, 3), ("metropolis", "megores", 4096, 2),
+                                             ("c2", "philox", 8192, 1), ("systematic", "megores", 10000, 3)])
+def test_resample_multi_device(mg, oracle, kind, rng, n, ndev):
+    """mgp_resample_multi (single process, several devices; here the one GPU listed ndev times):
+    stripes / contiguous slices, B from the epsilon rule, ancestors equal the single-device result."""
+    import ctypes
+
+    from paper_2109_13504_b200 import _lib
+
+    w = oracle.gen_gaussian_weights(2.0, n, 31, "single")
+    anc = np.empty(n, dtype=np.int64)
+    bu = ctypes.c_int32(0)
+    devs = (ctypes.c_int * ndev)(*([torch.cuda.current_device()] * ndev))
+    part = 256 if kind == "c2" else 0
+    _lib.check(_lib.lib().mgp_resample_multi(_lib.KIND[kind], w.ctypes.data, 0, n, 0, 0.01, 5, 32, part, 1,
+                                             _lib.RNG[rng], ndev, ctypes.cast(devs, ctypes.c_void_p),
+                                             anc.ctypes.data, ctypes.byref(bu)))
+    mean, mx = oracle.weight_mean_max(w)
+    b = oracle.compute_iterations(0.01, mean, mx)
+    if kind == "systematic":
+        ref = oracle.systematic(w, 5)
+    else:
+        assert bu.value == b
+        ref = oracle.resample(kind, w, b, 5, 32, part or None, True, rng)
+    assert np.array_equal(anc, ref)
+    with pytest.raises(ValueError, match="all weights are zero"):
+        z = np.zeros(64, np.float32)
+        _lib.check(_lib.lib().mgp_resample_multi(3, z.ctypes.data, 0, 64, 0, 0.01, 5, 32, 0, 1, 0, 1,
+                                                 ctypes.cast(devs, ctypes.c_void_p), anc.ctypes.data, None))
+
+
 def test_offspring_histogram_large(mg):
     """n >= 2^20 counts in an L2-resident int32 histogram and widens to int64: ragged n (the
     widen tail), n_anc != n, a single heavy ancestor, out-of-range detection, and an output
