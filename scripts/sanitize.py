@@ -62,6 +62,12 @@ for kind, layout, cols, dt in (("megopolis", 0, 2, torch.float32), ("megopolis",
         _lib.KIND[kind], wq.data_ptr(), 0, 4096, 9, 3, 32, 0, 1, _lib.RNG["philox"], 0, layout, lo, hi,
         ctypes.cast(tab, ctypes.c_void_p), 4, 1024, cols * own[0].element_size(), anc.data_ptr(), out.data_ptr(),
         torch.cuda.current_stream().cuda_stream))
+# single-process multi-device entry (the one GPU listed twice)
+wm = rr.random(4096).astype(np.float32)
+am = np.empty(4096, dtype=np.int64)
+devs = (ctypes.c_int * 2)(0, 0)
+_lib.check(_lib.lib().mgp_resample_multi(3, wm.ctypes.data, 0, 4096, 0, 0.01, 5, 32, 0, 1, 1, 2,
+                                         ctypes.cast(devs, ctypes.c_void_p), am.ctypes.data, None))
 acc = mg.QualityAccumulator(4096)
 acc.add_runs("megopolis", mg.WeightVector(wq, "single"), 5, [1, 2, 3])
 mg.estimate_ratio(mg.WeightVector(wq, "single"), 1000, 7)
