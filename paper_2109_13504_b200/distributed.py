@@ -557,3 +557,28 @@ def gather_from_peers(peer_states, n_local: int, anc, out=None):
     _lib.check(_lib.lib().mgp_gather_peers(ctypes.cast(arr, ctypes.c_void_p), len(ptrs), int(n_local), row_bytes,
                                            D.ptr(anc), anc.numel(), D.ptr(out), D.stream_ptr()))
     return out
+
+
+def resample_on_devices(kind: str, w, b: int | None = None, seed=0, devices=None, epsilon: float = 0.01,
+                        warp: WarpConfig = WarpConfig(), partition_bytes: int | None = None, strict: bool = True,
+                        rng: str = "megores"):
+    """One process driving several GPUs (mgp_resample_multi): host weights in, ``np.int64``
+    ancestors out, bit-identical to the single-device resampler.  ``devices`` defaults to every
+    visible GPU; B follows the epsilon rule when ``b`` is None.  Returns (ancestors, B)."""
+    import numpy as np
+
+    from .weights import _as_weight_vector
+
+    D.require_cuda()
+    t = D.torch()
+    wv = _as_weight_vector(w)
+    vals = wv.values.cpu().numpy() if D.is_tensor(wv.values) else np.ascontiguousarray(wv.values)
+    devs = list(range(t.cuda.device_count())) if devices is None else [int(d) for d in devices]
+    arr = (ctypes.c_int * len(devs))(*devs)
+    anc = np.empty(len(vals), dtype=np.int64)
+    bu = ctypes.c_int32(0)
+    _lib.check(_lib.lib().mgp_resample_multi(
+        _lib.KIND[kind], vals.ctypes.data, 0 if vals.dtype == np.float32 else 1, len(vals), int(b or 0),
+        float(epsilon), int(seed) & (2**64 - 1), int(warp.warp_size), int(partition_bytes or 0), int(bool(strict)),
+        _lib.RNG[rng], len(devs), ctypes.cast(arr, ctypes.c_void_p), anc.ctypes.data, ctypes.byref(bu)))
+    return anc, int(bu.value)

@@ -217,6 +217,11 @@ def test_resample_multi_device(mg, oracle, kind, rng, n, ndev):
         assert bu.value == b
         ref = oracle.resample(kind, w, b, 5, 32, part or None, True, rng)
     assert np.array_equal(anc, ref)
+    from paper_2109_13504_b200.distributed import resample_on_devices
+
+    anc2, b2 = resample_on_devices(kind, w, seed=5, devices=[torch.cuda.current_device()] * ndev, rng=rng,
+                                   partition_bytes=part or None)
+    assert np.array_equal(anc2, ref) and (kind == "systematic" or b2 == b)
     with pytest.raises(ValueError, match="all weights are zero"):
         z = np.zeros(64, np.float32)
         _lib.check(_lib.lib().mgp_resample_multi(3, z.ctypes.data, 0, 64, 0, 0.01, 5, 32, 0, 1, 0, 1,
