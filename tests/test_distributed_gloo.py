@@ -1,10 +1,12 @@
-"""Multi-process (world_size 2 and 3, gloo, CPU) tests of the sharded protocol:
-weight all-gather, per-slice resampling with global indices, the B rule on the
-replicated array, and the cross-rank state exchange.
+"""Multi-process (world sizes 2-4, gloo, CPU) tests of the sharded protocol: weight
+all-gather, per-slice resampling with global indices, the B rule (slice tree or replicated
+array), the cross-rank state exchange (all-to-all and the fused resample + gather), sharded
+offspring counts and quality statistics, and the prefix-sum kinds.
 
 The CUDA kernels are replaced by the CPU oracle through ShardedResampler's ``ops``
 hook (test infrastructure only); the GPU path is covered by tests/test_parity_gpu.py
-and by the peer-gather GPU test below.
+and, with real CUDA IPC mappings between processes, by tests/test_ipc_gpu.py.  The cases of a
+test run in one process group per world size (spawning costs seconds per group).
 """
 
 import os
@@ -106,121 +108,127 @@ class OracleOps:
         return states[idx]
 
 
-def _worker_stripes(rank, world, port, case, q):
-    sys.path.insert(0, ROOT)
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    try:
-        from oracle import oracle
-        from paper_2109_13504_b200.distributed import ShardedResampler
+def _worker_stripes(rank, world, case, q):
+    from oracle import oracle
+    from paper_2109_13504_b200.distributed import ShardedResampler
 
-        kind, n_local, y, prec, rng, b = case
-        n, h = n_local * world, n_local // 2
-        w_full = oracle.gen_gaussian_weights(y, n, 4343, prec)
-        sr = ShardedResampler(kind=kind, partition_bytes=128 if kind in ("c1", "c2") else None, rng=rng,
-                              ops=OracleOps(), layout="stripes")
-        (a0, a1), (b0, b1) = sr.owned(n_local)
-        w_local = torch.from_numpy(np.concatenate([w_full[a0:a1], w_full[b0:b1]]))
-        anc_local, b_used = sr.resample(w_local, b=b, seed=77)
-        states_full = np.stack([np.arange(n, dtype=np.float64) * 1.5, np.arange(n, dtype=np.float64)], axis=1)
-        s_local = torch.from_numpy(np.concatenate([states_full[a0:a1], states_full[b0:b1]]))
-        new_local = sr.exchange(s_local, anc_local)
-        # the fused path: every rank's state array addressable here (peer mappings, emulated)
-        peers = [torch.zeros_like(s_local) for _ in range(world)]
-        dist.all_gather(peers, s_local)
-        anc_f, rows_f, b_f = sr.resample_gather(w_local, peers, b=b, seed=77)
-        assert b_f == b_used and torch.equal(anc_f, anc_local) and torch.equal(rows_f, new_local)
-        parts = [torch.zeros(n_local, dtype=torch.int64) for _ in range(world)]
-        dist.all_gather(parts, anc_local)
-        news = [torch.zeros_like(new_local) for _ in range(world)]
-        dist.all_gather(news, new_local)
-        if rank == 0:  # back to global particle order
-            anc = np.concatenate([p[:h].numpy() for p in parts] + [p[h:].numpy() for p in parts])
-            st = np.concatenate([x[:h].numpy() for x in news] + [x[h:].numpy() for x in news])
-            q.put((int(b_used), anc, st))
-    finally:
-        dist.destroy_process_group()
+    kind, n_local, y, prec, rng, b = case
+    n, h = n_local * world, n_local // 2
+    w_full = oracle.gen_gaussian_weights(y, n, 4343, prec)
+    sr = ShardedResampler(kind=kind, partition_bytes=128 if kind in ("c1", "c2") else None, rng=rng,
+                          ops=OracleOps(), layout="stripes")
+    (a0, a1), (b0, b1) = sr.owned(n_local)
+    w_local = torch.from_numpy(np.concatenate([w_full[a0:a1], w_full[b0:b1]]))
+    anc_local, b_used = sr.resample(w_local, b=b, seed=77)
+    states_full = np.stack([np.arange(n, dtype=np.float64) * 1.5, np.arange(n, dtype=np.float64)], axis=1)
+    s_local = torch.from_numpy(np.concatenate([states_full[a0:a1], states_full[b0:b1]]))
+    new_local = sr.exchange(s_local, anc_local)
+    # the fused path: every rank's state array addressable here (peer mappings, emulated)
+    peers = [torch.zeros_like(s_local) for _ in range(world)]
+    dist.all_gather(peers, s_local)
+    anc_f, rows_f, b_f = sr.resample_gather(w_local, peers, b=b, seed=77)
+    assert b_f == b_used and torch.equal(anc_f, anc_local) and torch.equal(rows_f, new_local)
+    parts = [torch.zeros(n_local, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(parts, anc_local)
+    news = [torch.zeros_like(new_local) for _ in range(world)]
+    dist.all_gather(news, new_local)
+    if rank == 0:  # back to global particle order
+        anc = np.concatenate([p[:h].numpy() for p in parts] + [p[h:].numpy() for p in parts])
+        st = np.concatenate([x[:h].numpy() for x in news] + [x[h:].numpy() for x in news])
+        q.put((int(b_used), anc, st))
 
 
-def _worker(rank, world, port, case, q):
-    sys.path.insert(0, ROOT)
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    try:
-        from oracle import oracle
-        from paper_2109_13504_b200.distributed import ShardedResampler
-        from paper_2109_13504_b200.resample import WarpConfig
+def _worker(rank, world, case, q):
+    from oracle import oracle
+    from paper_2109_13504_b200.distributed import ShardedResampler
+    from paper_2109_13504_b200.resample import WarpConfig
 
-        kind, n_local, y, prec, rng, b = case
-        n = n_local * world
-        w_full = oracle.gen_gaussian_weights(y, n, 4242, prec)
-        w_local = torch.from_numpy(w_full[rank * n_local:(rank + 1) * n_local].copy())
-        sr = ShardedResampler(kind=kind, warp=WarpConfig(), partition_bytes=128 if kind in ("c1", "c2") else None,
-                              rng=rng, ops=OracleOps())
-        anc_local, b_used = sr.resample(w_local, b=b, seed=99)
-        # every rank derived the same B
-        bt = torch.tensor([b_used])
-        bs = [torch.zeros(1, dtype=bt.dtype) for _ in range(world)]
-        dist.all_gather(bs, bt)
-        parts = [torch.zeros(n_local, dtype=torch.int64) for _ in range(world)]
-        dist.all_gather(parts, anc_local)
-        # state exchange: states are (value, index) rows
-        states_full = np.stack([np.arange(n, dtype=np.float64) * 1.5, np.arange(n, dtype=np.float64)], axis=1)
-        s_local = torch.from_numpy(states_full[rank * n_local:(rank + 1) * n_local].copy())
-        new_local = sr.exchange(s_local, anc_local)
-        peers = [torch.zeros_like(s_local) for _ in range(world)]
-        dist.all_gather(peers, s_local)
-        anc_f, rows_f, b_f = sr.resample_gather(w_local, peers, b=b, seed=99)
-        assert b_f == b_used and torch.equal(anc_f, anc_local) and torch.equal(rows_f, new_local)
-        news = [torch.zeros_like(new_local) for _ in range(world)]
-        dist.all_gather(news, new_local)
-        if rank == 0:
-            q.put((int(b_used), [int(x) for x in bs], torch.cat(parts).numpy(), torch.cat(news).numpy()))
-    finally:
-        dist.destroy_process_group()
+    kind, n_local, y, prec, rng, b = case
+    n = n_local * world
+    w_full = oracle.gen_gaussian_weights(y, n, 4242, prec)
+    w_local = torch.from_numpy(w_full[rank * n_local:(rank + 1) * n_local].copy())
+    sr = ShardedResampler(kind=kind, warp=WarpConfig(), partition_bytes=128 if kind in ("c1", "c2") else None,
+                          rng=rng, ops=OracleOps())
+    anc_local, b_used = sr.resample(w_local, b=b, seed=99)
+    # every rank derived the same B
+    bt = torch.tensor([b_used])
+    bs = [torch.zeros(1, dtype=bt.dtype) for _ in range(world)]
+    dist.all_gather(bs, bt)
+    parts = [torch.zeros(n_local, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(parts, anc_local)
+    # state exchange: states are (value, index) rows
+    states_full = np.stack([np.arange(n, dtype=np.float64) * 1.5, np.arange(n, dtype=np.float64)], axis=1)
+    s_local = torch.from_numpy(states_full[rank * n_local:(rank + 1) * n_local].copy())
+    new_local = sr.exchange(s_local, anc_local)
+    peers = [torch.zeros_like(s_local) for _ in range(world)]
+    dist.all_gather(peers, s_local)
+    anc_f, rows_f, b_f = sr.resample_gather(w_local, peers, b=b, seed=99)
+    assert b_f == b_used and torch.equal(anc_f, anc_local) and torch.equal(rows_f, new_local)
+    news = [torch.zeros_like(new_local) for _ in range(world)]
+    dist.all_gather(news, new_local)
+    if rank == 0:
+        q.put((int(b_used), [int(x) for x in bs], torch.cat(parts).numpy(), torch.cat(news).numpy()))
 
 
-def _worker_quality(rank, world, port, case, q):
+def _worker_quality(rank, world, case, q):
     """K runs of the sharded resampler -> sharded offspring -> ShardedQuality, against the
     reference's own single-process QualityAccumulator arithmetic (numpy) on the same runs."""
+    from oracle import oracle
+    from paper_2109_13504_b200.distributed import ShardedResampler
+
+    layout, n_local, y, rng, runs = case
+    n = n_local * world
+    w_full = oracle.gen_gaussian_weights(y, n, 4545, "single")
+    sr = ShardedResampler(rng=rng, ops=OracleOps(), layout=layout)
+    idx = np.concatenate([np.arange(lo, hi) for lo, hi in sr.owned(n_local)])
+    w_local = torch.from_numpy(w_full[idx].copy())
+    acc = sr.quality(w_local)
+    for k in range(runs):
+        anc_local, _ = sr.resample(w_local, b=7, seed=1000 + k)
+        counts = sr.offspring(anc_local)
+        acc.add(counts)
+    st = acc.finalize()
+    if rank == 0:
+        q.put((acc.aligned, st))
+
+
+class _Collect:
+    def __init__(self):
+        self.items = []
+
+    def put(self, x):
+        self.items.append(x)
+
+
+def _batch(rank, world, port, fn, cases, q):
+    """One process group, every case of a test in turn (spawning per case costs seconds)."""
     sys.path.insert(0, ROOT)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from oracle import oracle
-        from paper_2109_13504_b200.distributed import ShardedResampler
-
-        layout, n_local, y, rng, runs = case
-        n = n_local * world
-        w_full = oracle.gen_gaussian_weights(y, n, 4545, "single")
-        sr = ShardedResampler(rng=rng, ops=OracleOps(), layout=layout)
-        idx = np.concatenate([np.arange(lo, hi) for lo, hi in sr.owned(n_local)])
-        w_local = torch.from_numpy(w_full[idx].copy())
-        acc = sr.quality(w_local)
-        for k in range(runs):
-            anc_local, _ = sr.resample(w_local, b=7, seed=1000 + k)
-            counts = sr.offspring(anc_local)
-            acc.add(counts)
-        st = acc.finalize()
+        out = []
+        for case in cases:
+            c = _Collect()
+            fn(rank, world, case, c)
+            out.append(c.items[0] if c.items else None)
         if rank == 0:
-            q.put((acc.aligned, st))
+            q.put(out)
     finally:
         dist.destroy_process_group()
 
 
-def _run(world, case, target=None):
+def _run(world, cases, target=None):
+    """Run ``target`` (default _worker) for every case on ``world`` gloo ranks; rank 0's results."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=target or _worker, args=(r, world, port, case, q)) for r in range(world)]
+    procs = [ctx.Process(target=_batch, args=(r, world, port, target or _worker, cases, q)) for r in range(world)]
     for p in procs:
         p.start()
     res, t0 = None, time.time()
     try:
-        while res is None and time.time() - t0 < 300:
+        while res is None and time.time() - t0 < 600:
             try:
                 res = q.get(timeout=1)
             except queue.Empty:
@@ -235,17 +243,24 @@ def _run(world, case, target=None):
     return res
 
 
-@pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("case", [
+SHARDED_CASES = [
     ("megopolis", 512, 3.0, "single", "megores", None),
     ("megopolis", 256, 1.0, "double", "philox", 9),
     ("metropolis", 320, 2.0, "single", "megores", 7),
     ("c1", 256, 4.0, "single", "megores", None),
     ("c2", 256, 0.0, "single", "philox", 5),
-])
-def test_sharded_equals_single_process(oracle, world, case):
+]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_equals_single_process(oracle, world):
+    for case, got in zip(SHARDED_CASES, _run(world, SHARDED_CASES)):
+        _check_sharded(oracle, world, case, got)
+
+
+def _check_sharded(oracle, world, case, got):
     kind, n_local, y, prec, rng, b = case
-    b_used, bs, anc, states = _run(world, case)
+    b_used, bs, anc, states = got
     n = n_local * world
     w_full = oracle.gen_gaussian_weights(y, n, 4242, prec)
     if b is None:
@@ -277,17 +292,24 @@ def test_slice_stats_combine_bit_exact(oracle, world, n_local):
     assert not slice_tree_aligned(3, 1024) and not slice_tree_aligned(2, 60) and not slice_tree_aligned(2, 1001)
 
 
-@pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("case", [
+STRIPES_CASES = [
     ("megopolis", 512, 4.0, "single", "philox", None),
     ("megopolis", 192, 2.0, "double", "megores", 5),
     ("c2", 256, 1.0, "single", "megores", 4),
-])
-def test_stripes_layout_equals_single_process(oracle, world, case):
+]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_stripes_layout_equals_single_process(oracle, world):
     """layout="stripes": rank r owns stripe r of each half (the half-split kernel's pairing);
     ancestors, the slice-statistics B and the exchanged states equal the single process's."""
+    for case, got in zip(STRIPES_CASES, _run(world, STRIPES_CASES, _worker_stripes)):
+        _check_stripes(oracle, world, case, got)
+
+
+def _check_stripes(oracle, world, case, got):
     kind, n_local, y, prec, rng, b = case
-    b_used, anc, states = _run(world, case, _worker_stripes)
+    b_used, anc, states = got
     n = n_local * world
     w_full = oracle.gen_gaussian_weights(y, n, 4343, prec)
     if b is None:
@@ -300,17 +322,25 @@ def test_stripes_layout_equals_single_process(oracle, world, case):
 
 
 
-@pytest.mark.parametrize("world,case", [
-    (2, ("contiguous", 256, 2.0, "philox", 3)),
-    (4, ("stripes", 256, 3.0, "megores", 3)),
-    (2, ("stripes", 512, 1.0, "philox", 2)),
-    (2, ("contiguous", 48, 2.0, "megores", 3)),  # not tree-aligned: the all-gather route
-])
-def test_sharded_offspring_quality(oracle, world, case):
+QUALITY_CASES = {
+    2: [("contiguous", 256, 2.0, "philox", 3), ("stripes", 512, 1.0, "philox", 2),
+        ("contiguous", 48, 2.0, "megores", 3)],  # the last is not tree-aligned: the all-gather route
+    4: [("stripes", 256, 3.0, "megores", 3)],
+}
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_offspring_quality(oracle, world):
     """ShardedResampler.offspring + ShardedQuality equal the reference's QualityAccumulator
     (M/metrics.py:71-110, numpy) over the same K runs of the whole population, bit for bit."""
+    cases = QUALITY_CASES[world]
+    for case, got in zip(cases, _run(world, cases, _worker_quality)):
+        _check_quality(oracle, world, case, got)
+
+
+def _check_quality(oracle, world, case, got):
     layout, n_local, y, rng, runs = case
-    aligned, st = _run(world, case, _worker_quality)
+    aligned, st = got
     assert aligned == (n_local >= 128 or (layout == "contiguous" and n_local > 64))
     n = n_local * world
     w_full = oracle.gen_gaussian_weights(y, n, 4545, "single")
@@ -330,43 +360,41 @@ def test_sharded_offspring_quality(oracle, world, case):
     assert st.mse_per_particle == st.mse / n
 
 
-@pytest.mark.parametrize("world,case", [
-    (2, ("multinomial", "contiguous", 200, "double")),
-    (4, ("systematic", "stripes", 256, "single")),
-    (3, ("systematic", "contiguous", 100, "single")),
-])
-def test_sharded_prefix_resamplers(oracle, world, case):
+PREFIX_CASES = {2: [("multinomial", "contiguous", 200, "double")], 4: [("systematic", "stripes", 256, "single")],
+                3: [("systematic", "contiguous", 100, "single")]}
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_sharded_prefix_resamplers(oracle, world):
     """Sharded multinomial / systematic (every rank scans the replicated weights, searches its own
     particles): the ancestors in global order equal the single-process prefix-sum resampler."""
+    cases = PREFIX_CASES[world]
+    for case, got in zip(cases, _run(world, cases, _worker_prefix)):
+        _check_prefix(oracle, world, case, got)
+
+
+def _check_prefix(oracle, world, case, got):
     kind, layout, n_local, prec = case
-    got = _run(world, case, _worker_prefix)
     n = n_local * world
     w_full = oracle.gen_gaussian_weights(2.0, n, 4646, prec)
     assert np.array_equal(got, getattr(oracle, kind)(w_full, 321))
 
 
-def _worker_prefix(rank, world, port, case, q):
-    sys.path.insert(0, ROOT)
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    try:
-        from oracle import oracle
-        from paper_2109_13504_b200.distributed import ShardedResampler
+def _worker_prefix(rank, world, case, q):
+    from oracle import oracle
+    from paper_2109_13504_b200.distributed import ShardedResampler
 
-        kind, layout, n_local, prec = case
-        n = n_local * world
-        w_full = oracle.gen_gaussian_weights(2.0, n, 4646, prec)
-        sr = ShardedResampler(kind=kind, ops=OracleOps(), layout=layout)
-        idx = np.concatenate([np.arange(lo, hi) for lo, hi in sr.owned(n_local)])
-        anc_local, b = sr.resample(torch.from_numpy(w_full[idx].copy()), seed=321)
-        parts = [torch.zeros(n_local, dtype=torch.int64) for _ in range(world)]
-        dist.all_gather(parts, anc_local)
-        if rank == 0:
-            if layout == "stripes":
-                h = n_local // 2
-                q.put(np.concatenate([p[:h].numpy() for p in parts] + [p[h:].numpy() for p in parts]))
-            else:
-                q.put(torch.cat(parts).numpy())
-    finally:
-        dist.destroy_process_group()
+    kind, layout, n_local, prec = case
+    n = n_local * world
+    w_full = oracle.gen_gaussian_weights(2.0, n, 4646, prec)
+    sr = ShardedResampler(kind=kind, ops=OracleOps(), layout=layout)
+    idx = np.concatenate([np.arange(lo, hi) for lo, hi in sr.owned(n_local)])
+    anc_local, b = sr.resample(torch.from_numpy(w_full[idx].copy()), seed=321)
+    parts = [torch.zeros(n_local, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(parts, anc_local)
+    if rank == 0:
+        if layout == "stripes":
+            h = n_local // 2
+            q.put(np.concatenate([p[:h].numpy() for p in parts] + [p[h:].numpy() for p in parts]))
+        else:
+            q.put(torch.cat(parts).numpy())
