@@ -136,7 +136,7 @@ int mgp_resample_multi(int kind, const void *h_w, int dtype, int64_t n, int32_t 
                        int32_t warp, int32_t partition_bytes, int strict, int rng, int ndev, const int *devs,
                        int64_t *h_anc, int32_t *b_used);
 
-/* Two-stripe particle range:/* Two-stripe particle range: particles [lo0, lo1) and [N/2 + lo0, N/2 + lo1) (0 <= lo0 <= lo1
+/* Two-stripe particle range: particles [lo0, lo1) and [N/2 + lo0, N/2 + lo1) (0 <= lo0 <= lo1
  * <= N/2, N even) into d_anc_local[0, L) and d_anc_local[L, 2L), L = lo1 - lo0.  This is the
  * sharded "stripes" layout (rank r owns stripe r of each half), under which every rank can run
  * the half-split Megopolis kernel. */
