@@ -511,6 +511,36 @@ def test_config5_2p28_single_gpu(mg, oracle, rng):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("n,rng,kind", [((1 << 30), "philox", "megopolis"), ((1 << 30) + 96 * 7, "megores", "megopolis"),
+                                        ((1 << 31) - 32, "philox", "megopolis"), ((1 << 29) + 64, "megores", "c2")])
+def test_maximum_sizes(mg, oracle, n, rng, kind):
+    """The largest particle counts (N < 2^31: 32-bit index arithmetic on the device; 2^31 - 32
+    is 8 GiB of weights and 16 GiB of ancestors): a handful of rounds (the index math does not
+    depend on B), oracle bit-exact on particle windows at the start, the middle and the end, and
+    conservation of the offspring counts over the full vector."""
+    free, _ = torch.cuda.mem_get_info()
+    if free < 3.5 * n * 8:
+        pytest.skip("not enough device memory")
+    wv = mg.gen_gaussian_weights(mg.GaussianWeightParams(2.0, n), 31, "single")
+    b = 6
+    part = mg.PartitionConfig(256) if kind == "c2" else None
+    anc = (mg.metropolis_c2(wv, b, part, seed=5, rng=rng) if kind == "c2"
+           else mg.megopolis(wv, b, seed=5, rng=rng))
+    w_np = wv.values.cpu().numpy()
+    got_idx = []
+    for p0 in (0, (n // 2) - 4096, n - 2048):
+        p0 -= p0 % 64
+        ref = oracle.resample(kind, w_np, b, 5, 32, 256 if kind == "c2" else None, True, rng, p0=p0, p1=p0 + 2048)
+        got_idx.append((p0, ref[p0:p0 + 2048]))
+    for p0, ref in got_idx:
+        assert np.array_equal(anc[p0:p0 + 2048].cpu().numpy(), ref), p0
+    del w_np
+    off = mg.ancestors_to_offspring(anc, n)
+    assert int(off.sum()) == n and int(anc.min()) >= 0 and int(anc.max()) < n
+    del anc, off, wv
+    torch.cuda.empty_cache()
+
+
 def test_storage_device_upload(mg, tmp_path, oracle):
     from paper_2109_13504_b200 import storage
 
