@@ -642,12 +642,16 @@ def test_resample_gather_fused(mg, oracle, rng, kind, warp, n, cols):
         assert torch.equal(out, states[torch.from_numpy(ref[p0:p1]).cuda()]), (p0, p1)
 
 
-@pytest.mark.parametrize("kind,rng,n,b,cols", [("megopolis", "philox", 1 << 14, 9, 2), ("megopolis", "megores", 4096, 6, 2),
-                                                ("megopolis", "philox", 4096, 1030, 2),
-                                                ("megopolis", "philox", 4096, 7, 3),  # 3-byte rows: unfused
-                                                ("metropolis", "megores", 4096, 5, 2),  # W != 32: unfused
-                                                ("c2", "philox", 8192, 5, 2)])
-def test_resample_gather_stripes(mg, oracle, kind, rng, n, b, cols):
+@pytest.mark.parametrize("kind,rng,n,b,cols,world", [
+    ("megopolis", "philox", 1 << 14, 9, 2, 4), ("megopolis", "megores", 4096, 6, 2, 4),
+    ("megopolis", "philox", 4096, 1030, 2, 4),
+    ("megopolis", "philox", 4096, 7, 3, 4),  # 3-byte rows: unfused
+    ("metropolis", "megores", 4096, 5, 2, 4),  # W != 32: unfused
+    ("c2", "philox", 8192, 5, 2, 4),
+    ("megopolis", "philox", 768, 5, 2, 4),  # N not a power of two: fused, two ranges per owner
+    ("megopolis", "philox", 4096, 5, 2, 32),  # stripes of 64 (not 128-aligned): fused, two ranges
+])
+def test_resample_gather_stripes(mg, oracle, kind, rng, n, b, cols, world):
     """mgp_resample_gather, stripes layout: 4 owners each holding stripe r of each half; the
     fused kernel (or the two-kernel route for other shapes) reads each ancestor's row from its
     owner (pointer table on one device)."""
@@ -661,7 +665,7 @@ def test_resample_gather_stripes(mg, oracle, kind, rng, n, b, cols):
           "metropolis": lambda: oracle.metropolis(w, b, seed=8, rng=rng),
           "c2": lambda: oracle.metropolis_c2(w, b, part, seed=8, rng=rng)}[kind]
     ref = fn()
-    world, half = 4, n // 2
+    half = n // 2
     h = half // world
     dt = torch.uint8 if cols == 3 else torch.float32
     rows_full = (torch.arange(n * cols, device="cuda") % 251).to(dt).reshape(n, cols)
