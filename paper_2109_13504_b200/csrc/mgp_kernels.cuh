@@ -637,6 +637,38 @@ __device__ __forceinline__ void wstat_observe(WStats& s, WT v) {
   if (d > s.max) s.max = d;
 }
 
+// Branch-free per-thread tallies for the 4096-element chunks (at most 16 elements per thread:
+// 32-bit counters, the max in the weights' own type -- the same first-maximum-wins comparison
+// as wstat_observe, NaN never wins); n_pos is the remainder of the observed count.
+template <typename WT>
+struct WTally {
+  uint32_t nonfinite = 0, zero = 0, neg = 0, notnormal = 0;
+  WT max = (WT)-1;
+};
+template <typename WT>
+__device__ __forceinline__ void wtally_observe(WTally<WT>& c, WT v) {
+  bool nf, zero, negb, sub;
+  if constexpr (sizeof(WT) == 4) {
+    const uint32_t bits = __float_as_uint(v), ex = (bits >> 23) & 0xFFu;
+    nf = ex == 0xFFu;
+    zero = (bits & 0x7FFFFFFFu) == 0;
+    negb = (bits >> 31) != 0;
+    sub = ex == 0;
+  } else {
+    const uint64_t bits = (uint64_t)__double_as_longlong(v);
+    const uint32_t ex = (uint32_t)(bits >> 52) & 0x7FFu;
+    nf = ex == 0x7FFu;
+    zero = (bits & 0x7FFFFFFFFFFFFFFFull) == 0;
+    negb = (bits >> 63) != 0;
+    sub = ex == 0;
+  }
+  c.nonfinite += nf;
+  c.zero += !nf && zero;
+  c.neg += !nf && !zero && negb;
+  c.notnormal += sub || nf || negb;
+  c.max = v > c.max ? v : c.max;
+}
+
 // One CTA per chunk.  The chunk's elements are staged (coalesced) into shared memory as
 // float64; its subtree is built level by level; each leaf (<= 128 elements) is summed by
 // 8 lanes, lane j owning numpy's accumulator r[j] (elements j, j+8, j+16, ...), then
@@ -755,30 +787,37 @@ __global__ void __launch_bounds__(PW_THREADS) k_pw_chunks4096(Elem e, const WT* 
   const int64_t lo0 = (int64_t)blockIdx.x * PW_CHUNK;
   const int leaf = threadIdx.x >> 3, jl = threadIdx.x & 7;
   const int64_t base = lo0 + leaf * 128 + jl;
-  double r = e(base);
-  WStats st{-1.0, 0, 0, 0, 0, 0};
-  if constexpr (STATS) wstat_observe<WT>(st, wraw[base]);
+  double r;
+  if constexpr (STATS) {  // Elem is ElemWeight<WT>: one load per element serves both
+    WTally<WT> c;
+    const WT v0 = wraw[base];
+    r = (double)v0;
+    wtally_observe<WT>(c, v0);
 #pragma unroll
-  for (int q = 1; q < 16; ++q) {
-    r = __dadd_rn(r, e(base + 8 * q));
-    if constexpr (STATS) wstat_observe<WT>(st, wraw[base + 8 * q]);
+    for (int q = 1; q < 16; ++q) {
+      const WT v = wraw[base + 8 * q];
+      r = __dadd_rn(r, (double)v);
+      wtally_observe<WT>(c, v);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const WT o = __shfl_xor_sync(0xffffffffu, c.max, off);
+      c.max = o > c.max ? o : c.max;
+    }
+    const uint32_t nf = __reduce_add_sync(0xffffffffu, c.nonfinite), nz = __reduce_add_sync(0xffffffffu, c.zero),
+                   nn = __reduce_add_sync(0xffffffffu, c.neg), nb = __reduce_add_sync(0xffffffffu, c.notnormal);
+    if ((threadIdx.x & 31) == 0)
+      s_red[threadIdx.x >> 5] = WStats{(double)c.max, (int64_t)(32 * 16 - nf - nz - nn), (int64_t)nz, (int64_t)nn,
+                                       (int64_t)nf, (int64_t)nb};
+  } else {
+    r = e(base);
+#pragma unroll
+    for (int q = 1; q < 16; ++q) r = __dadd_rn(r, e(base + 8 * q));
   }
   r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
   r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
   r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
   if (jl == 0) s_leaf[leaf] = r;
-  if constexpr (STATS) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      st.max = fmax(st.max, __shfl_xor_sync(0xffffffffu, st.max, off));
-      st.n_pos += __shfl_xor_sync(0xffffffffu, st.n_pos, off);
-      st.n_zero += __shfl_xor_sync(0xffffffffu, st.n_zero, off);
-      st.n_neg += __shfl_xor_sync(0xffffffffu, st.n_neg, off);
-      st.n_nonfinite += __shfl_xor_sync(0xffffffffu, st.n_nonfinite, off);
-      st.n_notnormal += __shfl_xor_sync(0xffffffffu, st.n_notnormal, off);
-    }
-    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = st;
-  }
   __syncthreads();
   if (threadIdx.x < 32) {
     double v = s_leaf[threadIdx.x];
