@@ -408,6 +408,27 @@ def main():
         te_o = e2e_time(_lib.RNG[other])
         res[other]["e2e"] = {"value": n_loc * world / te_o, "ms_per_step": te_o * 1e3}
 
+        # the B-rule reduction, H2D (4N B) and D2H (8N B) reported separately
+        # (CUDA events, outside the timed region, median of 5)
+        def ev_ms(fn, reps=5):
+            out = []
+            for _ in range(reps):
+                a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                fn()
+                z.record(stream)
+                z.synchronize()
+                out.append(a.elapsed_time(z))
+            return statistics.median(out)
+
+        d_w = torch.empty(n_loc, dtype=torch.float32, device=dev)
+        h2d = ev_ms(lambda: d_w.copy_(h_w, non_blocking=True))
+        d2h = ev_ms(lambda: h_anc.copy_(anc, non_blocking=True))
+        brule = ev_ms(lambda: _lib.check(L.mgp_weight_stats(D.ptr(d_w), 0, n_loc, D.ptr(stats), sp)))
+        e2e["transfers"] = {"h2d_ms": h2d, "h2d_GBps": 4 * n_loc / h2d / 1e6, "d2h_ms": d2h,
+                            "d2h_GBps": 8 * n_loc / d2h / 1e6, "b_rule_ms": brule}
+        del d_w
+
     # quality (offspring MSE / bias, M/metrics.py) outside the timed region.  N > 1: the sharded
     # path (stripes-layout resample -> owner-bucketed offspring -> ShardedQuality), which equals
     # one device's QualityAccumulator over the whole population bit for bit.
