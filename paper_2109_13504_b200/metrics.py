@@ -26,6 +26,32 @@ class QualityStats:  # M/metrics.py:33-39
     mse_per_particle: float
 
 
+@dataclass(frozen=True)
+class RunTimings:  # M/metrics.py:42-52: seconds in predict+update, resample, estimate
+    stage1: float
+    stage2: float
+    stage3: float
+
+    def __post_init__(self):
+        if min(self.stage1, self.stage2, self.stage3) < 0:
+            raise ValueError("stage timings must be non-negative")
+
+
+def rmse(truth, estimates) -> float:  # M/metrics.py:124-136 (host: T filter estimates)
+    truth = np.asarray(truth, dtype=np.float64)
+    estimates = np.asarray(estimates, dtype=np.float64)
+    if estimates.ndim != 2 or estimates.shape[1] != truth.shape[0]:
+        raise ValueError(f"estimates shape {estimates.shape} does not match truth length {truth.shape}")
+    return float(np.sqrt(np.mean((estimates - truth[None, :]) ** 2, axis=0)).mean())
+
+
+def resample_ratio(timings: RunTimings) -> float:  # M/metrics.py:139-144
+    total = timings.stage1 + timings.stage2 + timings.stage3
+    if total <= 0:
+        raise ValueError("total stage time must be positive")
+    return timings.stage2 / total
+
+
 def _dev_weights(w):
     t = D.torch()
     wv = _as_weight_vector(w)

@@ -27,7 +27,7 @@ import numpy as np
 
 from . import _device as D
 from . import _lib
-from .metrics import QualityStats  # noqa: F401  (re-export convenience)
+from .metrics import QualityStats, RunTimings, resample_ratio, rmse  # noqa: F401  (M/metrics.py names)
 from .resample import METROPOLIS_FAMILY, WarpConfig
 from .rng import derive_seed, gaussian_at
 from .weights import compute_iterations
@@ -64,17 +64,6 @@ class Trajectory:  # M/pfilter.py:68-75
     def __post_init__(self):
         if len(self.truth) != len(self.observations) or len(self.truth) < 1:
             raise ValueError("truth and observations must have equal positive length")
-
-
-@dataclass(frozen=True)
-class RunTimings:  # M/metrics.py:42-52
-    stage1: float
-    stage2: float
-    stage3: float
-
-    def __post_init__(self):
-        if min(self.stage1, self.stage2, self.stage3) < 0:
-            raise ValueError("stage timings must be non-negative")
 
 
 @dataclass
@@ -245,21 +234,6 @@ def run_filter(cfg: FilterConfig, trajectory: Trajectory, seed):  # M/pfilter.py
             stages += (tm.stage1, tm.stage2, tm.stage3)
     stages /= t_steps
     return estimates, RunTimings(*stages)
-
-
-def rmse(truth, estimates) -> float:  # M/metrics.py:124-136
-    truth = np.asarray(truth, dtype=np.float64)
-    estimates = np.asarray(estimates, dtype=np.float64)
-    if estimates.ndim != 2 or estimates.shape[1] != truth.shape[0]:
-        raise ValueError(f"estimates shape {estimates.shape} does not match truth length {truth.shape}")
-    return float(np.sqrt(np.mean((estimates - truth[None, :]) ** 2, axis=0)).mean())
-
-
-def resample_ratio(timings: RunTimings) -> float:  # M/metrics.py:139-144
-    total = timings.stage1 + timings.stage2 + timings.stage3
-    if total <= 0:
-        raise ValueError("total stage time must be positive")
-    return timings.stage2 / total
 
 
 def run_benchmark(base_cfg: FilterConfig, trajectories, runs_per_trajectory: int, b_values, algorithms, seed=0):
