@@ -1,4 +1,4 @@
-"""Host-side seed helpers and lane constants of the reference stream (M/rng.py).
+"""Host-side mirror of the reference stream's API (M/rng.py): seeds, lane constants, draws.
 
 The per-draw hash itself runs on the device (csrc/mgp_device.cuh); callers only
 need the seed derivation to build per-run seeds exactly like the reference's
@@ -78,3 +78,52 @@ def uniform_open01_at(seed, lane, counter):  # M/rng.py:134-137
 
     h = _hash_np(seed, lane, counter)
     return ((h >> np.uint64(11)).astype(np.float64) + 0.5) * (1.0 / 9007199254740992.0)
+
+
+def uniform_int_at(seed, lane, counter, n):  # M/rng.py:140-149: floor(u * n), clamped
+    import numpy as np
+
+    if n < 1:
+        raise ValueError(f"n must be >= 1, got {n}")
+    v = (uniform01_at(seed, lane, counter) * n).astype(np.int64)
+    return np.minimum(v, n - 1)
+
+
+# ---------------------------------------------------------------------------
+# Scalar API (M/rng.py:59-64, 92-121, 164-177): the same values as the array API and as the
+# device's per-draw hash (csrc/mgp_device.cuh).
+
+from dataclasses import dataclass  # noqa: E402
+
+
+@dataclass(frozen=True)
+class StreamKey:  # M/rng.py:59-64: coordinates of a single random draw
+    seed: int
+    lane: int
+    counter: int
+
+
+def hash_u64(seed, lane, counter, salt=0) -> int:  # M/rng.py:92-102
+    base = _mix((int(seed) + _M_LANE) & _MASK)
+    return _mix((base + int(lane) * _M_LANE + int(counter) * _M_CTR + int(salt) * _M_SALT) & _MASK)
+
+
+def u01(seed, lane, counter) -> float:  # M/rng.py:105-108
+    return float(hash_u64(seed, lane, counter) >> 11) * (1.0 / 9007199254740992.0)
+
+
+def uint_below(seed, lane, counter, n) -> int:  # M/rng.py:111-121
+    v = int(u01(seed, lane, counter) * float(n))
+    return n - 1 if v >= n else v
+
+
+def uniform01(key: StreamKey) -> float:
+    return float(uniform01_at(key.seed, key.lane, key.counter))
+
+
+def uniform_int(key: StreamKey, n: int) -> int:
+    return int(uniform_int_at(key.seed, key.lane, key.counter, n))
+
+
+def gaussian(key: StreamKey, mean: float = 0.0, stddev: float = 1.0) -> float:
+    return float(gaussian_at(key.seed, key.lane, key.counter, mean, stddev))
