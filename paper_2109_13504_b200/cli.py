@@ -86,6 +86,9 @@ def algorithm_token(token: str):
     return name, part_bytes
 
 
+parse_algorithm = algorithm_token  # the reference's name (M/bench.py:88)
+
+
 def token_id(token: str) -> int:
     """The algorithm's seed coordinate: its first 8 bytes, little-endian (M/bench.py:83-85)."""
     return int.from_bytes(token.encode()[:8].ljust(8, b"\0"), "little")
