@@ -687,3 +687,39 @@ def test_resample_gather_stripes(mg, oracle, kind, rng, n, b, cols, world):
         want = np.concatenate([ref[lo0:lo1], ref[half + lo0:half + lo1]])
         assert np.array_equal(anc.cpu().numpy(), want), r
         assert torch.equal(out, rows_full[torch.from_numpy(want).cuda()]), r
+
+
+def test_concurrent_host_threads(mg, oracle):
+    """SURVEY 8b threading contract: the entry points are reentrant.  Eight host threads call the
+    host-buffer path concurrently (ctypes releases the GIL) with different weights, seeds and
+    streams; every result equals the oracle's, and a failing call's message stays in its own
+    thread (mgp_last_error is thread-local)."""
+    import threading
+
+    results, errors = {}, {}
+
+    def work(k):
+        try:
+            n = 4096 * (1 + k % 3)
+            w = oracle.gen_gaussian_weights(1.0 + k % 4, n, 500 + k, "single")
+            rng = "philox" if k % 2 else "megores"
+            for rep in range(3):
+                anc = mg.megopolis(w, 5 + k, seed=k * 10 + rep, rng=rng)
+                ok = np.array_equal(anc, oracle.megopolis(w, 5 + k, seed=k * 10 + rep, rng=rng))
+                results[(k, rep)] = ok
+            if k == 3:  # an invalid call: its message must be this thread's
+                try:
+                    mg.megopolis(np.zeros(64, np.float32), 4, seed=1)
+                except ValueError as exc:
+                    errors[k] = str(exc)
+        except Exception as exc:  # pragma: no cover - reported below
+            errors[("fail", k)] = repr(exc)
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(8)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=300)
+    assert not [k for k in errors if isinstance(k, tuple)], errors
+    assert len(results) == 24 and all(results.values())
+    assert errors.get(3) == "all weights are zero"
