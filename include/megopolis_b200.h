@@ -147,7 +147,8 @@ int mgp_resample_stripes(int kind, const void *d_w, int dtype, int64_t n, int32_
 /* Host-buffer drop-in for make_resampler(kind, ...)(w, b, seed) (M/resample.py:431-455):
  * copies h_w to the device, validates (WeightVector + _check_weights), derives B
  * from epsilon when b <= 0 (reporting it in *b_used), resamples, and streams the
- * ancestors back into h_anc overlapped with the remaining compute. */
+ * ancestors back into h_anc overlapped with the remaining compute.  device: the CUDA device
+ * to run on (-1: the calling thread's current device, which is left unchanged either way). */
 int mgp_resample_host(int kind, const void *h_w, int dtype, int64_t n, int32_t b, double epsilon, uint64_t seed,
                       int32_t warp, int32_t partition_bytes, int strict, int rng, int64_t *h_anc, int32_t *b_used,
                       int device);

@@ -756,7 +756,16 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
   if (dtype != MGP_F32 && dtype != MGP_F64) return set_err(MGP_EINVAL, "dtype must be MGP_F32 or MGP_F64");
   if (n < 1) return set_err(MGP_EINVAL, "weights must be a non-empty 1-d sequence");
   if (n > MAX_N) return set_err(MGP_EUNSUPPORTED, "N exceeds 2^31-1");
-  if (device >= 0) CUDA_TRY(cudaSetDevice(device));
+  struct DeviceGuard {  // the caller's current device is restored on every return
+    int prev = -1;
+    ~DeviceGuard() {
+      if (prev >= 0) cudaSetDevice(prev);
+    }
+  } guard;
+  if (device >= 0) {
+    CUDA_TRY(cudaGetDevice(&guard.prev));
+    CUDA_TRY(cudaSetDevice(device));
+  }
   ensure_pool();
   HostCtx* hc = nullptr;
   if (int rc0 = host_ctx(&hc)) return rc0;

@@ -723,3 +723,18 @@ def test_concurrent_host_threads(mg, oracle):
     assert not [k for k in errors if isinstance(k, tuple)], errors
     assert len(results) == 24 and all(results.values())
     assert errors.get(3) == "all weights are zero"
+
+
+def test_host_path_keeps_current_device(mg, oracle):
+    """mgp_resample_host(device=d) runs on d and leaves the caller's current device as it was."""
+    import ctypes
+
+    from paper_2109_13504_b200 import _lib
+
+    w = oracle.gen_gaussian_weights(1.0, 4096, 3, "single")
+    anc = np.empty(4096, dtype=np.int64)
+    before = torch.cuda.current_device()
+    _lib.check(_lib.lib().mgp_resample_host(3, w.ctypes.data, 0, 4096, 5, 0.01, 9, 32, 0, 1, 0, anc.ctypes.data,
+                                            None, torch.cuda.device_count() - 1))
+    assert torch.cuda.current_device() == before
+    assert np.array_equal(anc, oracle.megopolis(w, 5, seed=9))
