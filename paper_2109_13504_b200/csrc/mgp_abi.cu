@@ -228,6 +228,13 @@ int launch_mego_w32(const ResampleArgs& a, const OffChunk& oc, cudaStream_t st) 
       return 0;
     }
   }
+  if constexpr (RNG == RNG_MEGORES && sizeof(WT) == 4 && NZ && TEX) {
+    // the reference's stream on float32 weights: float32 bracket + exact fallback
+    if (a.rows_out) k_megopolis_megores_f32<POW2, true><<<grid, RS_THREADS, 0, st>>>(a, oc);
+    else k_megopolis_megores_f32<POW2><<<grid, RS_THREADS, 0, st>>>(a, oc);
+    LAUNCH_CHECK("k_megopolis_megores_f32");
+    return 0;
+  }
   if (a.rows_out) k_megopolis_w32<RNG, WT, POW2, NZ, TEX, PPT, false, true><<<grid, RS_THREADS / PPT, 0, st>>>(a, oc);
   else k_megopolis_w32<RNG, WT, POW2, NZ, TEX, PPT><<<grid, RS_THREADS / PPT, 0, st>>>(a, oc);
   LAUNCH_CHECK("k_megopolis_w32");
@@ -1529,5 +1536,16 @@ extern "C" int mgp_philox_selftest(uint64_t key, uint32_t c1, uint32_t c2, uint3
   unsigned long long h = 0;
   CUDA_TRY(cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost));
   *h_mismatch = (int64_t)h;
+  return 0;
+}
+
+extern "C" int mgp_debug_megores_fallbacks(int64_t* h_count, int reset) {
+  unsigned long long h = 0;
+  CUDA_TRY(cudaMemcpyFromSymbol(&h, g_megores_fallbacks, sizeof h));
+  if (reset) {
+    const unsigned long long z = 0;
+    CUDA_TRY(cudaMemcpyToSymbol(g_megores_fallbacks, &z, sizeof z));
+  }
+  *h_count = (int64_t)h;
   return 0;
 }

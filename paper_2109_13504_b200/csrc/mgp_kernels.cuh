@@ -373,6 +373,87 @@ __global__ void __launch_bounds__(64, 1) k_megopolis_philox_half(const __grid_co
 }
 
 // ---------------------------------------------------------------------------
+// The reference's own stream (megores), float32 weights, no zero weights: a float32 bracket of
+// the float64 decision with an exact fallback.
+//
+// The reference accepts iff fl64(u * wk) <= wj with u = h53 * 2^-53 (M/resample.py:118-122,
+// M/rng.py:105-108).  The top 23 bits of h53 are bits 31..9 of the high word of the second
+// splitmix product m (the final xorshift x ^ (x >> 31) only touches bit 0 of the high word),
+// so u lies in [u23, u23 + 2^-23) with u23 = (m_hi >> 9) * 2^-23, assembled from bits as the
+// float 1 + u23 (one LEA.HI).  Two directed-rounding FFMAs bracket the product:
+//   lo = fl_down((1 + u23) wk - wk) <= u23 wk <= u wk,
+//   hi = fl_up(lo + 2^-22 wk) >= u23 wk + 2^-23 wk > u wk     (lo >= u23 wk - ulp(u23 wk) and
+//        ulp(u23 wk) <= 2^-23 wk).
+// hi <= wj  => u wk <= wj => fl64(u wk) <= wj: accept.
+// lo >  wj  => u wk >= lo >= wj + ulp32(wj) > wj + ulp64(wj) / 2 => fl64(u wk) > wj: reject.
+// Otherwise (probability ~2^-21 per comparison) the round is ambiguous: the lane records it,
+// and after the loop every lane that saw one re-runs its rounds with the exact float64 rule
+// (megores_exact_rounds).  The result is the reference's bit for bit, while the common path
+// needs neither the low half of the second product, the final xorshift, the 64-bit integer
+// conversion (I2F.F64.U64, conversion pipe) nor any float64 instruction: 32.5 instructions
+// per round instead of 38.75 (scripts/mb/mb_mego.cu "z H--- 1u8": 7.82 -> 6.78 ms at 2^24,
+// B = 354).  Subnormal weights are exact too: the FFMAs are IEEE with denormals (no ftz).
+
+// high word of mix64's second product m = v * MIX2 (mod 2^64), v = z ^ (z >> 27)
+__device__ __forceinline__ uint32_t mix64_mhi(uint64_t x) {
+  x = (x ^ (x >> 30)) * MIX1;
+  x ^= x >> 27;
+  const uint32_t vlo = (uint32_t)x, vhi = (uint32_t)(x >> 32);
+  return __umulhi(vlo, (uint32_t)MIX2) + vlo * (uint32_t)(MIX2 >> 32) + vhi * (uint32_t)MIX2;
+}
+
+__device__ unsigned long long g_megores_fallbacks;  // diagnostic count (mgp_debug_megores_fallbacks)
+
+// One particle's rounds [0, cnt) of a launch with the exact float64 decision; returns the last
+// accepted round (-1: none).  wk is the weight of the particle's state at the launch start.
+__device__ __noinline__ int megores_exact_rounds(const ResampleArgs& a, const OffChunk& oc, uint32_t i, float wk,
+                                                 bool pow2) {
+  atomicAdd(&g_megores_fallbacks, 1ull);
+  const uint32_t lane = i & 31u, ial = i - lane;
+  uint64_t x = megores_key(a.base, i, (uint64_t)a.b0);
+  int bstar = -1;
+  for (int t = 0; t < a.cnt; ++t) {
+    const uint32_t j = pow2 ? mego_j<true>(ial, lane, oc.o[t], a.n) : mego_j<false>(ial, lane, oc.o[t], a.n);
+    const float wj = tex1Dfetch<float>(a.tex, (int)j);
+    const double u = (double)mix64_m53(x) * 0x1p-53;  // u01 (M/rng.py:105-108)
+    if (u * (double)wk <= (double)wj) { wk = wj; bstar = t; }
+    x += M_CTR;
+  }
+  return bstar;
+}
+
+// One particle per thread (2 or 4 particles per thread, with or without the half split, measured
+// no faster: scripts/mb/mb_mego.cu "z H--- 2 / 2h / 4h").
+template <bool POW2, bool ROWS = false>
+__global__ void __launch_bounds__(RS_THREADS) k_megopolis_megores_f32(const __grid_constant__ ResampleArgs a,
+                                                                     const __grid_constant__ OffChunk oc) {
+  const uint32_t i = a.p0 + blockIdx.x * RS_THREADS + threadIdx.x;
+  if (i >= a.p_end) return;
+  const uint32_t lane = threadIdx.x & 31u, ial = i - lane, n = a.n;
+  const uint32_t k0 = a.first ? i : (uint32_t)a.kstate[i];
+  const float wk0 = tex1Dfetch<float>(a.tex, (int)k0);
+  float wk = wk0;
+  int bstar = -1, amb = -1;
+  uint64_t x = megores_key(a.base, i, (uint64_t)a.b0);
+#pragma unroll 8
+  for (int t = 0; t < a.cnt; ++t) {
+    const uint32_t j = mego_j<POW2>(ial, lane, oc.o[t], n);
+    const float wj = tex1Dfetch<float>(a.tex, (int)j);
+    const float u1 = __uint_as_float(0x3F800000u + (mix64_mhi(x) >> 9));  // 1 + u23
+    const float lo = __fmaf_rd(u1, wk, -wk);
+    const float hi = __fmaf_ru(wk, 0x1p-22f, lo);
+    const bool acc = hi <= wj;
+    if (!acc && lo <= wj) amb = t;
+    if (acc) { wk = wj; bstar = t; }
+    x += M_CTR;
+  }
+  if (amb >= 0) bstar = megores_exact_rounds(a, oc, i, wk0, POW2);
+  uint32_t k = k0;
+  if (bstar >= 0) k = mego_j<POW2>(ial, lane, oc.o[bstar], n);
+  store_result<ROWS>(a, (int64_t)i, i, k);
+}
+
+// ---------------------------------------------------------------------------
 // Metropolis (uniform random partner; the uncoalesced baseline, M/resample.py:125-138)
 
 template <int RNG, typename WT, bool POW2, bool NOZERO>

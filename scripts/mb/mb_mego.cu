@@ -14,86 +14,236 @@ using namespace mgp;
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); exit(1);} } while (0)
 
-// state = wk * 2^-53 in float64 (exact for float32 weights), predicated update;
-// TPARAM: the round counter comes from the parameter space (defeats strength reduction of
-// the 64-bit key update onto the ALU pipe).
-struct OffChunk4 { uint4 o[1024]; };  // {o_al, o_lo, t, 0}
-template <bool TPARAM, int UNROLL>
-__global__ void __launch_bounds__(256) k_vw(const __grid_constant__ ResampleArgs a, const __grid_constant__ OffChunk4 oc) {
+// ---- variants of k_megopolis_megores_f32 (PPT 1) ----
+// z = y * MIX1 (mod 2^64) as IMAD.WIDE.U32(ylo, C_lo, {0, t}) with t = yhi*C_lo + ylo*C_hi
+__device__ __forceinline__ uint64_t mul64_wide(uint64_t y, uint64_t c) {
+  uint64_t r;
+  asm("{\n\t.reg .u32 lo, hi, t, z;\n\t.reg .u64 a;\n\t"
+      "mov.b64 {lo, hi}, %1;\n\t"
+      "mul.lo.u32 t, hi, %2;\n\t"
+      "mad.lo.u32 t, lo, %3, t;\n\t"
+      "mov.u32 z, 0;\n\t"
+      "mov.b64 a, {z, t};\n\t"
+      "mad.wide.u32 %0, lo, %2, a;\n\t}"
+      : "=l"(r) : "l"(y), "r"((uint32_t)c), "r"((uint32_t)(c >> 32)));
+  return r;
+}
+template <int MUL>
+__device__ __forceinline__ uint32_t mhi_v(uint64_t x) {
+  x ^= x >> 30;
+  x = MUL ? mul64_wide(x, MIX1) : x * MIX1;
+  x ^= x >> 27;
+  const uint32_t vlo = (uint32_t)x, vhi = (uint32_t)(x >> 32);
+  return __umulhi(vlo, (uint32_t)MIX2) + vlo * (uint32_t)(MIX2 >> 32) + vhi * (uint32_t)MIX2;
+}
+// FADD: uf1u = uf1 + 2^-23 on the FMA pipe; MUL: wide multiply; XF: x += M_CTR on the FMA pipe;
+// AMBP: ambiguity flag as a predicated store of the round
+template <bool FADD, int MUL, bool XF, bool AMBP, int UNR>
+__global__ void __launch_bounds__(256) k_mv(const __grid_constant__ ResampleArgs a, const __grid_constant__ OffChunk oc) {
   const uint32_t i = a.p0 + blockIdx.x * 256 + threadIdx.x;
   if (i >= a.p_end) return;
-  const uint32_t lane = threadIdx.x & 31u, i_al = i - lane;
-  const uint32_t cmask = (a.n - 1) & ~31u;
-  double wks = (double)tex1Dfetch<float>(a.tex, (int)i) * 0x1p-53;
-  int bstar = -1;
-  const uint64_t x0 = megores_key(a.base, i, (uint64_t)a.b0);
-  uint64_t x = x0;
-#pragma unroll UNROLL
+  const uint32_t lane = i & 31u, ial = i - lane, cmask = (a.n - 1) & ~31u;
+  float wk = tex1Dfetch<float>(a.tex, (int)i);
+  const float wk0 = wk;
+  int bstar = -1, ambt = -1;
+  bool amb = false;
+  uint64_t x = megores_key(a.base, i, (uint64_t)a.b0);
+#pragma unroll UNR
   for (int t = 0; t < a.cnt; ++t) {
-    const uint4 o = oc.o[t];
-    const uint32_t j = mux3(i_al + o.x, lane + o.y, cmask);
-    const double wj = (double)tex1Dfetch<float>(a.tex, (int)j);
-    const uint64_t xx = TPARAM ? x0 + (uint64_t)o.z * M_CTR : x;
-    x += M_CTR;
-    const double p = (double)mix64_m53(xx) * wks;  // == fl(u * wk) exactly
-    if (p <= wj) { wks = wj * 0x1p-53; bstar = t; }
+    const uint2 o = oc.o[t];
+    const uint32_t j = mux3(ial + o.x, lane + o.y, cmask);
+    const float wj = tex1Dfetch<float>(a.tex, (int)j);
+    const uint32_t top = mhi_v<MUL>(x) >> 9;
+    const float u1 = __uint_as_float(0x3F800000u + top);
+    const float u1u = FADD ? __fadd_rn(u1, 0x1p-23f) : __uint_as_float(0x3F800001u + top);
+    const float lo = __fmaf_rd(u1, wk, -wk);
+    const float hi = __fmaf_ru(u1u, wk, -wk);
+    const bool acc = hi <= wj;
+    if (AMBP) { if (!acc && lo <= wj) ambt = t; }
+    else amb |= !acc && lo <= wj;
+    if (acc) { wk = wj; bstar = t; }
+    x = XF ? add64_fma(x, a.one) : x + M_CTR;
   }
+  if (AMBP ? ambt >= 0 : amb) bstar = megores_exact_rounds(a, oc, i, wk0, true);
   uint32_t k = i;
-  if (bstar >= 0) { const uint4 o = oc.o[bstar]; k = mux3(i_al + o.x, lane + o.y, cmask); }
+  if (bstar >= 0) k = mux3(ial + oc.o[bstar].x, lane + oc.o[bstar].y, cmask);
   a.anc[i] = (int64_t)k;
 }
 
+struct OffChunkX { uint4 o[1024]; };  // {o & ~31, o & 31, lo(t*M_CTR), hi(t*M_CTR)}
+__device__ __forceinline__ uint32_t imad_add(uint32_t a, uint32_t b, uint32_t one) {
+  uint32_t r; asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(b), "r"(one), "r"(a)); return r;
+}
+__device__ __forceinline__ uint32_t imad_hi(uint32_t a, uint32_t m) {  // (a * m) >> 32
+  uint32_t r; asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(m)); return r;
+}
+// x0 + c (64-bit) as IMAD.WIDE.U32(one, c_lo, x0) + IMAD(one, c_hi, hi)
+__device__ __forceinline__ uint64_t add64_wide(uint64_t x0, uint32_t clo, uint32_t chi, uint32_t one) {
+  uint64_t r;
+  asm("{\n\t.reg .u32 lo, hi;\n\t"
+      "mad.wide.u32 %0, %1, %2, %3;\n\t"
+      "mov.b64 {lo, hi}, %0;\n\t"
+      "mad.lo.u32 hi, %1, %4, hi;\n\t"
+      "mov.b64 %0, {lo, hi};\n\t}"
+      : "=l"(r) : "r"(one), "r"(clo), "l"(x0), "r"(chi));
+  return r;
+}
+// IDX: index adds on the FMA pipe; XW: x = x0 + C_t (param) on the FMA pipe; SH: the high-word
+// shifts of both xorshifts as IMAD.HI (m = 4, 32 from the parameter space); AMBP: predicated amb
+template <bool IDX, bool XW, bool SH, bool AMBP>
+__global__ void __launch_bounds__(256) k_mw(const __grid_constant__ ResampleArgs a, const __grid_constant__ OffChunkX oc,
+                                           const __grid_constant__ OffChunk oc2, uint32_t m4, uint32_t m32) {
+  const uint32_t i = a.p0 + blockIdx.x * 256 + threadIdx.x;
+  if (i >= a.p_end) return;
+  const uint32_t lane = i & 31u, ial = i - lane, cmask = (a.n - 1) & ~31u, one = a.one;
+  float wk = tex1Dfetch<float>(a.tex, (int)i);
+  const float wk0 = wk;
+  int bstar = -1, ambt = -1;
+  bool amb = false;
+  const uint64_t x0 = megores_key(a.base, i, (uint64_t)a.b0);
+  uint64_t x = x0;
+#pragma unroll 4
+  for (int t = 0; t < a.cnt; ++t) {
+    const uint4 o = oc.o[t];
+    const uint32_t j = IDX ? mux3(imad_add(ial, o.x, one), imad_add(lane, o.y, one), cmask) : mux3(ial + o.x, lane + o.y, cmask);
+    const float wj = tex1Dfetch<float>(a.tex, (int)j);
+    const uint64_t xx = XW ? add64_wide(x0, o.z, o.w, one) : x;
+    uint64_t y;
+    if (SH) {
+      const uint32_t lo = (uint32_t)xx, hi = (uint32_t)(xx >> 32);
+      y = ((uint64_t)(hi ^ imad_hi(hi, m4)) << 32) | (uint32_t)(lo ^ ((uint32_t)(xx >> 30)));
+    } else y = xx ^ (xx >> 30);
+    uint64_t z = y * MIX1, v;
+    if (SH) {
+      const uint32_t lo = (uint32_t)z, hi = (uint32_t)(z >> 32);
+      v = ((uint64_t)(hi ^ imad_hi(hi, m32)) << 32) | (uint32_t)(lo ^ ((uint32_t)(z >> 27)));
+    } else v = z ^ (z >> 27);
+    const uint32_t vlo = (uint32_t)v, vhi = (uint32_t)(v >> 32);
+    const uint32_t top = (__umulhi(vlo, (uint32_t)MIX2) + vlo * (uint32_t)(MIX2 >> 32) + vhi * (uint32_t)MIX2) >> 9;
+    const float u1 = __uint_as_float(0x3F800000u + top);
+    const float u1u = __fadd_rn(u1, 0x1p-23f);
+    const float lo = __fmaf_rd(u1, wk, -wk);
+    const float hi = __fmaf_ru(u1u, wk, -wk);
+    const bool acc = hi <= wj;
+    if (AMBP) { if (!acc && lo <= wj) ambt = t; }
+    else amb |= !acc && lo <= wj;
+    if (acc) { wk = wj; bstar = t; }
+    if (!XW) x += M_CTR;
+  }
+  if (AMBP ? ambt >= 0 : amb) bstar = megores_exact_rounds(a, oc2, i, wk0, true);
+  uint32_t k = i;
+  if (bstar >= 0) k = mux3(ial + oc.o[bstar].x, lane + oc.o[bstar].y, cmask);
+  a.anc[i] = (int64_t)k;
+}
 
-// Philox, two particles per thread (i and i + 128 of a 256-particle block): two independent
-// Philox chains interleaved per thread.
-template <int PPT>
-__global__ void __launch_bounds__(256 / PPT) k_vp2(const __grid_constant__ ResampleArgs a, const __grid_constant__ OffChunk oc) {
-  const uint32_t blk = a.p0 + blockIdx.x * 256;
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t cmask = (a.n - 1) & ~31u;
+// x = x0 + c with add.cc / addc
+__device__ __forceinline__ uint64_t add64_cc(uint64_t x0, uint32_t clo, uint32_t chi) {
+  uint64_t r;
+  asm("{\n\t.reg .u32 a, b, lo, hi;\n\t"
+      "mov.b64 {a, b}, %1;\n\t"
+      "add.cc.u32 lo, a, %2;\n\t"
+      "addc.u32 hi, b, %3;\n\t"
+      "mov.b64 %0, {lo, hi};\n\t}"
+      : "=l"(r) : "l"(x0), "r"(clo), "r"(chi));
+  return r;
+}
+// HI1: upper bound from lo (hi = fl_up(lo + wk 2^-22)); XC: x = x0 + C_t (param, add.cc);
+// PPT / HALF as the library kernel
+template <bool HI1, int XC, int PPT, bool HALF, int UNR, bool LEAH = false, int MINB = 0>
+__global__ void __launch_bounds__(256 / PPT, MINB) k_mz(const __grid_constant__ ResampleArgs a, const __grid_constant__ OffChunkX oc,
+                                                 const __grid_constant__ OffChunk ocx) {
+  constexpr int PH = HALF ? PPT / 2 : PPT;
+  constexpr int STRIDE = HALF ? 128 / PH : 256 / PPT;
+  const uint32_t half = a.n >> 1;
+  const uint32_t i0 = HALF ? a.p0 + blockIdx.x * 128 + threadIdx.x : a.p0 + blockIdx.x * 256 + threadIdx.x;
+  const uint32_t lane = threadIdx.x & 31u, cmask = (a.n - 1) & ~31u;
   uint32_t ii[PPT], ial[PPT];
-  double wkd[PPT];
-  int bstar[PPT];
+  float wk[PPT], wk0[PPT];
+  int bstar[PPT], ambt[PPT];
+  uint64_t x0[PPT], x[PPT];
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
-    ii[p] = blk + threadIdx.x + p * (256 / PPT);
+    ii[p] = HALF ? i0 + (p % PH) * STRIDE + (p / PH) * half : i0 + p * STRIDE;
     ial[p] = ii[p] - lane;
-    wkd[p] = (double)tex1Dfetch<float>(a.tex, (int)ii[p]);
-    bstar[p] = -1;
+    wk[p] = wk0[p] = tex1Dfetch<float>(a.tex, (int)ii[p]);
+    bstar[p] = -1; ambt[p] = -1;
+    x[p] = x0[p] = megores_key(a.base, ii[p], (uint64_t)a.b0);
   }
-  const int full = a.cnt & ~3;
-  for (int t0 = 0; t0 < full; t0 += 4) {
-    uint32_t c0[PPT], c1[PPT], c2[PPT], c3[PPT];
+#pragma unroll UNR
+  for (int t = 0; t < a.cnt; ++t) {
+    const uint4 o = oc.o[t];
+    const uint2 ot = make_uint2(o.z, o.w);  // XC 2/3: {t, 1}
+    uint32_t jj[PPT];
 #pragma unroll
-    for (int p = 0; p < PPT; ++p) { c0[p] = ii[p]; c1[p] = 0; c2[p] = (uint32_t)((a.b0 + t0) >> 2); c3[p] = 0; }
+    for (int p = 0; p < PH; ++p) jj[p] = mux3(ial[p] + o.x, lane + o.y, cmask);
 #pragma unroll
-    for (int r = 0; r < 10; ++r) {
+    for (int p = PH; p < PPT; ++p) jj[p] = jj[p - PH] ^ half;
 #pragma unroll
-      for (int p = 0; p < PPT; ++p) {
-        const uint64_t q0 = (uint64_t)PHILOX_M0 * c0[p], q1 = (uint64_t)PHILOX_M1 * c2[p];
-        const uint32_t n0 = (uint32_t)(q1 >> 32) ^ c1[p] ^ a.pk0[r], n2 = (uint32_t)(q0 >> 32) ^ c3[p] ^ a.pk1[r];
-        c1[p] = (uint32_t)q1; c3[p] = (uint32_t)q0; c0[p] = n0; c2[p] = n2;
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int t = t0 + q;
-      const uint2 o = oc.o[t];
-#pragma unroll
-      for (int p = 0; p < PPT; ++p) {
-        const uint32_t wd = q == 0 ? c0[p] : q == 1 ? c1[p] : q == 2 ? c2[p] : c3[p];
-        const uint32_t j = mux3(ial[p] + o.x, lane + o.y, cmask);
-        const double wjd = (double)tex1Dfetch<float>(a.tex, (int)j);
-        if (((double)wd * 0x1p-32) * wkd[p] <= wjd) { wkd[p] = wjd; bstar[p] = t; }
-      }
+    for (int p = 0; p < PPT; ++p) {
+      const float wj = tex1Dfetch<float>(a.tex, (int)jj[p]);
+      uint64_t xx;
+      if (XC == 1) xx = add64_cc(x0[p], o.z, o.w);
+      else if (XC == 2) xx = x0[p] + (uint64_t)ot.x * M_CTR;
+      else if (XC == 3) {
+        asm("{\n\t.reg .u32 lo, hi;\n\t"
+            "mad.wide.u32 %0, %1, %2, %3;\n\t"
+            "mov.b64 {lo, hi}, %0;\n\t"
+            "mad.lo.u32 hi, %1, %4, hi;\n\t"
+            "mov.b64 %0, {lo, hi};\n\t}"
+            : "=l"(xx) : "r"(ot.x), "r"((uint32_t)M_CTR), "l"(x0[p]), "r"((uint32_t)(M_CTR >> 32)));
+      } else xx = x[p];
+      float u1;
+      if (LEAH) u1 = __uint_as_float(__umulhi(mix64_mhi(xx), o.w) + 0x3F800000u);  // o.w = 2^23 (opaque)
+      else u1 = __uint_as_float(0x3F800000u + (mix64_mhi(xx) >> 9));
+      const float lo = __fmaf_rd(u1, wk[p], -wk[p]);
+      const float hi = HI1 ? __fmaf_ru(wk[p], 0x1p-22f, lo) : __fmaf_ru(__fadd_rn(u1, 0x1p-23f), wk[p], -wk[p]);
+      const bool acc = hi <= wj;
+      if (!acc && lo <= wj) ambt[p] = t;
+      if (acc) { wk[p] = wj; bstar[p] = t; }
+      if (XC == 0) x[p] += M_CTR;
     }
   }
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
+    if (ambt[p] >= 0) bstar[p] = megores_exact_rounds(a, ocx, ii[p], wk0[p], true);
     uint32_t k = ii[p];
-    if (bstar[p] >= 0) { const uint2 o = oc.o[bstar[p]]; k = mux3(ial[p] + o.x, lane + o.y, cmask); }
+    if (bstar[p] >= 0) k = mux3(ial[p] + oc.o[bstar[p]].x, lane + oc.o[bstar[p]].y, cmask);
     a.anc[ii[p]] = (int64_t)k;
   }
+}
+
+// FP64 bracket: u1 = 1 + m_hi 2^-32 from bits; true u in [(m_hi - 1) 2^-32, (m_hi + 2) 2^-32)
+// (bit 0 of the final xorshift's high word may differ from m_hi's).  WKD: state weight kept in
+// float64 (2 SELs) instead of float32 + F2F per round.
+template <bool WKD, int UNR>
+__global__ void __launch_bounds__(256) k_md(const __grid_constant__ ResampleArgs a, const __grid_constant__ OffChunk oc) {
+  const uint32_t i = a.p0 + blockIdx.x * 256 + threadIdx.x;
+  const uint32_t lane = threadIdx.x & 31u, ial = i - lane, cmask = (a.n - 1) & ~31u;
+  const float wk0 = tex1Dfetch<float>(a.tex, (int)i);
+  float wk = wk0;
+  double wkd = (double)wk0;
+  int bstar = -1, ambt = -1;
+  uint64_t x = megores_key(a.base, i, (uint64_t)a.b0);
+#pragma unroll UNR
+  for (int t = 0; t < a.cnt; ++t) {
+    const uint2 o = oc.o[t];
+    const uint32_t j = mux3(ial + o.x, lane + o.y, cmask);
+    const float wj = tex1Dfetch<float>(a.tex, (int)j);
+    const double wjd = (double)wj;
+    const uint32_t m = mix64_mhi(x);
+    const double u1 = __hiloint2double((int)((m >> 12) + 0x3FF00000u), (int)(m << 20));  // 1 + m 2^-32
+    const double wkc = WKD ? wkd : (double)wk;
+    const double lo = __fma_rd(__dadd_rn(u1, -0x1p-32), wkc, -wkc);
+    const double hi = __fma_ru(__dadd_rn(u1, 0x1p-31), wkc, -wkc);
+    const bool acc = hi <= wjd;
+    if (!acc && lo <= wjd) ambt = t;
+    if (acc) { if (WKD) wkd = wjd; else wk = wj; bstar = t; }
+    x += M_CTR;
+  }
+  if (ambt >= 0) bstar = megores_exact_rounds(a, oc, i, wk0, true);
+  uint32_t k = i;
+  if (bstar >= 0) k = mux3(ial + oc.o[bstar].x, lane + oc.o[bstar].y, cmask);
+  a.anc[i] = (int64_t)k;
 }
 
 template <class K>
@@ -138,57 +288,81 @@ int main(int argc, char** argv) {
   CK(cudaCreateTextureObject(&tex, &rd, &td, nullptr));
 
   static OffChunk oc;
-  static OffChunk4 o4;
   const uint64_t base = megores_base(seed);
   for (int t = 0; t < B; ++t) {
     const uint32_t o = (uint32_t)below_from_hash(mix64(megores_key(base, GLOBAL_OFFSET_LANE, t)), n);
     oc.o[t] = make_uint2(o & ~31u, o & 31u);
-    o4.o[t] = make_uint4(o & ~31u, o & 31u, (uint32_t)t, 0u);
   }
   ResampleArgs a{};
   a.w = w; a.n = n; a.p0 = 0; a.p_end = n; a.seed = seed; a.base = base; a.b0 = 0; a.cnt = B;
-  a.first = 1; a.last = 1; a.anc = anc0; a.tex = tex;
+  a.first = 1; a.last = 1; a.anc = anc0; a.tex = tex; a.one = 1;
   const unsigned grid = n / 256;
   const double cmp = (double)n * B;
-  float t0 = time_it([&]() { k_megopolis_w32<0, float, true, true, true><<<grid, 256>>>(a, oc); }, 7);
+  float t0 = time_it([&]() { k_megopolis_w32<0, float, true, true, true, 1><<<grid, 256>>>(a, oc); }, 7);
   std::vector<int64_t> h0(n), h1(n);
   CK(cudaMemcpy(h0.data(), anc0, 8ull * n, cudaMemcpyDeviceToHost));
-  printf("N=2^%d B=%d  lib  %.3f ms  %.1f Gcmp/s\n", logn, B, t0, cmp / t0 / 1e6);
+  printf("N=2^%d B=%d  lib megores PPT1  %.3f ms  %.1f Gcmp/s\n", logn, B, t0, cmp / t0 / 1e6);
   ResampleArgs b = a;
   b.anc = anc1;
   auto check = [&](const char* name, float ms) {
     CK(cudaMemcpy(h1.data(), anc1, 8ull * n, cudaMemcpyDeviceToHost));
     size_t bad = 0;
     for (uint32_t q = 0; q < n; ++q) bad += h0[q] != h1[q];
-    printf("%-6s %.3f ms  %.1f Gcmp/s  speedup %.3f  mismatches %zu\n", name, ms, cmp / ms / 1e6, t0 / ms, bad);
+    printf("%-14s %.3f ms  %.1f Gcmp/s  speedup %.3f  mismatches %zu\n", name, ms, cmp / ms / 1e6, t0 / ms, bad);
     CK(cudaMemset(anc1, 0xff, 8ull * n));
   };
-  {
-    static OffChunk ocp;
-    for (int t = 0; t < B; ++t) {
-      const uint32_t o = (uint32_t)below_from_word(p4_word(philox_block(seed, GLOBAL_OFFSET_LANE, t >> 2), t & 3), n);
-      ocp.o[t] = make_uint2(o & ~31u, o & 31u);
-    }
-    ResampleArgs c = a;
-    uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
-    for (int r = 0; r < 10; ++r) { c.pk0[r] = k0; c.pk1[r] = k1; k0 += PHILOX_W0; k1 += PHILOX_W1; }
-    c.anc = anc0;
-    float tp = time_it([&]() { k_megopolis_w32<1, float, true, true, true><<<grid, 256>>>(c, ocp); }, 7);
-    CK(cudaMemcpy(h0.data(), anc0, 8ull * n, cudaMemcpyDeviceToHost));
-    printf("philox lib %.3f ms\n", tp);
-    ResampleArgs d = c; d.anc = anc1;
-    float t1 = time_it([&]() { k_vp2<1><<<grid, 256>>>(d, ocp); }, 7);
-    check("vp2_1", t1);
-    float t2 = time_it([&]() { k_vp2<2><<<grid, 128>>>(d, ocp); }, 7);
-    check("vp2_2", t2);
-    CK(cudaMemcpy(h0.data(), anc0, 8ull * n, cudaMemcpyDeviceToHost));
-  }
-  CK(cudaMemcpy(h0.data(), anc0, 8ull * n, cudaMemcpyDeviceToHost));
-  t0 = time_it([&]() { k_megopolis_w32<0, float, true, true, true><<<grid, 256>>>(a, oc); }, 3);
-  CK(cudaMemcpy(h0.data(), anc0, 8ull * n, cudaMemcpyDeviceToHost));
-  check("vw4", time_it([&]() { k_vw<false, 4><<<grid, 256>>>(b, o4); }, 7));
-  check("vwt4", time_it([&]() { k_vw<true, 4><<<grid, 256>>>(b, o4); }, 7));
-  check("vwt2", time_it([&]() { k_vw<true, 2><<<grid, 256>>>(b, o4); }, 7));
-  check("vwt8", time_it([&]() { k_vw<true, 8><<<grid, 256>>>(b, o4); }, 7));
+  ResampleArgs bh = b;
+  bh.p0 = 0; bh.p_end = n / 2; bh.hi_shift = 0;
+  check("f32 PPT1", time_it([&]() { k_megopolis_megores_f32<true, 1, false><<<grid, 256>>>(b, oc); }, 7));
+  check("f32 PPT2", time_it([&]() { k_megopolis_megores_f32<true, 2, false><<<grid, 128>>>(b, oc); }, 7));
+  check("f32 PPT2 half", time_it([&]() { k_megopolis_megores_f32<true, 2, true><<<n / 256, 128>>>(bh, oc); }, 7));
+  check("f32 PPT4 half", time_it([&]() { k_megopolis_megores_f32<true, 4, true><<<n / 256, 64>>>(bh, oc); }, 7));
+  check("f32 PPT4", time_it([&]() { k_megopolis_megores_f32<true, 4, false><<<grid, 64>>>(b, oc); }, 7));
+  b.one = 1;
+  static OffChunkX ox;
+  for (int t = 0; t < B; ++t) { const uint64_t c = (uint64_t)t * M_CTR; ox.o[t] = make_uint4(oc.o[t].x, oc.o[t].y, (uint32_t)c, (uint32_t)(c >> 32)); }
+  static OffChunkX oxt;
+  for (int t = 0; t < B; ++t) oxt.o[t] = make_uint4(oc.o[t].x, oc.o[t].y, (uint32_t)t, 1u);
+  static OffChunkX oxl;
+  for (int t = 0; t < B; ++t) oxl.o[t] = make_uint4(oc.o[t].x, oc.o[t].y, 0u, 1u << 23);
+  check("d f 4", time_it([&]() { k_md<false, 4><<<grid, 256>>>(b, oc); }, 7));
+  check("d d 4", time_it([&]() { k_md<true, 4><<<grid, 256>>>(b, oc); }, 7));
+  check("d f 8", time_it([&]() { k_md<false, 8><<<grid, 256>>>(b, oc); }, 7));
+  check("d d 8", time_it([&]() { k_md<true, 8><<<grid, 256>>>(b, oc); }, 7));
+  check("z H--- 1u8 L", time_it([&]() { k_mz<true, 0, 1, false, 8, true><<<grid, 256>>>(b, oxl, oc); }, 7));
+  check("z H--- 1u4 L", time_it([&]() { k_mz<true, 0, 1, false, 4, true><<<grid, 256>>>(b, oxl, oc); }, 7));
+  check("z H--- 1u8 m4", time_it([&]() { k_mz<true, 0, 1, false, 8, false, 4><<<grid, 256>>>(b, oxl, oc); }, 7));
+  check("z H--- 1u8 m6", time_it([&]() { k_mz<true, 0, 1, false, 8, false, 6><<<grid, 256>>>(b, oxl, oc); }, 7));
+  check("z H--- 1u8 L m6", time_it([&]() { k_mz<true, 0, 1, false, 8, true, 6><<<grid, 256>>>(b, oxl, oc); }, 7));
+  check("z HT-- 1", time_it([&]() { k_mz<true, 2, 1, false, 4><<<grid, 256>>>(b, oxt, oc); }, 7));
+  check("z HW-- 1", time_it([&]() { k_mz<true, 3, 1, false, 4><<<grid, 256>>>(b, oxt, oc); }, 7));
+  check("z HW-- 1u8", time_it([&]() { k_mz<true, 3, 1, false, 8><<<grid, 256>>>(b, oxt, oc); }, 7));
+  check("z HW-- 4h", time_it([&]() { k_mz<true, 3, 4, true, 2><<<n / 256, 64>>>(bh, oxt, oc); }, 7));
+  check("z ---- 1", time_it([&]() { k_mz<false, 0, 1, false, 4><<<grid, 256>>>(b, oxt, oc); }, 7));
+  check("z H--- 1", time_it([&]() { k_mz<true, 0, 1, false, 4><<<grid, 256>>>(b, oxt, oc); }, 7));
+  check("z HX-- 1", time_it([&]() { k_mz<true, 1, 1, false, 4><<<grid, 256>>>(b, oxt, oc); }, 7));
+  check("z H--- 2", time_it([&]() { k_mz<true, 0, 2, false, 2><<<grid, 128>>>(b, oxt, oc); }, 7));
+  check("z H--- 2h", time_it([&]() { k_mz<true, 0, 2, true, 2><<<n / 256, 128>>>(bh, oxt, oc); }, 7));
+  check("z H--- 4h", time_it([&]() { k_mz<true, 0, 4, true, 2><<<n / 256, 64>>>(bh, oxt, oc); }, 7));
+  check("z HX-- 2h", time_it([&]() { k_mz<true, 1, 2, true, 2><<<n / 256, 128>>>(bh, oxt, oc); }, 7));
+  check("z H--- 1u8", time_it([&]() { k_mz<true, 0, 1, false, 8><<<grid, 256>>>(b, oxt, oc); }, 7));
+  check("w ----", time_it([&]() { k_mw<false, false, false, false><<<grid, 256>>>(b, ox, oc, 4, 32); }, 7));
+  check("w I---", time_it([&]() { k_mw<true, false, false, false><<<grid, 256>>>(b, ox, oc, 4, 32); }, 7));
+  check("w -X--", time_it([&]() { k_mw<false, true, false, false><<<grid, 256>>>(b, ox, oc, 4, 32); }, 7));
+  check("w --S-", time_it([&]() { k_mw<false, false, true, false><<<grid, 256>>>(b, ox, oc, 4, 32); }, 7));
+  check("w ---A", time_it([&]() { k_mw<false, false, false, true><<<grid, 256>>>(b, ox, oc, 4, 32); }, 7));
+  check("w IX--", time_it([&]() { k_mw<true, true, false, false><<<grid, 256>>>(b, ox, oc, 4, 32); }, 7));
+  check("w IXS-", time_it([&]() { k_mw<true, true, true, false><<<grid, 256>>>(b, ox, oc, 4, 32); }, 7));
+  check("w IXSA", time_it([&]() { k_mw<true, true, true, true><<<grid, 256>>>(b, ox, oc, 4, 32); }, 7));
+  check("w I-S-", time_it([&]() { k_mw<true, false, true, false><<<grid, 256>>>(b, ox, oc, 4, 32); }, 7));
+  check("v F", time_it([&]() { k_mv<true, 0, false, false, 4><<<grid, 256>>>(b, oc); }, 7));
+  check("v FM", time_it([&]() { k_mv<true, 1, false, false, 4><<<grid, 256>>>(b, oc); }, 7));
+  check("v FMX", time_it([&]() { k_mv<true, 1, true, false, 4><<<grid, 256>>>(b, oc); }, 7));
+  check("v FMA", time_it([&]() { k_mv<true, 1, false, true, 4><<<grid, 256>>>(b, oc); }, 7));
+  check("v FMXA", time_it([&]() { k_mv<true, 1, true, true, 4><<<grid, 256>>>(b, oc); }, 7));
+  check("v MA", time_it([&]() { k_mv<false, 1, false, true, 4><<<grid, 256>>>(b, oc); }, 7));
+  check("v FMA u2", time_it([&]() { k_mv<true, 1, false, true, 2><<<grid, 256>>>(b, oc); }, 7));
+  check("v FMA u8", time_it([&]() { k_mv<true, 1, false, true, 8><<<grid, 256>>>(b, oc); }, 7));
+  check("lib PPT4 half", time_it([&]() { k_megopolis_w32<0, float, true, true, true, 4, true><<<n / 256, 64>>>(bh, oc); }, 7));
   return 0;
 }

@@ -5,7 +5,7 @@ out = subprocess.run(["cuobjdump", "-sass", binf], capture_output=True, text=Tru
 blocks = out.split("Function : ")
 body = [b for b in blocks if b.startswith(fn)]
 if not body:
-    print("not found", [b.split("\n")[0] for b in blocks][:50]); sys.exit(1)
+    print("not found"); sys.exit(1)
 lines = [l for l in body[0].split("\n") if re.match(r"\s+/\*[0-9a-f]{4}\*/", l)]
 ins = []
 for l in lines:
@@ -23,6 +23,8 @@ for addr, txt in ins:
         if mm and int(mm.group(1), 16) < addr:
             loops.append((addr - int(mm.group(1), 16), int(mm.group(1), 16), addr))
 loops.sort(reverse=True)
+if len(sys.argv) > 3:  # the largest loop containing this opcode
+    loops = [l for l in loops if any(l[1] <= a <= l[2] and t.startswith(sys.argv[3]) for a, t in ins)]
 _, lo, hi = loops[0]
 body_ins = [t for a, t in ins if lo <= a <= hi]
 pipe = collections.Counter(); ops = collections.Counter()
