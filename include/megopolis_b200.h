@@ -24,8 +24,18 @@
  *   - Return codes: 0 = ok; MGP_EINVAL (< 0) = invalid argument, the reference's
  *     ValueError (message via mgp_last_error(), same text as the reference);
  *     MGP_EUNSUPPORTED = size/feature outside this build; > 0 = cudaError_t.
- *   - Thread-safe: no global mutable state; scratch is stream-ordered
- *     (cudaMallocAsync); mgp_last_error() is thread-local.
+ *   - Thread-safe; mgp_last_error() is thread-local.  Scratch is stream-ordered
+ *     (cudaMallocFromPoolAsync) from a private per-device cudaMemPool owned by the library;
+ *     the device's default pool and the host application's allocator settings are never
+ *     touched.  Library-internal caches (the per-device pool, per-thread host-path streams,
+ *     the bounded LRU of float32 weight texture objects) sit behind mutexes or are
+ *     thread-local.
+ *   - partition_bytes counts 4-byte words (n_w = partition_bytes / 4, the reference's
+ *     default word_bytes = 4, M/resample.py:64, 84-87); hosts with another word size pass
+ *     n_w * 4 (the Python layer's abi_partition_bytes).
+ *   - Host buffers: page-locked memory lets the ancestor download overlap the compute
+ *     chunk by chunk; pageable memory works too (every chunk kernel is queued first, then
+ *     the downloads), at the driver's pageable copy rate.
  *   - Particle counts are limited to N < 2^31 (32-bit index arithmetic on device).
  */
 #ifndef MEGOPOLIS_B200_H
@@ -71,6 +81,10 @@ typedef struct {
 
 int mgp_abi_version(void);
 const char *mgp_last_error(void);
+
+/* Return the library's cached scratch memory on `device` (-1: the current device) to the
+ * driver: trims the private stream-ordered pool (cudaMemPoolTrimTo(pool, 0)). */
+int mgp_release_cached_memory(int device);
 
 /* Replaces the f64 mean/max scan feeding compute_iterations (M/weights.py:114-131,
  * M/bench.py:119-120) and the WeightVector / _check_weights scans
@@ -236,6 +250,11 @@ int mgp_estimate_ratio_stats(const void *d_w, int dtype, int64_t n, int64_t subs
 
 /* gen_gaussian_weights (M/weights.py:100-104) on the device (synthetic inputs) */
 int mgp_gen_gaussian(double y, int64_t n, uint64_t seed, int dtype, void *d_out, void *stream);
+
+/* gen_gamma_weights (M/weights.py:107-111): d_out[i] = scipy.stats.gamma.ppf(u_i, a=alpha,
+ * scale=1/beta) with u_i = uniform_open01_at(seed, i, 0) (M/rng.py:134-137), evaluated in HBM
+ * (incomplete-gamma inversion in float64, ~1e-14 relative to scipy; not bit-exact). */
+int mgp_gen_gamma(double alpha, double beta, int64_t n, uint64_t seed, int dtype, void *d_out, void *stream);
 
 /* Prefix-sum resamplers (M/resample.py:285-336).  mgp_cumsum is np.cumsum(values) in the
  * weights' dtype (M/resample.py:288-291) -- numpy's sequential left-to-right rounding,

@@ -30,6 +30,7 @@ _u64, _i64, _i32, _vp, _dbl = ctypes.c_uint64, ctypes.c_int64, ctypes.c_int, cty
 SIGNATURES = {
     "mgp_abi_version": (_i32, []),
     "mgp_last_error": (ctypes.c_char_p, []),
+    "mgp_release_cached_memory": (_i32, [_i32]),
     "mgp_weight_stats": (_i32, [_vp, _i32, _i64, _vp, _vp]),
     "mgp_compute_iterations": (_i32, [_dbl, _dbl, _dbl, _vp]),
     "mgp_offsets_host": (_i32, [_u64, _i64, _i32, _i32, _vp]),
@@ -67,6 +68,7 @@ SIGNATURES = {
     "mgp_pf_predict_update": (_i32, [_vp, _i64, _dbl, _dbl, _u64, _dbl, _dbl, _i32, _vp, _vp, _vp, _vp]),
     "mgp_estimate_ratio_stats": (_i32, [_vp, _i32, _i64, _i64, _u64, _vp, _vp]),
     "mgp_gen_gaussian": (_i32, [_dbl, _i64, _u64, _i32, _vp, _vp]),
+    "mgp_gen_gamma": (_i32, [_dbl, _dbl, _i64, _u64, _i32, _vp, _vp]),
     "mgp_cumsum": (_i32, [_vp, _i32, _i64, _vp, _vp]),
     "mgp_multinomial": (_i32, [_vp, _i32, _i64, _u64, _vp, _vp]),
     "mgp_systematic": (_i32, [_vp, _i32, _i64, _u64, _vp, _vp]),

@@ -40,14 +40,30 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
-        return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", OUT + ".tmp", *SOURCES]
+# measurement probe (bench.py's L2 / HBM read peaks; not on the product path)
+PROBE_SRC = os.path.join(CSRC, "mgp_probe.cu")
+PROBE_OUT = os.path.join(HERE, "libmgp_probe.so")
+
+
+def _nvcc(src, out, verbose):
+    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", out + ".tmp", src]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
-    os.replace(OUT + ".tmp", OUT)
+    os.replace(out + ".tmp", out)
+
+
+def build_probe(force: bool = False, verbose: bool = False) -> str:
+    if force or not os.path.exists(PROBE_OUT) or os.path.getmtime(PROBE_SRC) > os.path.getmtime(PROBE_OUT):
+        _nvcc(PROBE_SRC, PROBE_OUT, verbose)
+    return PROBE_OUT
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    build_probe(force, verbose)
+    if not force and not needs_build():
+        return OUT
+    _nvcc(SOURCES[0], OUT, verbose)
     return OUT
 
 

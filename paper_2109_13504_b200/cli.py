@@ -18,7 +18,10 @@ DESIGN.md §8a).  ``traffic`` is the reference's analytical transaction model (M
 which has no GPU counterpart here: measured sectors per request come from ncu instead
 (DESIGN.md §4).
 
-Extra flag: ``--rng megores|philox`` (default megores, the reference's stream).
+Extra flags: ``--rng megores|philox`` (default megores, the reference's stream);
+``--device-weights-from N`` (quality, gen-weights): populations of at least N particles
+(default 2^24, above every profile's grid) are synthesised in HBM by the device generators
+(``weights.gen_gaussian_weights`` / ``gen_gamma_weights`` with ``device=``).
 """
 
 from __future__ import annotations
@@ -94,17 +97,27 @@ def token_id(token: str) -> int:
     return int.from_bytes(token.encode()[:8].ljust(8, b"\0"), "little")
 
 
-def experiment_weights(spec: ExperimentSpec, n: int, param: float, seq: int):
+# Populations of at least this many particles are synthesised in HBM (mgp_gen_gaussian /
+# mgp_gen_gamma) instead of by the reference's host formulas: --device-weights-from.  The
+# default lies above the paper profile's largest N (2^22), so the desk and paper grids keep the
+# reference's exact weight bytes (and byte-identical CSVs); 2^24 .. 2^28 grids skip the host
+# detour (scipy's gamma.ppf alone is ~1 s per 2^20 draws) at ~1e-14 relative (gamma) or
+# last-bit libm (gaussian) agreement with the host bytes.
+DEVICE_WEIGHTS_FROM = 1 << 24
+
+
+def experiment_weights(spec: ExperimentSpec, n: int, param: float, seq: int, device_from: int = DEVICE_WEIGHTS_FROM):
     """The (n, param, seq) weight vector of a grid (M/bench.py:99-104)."""
-    from .weights import GammaWeightParams, GaussianWeightParams, gen_gamma_weights, gen_gaussian_weights_host
+    from .weights import GammaWeightParams, GaussianWeightParams, gen_gamma_weights, gen_gaussian_weights
 
     wseed = _rng.derive_seed(spec.seed, 0 if spec.family == "gaussian" else 1, n, int(param * 1000), seq)
+    device = "cuda" if n >= device_from else None
     if spec.family == "gaussian":
-        return gen_gaussian_weights_host(GaussianWeightParams(param, n), wseed, spec.precision)
-    return gen_gamma_weights(GammaWeightParams(param, 1.0, n), wseed, spec.precision)
+        return gen_gaussian_weights(GaussianWeightParams(param, n), wseed, spec.precision, device=device)
+    return gen_gamma_weights(GammaWeightParams(param, 1.0, n), wseed, spec.precision, device=device)
 
 
-def quality_grid(spec: ExperimentSpec, rng_stream: str = "megores"):
+def quality_grid(spec: ExperimentSpec, rng_stream: str = "megores", device_from: int = DEVICE_WEIGHTS_FROM):
     """One averaged row per (algorithm, N, parameter); statistics per weight sequence, then
     averaged across sequences (M/bench.py:107-149).  All per-run work stays in HBM."""
     import torch
@@ -121,8 +134,9 @@ def quality_grid(spec: ExperimentSpec, rng_stream: str = "megores"):
             for param in spec.params:
                 stats, bs = [], []
                 for seq in range(spec.sequences):
-                    host = experiment_weights(spec, n, param, seq)
-                    w = WeightVector(torch.from_numpy(np.ascontiguousarray(host.values)).cuda(), spec.precision)
+                    wv = experiment_weights(spec, n, param, seq, device_from)
+                    w = wv if wv.on_device else WeightVector(torch.from_numpy(np.ascontiguousarray(wv.values)).cuda(),
+                                                             spec.precision)
                     b = iterations_for(w, spec.epsilon).b
                     bs.append(b)
                     acc = QualityAccumulator(n)
@@ -239,7 +253,9 @@ _FLAGS = {
                 ("--n-grid", "n_grid", str, "comma list of particle counts"),
                 ("--family", "family", "family", None), ("--params", "params", str, "comma list of y / shapes"),
                 ("--k-runs", "k_runs", int, None), ("--sequences", "sequences", int, None),
-                ("--epsilon", "epsilon", float, None), ("--rng", "rng", "rng", None)],
+                ("--epsilon", "epsilon", float, None), ("--rng", "rng", "rng", None),
+                ("--device-weights-from", "device_weights_from", int,
+                 "synthesise populations of at least this N in HBM (default 2^24)")],
     "traffic": [("--profile", "profile", "profile", None), ("--algorithms", "algorithms", str, None),
                 ("--n-grid", "n_grid", str, None), ("--b", "b", int, "iteration count to trace")],
     "pf": [("--precision", "precision", "precision", None), ("--algorithms", "algorithms", str, None),
@@ -247,7 +263,9 @@ _FLAGS = {
            ("--trajectories", "trajectories", int, None), ("--runs", "runs", int, None),
            ("--t-steps", "t_steps", int, None)],
     "gen-weights": [("--precision", "precision", "precision", None), ("--family", "family", "family!", None),
-                    ("--param", "param", "float!", "y or gamma shape alpha"), ("--n", "n", "int!", None)],
+                    ("--param", "param", "float!", "y or gamma shape alpha"), ("--n", "n", "int!", None),
+                    ("--device-weights-from", "device_weights_from", int,
+                     "generate in HBM when N is at least this (default 2^24)")],
     "plotdata": [("--results", "results", "str!", "input results CSV"), ("--figure", "figure", "figure!", None)],
 }
 _CHOICES = {"profile": sorted(PROFILES), "precision": ["single", "double"], "family": ["gaussian", "gamma"],
@@ -293,6 +311,11 @@ def spec_from_args(args) -> ExperimentSpec:
     return ExperimentSpec(**values)
 
 
+def _device_from(args) -> int:
+    v = getattr(args, "device_weights_from", None)
+    return DEVICE_WEIGHTS_FROM if v is None else int(v)
+
+
 def run(args) -> int:
     cmd = args.command
     if cmd == "plotdata":
@@ -302,7 +325,7 @@ def run(args) -> int:
         return 0
     spec = spec_from_args(args)
     if cmd == "quality":
-        write_csv(spec.out, quality_grid(spec, args.rng or "megores"))
+        write_csv(spec.out, quality_grid(spec, args.rng or "megores", _device_from(args)))
         print(f"wrote {spec.out}")
     elif cmd == "pf":
         rows, timings = pf_grid(spec)
@@ -310,12 +333,15 @@ def run(args) -> int:
         write_csv(spec.out + ".timings.csv", timings)
         print(f"wrote {spec.out} (+ timings sidecar)")
     elif cmd == "gen-weights":
-        from .weights import GammaWeightParams, GaussianWeightParams, gen_gamma_weights, gen_gaussian_weights_host
+        from .weights import GammaWeightParams, GaussianWeightParams, WeightVector, gen_gamma_weights, gen_gaussian_weights
 
+        device = "cuda" if args.n >= _device_from(args) else None
         if args.family == "gaussian":
-            w = gen_gaussian_weights_host(GaussianWeightParams(args.param, args.n), spec.seed, spec.precision)
+            w = gen_gaussian_weights(GaussianWeightParams(args.param, args.n), spec.seed, spec.precision, device=device)
         else:
-            w = gen_gamma_weights(GammaWeightParams(args.param, 1.0, args.n), spec.seed, spec.precision)
+            w = gen_gamma_weights(GammaWeightParams(args.param, 1.0, args.n), spec.seed, spec.precision, device=device)
+        if w.on_device:
+            w = WeightVector(w.values.cpu().numpy(), spec.precision)
         storage.save_weights(spec.out, w)
         wd = np.asarray(w.values, dtype=np.float64)
         print(f"wrote {spec.out}: n={args.n} mean={wd.mean():.6g} max={wd.max():.6g} ratio={wd.mean() / wd.max():.6g}")

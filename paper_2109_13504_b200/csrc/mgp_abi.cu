@@ -87,27 +87,47 @@ int check_partition(int64_t n, int32_t part_bytes, int64_t* n_w, int64_t* n_part
 }
 
 // ---------------------------------------------------------------------------
-// Stream-ordered scratch.  The device's default memory pool keeps freed blocks
-// (release threshold raised once per device), so the per-call cudaMallocAsync of
-// reduction heaps / offsets / the host-path buffers is a pool hit instead of a
-// remap after every synchronisation.
+// Stream-ordered scratch from a private per-device memory pool.  The pool keeps freed
+// blocks (release threshold UINT64_MAX), so the per-call allocation of reduction heaps,
+// offsets and the host-path buffers is a pool hit instead of a remap after every
+// synchronisation.  It is the library's own pool: the device's default pool (and with it
+// the host application's cudaMallocAsync behaviour) is never modified.
+// mgp_release_cached_memory() trims it.
 
 std::mutex g_pool_mu;
-std::vector<int> g_pool_ready;
+std::vector<std::pair<int, cudaMemPool_t>> g_pools;
 
-void ensure_pool() {
+cudaError_t lib_pool(cudaMemPool_t* out) {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
   std::lock_guard<std::mutex> lk(g_pool_mu);
-  for (int d : g_pool_ready)
-    if (d == dev) return;
+  for (auto& dp : g_pools)
+    if (dp.first == dev) { *out = dp.second; return cudaSuccess; }
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.handleTypes = cudaMemHandleTypeNone;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
   cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
-  cudaGetLastError();
-  g_pool_ready.push_back(dev);
+  if ((e = cudaMemPoolCreate(&pool, &props)) != cudaSuccess) return e;
+  uint64_t thr = UINT64_MAX;
+  if ((e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr)) != cudaSuccess) return e;
+  g_pools.emplace_back(dev, pool);
+  *out = pool;
+  return cudaSuccess;
+}
+
+// cudaMallocAsync from the library's pool on the current device
+template <typename T>
+cudaError_t pool_malloc(T** out, size_t bytes, cudaStream_t st) {
+  cudaMemPool_t pool;
+  cudaError_t e = lib_pool(&pool);
+  if (e != cudaSuccess) return e;
+  void* q = nullptr;
+  e = cudaMallocFromPoolAsync(&q, bytes ? bytes : 1, pool, st);
+  *out = static_cast<T*>(q);
+  return e;
 }
 
 // Stream-ordered scratch owned by one call: every block allocated through it is released
@@ -115,7 +135,7 @@ void ensure_pool() {
 // early returns of CUDA_TRY / LAUNCH_CHECK do not leak.
 class Scratch {
  public:
-  explicit Scratch(cudaStream_t st) : st_(st) { ensure_pool(); }
+  explicit Scratch(cudaStream_t st) : st_(st) {}
   ~Scratch() {
     for (auto it = p_.rbegin(); it != p_.rend(); ++it) cudaFreeAsync(*it, st_);
   }
@@ -124,7 +144,7 @@ class Scratch {
   template <typename T>
   cudaError_t alloc(T** out, size_t bytes) {
     void* q = nullptr;
-    const cudaError_t e = cudaMallocAsync(&q, bytes ? bytes : 1, st_);
+    const cudaError_t e = pool_malloc(&q, bytes, st_);
     if (e == cudaSuccess) p_.push_back(q);
     *out = static_cast<T*>(q);
     return e;
@@ -304,30 +324,60 @@ int dispatch_c12(const ResampleArgs& a, bool pow2, bool nz, bool no_stage, cudaS
 
 // ---------------------------------------------------------------------------
 // float32 weights as a 1-D linear texture: the texture unit does the partner-address
-// arithmetic.  Objects are cached per (device, pointer, length) and never destroyed
-// while the process lives (a kernel may still be reading through them).
+// arithmetic.  Objects are cached per (device, pointer, length) in a bounded LRU.  A
+// lookup pins its entry until tex_release() has recorded a "last use" event on the
+// launching stream (one event per stream that used the entry); eviction takes the least
+// recently used unpinned entry, waits for all of its events (the last kernels reading
+// through it) and destroys the object, so a texture is never destroyed under a running
+// kernel.
 
 struct TexEntry {
   int dev;
   const void* ptr;
   int64_t n;
   cudaTextureObject_t tex;
+  std::vector<std::pair<cudaStream_t, cudaEvent_t>> uses;  // last launch reading tex, per stream
+  uint64_t tick;  // LRU clock
+  int pins;       // lookups whose launch has not been recorded yet
 };
 std::mutex g_tex_mu;
 std::vector<TexEntry> g_tex;
-constexpr size_t TEX_CACHE_MAX = 1024;
+uint64_t g_tex_clock = 0;
+constexpr size_t TEX_CACHE_MAX = 64;
 
+// returns 0 (use LDG) when the array cannot be a texture; otherwise pinned until tex_release
 cudaTextureObject_t weights_texture(const float* w, int64_t n) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
   std::lock_guard<std::mutex> lk(g_tex_mu);
-  for (const auto& e : g_tex)
-    if (e.dev == dev && e.ptr == (const void*)w && e.n == n) return e.tex;
-  if (g_tex.size() >= TEX_CACHE_MAX) return 0;
+  for (auto& e : g_tex)
+    if (e.dev == dev && e.ptr == (const void*)w && e.n == n) {
+      e.tick = ++g_tex_clock;
+      ++e.pins;
+      return e.tex;
+    }
   int maxw = 0, align = 0;
   cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxTexture1DLinearWidth, dev);
   cudaDeviceGetAttribute(&align, cudaDevAttrTextureAlignment, dev);
   if (n > (int64_t)maxw || (align > 0 && ((uintptr_t)w % (uintptr_t)align) != 0)) return 0;
+  size_t slot = g_tex.size();
+  if (g_tex.size() >= TEX_CACHE_MAX) {  // evict the least recently used unpinned entry
+    uint64_t best = UINT64_MAX;
+    for (size_t k = 0; k < g_tex.size(); ++k)
+      if (g_tex[k].pins == 0 && g_tex[k].tick < best) { best = g_tex[k].tick; slot = k; }
+    if (slot == g_tex.size()) return 0;  // every entry is mid-launch on some thread
+    TexEntry& v = g_tex[slot];
+    int cur = dev;
+    if (v.dev != dev) cudaSetDevice(v.dev);
+    for (auto& u : v.uses) {
+      cudaEventSynchronize(u.second);
+      cudaEventDestroy(u.second);
+    }
+    cudaDestroyTextureObject(v.tex);
+    if (v.dev != dev) cudaSetDevice(cur);
+    g_tex.erase(g_tex.begin() + (std::ptrdiff_t)slot);
+    slot = g_tex.size();
+  }
   cudaResourceDesc rd{};
   rd.resType = cudaResourceTypeLinear;
   rd.res.linear.devPtr = const_cast<float*>(w);
@@ -340,8 +390,36 @@ cudaTextureObject_t weights_texture(const float* w, int64_t n) {
     cudaGetLastError();
     return 0;
   }
-  g_tex.push_back({dev, (const void*)w, n, tex});
+  g_tex.push_back({dev, (const void*)w, n, tex, {}, ++g_tex_clock, 1});
   return tex;
+}
+
+// after the launches that read through tex are queued on st: record the last use, unpin
+void tex_release(cudaTextureObject_t tex, cudaStream_t st) {
+  if (!tex) return;
+  std::lock_guard<std::mutex> lk(g_tex_mu);
+  for (auto& e : g_tex)
+    if (e.tex == tex) {
+      --e.pins;
+      cudaEvent_t ev = nullptr;
+      for (auto& u : e.uses)
+        if (u.first == st) ev = u.second;
+      if (!ev && e.uses.size() >= 16) {  // bound the per-entry stream list: retire the oldest
+        cudaEventSynchronize(e.uses.front().second);
+        cudaEventDestroy(e.uses.front().second);
+        e.uses.erase(e.uses.begin());
+      }
+      if (!ev) {
+        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+          cudaGetLastError();
+          cudaStreamSynchronize(st);  // no event to order the eviction: finish the launch now
+          return;
+        }
+        e.uses.emplace_back(st, ev);
+      }
+      cudaEventRecord(ev, st);
+      return;
+    }
 }
 
 template <int RNG, typename WT>
@@ -520,6 +598,11 @@ int run_range(Plan& p, int64_t p0, int64_t p_end, int64_t* anc, cudaStream_t st)
     for (int r = 0; r < 10; ++r) { a.pk0[r] = k0; a.pk1[r] = k1; k0 += PHILOX_W0; k1 += PHILOX_W1; }
   }
   if (p.kind == MGP_KIND_MEGOPOLIS && p.dtype == MGP_F32) a.tex = weights_texture((const float*)p.w, p.n);
+  struct TexPin {  // unpin (recording the last use on st) on every return path
+    cudaTextureObject_t t;
+    cudaStream_t s;
+    ~TexPin() { tex_release(t, s); }
+  } tex_pin{a.tex, st};
   const int cap = (p.kind == MGP_KIND_MEGOPOLIS) ? OFF_CAP : p.b;  // only Megopolis carries params
   for (int b0 = 0; b0 < p.b; b0 += cap) {
     a.b0 = b0;
@@ -599,18 +682,17 @@ int make_plan(Plan& p, int kind, const void* w, int dtype, int64_t n, int32_t b,
 }
 
 int plan_alloc(Plan& p, cudaStream_t st) {
-  ensure_pool();
   p.alloc_st = st;
   if (is_prefix_kind(p.kind)) {  // the prefix sum is shared by every particle range
-    CUDA_TRY(cudaMallocAsync(&p.cum, (size_t)p.n * (p.dtype == MGP_F32 ? 4 : 8), st));
+    CUDA_TRY(pool_malloc(&p.cum, (size_t)p.n * (p.dtype == MGP_F32 ? 4 : 8), st));
     return px_cumsum_any(p.w, p.dtype, p.n, p.cum, st);
   }
   if (!plan_uses_w32(p) && p.kind == MGP_KIND_MEGOPOLIS) {
-    CUDA_TRY(cudaMallocAsync(&p.d_off, sizeof(int64_t) * p.b, st));
+    CUDA_TRY(pool_malloc(&p.d_off, sizeof(int64_t) * p.b, st));
     CUDA_TRY(cudaMemcpyAsync(p.d_off, p.off.data(), sizeof(int64_t) * p.b, cudaMemcpyHostToDevice, st));
   }
   if (plan_uses_w32(p) && p.kind == MGP_KIND_MEGOPOLIS && p.b > OFF_CAP)
-    CUDA_TRY(cudaMallocAsync(&p.kstate, sizeof(int32_t) * p.n, st));
+    CUDA_TRY(pool_malloc(&p.kstate, sizeof(int32_t) * p.n, st));
   return 0;
 }
 
@@ -653,6 +735,16 @@ int host_ctx(HostCtx** out) {
   return 0;
 }
 
+// true when the host pointer is page-locked (cudaHostAlloc / cudaHostRegister / torch pin_memory)
+bool host_is_pinned(const void* h) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
 int resample_device(int kind, const void* w, int dtype, int64_t n, int32_t b, uint64_t seed, int32_t warp,
                     int32_t part_bytes, int strict, int rng, int flags, int64_t* anc, void* stream) {
   Plan p;
@@ -674,6 +766,17 @@ extern "C" {
 int mgp_abi_version(void) { return MGP_ABI_VERSION; }
 
 const char* mgp_last_error(void) { return g_err.c_str(); }
+
+int mgp_release_cached_memory(int device) {
+  int prev = 0;
+  CUDA_TRY(cudaGetDevice(&prev));
+  if (device >= 0) CUDA_TRY(cudaSetDevice(device));
+  cudaMemPool_t pool;
+  cudaError_t e = lib_pool(&pool);
+  if (e == cudaSuccess) e = cudaMemPoolTrimTo(pool, 0);
+  if (device >= 0) cudaSetDevice(prev);
+  return e == cudaSuccess ? 0 : cuda_err(e, "cudaMemPoolTrimTo");
+}
 
 int mgp_weight_stats(const void* d_w, int dtype, int64_t n, mgp_weight_stats_t* d_out, void* stream) {
   if (dtype != MGP_F32 && dtype != MGP_F64) return set_err(MGP_EINVAL, "dtype must be MGP_F32 or MGP_F64");
@@ -773,7 +876,6 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
     CUDA_TRY(cudaGetDevice(&guard.prev));
     CUDA_TRY(cudaSetDevice(device));
   }
-  ensure_pool();
   HostCtx* hc = nullptr;
   if (int rc0 = host_ctx(&hc)) return rc0;
   cudaStream_t st = hc->st, st2 = hc->st2, cp = hc->cp;
@@ -806,9 +908,9 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
     cudaError_t e_ = (x);                               \
     if (e_ != cudaSuccess) { rc = cuda_err(e_, #x); cleanup(); return rc; } \
   } while (0)
-  HCUDA(cudaMallocAsync(&d_w, wbytes, st));
-  HCUDA(cudaMallocAsync(&d_anc, sizeof(int64_t) * n, st));
-  HCUDA(cudaMallocAsync(&d_stats, sizeof(mgp_weight_stats_t), st));
+  HCUDA(pool_malloc(&d_w, wbytes, st));
+  HCUDA(pool_malloc(&d_anc, sizeof(int64_t) * n, st));
+  HCUDA(pool_malloc(&d_stats, sizeof(mgp_weight_stats_t), st));
   HCUDA(cudaMemcpyAsync(d_w, h_w, wbytes, cudaMemcpyHostToDevice, st));
   HTRY(mgp_weight_stats(d_w, dtype, n, d_stats, st));
   HCUDA(cudaMemcpyAsync(&hs, d_stats, sizeof hs, cudaMemcpyDeviceToHost, st));
@@ -824,6 +926,25 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
   HTRY(plan_alloc(p, st));
   // Overlap the ancestor download with the remaining compute: particle chunks are
   // independent given (w, offsets, seed); each chunk's D2H waits only on its kernel.
+  // A D2H into pageable memory returns only once it has completed, so for a pageable h_anc
+  // every chunk kernel is queued first and the downloads follow (each still overlaps the
+  // chunks behind it); with pinned memory the copies are queued as the chunks are.
+  const bool pinned = host_is_pinned(h_anc);
+  struct Pending { int64_t dst, src, cnt; };
+  std::vector<Pending> pend;
+  auto d2h = [&](int64_t dst, int64_t src, int64_t cnt) -> cudaError_t {
+    if (!pinned) { pend.push_back({dst, src, cnt}); return cudaSuccess; }
+    return cudaMemcpyAsync(h_anc + dst, d_anc + src, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost, cp);
+  };
+  auto flush_pending = [&]() -> cudaError_t {
+    for (const Pending& q : pend) {
+      const cudaError_t e = cudaMemcpyAsync(h_anc + q.dst, d_anc + q.src, sizeof(int64_t) * q.cnt,
+                                            cudaMemcpyDeviceToHost, cp);
+      if (e != cudaSuccess) return e;
+    }
+    pend.clear();
+    return cudaSuccess;
+  };
   if (plan_half_ok(p)) {  // half-split kernel: chunk c = lower-half range [c0, c1) + its mirror
     p.half = true;
     const int64_t half = n / 2;
@@ -843,10 +964,10 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
       cudaEvent_t ev = new_event();
       HCUDA(cudaEventRecord(ev, ks));
       HCUDA(cudaStreamWaitEvent(cp, ev, 0));
-      HCUDA(cudaMemcpyAsync(h_anc + c0, d_anc + c0, sizeof(int64_t) * (c1 - c0), cudaMemcpyDeviceToHost, cp));
-      HCUDA(cudaMemcpyAsync(h_anc + half + c0, d_anc + half + c0, sizeof(int64_t) * (c1 - c0),
-                            cudaMemcpyDeviceToHost, cp));
+      HCUDA(d2h(c0, c0, c1 - c0));
+      HCUDA(d2h(half + c0, half + c0, c1 - c0));
     }
+    HCUDA(flush_pending());
     HCUDA(cudaStreamSynchronize(cp));
     HCUDA(cudaStreamSynchronize(st2));
     HCUDA(cudaStreamSynchronize(st));
@@ -864,8 +985,9 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
     cudaEvent_t ev = new_event();
     HCUDA(cudaEventRecord(ev, st));
     HCUDA(cudaStreamWaitEvent(cp, ev, 0));
-    HCUDA(cudaMemcpyAsync(h_anc + c0, d_anc + c0, sizeof(int64_t) * (c1 - c0), cudaMemcpyDeviceToHost, cp));
+    HCUDA(d2h(c0, c0, c1 - c0));
   }
+  HCUDA(flush_pending());
   HCUDA(cudaStreamSynchronize(cp));
   HCUDA(cudaStreamSynchronize(st));
   cleanup();
@@ -1222,6 +1344,20 @@ int mgp_gen_gaussian(double y, int64_t n, uint64_t seed, int dtype, void* d_out,
   return 0;
 }
 
+int mgp_gen_gamma(double alpha, double beta, int64_t n, uint64_t seed, int dtype, void* d_out, void* stream) {
+  if (!(alpha > 0) || !(beta > 0))
+    return set_err(MGP_EINVAL, "alpha and beta must be > 0, got %.17g, %.17g", alpha, beta);
+  if (n < 1) return set_err(MGP_EINVAL, "n must be >= 1, got %lld", (long long)n);
+  if (!d_out) return set_err(MGP_EINVAL, "null pointer");
+  const double lga = std::lgamma(alpha), scale = 1.0 / beta;  // scipy: ppf * scale, scale = 1 / beta
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
+  if (dtype == MGP_F32) k_gen_gamma<float><<<grid, 256, 0, S(stream)>>>(alpha, lga, scale, n, seed, (float*)d_out);
+  else if (dtype == MGP_F64) k_gen_gamma<double><<<grid, 256, 0, S(stream)>>>(alpha, lga, scale, n, seed, (double*)d_out);
+  else return set_err(MGP_EINVAL, "dtype must be MGP_F32 or MGP_F64");
+  LAUNCH_CHECK("k_gen_gamma");
+  return 0;
+}
+
 }  // extern "C"
 
 // ---------------------------------------------------------------------------
@@ -1390,15 +1526,14 @@ extern "C" int mgp_resample_multi(int kind, const void* h_w, int dtype, int64_t 
     Dev& D = dv[(size_t)d];
     D.id = devs[d];
     MTRY(cudaSetDevice(D.id));
-    ensure_pool();
     MTRY(cudaStreamCreateWithFlags(&D.st, cudaStreamNonBlocking));
-    MTRY(cudaMallocAsync(&D.w, wbytes, D.st));
-    MTRY(cudaMallocAsync((void**)&D.anc, sizeof(int64_t) * (stripes ? 2 * h : chunk), D.st));
+    MTRY(pool_malloc(&D.w, wbytes, D.st));
+    MTRY(pool_malloc(&D.anc, sizeof(int64_t) * (stripes ? 2 * h : chunk), D.st));
   }
   // weights: host -> device 0 -> every other device (peer copies)
   MTRY(cudaSetDevice(dv[0].id));
   MTRY(cudaMemcpyAsync(dv[0].w, h_w, wbytes, cudaMemcpyHostToDevice, dv[0].st));
-  MTRY(cudaMallocAsync((void**)&dv[0].stats, sizeof(mgp_weight_stats_t), dv[0].st));
+  MTRY(pool_malloc(&dv[0].stats, sizeof(mgp_weight_stats_t), dv[0].st));
   if ((rc = mgp_weight_stats(dv[0].w, dtype, n, dv[0].stats, dv[0].st))) return finish(rc);
   MTRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
   MTRY(cudaEventRecord(ready, dv[0].st));
@@ -1426,14 +1561,26 @@ extern "C" int mgp_resample_multi(int kind, const void* h_w, int dtype, int64_t 
       if ((rc = mgp_resample_stripes(kind, D.w, dtype, n, b, seed, warp, partition_bytes, strict, rng, flags, lo0,
                                      lo0 + h, D.anc, D.st)))
         return finish(rc);
-      MTRY(cudaMemcpyAsync(h_anc + lo0, D.anc, sizeof(int64_t) * h, cudaMemcpyDeviceToHost, D.st));
-      MTRY(cudaMemcpyAsync(h_anc + half + lo0, D.anc + h, sizeof(int64_t) * h, cudaMemcpyDeviceToHost, D.st));
     } else {
       const int64_t p0 = std::min<int64_t>(n, d * chunk), p1 = std::min<int64_t>(n, p0 + chunk);
       if (p1 <= p0) continue;
       if ((rc = mgp_resample_range(kind, D.w, dtype, n, b, seed, warp, partition_bytes, strict, rng, flags, p0, p1,
                                    D.anc, D.st)))
         return finish(rc);
+    }
+  }
+  // downloads after every device's kernels are queued: a D2H into pageable memory returns
+  // only when complete, which would otherwise hold device d+1's launch behind device d
+  for (int d = 0; d < ndev; ++d) {
+    Dev& D = dv[(size_t)d];
+    MTRY(cudaSetDevice(D.id));
+    if (stripes) {
+      const int64_t lo0 = d * h;
+      MTRY(cudaMemcpyAsync(h_anc + lo0, D.anc, sizeof(int64_t) * h, cudaMemcpyDeviceToHost, D.st));
+      MTRY(cudaMemcpyAsync(h_anc + half + lo0, D.anc + h, sizeof(int64_t) * h, cudaMemcpyDeviceToHost, D.st));
+    } else {
+      const int64_t p0 = std::min<int64_t>(n, d * chunk), p1 = std::min<int64_t>(n, p0 + chunk);
+      if (p1 <= p0) continue;
       MTRY(cudaMemcpyAsync(h_anc + p0, D.anc, sizeof(int64_t) * (p1 - p0), cudaMemcpyDeviceToHost, D.st));
     }
   }

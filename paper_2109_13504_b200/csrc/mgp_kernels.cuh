@@ -519,12 +519,16 @@ template <int RNG, typename WT, bool POW2, bool NOZERO, bool C2, bool STAGE>
 __global__ void __launch_bounds__(RS_THREADS) k_c12_w32(const __grid_constant__ ResampleArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t i = a.p0 + blockIdx.x * RS_THREADS + threadIdx.x;
-  if (i >= a.p_end) return;  // n % 32 == 0: whole warps leave together
+  // Whole warps past the range leave together.  A warp straddling p_end (p_end % 32 != 0)
+  // stays complete -- every lane takes part in the partition staging and the C2 owner
+  // shuffles (n % 32 == 0, so i < n) -- and only the lanes inside the range store.
+  if ((i & ~31u) >= a.p_end) return;
+  const bool live = i < a.p_end;
   const WT* __restrict__ w = reinterpret_cast<const WT*>(a.w);
   const uint32_t lane = threadIdx.x & 31u, warp_g = i >> 5;
   const uint32_t n_w = a.n_w;
   const uint64_t wlane = WARP_LANE_BASE + warp_g;
-  uint32_t k = a.first ? i : (uint32_t)a.kstate[i];
+  uint32_t k = (a.first || !live) ? i : (uint32_t)a.kstate[i];
   WT wk = __ldg(w + k);
   uint32_t lo = 0;
   WT* part = reinterpret_cast<WT*>(smem_raw) + (threadIdx.x >> 5) * n_w;
@@ -575,7 +579,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_c12_w32(const __grid_constant__ 
       }
     }
   }
-  store_result(a, i, i, k);
+  if (live) store_result(a, i, i, k);
 }
 
 // ---------------------------------------------------------------------------
@@ -1165,6 +1169,102 @@ __global__ void k_gen_gaussian(double y, int64_t n, uint64_t seed, WT* out) {
     const double z = sqrt(-2.0 * log(u1)) * cos(2.0 * 3.141592653589793 * u2);
     const double d = z - y;
     out[i] = (WT)(exp(-0.5 * (d * d)) * 0.3989422804014327);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// gen_gamma_weights (M/weights.py:107-111): w_i = F^-1(u_i; alpha) / beta, the inverse CDF of
+// gamma(alpha, rate beta) at u_i = uniform_open01_at(seed, i, 0) (M/rng.py:134-137).  The
+// reference evaluates scipy.stats.gamma.ppf (Boost's gamma_p_inv); here: the regularized
+// incomplete gamma P/Q (series below a + 1, Lentz continued fraction above) and Halley steps
+// on P(x) = u (u <= 1/2) or Q(x) = 1 - u (u > 1/2, exact there) from the Wilson-Hilferty /
+// small-shape starting point.  float64 throughout; agrees with scipy to ~1e-14 relative
+// (tests/test_gamma_gpu.py states the tolerance), so float32 weights match scipy's except
+// in the last ulp of a tiny fraction of draws.
+
+// P(a, x) and Q(a, x) = 1 - P; the one computed directly keeps full relative accuracy
+__device__ __forceinline__ void gamma_pq(double a, double x, double lga, double& P, double& Q, double& dens) {
+  const double lpre = a * log(x) - x - lga;  // log(x^a e^-x / Gamma(a))
+  const double pre = exp(lpre);
+  dens = pre / x;  // the gamma(a) density at x
+  if (x < a + 1.0) {  // P = pre * sum_k x^k / (a (a+1) ... (a+k))
+    double ap = a, del = 1.0 / a, sum = del;
+    for (int k = 0; k < 2000; ++k) {
+      ap += 1.0;
+      del *= x / ap;
+      sum += del;
+      if (fabs(del) < fabs(sum) * 1e-17) break;
+    }
+    P = pre * sum;
+    Q = 1.0 - P;
+  } else {  // Q = pre / (x + 1 - a - 1 (1 - a) / (x + 3 - a - ...)), modified Lentz
+    const double tiny = 1e-300;
+    double b = x + 1.0 - a, c = 1.0 / tiny, d = 1.0 / b, h = d;
+    for (int k = 1; k < 2000; ++k) {
+      const double an = -k * (k - a);
+      b += 2.0;
+      d = an * d + b;
+      if (fabs(d) < tiny) d = tiny;
+      c = b + an / c;
+      if (fabs(c) < tiny) c = tiny;
+      d = 1.0 / d;
+      const double del = d * c;
+      h *= del;
+      if (fabs(del - 1.0) < 1e-17) break;
+    }
+    Q = pre * h;
+    P = 1.0 - Q;
+  }
+}
+
+// x with P(a, x) = p, given q = 1 - p (both exact inputs)
+__device__ double gamma_p_inv_dev(double a, double p, double q, double lga) {
+  double x;
+  if (a > 1.0) {  // Wilson-Hilferty from the normal quantile (Abramowitz-Stegun 26.2.22)
+    const double pp = p < 0.5 ? p : q;
+    const double t = sqrt(-2.0 * log(pp));
+    double z = (2.30753 + t * 0.27061) / (1.0 + t * (0.99229 + t * 0.04481)) - t;  // -z_p (p >= 1/2)
+    if (p < 0.5) z = -z;
+    const double c = 1.0 - 1.0 / (9.0 * a) - z / (3.0 * sqrt(a));
+    x = a * c * c * c;
+    if (!(x > 1e-3)) x = 1e-3;
+  } else {  // small shape: P ~ (x^a / Gamma(a+1)) near 0, exponential tail above
+    const double t = 1.0 - a * (0.253 + a * 0.12);
+    x = p < t ? pow(p / t, 1.0 / a) : 1.0 - log(q / (1.0 - t));
+    if (!(x > 0.0)) x = 1e-300;
+  }
+  const bool lower = p <= 0.5;
+  double lo = 0.0, hi = INFINITY;  // bracket of the root, tightened every step
+  for (int it = 0; it < 200; ++it) {
+    double P, Q, f;
+    gamma_pq(a, x, lga, P, Q, f);
+    // g = P - p (lower) or q - Q (upper): increasing in x, g' = f, g''/g' = (a - 1)/x - 1
+    const double g = lower ? P - p : q - Q;
+    if (g == 0.0) break;
+    if (g > 0.0) hi = x; else lo = x;
+    double xn;
+    if (f > 0.0 && isfinite(f)) {
+      const double tt = g / f;
+      const double hal = 1.0 - 0.5 * tt * ((a - 1.0) / x - 1.0);
+      xn = x - ((hal > 0.5 && hal < 2.0) ? tt / hal : tt);  // Halley; Newton when it would overshoot
+    } else {
+      xn = -1.0;
+    }
+    if (!(xn > lo && xn < hi))  // outside the bracket: bisect it (geometrically when unbounded)
+      xn = isfinite(hi) ? (lo > 0.0 && hi > 4.0 * lo ? sqrt(lo * hi) : 0.5 * (lo + hi)) : 2.0 * x + 1.0;
+    if (fabs(xn - x) <= 2e-16 * xn) { x = xn; break; }
+    x = xn;
+  }
+  return x;
+}
+
+template <typename WT>
+__global__ void k_gen_gamma(double a, double lga, double scale, int64_t n, uint64_t seed, WT* out) {
+  const uint64_t base = megores_base(seed);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t h = mix64(megores_key(base, (uint64_t)i, 0));
+    const double u = __dmul_rn(__dadd_rn((double)(h >> 11), 0.5), 0x1p-53);  // uniform_open01_at
+    out[i] = (WT)__dmul_rn(gamma_p_inv_dev(a, u, 1.0 - u, lga), scale);
   }
 }
 

@@ -35,7 +35,7 @@ from dataclasses import dataclass
 
 from . import _device as D
 from . import _lib
-from .resample import PartitionConfig, WarpConfig
+from .resample import PartitionConfig, WarpConfig, abi_partition_bytes
 from .weights import WeightStats, compute_iterations, device_stats
 
 
@@ -300,7 +300,8 @@ class ShardedResampler:
         full = self.replicate_weights(w_local)
         b = self._checked_b(full, w_local, b, epsilon)
         st = self._last_stats
-        args = (self.kind, full, b, seed, self.warp.warp_size, self.partition_bytes, self.strict, self.rng,
+        args = (self.kind, full, b, seed, self.warp.warp_size, abi_partition_bytes(self.partition_bytes, self.warp),
+                self.strict, self.rng,
                 st.n_zero == 0)
         if self.layout == "stripes":
             (lo0, lo1), _ = self.owned(n_local)
@@ -318,7 +319,8 @@ class ShardedResampler:
         b = self._checked_b(full, w_local, b, epsilon)
         st = self._last_stats
         (p0, p1) = self.owned(n_local)[0]
-        anc, rows = self.ops.resample_gather(self.kind, full, b, seed, self.warp.warp_size, self.partition_bytes,
+        anc, rows = self.ops.resample_gather(self.kind, full, b, seed, self.warp.warp_size,
+                                             abi_partition_bytes(self.partition_bytes, self.warp),
                                              self.strict, self.rng, st.n_zero == 0, self.layout, p0, p1,
                                              peer_states)
         return anc, rows, b
@@ -579,6 +581,6 @@ def resample_on_devices(kind: str, w, b: int | None = None, seed=0, devices=None
     bu = ctypes.c_int32(0)
     _lib.check(_lib.lib().mgp_resample_multi(
         _lib.KIND[kind], vals.ctypes.data, 0 if vals.dtype == np.float32 else 1, len(vals), int(b or 0),
-        float(epsilon), int(seed) & (2**64 - 1), int(warp.warp_size), int(partition_bytes or 0), int(bool(strict)),
-        _lib.RNG[rng], len(devs), ctypes.cast(arr, ctypes.c_void_p), anc.ctypes.data, ctypes.byref(bu)))
+        float(epsilon), int(seed) & (2**64 - 1), int(warp.warp_size), abi_partition_bytes(partition_bytes, warp),
+        int(bool(strict)), _lib.RNG[rng], len(devs), ctypes.cast(arr, ctypes.c_void_p), anc.ctypes.data, ctypes.byref(bu)))
     return anc, int(bu.value)

@@ -108,11 +108,21 @@ class QualityAccumulator:
         self._se = t.zeros(2, dtype=t.float64, device=self.device)  # [se_total, se_last_run]
         self._expected = None
 
+    def _check_len(self, what: str, m: int) -> None:
+        # the reference fails these as numpy broadcast ValueErrors (M/metrics.py:86-93); the
+        # device kernels read self.n elements, so the lengths are checked before any launch
+        if m != self.n:
+            raise ValueError(f"length mismatch: {m} {what} vs accumulator length {self.n}")
+
     def add(self, offspring, w) -> None:
         t = D.torch()
+        self._check_len("offspring", offspring.shape[0] if D.is_tensor(offspring) else len(offspring))
         if self._expected is None:
-            self._expected = _expected(_dev_weights(w).to(self.device))
+            wd = _dev_weights(w).to(self.device)
+            self._check_len("weights", wd.numel())
+            self._expected = _expected(wd)
         o = _dev_counts(offspring, self.device)
+        self._check_len("offspring", o.numel())
         self.k += 1
         with t.cuda.device(self.device):
             _lib.check(_lib.lib().mgp_quality_add(D.ptr(o), D.ptr(self._expected), self.n, D.ptr(self._sum),
@@ -128,6 +138,7 @@ class QualityAccumulator:
 
         t = D.torch()
         wd = _dev_weights(w).to(self.device)
+        self._check_len("weights", wd.numel())
         if self._expected is None:
             self._expected = _expected(wd)
         from .weights import device_stats

@@ -28,7 +28,7 @@ import numpy as np
 from . import _device as D
 from . import _lib
 from .metrics import QualityStats, RunTimings, resample_ratio, rmse  # noqa: F401  (M/metrics.py names)
-from .resample import METROPOLIS_FAMILY, WarpConfig
+from .resample import METROPOLIS_FAMILY, WarpConfig, abi_partition_bytes
 from .rng import derive_seed, gaussian_at
 from .weights import compute_iterations
 
@@ -159,7 +159,7 @@ def _resample_device(cfg: FilterConfig, w, b: int, seed):
     flags = _lib.FLAG_NONZERO if cfg.precision == "double" else 0  # float32 cast can underflow to 0
     _lib.check(_lib.lib().mgp_resample_range(
         _lib.KIND[kind], D.ptr(w), D.wdtype(w), n, 1 if prefix else int(b), int(seed) & (2**64 - 1),
-        cfg.warp.warp_size, int(cfg.partition_bytes or 0), 1, _lib.RNG["megores" if prefix else cfg.rng], flags, 0, n,
+        cfg.warp.warp_size, abi_partition_bytes(cfg.partition_bytes, cfg.warp), 1, _lib.RNG["megores" if prefix else cfg.rng], flags, 0, n,
         D.ptr(anc), D.stream_ptr()))
     return anc
 

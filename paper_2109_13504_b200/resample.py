@@ -73,6 +73,16 @@ class PartitionConfig:
         return n // n_w
 
 
+def abi_partition_bytes(partition_bytes, warp: WarpConfig) -> int:
+    """The C-ABI's ``partition_bytes`` counts 4-byte words (n_w = partition_bytes / 4,
+    include/megopolis_b200.h).  The reference sizes a partition as
+    partition_bytes // warp.word_bytes (M/resample.py:84-87), so a WarpConfig with another
+    word size is translated here to the same n_w (0 = no partition)."""
+    if partition_bytes is None or partition_bytes == 0:
+        return 0
+    return PartitionConfig(int(partition_bytes)).n_weights(warp) * 4
+
+
 def _seed(seed) -> int:
     return int(np.uint64(seed)) if not isinstance(seed, int) else seed & (2**64 - 1)
 
@@ -116,7 +126,7 @@ def _resample(kind, w, b, seed, warp, part, strict, rng, name):
     _validate(w, b, warp, strict, part, name)
     L = _lib.lib()
     ws = warp.warp_size if warp is not None else 32
-    pb = part.partition_bytes if part is not None else 0
+    pb = abi_partition_bytes(part.partition_bytes, warp) if part is not None else 0
     if w.on_device:
         t = D.torch()
         vals = w.values

@@ -76,18 +76,14 @@ class WeightVector:
             raise ValueError(f"precision must be 'single' or 'double', got {precision!r}")
         self.precision = precision
         self._stats = None
+        self._ver = None
         if D.is_cuda_tensor(values):
             t = D.torch()
             values = values.to(getattr(t, _TORCH_DTYPES[precision])).contiguous()
             if values.dim() != 1 or values.numel() < 1:
                 raise ValueError("weights must be a non-empty 1-d sequence")
-            st = device_stats(values)
-            if st.n_nonfinite:
-                raise ValueError("weights must be finite")
-            if st.n_neg:
-                raise ValueError("weights must be non-negative")
-            self._stats = st
             self.values = values
+            self.stats()  # validates: finite, non-negative
             return
         if D.is_tensor(values):
             values = values.detach().cpu().numpy()
@@ -108,12 +104,22 @@ class WeightVector:
         return D.is_cuda_tensor(self.values)
 
     def stats(self) -> WeightStats:
-        """Device statistics (cached for device-resident weights)."""
-        if self._stats is None:
+        """Device statistics of the current values, re-validated like the reference's per-call
+        ``_check_weights`` (M/resample.py:96-100, M/weights.py:53-61).  For device-resident
+        weights the pass is cached against the tensor's version counter, so an in-place update
+        of the caller's tensor (``values`` aliases it) invalidates it; host arrays are re-read
+        every call."""
+        ver = self.values._version if self.on_device else None
+        if self._stats is None or not self.on_device or ver != self._ver:
             D.require_cuda()
             t = D.torch()
             vals = self.values if self.on_device else t.from_numpy(np.ascontiguousarray(self.values)).cuda()
-            self._stats = device_stats(vals)
+            st = device_stats(vals)
+            if st.n_nonfinite:
+                raise ValueError("weights must be finite")
+            if st.n_neg:
+                raise ValueError("weights must be non-negative")
+            self._stats, self._ver = st, ver
         return self._stats
 
 
@@ -176,14 +182,27 @@ def iterations_for(w, epsilon: float = 0.01) -> IterationBudget:
 
 
 def gen_gaussian_weights(params: GaussianWeightParams, seed, precision="single", device=None) -> WeightVector:
-    """w_i = exp(-(x_i - y)^2 / 2) / sqrt(2 pi), x_i ~ N(0,1) by Box-Muller on the
-    reference's stream (M/weights.py:100-104, M/rng.py:152-161), generated in HBM.
-    libm rounding on the device may differ from the host's in the last float64 bit."""
-    D.require_cuda()
-    t = D.torch()
+    """w_i = exp(-(x_i - y)^2 / 2) / sqrt(2 pi), x_i ~ N(0,1) by Box-Muller on the reference's
+    stream (M/weights.py:100-104, M/rng.py:152-161).
+
+    Default (``device=None``): the reference's own bytes -- a host numpy WeightVector
+    identical to ``megores.gen_gaussian_weights`` (same formula, same numpy libm), so B and
+    every ancestor downstream match the reference exactly.
+
+    ``device="cuda"`` (or a device index): generated in HBM by one kernel
+    (``mgp_gen_gaussian``) and returned as a CUDA-tensor WeightVector -- for populations too
+    large for a host detour (2^28).  NOT bit-exact: the device libm may round
+    log/cos/exp differently from the host's in the last float64 bit, which moves a small
+    fraction of float32 weights by one ulp."""
     if precision not in _DTYPES:
         raise ValueError(f"precision must be 'single' or 'double', got {precision!r}")
-    dev = t.device("cuda") if device is None else t.device(device)
+    if device is None:
+        return gen_gaussian_weights_host(params, seed, precision)
+    D.require_cuda()
+    t = D.torch()
+    dev = t.device(device) if not isinstance(device, int) else t.device("cuda", device)
+    if dev.type != "cuda":
+        raise ValueError(f"device must be a CUDA device, got {device!r}")
     out = t.empty(params.n, dtype=getattr(t, _TORCH_DTYPES[precision]), device=dev)
     with t.cuda.device(dev):
         _lib.check(_lib.lib().mgp_gen_gaussian(float(params.y), params.n, int(seed) & (2**64 - 1),
@@ -218,14 +237,33 @@ def gen_gaussian_weights_host(params: GaussianWeightParams, seed, precision="sin
     return WeightVector(np.exp(-0.5 * (x - params.y) ** 2) * GAUSSIAN_PEAK, precision)
 
 
-def gen_gamma_weights(params: GammaWeightParams, seed, precision="single") -> WeightVector:
-    """I.i.d. gamma(alpha, rate=beta) weights by inverse-CDF sampling (M/weights.py:107-111)."""
-    from scipy import stats
+def gen_gamma_weights(params: GammaWeightParams, seed, precision="single", device=None) -> WeightVector:
+    """I.i.d. gamma(alpha, rate=beta) weights by inverse-CDF sampling (M/weights.py:107-111).
 
-    from .rng import uniform_open01_at
+    Default: the reference's own bytes -- ``scipy.stats.gamma.ppf`` of
+    ``uniform_open01_at(seed, i, 0)`` on the host.  ``device="cuda"`` (or an index): the same
+    inverse CDF evaluated in HBM by ``mgp_gen_gamma`` (float64 incomplete-gamma inversion,
+    ~1e-14 relative to scipy for alpha <= 1000; tests/test_gamma_gpu.py), returned as a
+    CUDA-tensor WeightVector -- the 2^28-population route without a host detour."""
+    if precision not in _DTYPES:
+        raise ValueError(f"precision must be 'single' or 'double', got {precision!r}")
+    if device is None:
+        from scipy import stats
 
-    u = uniform_open01_at(seed, np.arange(params.n), 0)
-    return WeightVector(stats.gamma.ppf(u, a=params.alpha, scale=1.0 / params.beta), precision)
+        from .rng import uniform_open01_at
+
+        u = uniform_open01_at(seed, np.arange(params.n), 0)
+        return WeightVector(stats.gamma.ppf(u, a=params.alpha, scale=1.0 / params.beta), precision)
+    D.require_cuda()
+    t = D.torch()
+    dev = t.device(device) if not isinstance(device, int) else t.device("cuda", device)
+    if dev.type != "cuda":
+        raise ValueError(f"device must be a CUDA device, got {device!r}")
+    out = t.empty(params.n, dtype=getattr(t, _TORCH_DTYPES[precision]), device=dev)
+    with t.cuda.device(dev):
+        _lib.check(_lib.lib().mgp_gen_gamma(float(params.alpha), float(params.beta), params.n,
+                                            int(seed) & (2**64 - 1), D.wdtype(out), D.ptr(out), D.stream_ptr()))
+    return WeightVector(out, precision)
 
 
 def estimate_ratio(w, subset_size: int, seed) -> float:

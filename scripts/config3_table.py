@@ -38,7 +38,7 @@ def timeit(fn, reps=5):
 
 
 for y in (0.0, 4.0):
-    w = mg.gen_gaussian_weights(mg.GaussianWeightParams(y, n), 2024, "single")
+    w = mg.gen_gaussian_weights(mg.GaussianWeightParams(y, n), 2024, "single", device="cuda")
     b = mg.iterations_for(w, 0.01).b
     for rng in ("megores", "philox"):
         def run(kind, ps, flags, dst):

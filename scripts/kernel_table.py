@@ -25,7 +25,7 @@ ap.add_argument("--reps", type=int, default=5)
 a = ap.parse_args()
 L = _lib.lib()
 n = a.n
-w = mg.gen_gaussian_weights(mg.GaussianWeightParams(a.y, n), 20240, "single").values
+w = mg.gen_gaussian_weights(mg.GaussianWeightParams(a.y, n), 20240, "single", device="cuda").values
 st = mg.WeightVector(w, "single").stats()
 b = mg.compute_iterations(0.01, st.mean, st.max).b
 anc = torch.empty(n, dtype=torch.int64, device="cuda")

@@ -7,7 +7,7 @@ for lib in /tmp/libmgp_default.so scripts/mb/libmgp_off1.so scripts/mb/libmgp_of
   python - <<'PY'
 import torch, numpy as np, paper_2109_13504_b200 as mg
 for y in (4.0, 1.0):
-    w = mg.gen_gaussian_weights(mg.GaussianWeightParams(y, 1 << 24), 20240, "single")
+    w = mg.gen_gaussian_weights(mg.GaussianWeightParams(y, 1 << 24), 20240, "single", device="cuda")
     b = mg.iterations_for(w).b
     anc = mg.megopolis(w, b, seed=7, rng="philox")
     ref = mg.ancestors_to_offspring(anc, 1 << 24)

@@ -1,7 +1,7 @@
 # time the megores Megopolis kernel with alternative particles-per-thread builds of libmgp.so
 python - <<'PY' > gpurun_out/ref_anc.txt
 import torch, numpy as np, paper_2109_13504_b200 as mg, hashlib
-w = mg.gen_gaussian_weights(mg.GaussianWeightParams(4.0, 1 << 24), 20240, "single")
+w = mg.gen_gaussian_weights(mg.GaussianWeightParams(4.0, 1 << 24), 20240, "single", device="cuda")
 a = mg.megopolis(w, 354, seed=7).cpu().numpy()
 print(hashlib.sha256(a.tobytes()).hexdigest())
 PY
@@ -11,7 +11,7 @@ for lib in scripts/mb/libmgp_megores_p2.so scripts/mb/libmgp_megores_p4.so /tmp/
   echo "== $lib"
   python - <<'PY'
 import torch, numpy as np, paper_2109_13504_b200 as mg, hashlib
-w = mg.gen_gaussian_weights(mg.GaussianWeightParams(4.0, 1 << 24), 20240, "single")
+w = mg.gen_gaussian_weights(mg.GaussianWeightParams(4.0, 1 << 24), 20240, "single", device="cuda")
 mg.megopolis(w, 354, seed=7); torch.cuda.synchronize()
 ts = []
 for r in range(5):

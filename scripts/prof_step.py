@@ -27,7 +27,7 @@ ap.add_argument("--dtype", default="single")
 a = ap.parse_args()
 
 L = _lib.lib()
-w = mg.gen_gaussian_weights(mg.GaussianWeightParams(a.y, a.n), 20240, a.dtype)
+w = mg.gen_gaussian_weights(mg.GaussianWeightParams(a.y, a.n), 20240, a.dtype, device="cuda")
 stats = torch.empty(8, dtype=torch.float64, device="cuda")
 anc = torch.empty(a.n, dtype=torch.int64, device="cuda")
 sp = D.stream_ptr()

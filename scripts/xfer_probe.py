@@ -16,7 +16,7 @@ for name, fn in (("h2d 64MiB", lambda: d.copy_(h, non_blocking=True)), ("d2h 128
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 10
     print(name, ms, "ms", (h.numel()*h.element_size() if 'h2d' in name else ha.numel()*8) / ms / 1e6, "GB/s")
-w = mg.gen_gaussian_weights(mg.GaussianWeightParams(4.0, n), 20240, "single").values
+w = mg.gen_gaussian_weights(mg.GaussianWeightParams(4.0, n), 20240, "single", device="cuda").values
 hw = w.cpu().pin_memory()
 L = _lib.lib()
 bu = ctypes.c_int32(0)

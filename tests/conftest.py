@@ -31,3 +31,20 @@ def oracle():
 
     o.lib()
     return o
+
+
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+@pytest.fixture(scope="session")
+def ref_megores():
+    """The UNMODIFIED reference package staged under baseline/_ref (scripts/stage_reference.sh);
+    a missing stage is a failure, not a skip."""
+    if not os.path.isfile(os.path.join(REF_DIR, "megores", "resample.py")):
+        pytest.fail("unmodified reference not staged under baseline/_ref (run scripts/stage_reference.sh)")
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import megores
+
+    assert os.path.realpath(os.path.dirname(megores.__file__)) == os.path.realpath(os.path.join(REF_DIR, "megores"))
+    return megores

@@ -433,29 +433,50 @@ def test_nondefault_stream(mg, oracle):
     assert np.array_equal(anc.cpu().numpy(), oracle.megopolis(w, 16, seed=3))
 
 
-def test_shim_routes_reference_api(mg, golden):
-    """The shim replaces megores' resamplers when the reference package is importable
-    (in the build container); on the GPU box the reference is absent."""
-    megores = pytest.importorskip("megores")
+def test_shim_routes_reference_api(mg, golden, ref_megores):
+    """The shim replaces the unmodified reference's resamplers (megores staged under
+    baseline/_ref by scripts/stage_reference.sh; M/__init__.py:12-28, M/resample.py:431-455)."""
+    megores = ref_megores
     from paper_2109_13504_b200 import shim
 
-    saved = shim.install(megores)
+    rs = np.random.default_rng(11)
+    cases = [(megores.WeightVector(rs.random(4096).astype(np.float32) ** 4, "single"), 37),
+             (megores.WeightVector(rs.random(2048), "double"), 9)]
+    kinds = [("megopolis", None), ("metropolis", None), ("c1", 256), ("c2", 512), ("multinomial", None),
+             ("systematic", None)]
+    # the reference's own numba kernels, unpatched
+    want = {(k, i): megores.make_resampler(k, partition_bytes=p)(w, b, 99) for k, p in kinds
+            for i, (w, b) in enumerate(cases)}
+    saved = shim.install(megores, offspring=True)
     try:
+        assert megores.megopolis is mg.megopolis and megores.resample.megopolis is mg.megopolis
         w = megores.WeightVector(np.arange(1, 65, dtype=np.float32), "single")
         fn = megores.make_resampler("megopolis")
         assert list(fn(w, 5, 3)[:8]) == [21, 22, 23, 29, 25, 26, 27, 28]
+        for k, p in kinds:
+            for i, (w, b) in enumerate(cases):
+                got = megores.make_resampler(k, partition_bytes=p)(w, b, 99)
+                assert isinstance(got, np.ndarray) and got.dtype == np.int64
+                assert np.array_equal(got, want[(k, i)]), (k, i)
+                assert np.array_equal(megores.ancestors_to_offspring(got, len(got)), np.bincount(got, minlength=len(got)))
     finally:
         shim.uninstall(megores, saved)
+    assert megores.megopolis is not mg.megopolis
 
 
 def test_device_weight_generator(mg, oracle):
     n = 1 << 16
     for y in (0.0, 4.0):
-        wv = mg.gen_gaussian_weights(mg.GaussianWeightParams(y, n), 123, "double")
+        # device= opt-in: in HBM, libm-rounding close (not bit-exact) to the reference bytes
+        wv = mg.gen_gaussian_weights(mg.GaussianWeightParams(y, n), 123, "double", device="cuda")
+        assert wv.on_device
         host = oracle.gen_gaussian_weights(y, n, 123, "double")
         assert np.allclose(wv.values.cpu().numpy(), host, rtol=1e-13, atol=0)
-        w32 = mg.gen_gaussian_weights(mg.GaussianWeightParams(y, n), 123, "single")
+        w32 = mg.gen_gaussian_weights(mg.GaussianWeightParams(y, n), 123, "single", device=0)
         assert (w32.values.cpu().numpy() != host.astype(np.float32)).mean() < 1e-3
+        # the default is the reference's own bytes, on the host
+        d = mg.gen_gaussian_weights(mg.GaussianWeightParams(y, n), 123, "single")
+        assert isinstance(d.values, np.ndarray) and np.array_equal(d.values, host.astype(np.float32))
 
 
 def test_gather_from_peers_kernel(mg):
@@ -526,7 +547,7 @@ def test_config5_2p28_single_gpu(mg, oracle, rng):
     free, _ = torch.cuda.mem_get_info()
     if free < 6 * n * 4:
         pytest.skip("not enough device memory")
-    wv = mg.gen_gaussian_weights(mg.GaussianWeightParams(4.0, n), 777, "single")
+    wv = mg.gen_gaussian_weights(mg.GaussianWeightParams(4.0, n), 777, "single", device="cuda")
     b = mg.iterations_for(wv, 0.01).b
     anc = mg.megopolis(wv, b, seed=123, rng=rng)
     w_np = wv.values.cpu().numpy()
@@ -552,7 +573,7 @@ def test_maximum_sizes(mg, oracle, n, rng, kind):
     free, _ = torch.cuda.mem_get_info()
     if free < 3.5 * n * 8:
         pytest.skip("not enough device memory")
-    wv = mg.gen_gaussian_weights(mg.GaussianWeightParams(2.0, n), 31, "single")
+    wv = mg.gen_gaussian_weights(mg.GaussianWeightParams(2.0, n), 31, "single", device="cuda")
     b = 6
     part = mg.PartitionConfig(256) if kind == "c2" else None
     anc = (mg.metropolis_c2(wv, b, part, seed=5, rng=rng) if kind == "c2"
