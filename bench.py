@@ -71,6 +71,8 @@ def parse():
     ap.add_argument("--no-config5", action="store_true")
     ap.add_argument("--no-probe", action="store_true", help="skip the L2 read-bandwidth probe")
     ap.add_argument("--quality-runs", type=int, default=32)  # K >= 32
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the sharded NCCL step even at one rank (torchrun --nproc-per-node 1)")
     return ap.parse_args()
 
 
@@ -319,10 +321,13 @@ def l2_probe(probe, w, off_dev, b, stream):
     return out
 
 
-def issue_block():
+def issue_block(rng, n):
+    """The committed ncu summary of the kernel at this stream and size (profiles/megopolis_issue.json,
+    made by scripts/issue_block.py from an ncu --set full capture of the same launch)."""
     try:
         with open(os.path.join(ROOT, "profiles", "megopolis_issue.json")) as f:
-            return json.load(f)
+            d = json.load(f)
+        return dict(d[f"{rng}@{n}"], file="profiles/megopolis_issue.json")
     except Exception:
         return None
 
@@ -347,7 +352,8 @@ def main():
         local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    sharded = world > 1 or args.sharded  # the stripes layout + NCCL exchange (also at world 1)
+    if sharded:
         if loopback:
             dist.init_process_group("gloo")
         else:
@@ -366,26 +372,26 @@ def main():
             self.n = n
             self.h, self.half = n // 2 // world, n // 2
             self.lo0, self.lo1 = rank * self.h, (rank + 1) * self.h
-            self.n_loc = 2 * self.h if world > 1 else n
-            if world > 1 and (n % (2 * world) or self.h % 32):
+            self.n_loc = 2 * self.h if sharded else n
+            if sharded and (n % (2 * world) or self.h % 32):
                 raise SystemExit(f"N={n} does not split into 32-aligned stripes over {world} ranks")
             if w_dev_full is None:
                 w_dev_full = torch.from_numpy(w_host).to(dev)
-            if world > 1:
+            if sharded:
                 self.local_w = torch.cat([w_dev_full[self.lo0:self.lo1], w_dev_full[self.half + self.lo0:self.half + self.lo1]])
                 self.full = torch.empty(n, dtype=torch.float32, device=dev)
                 del w_dev_full
             else:
                 self.full = w_dev_full
                 self.local_w = w_dev_full
-            self.aligned = world > 1 and slice_tree_aligned(world, self.h)
+            self.aligned = sharded and slice_tree_aligned(world, self.h)
             self.stats = torch.empty(16, dtype=torch.float64, device=dev)
             self.stats_all = torch.empty(world * 16, dtype=torch.int64, device=dev)
             self.anc = torch.empty(self.n_loc, dtype=torch.int64, device=dev)
             self.b = None
 
         def gather_weights(self, async_op=False):
-            if world > 1:
+            if sharded:
                 h, half = self.h, self.half
                 w1 = dist.all_gather_into_tensor(self.full[:half], self.local_w[:h], async_op=async_op)
                 w2 = dist.all_gather_into_tensor(self.full[half:], self.local_w[h:], async_op=async_op)
@@ -395,7 +401,7 @@ def main():
         def step(self, rng_id, ev=None):
             """(all-gather) -> stats -> B -> megopolis over this rank's particles."""
             h = self.h
-            if world > 1 and self.aligned:
+            if sharded and self.aligned:
                 # stripe statistics + a 16-word all-gather give the global B bit for bit (numpy's
                 # tree: lower half + upper half, each the rank stripes in order;
                 # distributed.combine_slice_stats); B is derived while the weights are in flight
@@ -419,7 +425,7 @@ def main():
                 flags = _lib.FLAG_NONZERO if host.view(np.int64)[4] == 0 else 0
             if ev is not None:
                 ev[0].record(stream)
-            if world > 1:
+            if sharded:
                 _lib.check(L.mgp_resample_stripes(_lib.KIND["megopolis"], D.ptr(self.full), 0, self.n, b, RUN_SEED, 32,
                                                   0, 1, rng_id, flags, self.lo0, self.lo1, D.ptr(self.anc), sp))
             else:
@@ -437,7 +443,7 @@ def main():
             starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
             ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
             kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-            if world > 1:
+            if sharded:
                 dist.barrier()
             torch.cuda.synchronize()
             import gc
@@ -452,12 +458,12 @@ def main():
                     ends[s].record(stream)
                 torch.cuda.synchronize()
             gc.enable()
-            if world > 1:
+            if sharded:
                 dist.barrier()
             step_ms = [starts[s].elapsed_time(ends[s]) for s in range(steps)]
             kern_ms = [kev[s][0].elapsed_time(kev[s][1]) for s in range(steps)]
             t_total = sum(step_ms)
-            if world > 1:
+            if sharded:
                 tt = torch.tensor([t_total], dtype=torch.float64, device=dev)
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
                 t_total = float(tt.item())
@@ -466,7 +472,7 @@ def main():
 
         def owned_ranges(self):
             """(global range, offset into anc) pairs of this rank's particles."""
-            if world == 1:
+            if not sharded:
                 return [((0, self.n), 0)]
             return [((self.lo0, self.lo1), 0), ((self.half + self.lo0, self.half + self.lo1), self.h)]
 
@@ -498,12 +504,8 @@ def main():
     achieved = alg_bytes / kern_avg(head) / 1e9
     mego_kernel = ("k_megopolis_philox_half (half-split, 4 particles/thread)" if args.rng == "philox"
                    else "k_megopolis_megores_f32 (float32 decision bracket, exact float64 fallback)")
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "megopolis_traffic.json")) as f:
-            traffic = json.load(f).get(args.rng, {}).get("dram_bytes_per_launch")
-    except Exception:
-        pass
+    ib = issue_block(args.rng, n_loc)
+    traffic = ib.get("dram_bytes_per_launch") if ib else None
     probe_res = None
     if not args.no_probe:
         try:
@@ -528,7 +530,7 @@ def main():
                     "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": hbm_src}
     roofline.update({"kernel": mego_kernel, "kernel_ms": kern_avg(head) * 1e3, "alg_bytes_per_launch": alg_bytes,
                      "hbm": {"peak": hbm_peak, "frac": achieved / hbm_peak, "peak_source": hbm_src},
-                     "probe": probe_res, "issue": issue_block()})
+                     "probe": probe_res, "issue": ib})
 
     # parity of what was timed: rank 0's timed ancestors vs the oracle on the same inputs
     parity = None
@@ -679,7 +681,9 @@ def main():
                        "N": N_CONFIG5, "B": b5, "value": N_CONFIG5 / (r5["ms_per_step"] / 1e3), "unit": "particles/s",
                        "ms_per_step": r5["ms_per_step"], "kernel_ms": kern_avg(r5) * 1e3,
                        "roofline": {"bound": "hbm", "achieved": ach5, "peak": hbm_peak, "unit": "GB/s",
-                                    "frac": ach5 / hbm_peak, "alg_bytes_per_launch": alg5},
+                                    "frac": ach5 / hbm_peak, "alg_bytes_per_launch": alg5,
+                                    "traffic": (issue_block(args.rng, nl5) or {}).get("dram_bytes_per_launch"),
+                                    "issue": issue_block(args.rng, nl5)},
                        "clocks": r5["clocks"]}
             if rank == 0:
                 from oracle import oracle
@@ -705,7 +709,7 @@ def main():
     if args.quality_runs >= 2:
         qs = {}
         for kind in ("megopolis", "metropolis"):
-            if world == 1:
+            if not sharded:
                 wv = mg.WeightVector(pop.full, "single")
                 acc = mg.QualityAccumulator(n_glob)
                 fn = mg.make_resampler(kind, rng=args.rng)
@@ -714,7 +718,7 @@ def main():
             else:
                 from paper_2109_13504_b200.distributed import ShardedResampler
 
-                sr = ShardedResampler(kind=kind, rng=args.rng, layout="stripes")
+                sr = ShardedResampler(kind=kind, rng=args.rng, layout="stripes", force_collectives=True)
                 acc = sr.quality(pop.local_w)
                 for k in range(args.quality_runs):
                     a_loc, _ = sr.resample(pop.local_w, b=b, seed=mg.derive_seed(2002, k))
@@ -734,7 +738,7 @@ def main():
             "step_breakdown_ms": {"step": [round(x, 3) for x in head["step_ms"]],
                                   "kernel": [round(x, 3) for x in head["kern_ms"]],
                                   "what": "weight stats -> B (host) -> megopolis" +
-                                          (" (+ NCCL all-gather of the weight stripes)" if world > 1 else "")},
+                                          (" (sharded: + NCCL all-gather of the weight stripes)" if sharded else "")},
             "clocks": head["clocks"],
             "streams": {k: {"value": n_glob / (r["ms_per_step"] / 1e3), "ms_per_step": r["ms_per_step"],
                             "kernel_ms": kern_avg(r) * 1e3,
@@ -746,7 +750,7 @@ def main():
             "quality": quality,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
 
 

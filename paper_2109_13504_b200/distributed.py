@@ -183,6 +183,9 @@ class ShardedResampler:
     group: object = None
     ops: object = None
     layout: str = "contiguous"  # or "stripes": rank r owns stripe r of each half of the population
+    # run the exchange collectives even at world size 1 (instead of local copies): exercises
+    # the NCCL data plane on a single GPU (tests/test_nccl_gpu.py)
+    force_collectives: bool = False
 
     def __post_init__(self):
         import torch.distributed as dist
@@ -223,7 +226,7 @@ class ShardedResampler:
 
     # -- 1. replicated weights ---------------------------------------------
     def _gather_into(self, out, part):
-        if self.world == 1:
+        if self.world == 1 and not self.force_collectives:
             out.copy_(part)
             return
         try:
@@ -354,7 +357,7 @@ class ShardedResampler:
         n_all = n_local * self.world
         if anc.numel() and (int(anc.min()) < 0 or int(anc.max()) >= n_all):
             raise ValueError("ancestor indices out of range")
-        if self.world == 1:
+        if self.world == 1 and not self.force_collectives:
             return self.ops.offspring(anc, n_local)
         _, _, _, recv_idx = self._send_to_owners(anc, n_local)
         return self.ops.offspring(recv_idx, n_local)
@@ -374,7 +377,7 @@ class ShardedResampler:
         n_local = states_local.shape[0]
         dev = states_local.device
         anc = anc_local.to(device=dev, dtype=t.int64)
-        if self.world == 1:
+        if self.world == 1 and not self.force_collectives:
             return self.ops.gather_rows(states_local, self._owner_local(anc, n_local)[1])
         order, sc, rc, recv_idx = self._send_to_owners(anc, n_local)
         rows = self.ops.gather_rows(states_local, recv_idx)

@@ -27,7 +27,10 @@ ap.add_argument("--dtype", default="single")
 a = ap.parse_args()
 
 L = _lib.lib()
-w = mg.gen_gaussian_weights(mg.GaussianWeightParams(a.y, a.n), 20240, a.dtype, device="cuda")
+# the reference's weight bytes (bench.py's input) up to 2^24; device-generated above (config 5)
+w = mg.gen_gaussian_weights(mg.GaussianWeightParams(a.y, a.n), 20240, a.dtype, device="cuda" if a.n > 1 << 24 else None)
+if not w.on_device:
+    w = mg.WeightVector(torch.from_numpy(w.values).cuda(), a.dtype)
 stats = torch.empty(8, dtype=torch.float64, device="cuda")
 anc = torch.empty(a.n, dtype=torch.int64, device="cuda")
 sp = D.stream_ptr()

@@ -40,6 +40,10 @@ REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 def ref_megores():
     """The UNMODIFIED reference package staged under baseline/_ref (scripts/stage_reference.sh);
     a missing stage is a failure, not a skip."""
+    if not os.path.isfile(os.path.join(REF_DIR, "megores", "resample.py")) and os.path.isdir("/root/reference/pkg"):
+        import subprocess  # build container only: the GPU box has no /root/reference (it gets the staged copy)
+
+        subprocess.run(["sh", os.path.join(ROOT, "scripts", "stage_reference.sh")], check=True)
     if not os.path.isfile(os.path.join(REF_DIR, "megores", "resample.py")):
         pytest.fail("unmodified reference not staged under baseline/_ref (run scripts/stage_reference.sh)")
     if REF_DIR not in sys.path:

@@ -51,9 +51,10 @@ def test_indices_and_csv(tmp_path):
         storage.save_trajectory_csv(tmp_path / "t.csv", [1.0], [1.0, 2.0])
 
 
-def test_reads_files_written_by_the_reference(tmp_path):
-    """Byte compatibility with megores.storage when the reference is importable (build container)."""
-    megores = pytest.importorskip("megores")
+def test_reads_files_written_by_the_reference(tmp_path, ref_megores):
+    """Byte compatibility with the unmodified reference's storage module (staged under
+    baseline/_ref by scripts/stage_reference.sh)."""
+    megores = ref_megores
     from megores import storage as ref_storage
 
     w = megores.WeightVector(np.arange(1, 9, dtype=np.float32), "single")
