@@ -82,6 +82,11 @@ typedef struct {
 int mgp_abi_version(void);
 const char *mgp_last_error(void);
 
+/* WeightVector's host-side validation (M/weights.py:53-59) in one parallel pass over host memory
+ * (no device work): counts[0..3] = non-finite, negative (finite, < 0; -0.0 is not), zero and
+ * positive elements. */
+int mgp_check_host_weights(const void *h_w, int dtype, int64_t n, int64_t *counts);
+
 /* Return the library's cached scratch memory on `device` (-1: the current device) to the
  * driver: trims the private stream-ordered pool (cudaMemPoolTrimTo(pool, 0)). */
 int mgp_release_cached_memory(int device);

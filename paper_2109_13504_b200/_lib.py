@@ -31,6 +31,7 @@ SIGNATURES = {
     "mgp_abi_version": (_i32, []),
     "mgp_last_error": (ctypes.c_char_p, []),
     "mgp_release_cached_memory": (_i32, [_i32]),
+    "mgp_check_host_weights": (_i32, [_vp, _i32, _i64, _vp]),
     "mgp_weight_stats": (_i32, [_vp, _i32, _i64, _vp, _vp]),
     "mgp_compute_iterations": (_i32, [_dbl, _dbl, _dbl, _vp]),
     "mgp_offsets_host": (_i32, [_u64, _i64, _i32, _i32, _vp]),

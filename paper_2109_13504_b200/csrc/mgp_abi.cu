@@ -6,12 +6,19 @@
 // the device in the kernel parameter space), stream-ordered scratch, and the
 // host-buffer path that overlaps ancestor download with compute.
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <functional>
+#include <memory>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -710,14 +717,201 @@ int plan_free(Plan& p, cudaStream_t st) {
 #define MGP_HOST_CHUNKS 16  // lower/upper chunk pairs of the half-split host path
 #endif
 
+// ---------------------------------------------------------------------------
+// Pageable host buffers.  A cudaMemcpyAsync from or to pageable memory is staged by the
+// driver through its own bounce buffer, one copy at a time and synchronously for D2H.  The
+// host entry instead streams pageable buffers through page-locked staging slots of its own:
+// host threads copy (and first-touch) the pageable side in parallel while the DMA engine
+// moves the previous slot, so the pageable copy overlaps both the transfer and the kernel.
+
+// A small persistent pool of host threads (created on first use) for the host-side work of
+// the host-buffer entry: the pageable<->staging memcpys, pre-faulting a pageable output while
+// the kernels run, and the host weight validation.  A batch of tasks is awaited through its
+// own ticket, so concurrent callers share the pool without waiting for each other.
+class HostPool {
+ public:
+  using Ticket = std::shared_ptr<std::atomic<int>>;
+  static HostPool& get() {
+    static HostPool pool;
+    return pool;
+  }
+  int threads() const { return nthreads_; }
+  // queue tasks; returns the ticket to wait on
+  Ticket submit(std::vector<std::function<void()>> tasks) {
+    auto left = std::make_shared<std::atomic<int>>((int)tasks.size());
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      for (auto& t : tasks) q_.push_back({std::move(t), left});
+    }
+    cv_.notify_all();
+    return left;
+  }
+  void wait(const Ticket& t) {
+    if (!t) return;
+    for (;;) {  // help with queued work while waiting (the caller is a worker too)
+      Job j;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        if (t->load() == 0) return;
+        if (q_.empty()) {
+          done_.wait(lk, [&] { return t->load() == 0 || !q_.empty(); });
+          continue;
+        }
+        j = std::move(q_.front());
+        q_.pop_front();
+      }
+      finish(j);
+    }
+  }
+  // n bytes in parallel pieces of at least 1 MiB
+  void copy(void* dst, const void* src, size_t n) {
+    const size_t piece = std::max<size_t>(1 << 20, (n + nthreads_ - 1) / nthreads_);
+    if (n <= piece) { std::memcpy(dst, src, n); return; }
+    std::vector<std::function<void()>> tasks;
+    for (size_t off = 0; off < n; off += piece) {
+      const size_t len = std::min(piece, n - off);
+      tasks.push_back([=] { std::memcpy((char*)dst + off, (const char*)src + off, len); });
+    }
+    wait(submit(std::move(tasks)));
+  }
+
+ private:
+  struct Job {
+    std::function<void()> fn;
+    Ticket left;
+  };
+  HostPool() {
+    const unsigned hw = std::thread::hardware_concurrency();
+    nthreads_ = (int)std::max(2u, std::min(hw ? hw : 4u, 16u));
+    for (int t = 0; t < nthreads_ - 1; ++t) th_.emplace_back([this] { run(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  void finish(Job& j) {
+    j.fn();
+    if (j.left->fetch_sub(1) == 1) {
+      std::lock_guard<std::mutex> lk(mu_);
+      done_.notify_all();
+    }
+  }
+  void run() {
+    for (;;) {
+      Job j;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || !q_.empty(); });
+        if (q_.empty()) return;
+        j = std::move(q_.front());
+        q_.pop_front();
+      }
+      finish(j);
+    }
+  }
+  int nthreads_ = 4;
+  std::vector<std::thread> th_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  std::deque<Job> q_;
+  bool stop_ = false;
+};
+
+// Fault in a pageable output buffer (one byte written per 4 KiB page, in parallel) while the
+// device works: the staged downloads then copy into resident pages.  The caller overwrites
+// every byte afterwards.
+HostPool::Ticket prefault(void* h, size_t n) {
+  HostPool& hp = HostPool::get();
+  const size_t piece = std::max<size_t>(4 << 20, (n + hp.threads() - 1) / hp.threads());
+  std::vector<std::function<void()>> tasks;
+  for (size_t off = 0; off < n; off += piece) {
+    const size_t len = std::min(piece, n - off);
+    tasks.push_back([=] {
+      volatile char* c = (volatile char*)h + off;
+      for (size_t q = 0; q < len; q += 4096) c[q] = 0;
+    });
+  }
+  return hp.submit(std::move(tasks));
+}
+
+constexpr size_t STAGE_SLOT = 8u << 20;  // bytes per page-locked staging slot
+constexpr int STAGE_SLOTS = 3;
+constexpr size_t STAGE_MIN = 4u << 20;   // smaller pageable buffers go through the driver
+
 // Per-thread, per-device streams and events of the host-buffer path, created once (stream
-// and event creation would otherwise cost tens of microseconds per call).
+// and event creation would otherwise cost tens of microseconds per call), plus the staging
+// slots for pageable buffers (allocated on first pageable use).
 struct HostCtx {
   int dev;
   cudaStream_t st, st2, cp;
   std::vector<cudaEvent_t> ev;
+  char* stage = nullptr;                // STAGE_SLOTS x STAGE_SLOT page-locked bytes
+  cudaEvent_t slot_ev[STAGE_SLOTS] = {};  // last DMA using each slot
 };
 thread_local std::vector<HostCtx*> g_host_ctx;
+
+int stage_ready(HostCtx* c) {
+  if (c->stage) return 0;
+  CUDA_TRY(cudaHostAlloc((void**)&c->stage, STAGE_SLOT * STAGE_SLOTS, cudaHostAllocPortable));
+  for (auto& e : c->slot_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return 0;
+}
+
+// pageable h_src -> device, through the staging slots on stream st (returns after the last
+// slot is queued; the DMA of slot k overlaps the host copy into slot k+1)
+int staged_h2d(HostCtx* c, void* d_dst, const void* h_src, size_t n, cudaStream_t st) {
+  if (int rc = stage_ready(c)) return rc;
+  int k = 0;
+  for (size_t off = 0; off < n; off += STAGE_SLOT, k = (k + 1) % STAGE_SLOTS) {
+    const size_t len = std::min(STAGE_SLOT, n - off);
+    char* slot = c->stage + (size_t)k * STAGE_SLOT;
+    CUDA_TRY(cudaEventSynchronize(c->slot_ev[k]));  // the slot's previous DMA has drained
+    HostPool::get().copy(slot, (const char*)h_src + off, len);
+    CUDA_TRY(cudaMemcpyAsync((char*)d_dst + off, slot, len, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaEventRecord(c->slot_ev[k], st));
+  }
+  return 0;
+}
+
+// device -> pageable h_dst for a list of (dst offset, src offset, bytes) pieces, each queued on
+// stream cp after its ready event; the host copy of one slot overlaps the DMA of the next
+struct StagePiece {
+  size_t dst, src, len;
+  cudaEvent_t ready;
+};
+int staged_d2h(HostCtx* c, void* h_dst, const void* d_src, const std::vector<StagePiece>& pieces, cudaStream_t cp,
+               const HostPool::Ticket& faulted) {
+  if (int rc = stage_ready(c)) return rc;
+  std::vector<StagePiece> segs;  // split into slot-sized segments
+  for (const auto& p : pieces)
+    for (size_t o = 0; o < p.len; o += STAGE_SLOT)
+      segs.push_back({p.dst + o, p.src + o, std::min(STAGE_SLOT, p.len - o), o == 0 ? p.ready : nullptr});
+  size_t issued = 0;
+  auto issue = [&](size_t q) -> cudaError_t {
+    const int k = (int)(q % STAGE_SLOTS);
+    if (segs[q].ready) {
+      const cudaError_t e = cudaStreamWaitEvent(cp, segs[q].ready, 0);
+      if (e != cudaSuccess) return e;
+    }
+    const cudaError_t e = cudaMemcpyAsync(c->stage + (size_t)k * STAGE_SLOT, (const char*)d_src + segs[q].src,
+                                          segs[q].len, cudaMemcpyDeviceToHost, cp);
+    if (e != cudaSuccess) return e;
+    return cudaEventRecord(c->slot_ev[k], cp);
+  };
+  for (; issued < segs.size() && issued < (size_t)STAGE_SLOTS - 1; ++issued) CUDA_TRY(issue(issued));
+  HostPool::get().wait(faulted);  // the output's pages are resident before the first host copy
+  for (size_t q = 0; q < segs.size(); ++q) {
+    if (issued < segs.size()) CUDA_TRY(issue(issued++));  // keep the next slots' DMAs in flight
+    const int k = (int)(q % STAGE_SLOTS);
+    CUDA_TRY(cudaEventSynchronize(c->slot_ev[k]));
+    HostPool::get().copy((char*)h_dst + segs[q].dst, c->stage + (size_t)k * STAGE_SLOT, segs[q].len);
+  }
+  return 0;
+}
 
 int host_ctx(HostCtx** out) {
   int dev = 0;
@@ -766,6 +960,46 @@ extern "C" {
 int mgp_abi_version(void) { return MGP_ABI_VERSION; }
 
 const char* mgp_last_error(void) { return g_err.c_str(); }
+
+int mgp_check_host_weights(const void* h_w, int dtype, int64_t n, int64_t* counts) {
+  if ((!h_w && n > 0) || !counts) return set_err(MGP_EINVAL, "null pointer");
+  if (dtype != MGP_F32 && dtype != MGP_F64) return set_err(MGP_EINVAL, "dtype must be MGP_F32 or MGP_F64");
+  if (n < 0) return set_err(MGP_EINVAL, "negative length");
+  HostPool& hp = HostPool::get();
+  const int64_t piece = std::max<int64_t>(1 << 18, (n + hp.threads() - 1) / hp.threads());
+  const int64_t np_ = (n + piece - 1) / piece;
+  std::vector<std::array<int64_t, 4>> part((size_t)std::max<int64_t>(np_, 1), std::array<int64_t, 4>{0, 0, 0, 0});
+  std::vector<std::function<void()>> tasks;
+  for (int64_t q = 0; q < np_; ++q) {
+    tasks.push_back([=, &part] {
+      const int64_t lo = q * piece, hi = std::min(n, lo + piece);
+      int64_t nf = 0, ng = 0, nz = 0;
+      if (dtype == MGP_F32) {
+        const uint32_t* b = (const uint32_t*)h_w;
+        for (int64_t i = lo; i < hi; ++i) {
+          const uint32_t v = b[i], mag = v & 0x7FFFFFFFu;
+          nf += mag >= 0x7F800000u;                       // inf / nan
+          ng += (v >> 31) & (mag != 0) & (mag < 0x7F800000u);  // finite and < 0 (-0.0 is not)
+          nz += mag == 0;
+        }
+      } else {
+        const uint64_t* b = (const uint64_t*)h_w;
+        for (int64_t i = lo; i < hi; ++i) {
+          const uint64_t v = b[i], mag = v & 0x7FFFFFFFFFFFFFFFull;
+          nf += mag >= 0x7FF0000000000000ull;
+          ng += (v >> 63) & (mag != 0) & (mag < 0x7FF0000000000000ull);
+          nz += mag == 0;
+        }
+      }
+      part[(size_t)q] = {nf, ng, nz, (hi - lo) - nf - ng - nz};
+    });
+  }
+  hp.wait(hp.submit(std::move(tasks)));
+  for (int k = 0; k < 4; ++k) counts[k] = 0;
+  for (const auto& pc : part)
+    for (int k = 0; k < 4; ++k) counts[k] += pc[k];
+  return 0;
+}
 
 int mgp_release_cached_memory(int device) {
   int prev = 0;
@@ -911,7 +1145,16 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
   HCUDA(pool_malloc(&d_w, wbytes, st));
   HCUDA(pool_malloc(&d_anc, sizeof(int64_t) * n, st));
   HCUDA(pool_malloc(&d_stats, sizeof(mgp_weight_stats_t), st));
-  HCUDA(cudaMemcpyAsync(d_w, h_w, wbytes, cudaMemcpyHostToDevice, st));
+  if (wbytes >= STAGE_MIN && !host_is_pinned(h_w)) HTRY(staged_h2d(hc, d_w, h_w, wbytes, st));
+  else HCUDA(cudaMemcpyAsync(d_w, h_w, wbytes, cudaMemcpyHostToDevice, st));
+  // a pageable output is faulted in by the host pool while the device validates and resamples
+  const bool anc_pinned = host_is_pinned(h_anc);
+  HostPool::Ticket faulted;
+  if (!anc_pinned && sizeof(int64_t) * (size_t)n >= STAGE_MIN) faulted = prefault(h_anc, sizeof(int64_t) * (size_t)n);
+  struct FaultWait {  // never return while pool threads still write into h_anc
+    const HostPool::Ticket& t;
+    ~FaultWait() { HostPool::get().wait(t); }
+  } fault_wait{faulted};
   HTRY(mgp_weight_stats(d_w, dtype, n, d_stats, st));
   HCUDA(cudaMemcpyAsync(&hs, d_stats, sizeof hs, cudaMemcpyDeviceToHost, st));
   HCUDA(cudaStreamSynchronize(st));
@@ -929,21 +1172,32 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
   // A D2H into pageable memory returns only once it has completed, so for a pageable h_anc
   // every chunk kernel is queued first and the downloads follow (each still overlaps the
   // chunks behind it); with pinned memory the copies are queued as the chunks are.
-  const bool pinned = host_is_pinned(h_anc);
-  struct Pending { int64_t dst, src, cnt; };
-  std::vector<Pending> pend;
-  auto d2h = [&](int64_t dst, int64_t src, int64_t cnt) -> cudaError_t {
-    if (!pinned) { pend.push_back({dst, src, cnt}); return cudaSuccess; }
+  // Pinned h_anc: each chunk's download is queued behind its kernel as the chunks are launched.
+  // Pageable h_anc: the chunks are listed with their ready events and, once every chunk kernel
+  // is queued, streamed through the page-locked staging slots (staged_d2h: parallel host
+  // copies overlap the next slot's DMA and the remaining kernels); small pageable buffers take
+  // the driver's own staging after the launches.
+  const bool pinned = anc_pinned;
+  std::vector<StagePiece> pend;
+  auto d2h = [&](int64_t dst, int64_t src, int64_t cnt, cudaEvent_t ready) -> cudaError_t {
+    if (!pinned) {
+      pend.push_back({sizeof(int64_t) * (size_t)dst, sizeof(int64_t) * (size_t)src, sizeof(int64_t) * (size_t)cnt, ready});
+      return cudaSuccess;
+    }
+    cudaError_t e = cudaStreamWaitEvent(cp, ready, 0);
+    if (e != cudaSuccess) return e;
     return cudaMemcpyAsync(h_anc + dst, d_anc + src, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost, cp);
   };
-  auto flush_pending = [&]() -> cudaError_t {
-    for (const Pending& q : pend) {
-      const cudaError_t e = cudaMemcpyAsync(h_anc + q.dst, d_anc + q.src, sizeof(int64_t) * q.cnt,
-                                            cudaMemcpyDeviceToHost, cp);
-      if (e != cudaSuccess) return e;
+  auto flush_pending = [&]() -> int {
+    if (pend.empty()) return 0;
+    size_t total = 0;
+    for (const auto& q : pend) total += q.len;
+    if (total >= STAGE_MIN) return staged_d2h(hc, h_anc, d_anc, pend, cp, faulted);
+    for (const auto& q : pend) {
+      CUDA_TRY(cudaStreamWaitEvent(cp, q.ready, 0));
+      CUDA_TRY(cudaMemcpyAsync((char*)h_anc + q.dst, (const char*)d_anc + q.src, q.len, cudaMemcpyDeviceToHost, cp));
     }
-    pend.clear();
-    return cudaSuccess;
+    return 0;
   };
   if (plan_half_ok(p)) {  // half-split kernel: chunk c = lower-half range [c0, c1) + its mirror
     p.half = true;
@@ -963,11 +1217,10 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
       HTRY(run_range(p, c0, c1, d_anc, ks));
       cudaEvent_t ev = new_event();
       HCUDA(cudaEventRecord(ev, ks));
-      HCUDA(cudaStreamWaitEvent(cp, ev, 0));
-      HCUDA(d2h(c0, c0, c1 - c0));
-      HCUDA(d2h(half + c0, half + c0, c1 - c0));
+      HCUDA(d2h(c0, c0, c1 - c0, ev));
+      HCUDA(d2h(half + c0, half + c0, c1 - c0, ev));
     }
-    HCUDA(flush_pending());
+    HTRY(flush_pending());
     HCUDA(cudaStreamSynchronize(cp));
     HCUDA(cudaStreamSynchronize(st2));
     HCUDA(cudaStreamSynchronize(st));
@@ -984,10 +1237,9 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
     HTRY(run_range(p, c0, c1, d_anc, st));
     cudaEvent_t ev = new_event();
     HCUDA(cudaEventRecord(ev, st));
-    HCUDA(cudaStreamWaitEvent(cp, ev, 0));
-    HCUDA(d2h(c0, c0, c1 - c0));
+    HCUDA(d2h(c0, c0, c1 - c0, ev));
   }
-  HCUDA(flush_pending());
+  HTRY(flush_pending());
   HCUDA(cudaStreamSynchronize(cp));
   HCUDA(cudaStreamSynchronize(st));
   cleanup();

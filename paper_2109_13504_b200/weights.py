@@ -64,6 +64,18 @@ def device_stats(values) -> WeightStats:
                        s.n_notnormal)
 
 
+def _host_flags(values: np.ndarray):
+    """(any non-finite, any negative) of a host float array: one parallel pass in libmgp
+    (mgp_check_host_weights, host threads only) -- the reference's two numpy scans
+    (M/weights.py:56-59) cost ~16 ms at 2^24."""
+    if values.size >= 1 << 16 and values.flags.c_contiguous:
+        counts = np.zeros(4, dtype=np.int64)
+        _lib.check(_lib.lib().mgp_check_host_weights(values.ctypes.data, 0 if values.dtype == np.float32 else 1,
+                                                     values.size, counts.ctypes.data))
+        return bool(counts[0]), bool(counts[1])
+    return (not np.all(np.isfinite(values))), bool(np.any(values < 0))
+
+
 class WeightVector:
     """Non-negative particle weights; normalisation is not required (M/weights.py:42-62).
 
@@ -90,9 +102,10 @@ class WeightVector:
         values = np.asarray(values, dtype=_DTYPES[precision])
         if values.ndim != 1 or len(values) < 1:
             raise ValueError("weights must be a non-empty 1-d sequence")
-        if not np.all(np.isfinite(values)):
+        nonfinite, negative = _host_flags(values)
+        if nonfinite:
             raise ValueError("weights must be finite")
-        if np.any(values < 0):
+        if negative:
             raise ValueError("weights must be non-negative")
         self.values = values
 

@@ -117,3 +117,26 @@ def test_pw_depth_tree_covers_all(oracle):
             pos += ln
         assert pos == n
         assert math.isfinite(oracle.pairwise_sum(np.ones(n)))
+
+
+def test_host_weight_validation_matches_numpy():
+    """mgp_check_host_weights (WeightVector's host validation, M/weights.py:53-59) against the
+    reference's numpy scans on arrays seeded with non-finite, negative, -0.0 and zero values."""
+    from paper_2109_13504_b200 import _lib
+
+    rs = np.random.default_rng(8)
+    specials = [np.inf, -np.inf, np.nan, -1e-30, -0.0, 0.0, 1e-45, -5.0]
+    for dt in (np.float32, np.float64):
+        for n in (1, 7, (1 << 18) + 3, 1 << 20):
+            for k in range(6):
+                x = rs.random(n).astype(dt)
+                for _ in range(k):
+                    x[rs.integers(0, n)] = rs.choice(specials)
+                counts = np.zeros(4, dtype=np.int64)
+                _lib.check(_lib.lib().mgp_check_host_weights(x.ctypes.data, 0 if dt == np.float32 else 1, n,
+                                                             counts.ctypes.data))
+                fin = np.isfinite(x)
+                assert counts[0] == int((~fin).sum())
+                assert counts[1] == int((x[fin] < 0).sum())
+                assert counts[2] == int((x == 0).sum())
+                assert counts.sum() == n
