@@ -286,6 +286,10 @@ int mgp_philox_selftest(uint64_t key, uint32_t c1, uint32_t c2, uint32_t c3, int
  * since the last reset).  reset != 0 zeroes the counter after reading it. */
 int mgp_debug_megores_fallbacks(int64_t *h_count, int reset);
 
+/* Measurement switch for mgp_offspring: 1 = the int32 global-atomic histogram (round 1), 0 = the
+ * bucketed shared-memory histogram (default).  Process-wide; for A/B timing and tests only. */
+int mgp_debug_offspring_mode(int atomic_histogram);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1252,6 +1252,9 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
 #define MGP_OFFSPRING_I32_MIN (1ll << 20)
 #endif
 
+// measurement switch (mgp_debug_offspring_mode): 1 = the round-1 int32 atomic histogram, for A/B
+static std::atomic<int> g_offspring_atomic{0};
+
 int mgp_offspring(const int64_t* d_anc, int64_t n_anc, int64_t n, int64_t* d_counts, int32_t* d_bad, void* stream) {
   if (n < 0 || n_anc < 0) return set_err(MGP_EINVAL, "negative size");
   cudaStream_t st = S(stream);
@@ -1260,6 +1263,35 @@ int mgp_offspring(const int64_t* d_anc, int64_t n_anc, int64_t n, int64_t* d_cou
   int32_t* bad = d_bad;
   if (!bad && n_anc) CUDA_TRY(sc.alloc(&bad, sizeof(int32_t)));
   const unsigned grid = (unsigned)((n_anc + 255) / 256);
+  // Large histograms: bucketed (no per-particle global atomics; mgp_kernels.cuh k_offb_*)
+  const int64_t K = (n + OFFB_BINS - 1) / OFFB_BINS;
+  const int64_t tiles = (n_anc + OFFB_TILE - 1) / OFFB_TILE;
+  if (n >= MGP_OFFSPRING_I32_MIN && K <= OFFB_KMAX && n_anc > 0 && n_anc <= MAX_N && K * tiles < (1ll << 30) &&
+      !g_offspring_atomic) {
+    const int64_t m = K * tiles + 1;  // the bucket-major count matrix plus the total
+    uint32_t *mat = nullptr, *off = nullptr;
+    uint16_t* runs = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, mat, off, (int)m, st));
+    CUDA_TRY(sc.alloc(&mat, sizeof(uint32_t) * m));
+    CUDA_TRY(sc.alloc(&off, sizeof(uint32_t) * m));
+    CUDA_TRY(sc.alloc(&runs, sizeof(uint16_t) * n_anc));
+    CUDA_TRY(sc.alloc(&tmp, tmp_bytes + 16));
+    CUDA_TRY(cudaMemsetAsync(mat + (m - 1), 0, sizeof(uint32_t), st));
+    k_offb_count<<<(unsigned)tiles, OFFB_THREADS, 0, st>>>(d_anc, n_anc, n, (int)K, tiles, mat, bad);
+    LAUNCH_CHECK("k_offb_count");
+    CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, mat, off, (int)m, st));
+    const size_t ssm = sizeof(uint32_t) * (3 * K + OFFB_TILE);
+    CUDA_TRY(cudaFuncSetAttribute(k_offb_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+    k_offb_scatter<<<(unsigned)tiles, OFFB_THREADS, ssm, st>>>(d_anc, n_anc, n, (int)K, tiles, mat, off, runs);
+    LAUNCH_CHECK("k_offb_scatter");
+    const size_t hsm = sizeof(uint32_t) * OFFB_BINS;
+    CUDA_TRY(cudaFuncSetAttribute(k_offb_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+    k_offb_hist<<<(unsigned)K, 512, hsm, st>>>(runs, off, tiles, n, d_counts);
+    LAUNCH_CHECK("k_offb_hist");
+    return 0;
+  }
   // Large histograms count in int32 (counts <= n_anc < 2^31): half the footprint of the int64
   // array, so the random-address atomics stay in L2 instead of read-modify-writing DRAM
   // sectors; one streaming pass widens to the ABI's int64.
@@ -1935,6 +1967,11 @@ extern "C" int mgp_philox_selftest(uint64_t key, uint32_t c1, uint32_t c2, uint3
   unsigned long long h = 0;
   CUDA_TRY(cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost));
   *h_mismatch = (int64_t)h;
+  return 0;
+}
+
+extern "C" int mgp_debug_offspring_mode(int atomic_histogram) {
+  g_offspring_atomic.store(atomic_histogram ? 1 : 0);
   return 0;
 }
 

@@ -1005,6 +1005,119 @@ __global__ void k_offspring(const int64_t* __restrict__ anc, int64_t n_anc, int6
   }
 }
 
+// ---------------------------------------------------------------------------
+// Bucketed offspring histogram (no per-particle global atomics).  The bins [0, n) are split into
+// K = ceil(n / 2^14) buckets; the ancestors are moved into per-bucket runs, then every bucket is
+// histogrammed by one CTA in shared memory (2^14 uint32 bins, 64 KB) and written out as the
+// ABI's int64 counts in one coalesced pass.  Launches:
+//   k_offb_count    per tile of OFFB_TILE ancestors: bucket counts in shared memory, written to
+//                   the bucket-major matrix cnt[b * tiles + tile]; validates the range (bad flag)
+//   (CUB exclusive scan of the matrix: every (bucket, tile) run's start; bucket b's run is
+//    [off[b * tiles], off[(b + 1) * tiles]))
+//   k_offb_scatter  per tile: a counting sort by bucket in shared memory (from the tile's column
+//                   of the count matrix), then every (tile, bucket) run leaves as one contiguous
+//                   uint16 store of the low 14 bits (scattered 2-byte stores would run at the L2's
+//                   random-transaction rate, like the atomics this replaces)
+//   k_offb_hist     one CTA per bucket: shared-memory atomics over its run, then 2^14 int64
+//                   counts (coalesced streaming stores)
+// HBM traffic per call: 2 x 8N (ancestors read twice) + 8N (counts) against the algorithmic
+// 16N; the 2N-byte runs stay in L2.  Used for K <= OFFB_KMAX (n <= 2^27).  (Staging the
+// ancestors as uint32 for the second pass was slower: 0.162 ms.)
+// Measured at 2^24 (Megopolis ancestors, y = 4): 0.149 ms against 0.212 ms for the int32
+// global-atomic histogram + widening pass (scripts/mb/offspring_time.py).  A variant that sorted
+// each tile once and let the bucket CTAs gather ~16-element runs from every tile ran at 0.204 ms
+// (the gathers are latency-bound).
+constexpr int OFFB_BITS = 14;
+constexpr int OFFB_BINS = 1 << OFFB_BITS;
+constexpr int OFFB_TILE = 16384;
+constexpr int OFFB_THREADS = 512;
+constexpr int OFFB_KMAX = 8192;
+
+__global__ void __launch_bounds__(OFFB_THREADS) k_offb_count(const int64_t* __restrict__ anc, int64_t n_anc, int64_t n,
+                                                             int K, int64_t tiles, uint32_t* __restrict__ cnt_mat,
+                                                             int* bad) {
+  __shared__ uint32_t cnt[OFFB_KMAX];
+  for (int b = threadIdx.x; b < K; b += OFFB_THREADS) cnt[b] = 0;
+  __syncthreads();
+  const int64_t t0 = (int64_t)blockIdx.x * OFFB_TILE;
+  const int len = (int)min((int64_t)OFFB_TILE, n_anc - t0);
+  bool oob = false;
+  for (int q = threadIdx.x; q < len; q += OFFB_THREADS) {
+    const int64_t a = anc[t0 + q];
+    if (a < 0 || a >= n) { oob = true; continue; }
+    atomicAdd(&cnt[(unsigned)(a >> OFFB_BITS)], 1u);
+  }
+  if (oob) atomicExch(bad, 1);
+  __syncthreads();
+  for (int b = threadIdx.x; b < K; b += OFFB_THREADS) cnt_mat[(int64_t)b * tiles + blockIdx.x] = cnt[b];
+}
+
+__global__ void __launch_bounds__(OFFB_THREADS) k_offb_scatter(const int64_t* __restrict__ anc, int64_t n_anc, int64_t n,
+                                                               int K, int64_t tiles,
+                                                               const uint32_t* __restrict__ cnt_mat,
+                                                               const uint32_t* __restrict__ off_mat,
+                                                               uint16_t* __restrict__ runs) {
+  extern __shared__ __align__(16) unsigned char offb_smem[];
+  uint32_t* cur = reinterpret_cast<uint32_t*>(offb_smem);  // K: local cursors
+  uint32_t* loc = cur + K;                                 // K: local run starts
+  uint32_t* gst = loc + K;                                 // K: global run starts
+  uint32_t* keys = gst + K;                                // OFFB_TILE: the tile sorted by bucket
+  __shared__ uint32_t wsum[OFFB_THREADS / 32];
+  const int64_t t0 = (int64_t)blockIdx.x * OFFB_TILE;
+  const int len = (int)min((int64_t)OFFB_TILE, n_anc - t0);
+  uint32_t carry = 0;
+  for (int c0 = 0; c0 < K; c0 += OFFB_THREADS) {  // exclusive scan of the tile's bucket counts
+    const int b = c0 + threadIdx.x;
+    const uint32_t v = b < K ? cnt_mat[(int64_t)b * tiles + blockIdx.x] : 0;
+    uint32_t x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+      if ((threadIdx.x & 31) >= d) x += y;
+    }
+    if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = x;
+    __syncthreads();
+    uint32_t wb = 0, tot = 0;
+#pragma unroll
+    for (int q = 0; q < OFFB_THREADS / 32; ++q) {
+      wb += q < (int)(threadIdx.x >> 5) ? wsum[q] : 0u;
+      tot += wsum[q];
+    }
+    if (b < K) {
+      loc[b] = cur[b] = carry + wb + x - v;
+      gst[b] = off_mat[(int64_t)b * tiles + blockIdx.x];
+    }
+    carry += tot;
+    __syncthreads();
+  }
+  for (int q = threadIdx.x; q < len; q += OFFB_THREADS) {
+    const int64_t a = __ldcs(anc + t0 + q);  // last read of the ancestors
+    if (a < 0 || a >= n) continue;           // flagged by k_offb_count
+    keys[atomicAdd(&cur[(unsigned)(a >> OFFB_BITS)], 1u)] = (uint32_t)a;
+  }
+  __syncthreads();
+  const int valid = (int)carry;
+  for (int q = threadIdx.x; q < valid; q += OFFB_THREADS) {
+    const uint32_t k = keys[q], b = k >> OFFB_BITS;
+    runs[gst[b] + (uint32_t)q - loc[b]] = (uint16_t)(k & (OFFB_BINS - 1));
+  }
+}
+
+__global__ void __launch_bounds__(512) k_offb_hist(const uint16_t* __restrict__ runs, const uint32_t* __restrict__ off_mat,
+                                                   int64_t tiles, int64_t n, int64_t* __restrict__ counts) {
+  extern __shared__ __align__(16) unsigned char offb_smem[];
+  uint32_t* bins = reinterpret_cast<uint32_t*>(offb_smem);
+  const int b = blockIdx.x;
+  for (int q = threadIdx.x; q < OFFB_BINS / 4; q += 512) reinterpret_cast<uint4*>(bins)[q] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  const uint32_t r0 = off_mat[(int64_t)b * tiles], r1 = off_mat[(int64_t)(b + 1) * tiles];
+  for (uint32_t q = r0 + threadIdx.x; q < r1; q += 512) atomicAdd(&bins[runs[q]], 1u);
+  __syncthreads();
+  const int64_t c0 = (int64_t)b << OFFB_BITS;
+  const int nb = (int)min((int64_t)OFFB_BINS, n - c0);
+  for (int q = threadIdx.x; q < nb; q += 512) __stcs(counts + c0 + q, (int64_t)bins[q]);
+}
+
 // int32 histogram -> the int64 counts of the ABI (4 counts per thread, 16-byte loads)
 __global__ void k_widen_counts(const int32_t* __restrict__ c32, int64_t n, int64_t* __restrict__ c64) {
   const int64_t n4 = n >> 2;

@@ -81,5 +81,28 @@ mg.comparison_indices("megopolis", 700, 3, 1, mg.WarpConfig(7))
 count_transactions(np.arange(-5, 60, 3))
 traj = pf.generate_trajectory(3, 0.0, 1)
 pf.run_filter(pf.FilterConfig(n_particles=8192, b_fixed=None), traj, 2)
+# round 2: gamma generator, pageable host buffers through the staging slots (>= 4 MiB), the
+# texture LRU past its capacity, C1/C2 over ranges whose end is not warp-aligned
+mg.gen_gamma_weights(mg.GammaWeightParams(2.0, 1.0, 5000), 3, "single", device="cuda")
+mg.gen_gamma_weights(mg.GammaWeightParams(0.5, 2.0, 777), 4, "double", device="cuda")
+wp = rr.random(1 << 20).astype(np.float32)
+mg.megopolis(mg.WeightVector(wp, "single"), 3, seed=2, rng="philox")  # half-split, staged in and out
+mg.metropolis_c1(mg.WeightVector(wp[:1 << 19], "single"), 3, mg.PartitionConfig(256), seed=2)
+for k in range(70):
+    mg.megopolis(mg.WeightVector(torch.rand(512, device="cuda"), "single"), 2, seed=k)
+for kind, part in (("c1", 256), ("c2", 128)):
+    out = torch.empty(61 - 32, dtype=torch.int64, device="cuda")
+    _lib.check(_lib.lib().mgp_resample_range(_lib.KIND[kind], wq.data_ptr(), 0, 4096, 7, 3, 32, part, 1,
+                                             _lib.RNG["megores"], 0, 32, 61, out.data_ptr(),
+                                             torch.cuda.current_stream().cuda_stream))
+# bucketed offspring histogram (n >= 2^20), incl. a ragged n and an out-of-range ancestor
+for nn in (1 << 20, (1 << 20) + 77):
+    aa = torch.from_numpy(rr.integers(0, nn, nn)).cuda()
+    mg.ancestors_to_offspring(aa, nn)
+try:
+    aa[5] = nn
+    mg.ancestors_to_offspring(aa, nn)
+except ValueError:
+    pass
 torch.cuda.synchronize()
 print("sanitize workload done")
