@@ -445,7 +445,11 @@ __global__ void __launch_bounds__(RS_THREADS) k_megopolis_megores_f32(const __gr
     const bool acc = hi <= wj;
     if (!acc && lo <= wj) amb = t;
     if (acc) { wk = wj; bstar = t; }
-    x += M_CTR;
+    // x += M_CTR: ptxas hoists one * M_CTR and splits the add into IADD3 (ALU) + IMAD.X (FMA
+    // pipe) -- 3% faster than IADD3 + IADD3.X (scripts/mb/mb_mego2.cu "ADDW u8": 6.84 -> 6.69 ms);
+    // moving more of the hash to the heavy FMA pipe (IMAD.WIDE adds, IMAD.HI shifts, I2F for
+    // the bracket) measured 1-12% slower there.
+    x = add64_fma(x, a.one);
   }
   if (amb >= 0) bstar = megores_exact_rounds(a, oc, i, wk0, POW2);
   uint32_t k = k0;
