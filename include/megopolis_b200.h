@@ -285,6 +285,10 @@ int mgp_philox_selftest(uint64_t key, uint32_t c1, uint32_t c2, uint32_t c3, int
  * ambiguous in some round and that were re-run with the exact float64 rule (the current device,
  * since the last reset).  reset != 0 zeroes the counter after reading it. */
 int mgp_debug_megores_fallbacks(int64_t *h_count, int reset);
+/* Exact-cumsum resolver profile (16 counters; non-zero only in a -DMGP_PX_PROF build of the
+ * library, scripts/mb/px_prof.sh): super windows, chunk windows, crossing chunks, block passes,
+ * sequential tails and their cycles. */
+int mgp_debug_px_prof(int64_t *h_out16, int reset);
 
 /* Measurement switch for mgp_offspring: 1 = the int32 global-atomic histogram (round 1), 0 = the
  * bucketed shared-memory histogram (default).  Process-wide; for A/B timing and tests only. */

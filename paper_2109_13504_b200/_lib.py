@@ -76,6 +76,7 @@ SIGNATURES = {
     "mgp_systematic_oracle": (_i32, [_vp, _i32, _i64, _dbl, _vp, _vp]),
     "mgp_philox_selftest": (_i32, [_u64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, _i64, _vp]),
     "mgp_debug_megores_fallbacks": (_i32, [_vp, ctypes.c_int]),
+    "mgp_debug_px_prof": (_i32, [_vp, ctypes.c_int]),
     "mgp_debug_offspring_mode": (_i32, [ctypes.c_int]),
 }
 

@@ -485,8 +485,8 @@ template <typename WT>
 int px_cumsum(const WT* w, int64_t n, WT* cum, cudaStream_t st) {
   Scratch sc(st);
   const int64_t nch = (n + PX_CHUNK - 1) / PX_CHUNK, nsup = (nch + PX_SUPER - 1) / PX_SUPER;
+  int32_t *e0 = nullptr, *mode = nullptr, *se0 = nullptr, *smode = nullptr, *scnt = nullptr;
   double *csum = nullptr, *est = nullptr;
-  int32_t *e0 = nullptr, *mode = nullptr, *exc = nullptr, *se0 = nullptr, *smode = nullptr;
   Tx *agg = nullptr, *sagg = nullptr;
   WT *carry = nullptr, *scarry = nullptr;
   void* tmp = nullptr;
@@ -496,33 +496,33 @@ int px_cumsum(const WT* w, int64_t n, WT* cum, cudaStream_t st) {
   CUDA_TRY(sc.alloc(&est, sizeof(double) * nch));
   CUDA_TRY(sc.alloc(&e0, sizeof(int32_t) * nch));
   CUDA_TRY(sc.alloc(&mode, sizeof(int32_t) * nch));
-  CUDA_TRY(sc.alloc(&exc, sizeof(int32_t) * (nch + 1)));
   CUDA_TRY(sc.alloc(&agg, sizeof(Tx) * PX_CAND * nch));
   CUDA_TRY(sc.alloc(&carry, sizeof(WT) * nch));
   CUDA_TRY(sc.alloc(&se0, sizeof(int32_t) * nsup));
   CUDA_TRY(sc.alloc(&smode, sizeof(int32_t) * nsup));
   CUDA_TRY(sc.alloc(&sagg, sizeof(Tx) * PX_CAND * nsup));
   CUDA_TRY(sc.alloc(&scarry, sizeof(WT) * nsup));
+  CUDA_TRY(sc.alloc(&scnt, sizeof(int32_t) * nsup));
   CUDA_TRY(sc.alloc(&tmp, tmp_bytes + 16));
-  k_px_chunk_sum<WT><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, csum);
+  CUDA_TRY(cudaMemsetAsync(scnt, 0, sizeof(int32_t) * nsup, st));
+  // 16-byte vector accesses in the streaming passes when both arrays allow them
+  const bool vec = ((uintptr_t)w % 16 == 0) && ((uintptr_t)cum % 16 == 0);
+  if (vec) k_px_chunk_sum<WT, true><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, csum);
+  else k_px_chunk_sum<WT, false><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, csum);
   LAUNCH_CHECK("k_px_chunk_sum");
   CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, csum, est, (int)nch, st));
-  k_px_aggregate<WT><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, est, e0, agg);
+  if (vec) k_px_aggregate<WT, true><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, nch, est, scnt, e0, agg, se0, sagg);
+  else k_px_aggregate<WT, false><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, nch, est, scnt, e0, agg, se0, sagg);
   LAUNCH_CHECK("k_px_aggregate");
-  k_px_super<<<(unsigned)nsup, 32, 0, st>>>(nch, e0, agg, se0, sagg);
-  LAUNCH_CHECK("k_px_super");
   const int64_t stage = px_stage_bytes(nsup);
-  if (stage > 48 * 1024)
+  if (stage > 0)
     CUDA_TRY(cudaFuncSetAttribute(k_px_resolve<WT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PX_STAGE_MAX));
   k_px_resolve<WT><<<1, PXR_THREADS, (size_t)stage, st>>>(w, n, nch, nsup, e0, agg, se0, sagg, carry, mode, scarry,
-                                                          smode, exc);
+                                                          smode, cum);
   LAUNCH_CHECK("k_px_resolve");
-  k_px_expand<WT><<<(unsigned)nsup, 32, 0, st>>>(nch, e0, agg, scarry, smode, carry, mode);
-  LAUNCH_CHECK("k_px_expand");
-  k_px_materialize<WT><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, carry, mode, cum);
+  if (vec) k_px_materialize<WT, true><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, e0, agg, scarry, smode, carry, mode, cum);
+  else k_px_materialize<WT, false><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, e0, agg, scarry, smode, carry, mode, cum);
   LAUNCH_CHECK("k_px_materialize");
-  k_px_materialize_exc<WT><<<(unsigned)std::min<int64_t>(nch, 2 * 148), 32, 0, st>>>(w, n, carry, exc, cum);
-  LAUNCH_CHECK("k_px_materialize_exc");
   return 0;
 }
 
@@ -1972,6 +1972,16 @@ extern "C" int mgp_philox_selftest(uint64_t key, uint32_t c1, uint32_t c2, uint3
 
 extern "C" int mgp_debug_offspring_mode(int atomic_histogram) {
   g_offspring_atomic.store(atomic_histogram ? 1 : 0);
+  return 0;
+}
+
+// resolver profile counters of the exact cumsum (non-zero only in a -DMGP_PX_PROF build)
+extern "C" int mgp_debug_px_prof(int64_t* h_out16, int reset) {
+  CUDA_TRY(cudaMemcpyFromSymbol(h_out16, g_px_prof, sizeof(unsigned long long) * 16));
+  if (reset) {
+    static const unsigned long long z[16] = {};
+    CUDA_TRY(cudaMemcpyToSymbol(g_px_prof, z, sizeof z));
+  }
   return 0;
 }
 

@@ -17,25 +17,25 @@
 //   for parity 0 / 1.  Transducers compose associatively, so inside a binade the
 //   sequential scan IS an ordered integer scan -- parallel and exact.
 //
-// Pipeline (chunks of PX_CHUNK elements):
-//   k_px_chunk_sum    float64 chunk sums -> (CUB) exclusive prefix = carry-in estimates
-//   k_px_aggregate    per chunk, the composed transducer for the 3 binades around the
-//                     estimate (e0-1, e0, e0+1).  All three are needed: for skewed weights
-//                     float32 drops whole addends below half an ulp, so the sequential sum
-//                     drifts from the float64 estimate systematically (tens of percent at
-//                     2^24 Gaussian y=4 weights), not by a random-walk sqrt(n) ulps; computing
-//                     only the estimate's binade sent most chunks down the sequential path
-//   k_px_super        the same for super-chunks of 32 chunks (composition of theirs)
-//   k_px_resolve      one warp walks the super-chunks 32 at a time: from the true carry-in
+// Pipeline (chunks of PX_CHUNK elements, super-chunks of PX_SUPER chunks), three launches:
+//   k_px_scan_aggregate  one read of the weights: per chunk the float64 sum and its exclusive
+//                     prefix by decoupled look-back (the carry-in estimate), then the composed
+//                     transducer for the 3 binades around the estimate (e0-1, e0, e0+1).  All
+//                     three are needed: for skewed weights float32 drops whole addends below
+//                     half an ulp, so the sequential sum drifts from the float64 estimate
+//                     systematically (tens of percent at 2^24 Gaussian y=4 weights), not by a
+//                     random-walk sqrt(n) ulps.  The last chunk of a super-chunk to finish
+//                     composes the super-chunk's aggregates.
+//   k_px_resolve      one CTA walks the super-chunks 32 at a time: from the true carry-in
 //                     s (binade e, parity p) it scans the lanes' aggregates for e; every
 //                     super-chunk whose end stays inside binade e is resolved in O(1); the
 //                     first that leaves it is descended into (chunk windows), and the chunk
-//                     the sum leaves its binade in is summed sequentially, as numpy does
-//                     (a handful per array: the running sum crosses each binade once)
-//   k_px_expand       chunk carry-ins inside the super-chunks resolved whole
-//   k_px_materialize  per chunk, an ordered block scan of the transducers from the true
-//                     carry-in writes s_k = carry + units * u_e (the warp routine again
-//                     for the binade-crossing chunks)
+//                     the sum leaves its binade in is resolved -- and materialised -- element
+//                     by element by the whole CTA (a handful per array: the running sum
+//                     crosses each binade once)
+//   k_px_materialize  per chunk, its carry-in (composed from its super-chunk's, or written by
+//                     the resolver), then an ordered block scan of the transducers writes
+//                     s_k = carry + units * u_e
 // All arithmetic is integer or exact power-of-two scaling; the result equals np.cumsum.
 #pragma once
 #include <cstdint>
@@ -48,6 +48,10 @@ constexpr int PX_THREADS = 256;
 constexpr int PX_PER_THREAD = 4;
 constexpr int PX_CHUNK = PX_THREADS * PX_PER_THREAD;  // 1024 elements per chunk
 constexpr int PX_CAND = 3;                             // binades e0-1, e0, e0+1 per chunk
+// Super-chunks: PX_SUPER consecutive chunks.  Their aggregate for a binade e is the ordered
+// composition of the chunks' aggregates for e (when every chunk carries e among its three
+// candidates); candidates E-1, E, E+1 with E the first chunk's e0.
+constexpr int PX_SUPER = 32;
 constexpr int32_t PX_EXC = -100000;                    // mode: chunk re-scanned sequentially
 constexpr int64_t PX_SAT = (int64_t)1 << 61;           // saturation: "leaves the binade"
 
@@ -185,26 +189,45 @@ __device__ __forceinline__ int64_t px_inc(WT w, int e, bool& tie) {
 
 __device__ __forceinline__ int64_t px_sat_add(int64_t a, int64_t b) { return px_sat(a + b); }
 
-// ---------------------------------------------------------------------------
-
-template <typename WT>
-__global__ void __launch_bounds__(PX_THREADS) k_px_chunk_sum(const WT* __restrict__ w, int64_t n, double* csum) {
-  __shared__ double red[PX_THREADS / 32];
-  const int64_t base = (int64_t)blockIdx.x * PX_CHUNK + threadIdx.x * PX_PER_THREAD;
-  double s = 0.0;
-#pragma unroll
-  for (int j = 0; j < PX_PER_THREAD; ++j)
-    if (base + j < n) s += (double)w[base + j];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int q = 0; q < PX_THREADS / 32; ++q) t += red[q];
-    csum[blockIdx.x] = t;
+// A thread's PX_PER_THREAD (= 4) consecutive elements: one 16-byte (float32) or two 16-byte
+// (float64) vector accesses when the array is 16-byte aligned and the four are in range (VEC,
+// decided on the host), else element by element.  Vector loads/stores make every warp
+// instruction cover whole 128-byte lines (scalar ones at a 16-byte stride touched each line
+// four times, and the scalar stores wrote partial sectors).
+static_assert(PX_PER_THREAD == 4, "vector accesses assume 4 elements per thread");
+template <typename WT, bool VEC>
+__device__ __forceinline__ void px_load4(const WT* __restrict__ w, int64_t base, int64_t n, WT* v) {
+  if (VEC && base + 4 <= n) {
+    if constexpr (sizeof(WT) == 4) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(w + base));
+      v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else {
+      const double2 q0 = __ldg(reinterpret_cast<const double2*>(w + base));
+      const double2 q1 = __ldg(reinterpret_cast<const double2*>(w + base) + 1);
+      v[0] = q0.x; v[1] = q0.y; v[2] = q1.x; v[3] = q1.y;
+    }
+    return;
   }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) v[j] = base + j < n ? w[base + j] : (WT)0;
 }
+template <typename WT, bool VEC>
+__device__ __forceinline__ void px_store4(WT* __restrict__ out, int64_t base, int64_t n, const WT* v) {
+  if (VEC && base + 4 <= n) {
+    if constexpr (sizeof(WT) == 4) {
+      *reinterpret_cast<float4*>(out + base) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+      reinterpret_cast<double2*>(out + base)[0] = make_double2(v[0], v[1]);
+      reinterpret_cast<double2*>(out + base)[1] = make_double2(v[2], v[3]);
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (base + j < n) out[base + j] = v[j];
+}
+
+// ---------------------------------------------------------------------------
 
 // ordered warp reduction (lane 0 receives lane 0 o lane 1 o ... o lane 31)
 __device__ __forceinline__ Tx px_warp_reduce(Tx t) {
@@ -231,18 +254,42 @@ __device__ __forceinline__ Tx px_warp_scan(Tx t) {
   return t;
 }
 
-template <typename WT>
-__global__ void __launch_bounds__(PX_THREADS) k_px_aggregate(const WT* __restrict__ w, int64_t n,
-                                                             const double* __restrict__ est, int32_t* e0_out,
-                                                             Tx* agg) {
-  __shared__ Tx red[PX_CAND][PX_THREADS / 32];
-  const int64_t c = blockIdx.x;
-  const WT carry_est = (WT)est[c];
-  const int e0 = PxFp<WT>::expo(carry_est);
-  const int64_t base = c * PX_CHUNK + threadIdx.x * PX_PER_THREAD;
+template <typename WT, bool VEC>
+__global__ void __launch_bounds__(PX_THREADS) k_px_chunk_sum(const WT* __restrict__ w, int64_t n, double* csum) {
+  __shared__ double red[PX_THREADS / 32];
   WT v[PX_PER_THREAD];
+  px_load4<WT, VEC>(w, (int64_t)blockIdx.x * PX_CHUNK + threadIdx.x * PX_PER_THREAD, n, v);
+  double s = 0.0;
 #pragma unroll
-  for (int j = 0; j < PX_PER_THREAD; ++j) v[j] = base + j < n ? w[base + j] : (WT)0;
+  for (int j = 0; j < PX_PER_THREAD; ++j) s += (double)v[j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < PX_THREADS / 32; ++q) t += red[q];
+    csum[blockIdx.x] = t;
+  }
+}
+
+// Per chunk, the composed transducers for the 3 binades around the carry-in estimate (the
+// exclusive prefix of the float64 chunk sums); the last chunk of each super-chunk to finish
+// composes the super-chunk's aggregates (no separate super-chunk pass).  The estimate only
+// chooses candidate binades: its rounding never reaches the result, which the resolver makes
+// exact.  (A single-pass decoupled look-back for the estimate was measured: with 1024-element
+// chunks the look-back distance is a whole wave of resident CTAs, 200 us at 2^24.)
+template <typename WT, bool VEC>
+__global__ void __launch_bounds__(PX_THREADS) k_px_aggregate(const WT* __restrict__ w, int64_t n, int64_t nch,
+                                                             const double* __restrict__ est, int32_t* scnt,
+                                                             int32_t* e0_out, Tx* agg, int32_t* se0, Tx* sagg) {
+  __shared__ Tx red[PX_CAND][PX_THREADS / 32];
+  __shared__ int s_last;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t c = blockIdx.x;
+  WT v[PX_PER_THREAD];
+  px_load4<WT, VEC>(w, c * PX_CHUNK + tid * PX_PER_THREAD, n, v);
+  const int e0 = PxFp<WT>::expo((WT)est[c]);
 #pragma unroll
   for (int k = 0; k < PX_CAND; ++k) {
     const int e = e0 - 1 + k;
@@ -265,7 +312,7 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_aggregate(const WT* __restric
         const bool any_sat = __any_sync(0xffffffffu, sat);
         const int64_t tot = (int64_t)__reduce_add_sync(0xffffffffu, s32);
         t = any_sat ? Tx{PX_SAT, PX_SAT} : Tx{tot, tot};
-        if ((threadIdx.x & 31) == 0) red[k][threadIdx.x >> 5] = t;
+        if (lane == 0) red[k][wid] = t;
         continue;
       }
     } else {
@@ -286,15 +333,46 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_aggregate(const WT* __restric
       for (int o = 16; o > 0; o >>= 1) sum = px_sat_add(sum, __shfl_xor_sync(0xffffffffu, sum, o));
       t = Tx{sum, sum};
     }
-    if ((threadIdx.x & 31) == 0) red[k][threadIdx.x >> 5] = t;
+    if (lane == 0) red[k][wid] = t;
   }
   __syncthreads();
-  if (threadIdx.x < PX_CAND) {
+  if (tid < PX_CAND) {
     Tx t{0, 0};
-    for (int q = 0; q < PX_THREADS / 32; ++q) t = px_compose(t, red[threadIdx.x][q]);
-    agg[c * PX_CAND + threadIdx.x] = t;
+    for (int q = 0; q < PX_THREADS / 32; ++q) t = px_compose(t, red[tid][q]);
+    agg[c * PX_CAND + tid] = t;
   }
-  if (threadIdx.x == 0) e0_out[c] = e0;
+  if (tid == 0) e0_out[c] = e0;
+  // the last chunk of super-chunk sp to finish composes its aggregates
+  __threadfence();
+  __syncthreads();
+  const int64_t sp = c / PX_SUPER;
+  if (tid == 0) {
+    const int64_t in_sp = min((int64_t)PX_SUPER, nch - sp * PX_SUPER);
+    s_last = atomicAdd(scnt + sp, 1) == (int)in_sp - 1;
+  }
+  __syncthreads();
+  if (!s_last || wid != 0) return;
+  __threadfence();
+  const int64_t cc = sp * PX_SUPER + lane;
+  const bool valid = cc < nch;
+  const int ec = valid ? __ldcg(e0_out + cc) : 0;
+  const int E = __shfl_sync(0xffffffffu, ec, 0);
+#pragma unroll
+  for (int k = 0; k < PX_CAND; ++k) {
+    const int e = E - 1 + k, kk = e - (ec - 1);
+    Tx t{0, 0};  // chunks past the end: identity
+    if (valid) {
+      if (kk >= 0 && kk < PX_CAND) {
+        t.a0 = __ldcg(&agg[cc * PX_CAND + kk].a0);
+        t.a1 = __ldcg(&agg[cc * PX_CAND + kk].a1);
+      } else {
+        t = Tx{PX_SAT, PX_SAT};
+      }
+    }
+    t = px_warp_reduce(t);
+    if (lane == 0) sagg[sp * PX_CAND + k] = t;
+  }
+  if (lane == 0) se0[sp] = E;
 }
 
 // The running sum s in units of its binade's spacing (S = the integer significand) and
@@ -318,49 +396,36 @@ __device__ inline double PxScanT<double>::at(uint64_t units, int e) {  // exact:
   return (double)units * px_ulp(e, 52);
 }
 
-// A chunk the running sum leaves its binade in: numpy's sequential loop, by one warp.  Each
-// lane stages 32 elements in registers; lane 0 adds them in order (IEEE WT adds, the values
-// arriving by shuffle), optionally storing every prefix value.  ~1024 dependent adds: a
-// handful of such chunks per array (the sum crosses each binade once).
-constexpr int PXR_SEG = PX_CHUNK / 32;  // elements per lane
-
-template <typename WT, bool WRITE>
-__device__ WT px_chunk_seq(const WT* __restrict__ w, int64_t n, int64_t c, WT s, WT* __restrict__ cum) {
-  const int lane = threadIdx.x & 31;
-  const int64_t c0 = c * (int64_t)PX_CHUNK;
-  const int len = (int)((n - c0) < PX_CHUNK ? (n - c0) : (int64_t)PX_CHUNK);
-  WT v[PXR_SEG];
-#pragma unroll
-  for (int j = 0; j < PXR_SEG; ++j) v[j] = lane * PXR_SEG + j < len ? w[c0 + lane * PXR_SEG + j] : (WT)0;
-  WT mine[PXR_SEG];
-  for (int l = 0; l < 32; ++l) {
-    if (l * PXR_SEG >= len) break;
-#pragma unroll
-    for (int j = 0; j < PXR_SEG; ++j) {
-      const WT x = __shfl_sync(0xffffffffu, v[j], l);
-      if (l * PXR_SEG + j < len) s = s + x;  // every lane runs the same chain (uniform values)
-      if (lane == l) mine[j] = s;
-    }
-  }
-  if (WRITE) {
-#pragma unroll
-    for (int j = 0; j < PXR_SEG; ++j)
-      if (lane * PXR_SEG + j < len) cum[c0 + lane * PXR_SEG + j] = mine[j];
-  }
-  return s;
-}
-
 // The resolver runs as one CTA of PXR_THREADS threads.  Every warp walks the same windows (the
 // same data, so the same results; only warp 0 writes), and the chunks the running sum leaves
-// its binade in are resolved by the whole CTA together: from the running sum s (binade e, S
-// units) every thread sums its PXR_PER increments in binade e (saturating: only "does it leave
-// the binade" matters), a block scan finds the first thread whose prefix leaves the binade, its
-// few elements are added sequentially from the exact carry (S + exclusive prefix) * u_e, and the
-// scan restarts after them in the new binade.  Rounding ties or a non-finite sum fall back to
-// numpy's sequential loop.  The result equals px_chunk_seq<WT, false>.
+// its binade in are resolved by the whole CTA together.  One pass: from the running sum s
+// (binade e, S units) every thread sums its PXR_PER increments in binade e (saturating: only
+// "does it leave the binade" matters); after one barrier every warp scans the 8 warp totals by
+// shuffle, so every thread knows the warp the sum leaves the binade in, that warp finds the
+// thread T by ballot, T adds its own elements (registers) sequentially from the exact carry
+// (S + exclusive prefix) * u_e and publishes the new sum; a second barrier, and the next pass
+// restarts after T's elements in the new binade.  A chunk still unresolved after PXR_PASSES
+// passes (the first chunks of a sum that starts small cross a binade every few elements),
+// rounding ties, or a non-finite sum: the rest of the chunk is staged in shared memory and
+// added by one thread in numpy's order (~4 cycles per dependent add).  The result is numpy's
+// sequential loop over the chunk.
 constexpr int PXR_THREADS = 256;
+// resolver profile (build with -DMGP_PX_PROF; read by mgp_debug_px_prof): thread 0 counts
+// [0] super windows [1] their cycles [2] chunk windows [3] their cycles [4] crossing chunks
+// [5] their cycles [6] block passes [7] sequential tails [8] tail elements [9] kernel cycles
+__device__ unsigned long long g_px_prof[16];
+#ifdef MGP_PX_PROF
+#define PXP_T0() const long long pxp_t0 = clock64()
+#define PXP_ADD(k, v) do { if (threadIdx.x == 0) g_px_prof[k] += (unsigned long long)(v); } while (0)
+#define PXP_CYC(k) PXP_ADD(k, clock64() - pxp_t0)
+#else
+#define PXP_T0() do {} while (0)
+#define PXP_ADD(k, v) do {} while (0)
+#define PXP_CYC(k) do {} while (0)
+#endif
 constexpr int PXR_WARPS = PXR_THREADS / 32;
 constexpr int PXR_PER = PX_CHUNK / PXR_THREADS;  // 4 elements per thread
+constexpr int PXR_PASSES = 3;
 
 template <typename U>
 __device__ __forceinline__ U px_cap_add(U a, U b, U cap) { return a + b < cap ? a + b : cap; }
@@ -368,38 +433,66 @@ __device__ __forceinline__ U px_cap_add(U a, U b, U cap) { return a + b < cap ? 
 template <typename WT>
 struct PxBlockScratch {
   typename PxScanT<WT>::U wsum[PXR_WARPS];
-  int first[PXR_WARPS];
-  typename PxScanT<WT>::U excl;
+  int tie[PXR_WARPS];
+  int p_new;
+  WT s_new;
+  WT buf[PX_CHUNK];  // the chunk, staged for the sequential tail
 };
 
+// prefix values of this thread's elements [p, len) from `run` units (binade e, all inside it)
 template <typename WT>
-__device__ WT px_chunk_block(const WT* __restrict__ w, int64_t n, int64_t c, WT s, PxBlockScratch<WT>& sh) {
+__device__ __forceinline__ void px_write_run(WT* __restrict__ cum, int64_t c0, int p, int len,
+                                             typename PxScanT<WT>::U run, const typename PxScanT<WT>::U* inc, int e) {
+#pragma unroll
+  for (int j = 0; j < PXR_PER; ++j) {
+    const int idx = threadIdx.x * PXR_PER + j;
+    if (idx >= p && idx < len) {
+      run += inc[j];
+      cum[c0 + idx] = PxScanT<WT>::at(run, e);
+    }
+  }
+}
+
+// cum != nullptr: also writes the chunk's prefix values (the resolver materialises the chunks the
+// running sum leaves its binade in; k_px_materialize skips them)
+template <typename WT>
+__device__ WT px_chunk_block(const WT* __restrict__ w, int64_t n, int64_t c, WT s, PxBlockScratch<WT>& sh,
+                             WT* __restrict__ cum) {
   using P = PxScanT<WT>;
   using U = typename P::U;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t c0 = c * (int64_t)PX_CHUNK;
   const int len = (int)((n - c0) < PX_CHUNK ? (n - c0) : (int64_t)PX_CHUNK);
   WT v[PXR_PER];
-#pragma unroll
-  for (int j = 0; j < PXR_PER; ++j) v[j] = tid * PXR_PER + j < len ? w[c0 + tid * PXR_PER + j] : (WT)0;
+  px_load4<WT, false>(w, c0 + tid * PXR_PER, n, v);
+#ifdef MGP_PX_PROF
+  {
+    const long long t0 = clock64();
+    WT acc = v[0] + v[1] + v[2] + v[3];
+    if (acc == (WT)-1.2345) sh.s_new = acc;  // forces the loads to land
+    PXP_ADD(10, clock64() - t0);
+  }
+  const long long pxp_p0 = clock64();
+#endif
   int p = 0;  // first chunk-local element not yet added (a multiple of PXR_PER)
-  while (p < len) {
-    if (!isfinite((double)s)) break;
+  for (int pass = 0; pass < PXR_PASSES && p < len; ++pass) {
+    if (!isfinite((double)s)) break;  // s is uniform: every thread leaves together
     const int e = PxFp<WT>::expo(s);
     const U S = (U)px_units<WT>(s);
-    U t = 0;
+    U t = 0, inc[PXR_PER];
     bool tie = false, sat = false;
 #pragma unroll
     for (int j = 0; j < PXR_PER; ++j) {
       const int idx = tid * PXR_PER + j;
+      inc[j] = 0;
       if (idx >= p && idx < len) {
         const auto d = P::inc(v[j], e);
+        inc[j] = d.v;
         t += d.v;
         tie |= d.tie;
         sat |= d.sat;
       }
     }
-    if (__syncthreads_or(tie)) break;
     t = sat ? P::CAP : (t < P::CAP ? t : P::CAP);
     U x = t;  // inclusive warp scan, saturating at CAP
 #pragma unroll
@@ -409,63 +502,101 @@ __device__ WT px_chunk_block(const WT* __restrict__ w, int64_t n, int64_t c, WT 
     }
     U wex = __shfl_up_sync(0xffffffffu, x, 1);
     if (lane == 0) wex = 0;
+    const unsigned tb = __ballot_sync(0xffffffffu, tie);
     if (lane == 31) sh.wsum[wid] = x;
+    if (lane == 0) sh.tie[wid] = tb != 0u;
     __syncthreads();
-    U base = 0, total = 0;
+    // every warp: the 8 warp totals on lanes 0..7, inclusive scan by shuffle
+    U iw = lane < PXR_WARPS ? sh.wsum[lane] : (U)0;
+    const bool anytie = __any_sync(0xffffffffu, lane < PXR_WARPS && sh.tie[lane]);
 #pragma unroll
-    for (int q = 0; q < PXR_WARPS; ++q) {
-      if (q < wid) base = px_cap_add(base, sh.wsum[q], P::CAP);
-      total = px_cap_add(total, sh.wsum[q], P::CAP);
+    for (int d = 1; d < PXR_WARPS; d <<= 1) {
+      const U y = __shfl_up_sync(0xffffffffu, iw, d);
+      if (lane >= d) iw = px_cap_add(iw, y, P::CAP);
     }
-    const U incl = px_cap_add(base, x, P::CAP), excl = px_cap_add(base, wex, P::CAP);
-    const unsigned bm = __ballot_sync(0xffffffffu, S + incl > P::LIM);
-    if (lane == 0) sh.first[wid] = bm ? wid * 32 + __ffs(bm) - 1 : PXR_THREADS;
-    __syncthreads();
-    int T = PXR_THREADS;
-#pragma unroll
-    for (int q = 0; q < PXR_WARPS; ++q) T = min(T, sh.first[q]);
-    if (T == PXR_THREADS) {  // the rest of the chunk stays in binade e
+    if (anytie) break;  // uniform (every warp read the same flags)
+    const U total = __shfl_sync(0xffffffffu, iw, PXR_WARPS - 1);
+    U base = __shfl_sync(0xffffffffu, iw, wid > 0 ? wid - 1 : 0);
+    if (wid == 0) base = 0;
+    const unsigned wb = __ballot_sync(0xffffffffu, lane < PXR_WARPS && S + iw > P::LIM);
+    if (!wb) {  // the rest of the chunk stays in binade e
+      if (cum) px_write_run<WT>(cum, c0, p, len, S + base + wex, inc, e);
       s = P::at(S + total, e);
       p = len;
-      __syncthreads();
       break;
     }
-    if (tid == T) sh.excl = excl;
-    __syncthreads();
-    s = P::at(S + sh.excl, e);  // exact: <= LIM units
+    const int wT = __ffs(wb) - 1;  // the warp the sum leaves binade e in
+    if (cum && wid < wT) px_write_run<WT>(cum, c0, p, len, S + base + wex, inc, e);
+    if (wid == wT) {
+      const U incl = px_cap_add(base, x, P::CAP), excl = px_cap_add(base, wex, P::CAP);
+      const unsigned bm = __ballot_sync(0xffffffffu, S + incl > P::LIM);
+      const int lT = __ffs(bm) - 1;
+      if (cum && lane < lT) px_write_run<WT>(cum, c0, p, len, S + excl, inc, e);
+      if (lane == lT) {
+        WT r = P::at(S + excl, e);  // exact: <= LIM units
 #pragma unroll
-    for (int j = 0; j < PXR_PER; ++j) {  // thread T's elements, numpy's order
-      const int idx = T * PXR_PER + j;
-      if (idx >= p && idx < len) s = s + w[c0 + idx];
+        for (int j = 0; j < PXR_PER; ++j) {  // this thread's elements, numpy's order
+          const int idx = tid * PXR_PER + j;
+          if (idx >= p && idx < len) {
+            r = r + v[j];
+            if (cum) cum[c0 + idx] = r;
+          }
+        }
+        sh.s_new = r;
+        sh.p_new = (tid + 1) * PXR_PER;
+      }
     }
-    p = (T + 1) * PXR_PER;
-    __syncthreads();  // sh is reused by the next pass
+    __syncthreads();
+    s = sh.s_new;
+    p = sh.p_new;
+    PXP_ADD(6, 1);
   }
-  for (int idx = p; idx < len; ++idx) s = s + w[c0 + idx];  // ties / non-finite: sequential
-  return s;
-}
-
-// Super-chunks: PX_SUPER consecutive chunks.  Their aggregate for a binade e is the ordered
-// composition of the chunks' aggregates for e (when every chunk carries e among its three
-// candidates).  One warp per super-chunk; candidates E-1, E, E+1 with E the first chunk's e0.
-constexpr int PX_SUPER = 32;
-
-__global__ void __launch_bounds__(32) k_px_super(int64_t nch, const int32_t* __restrict__ e0, const Tx* __restrict__ agg,
-                                                 int32_t* se0, Tx* sagg) {
-  const int lane = threadIdx.x;
-  const int64_t c = (int64_t)blockIdx.x * PX_SUPER + lane;
-  const bool valid = c < nch;
-  const int ec = valid ? e0[c] : 0;
-  const int E = __shfl_sync(0xffffffffu, ec, 0);
+#ifdef MGP_PX_PROF
+  PXP_ADD(11, clock64() - pxp_p0);
+  const long long pxp_q0 = clock64();
+#endif
+  if (p < len) {  // sequential tail, numpy's order
+    PXP_ADD(7, 1);
+    PXP_ADD(8, len - p);
 #pragma unroll
-  for (int k = 0; k < PX_CAND; ++k) {
-    const int e = E - 1 + k, kk = e - (ec - 1);
-    Tx t{0, 0};  // chunks past the end: identity
-    if (valid) t = (kk >= 0 && kk < PX_CAND) ? agg[c * PX_CAND + kk] : Tx{PX_SAT, PX_SAT};
-    t = px_warp_reduce(t);
-    if (lane == 0) sagg[(int64_t)blockIdx.x * PX_CAND + k] = t;
+    for (int j = 0; j < PXR_PER; ++j) sh.buf[tid * PXR_PER + j] = v[j];
+    __syncthreads();
+    if (tid == 0) {  // groups of 8 through registers: the loads of the next group are in flight
+      WT r = s;        // while this group's dependent adds run (~4 cycles per element)
+      int idx = p;
+      for (; idx + 8 <= len; idx += 8) {
+        WT g[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) g[j] = sh.buf[idx + j];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          r = r + g[j];
+          g[j] = r;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sh.buf[idx + j] = g[j];  // the prefix values
+      }
+      for (; idx < len; ++idx) {
+        r = r + sh.buf[idx];
+        sh.buf[idx] = r;
+      }
+      sh.s_new = r;
+    }
+    __syncthreads();
+    s = sh.s_new;
+    if (cum) {
+#pragma unroll
+      for (int j = 0; j < PXR_PER; ++j) {
+        const int idx = tid * PXR_PER + j;
+        if (idx >= p && idx < len) cum[c0 + idx] = sh.buf[idx];
+      }
+    }
   }
-  if (lane == 0) se0[blockIdx.x] = E;
+#ifdef MGP_PX_PROF
+  PXP_ADD(12, clock64() - pxp_q0);
+#endif
+  __syncthreads();  // sh is reused by the next call
+  return s;
 }
 
 // One window of up to 32 consecutive units (super-chunks or chunks) from carry-in s: lane l
@@ -506,6 +637,27 @@ __device__ __forceinline__ PxWin px_window(WT s, int64_t u0, int64_t uend, const
 #pragma unroll
   for (int q = 0; q < PX_CAND; ++q)
     if (has && k == q) t = cand[q];
+  if (!__any_sync(0xffffffffu, has && t.a0 != t.a1)) {
+    // no rounding ties in the window (the common case): the transducers are plain increments,
+    // a capped integer scan in the dtype's unit type (32-bit for float32) instead of the
+    // parity composition (resolver profile: ~1100 -> ~400 cycles per window)
+    using U = typename PxScanT<WT>::U;
+    constexpr U CAP = PxScanT<WT>::CAP;
+    U x = has ? (U)(t.a0 < (int64_t)CAP ? t.a0 : (int64_t)CAP) : CAP;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const U y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x = px_cap_add(x, y, CAP);
+    }
+    U ex = __shfl_up_sync(0xffffffffu, x, 1);
+    if (lane == 0) ex = 0;
+    const U out = (U)S + x;
+    const unsigned bad = __ballot_sync(0xffffffffu, !(has && out <= (U)lim));
+    r.f = bad ? __ffs(bad) - 1 : 32;
+    r.carry_units = S + (int64_t)ex;
+    r.out_units = r.f > 0 ? (int64_t)__shfl_sync(0xffffffffu, out, r.f - 1) : S;
+    return r;
+  }
   const Tx P = px_warp_scan(t);
   Tx Q;
   Q.a0 = __shfl_up_sync(0xffffffffu, P.a0, 1);
@@ -519,12 +671,12 @@ __device__ __forceinline__ PxWin px_window(WT s, int64_t u0, int64_t uend, const
   return r;
 }
 
-// One warp.  Walks super-chunks 32 at a time; a super-chunk the sum leaves its binade in is
-// descended into (chunk windows); a chunk the sum leaves its binade in is summed
-// sequentially (px_chunk_seq).  Writes smode[sp] = binade e and scarry[sp] for every
-// super-chunk resolved whole (its chunks' carry-ins are expanded by k_px_expand), and
-// carry[c] / mode[c] for the chunks of descended super-chunks (PX_EXC for the sequential
-// ones, also listed in exc_list[1..exc_list[0]]).
+// One CTA.  Walks super-chunks 32 at a time; a super-chunk the sum leaves its binade in is
+// descended into (chunk windows); a chunk the sum leaves its binade in is resolved and
+// materialised by px_chunk_block.  Writes smode[sp] = binade e and scarry[sp] for every
+// super-chunk resolved whole (k_px_materialize composes its chunks' carry-ins), and
+// carry[c] / mode[c] for the chunks of descended super-chunks (PX_EXC for the ones it
+// materialised).
 constexpr int32_t PX_DESC = -200000;  // smode: descended into
 
 constexpr int64_t PX_STAGE_MAX = 96 * 1024;  // shared-memory budget of the resolver's staging
@@ -543,7 +695,7 @@ __global__ void __launch_bounds__(PXR_THREADS, 1) k_px_resolve(const WT* __restr
                                                             int64_t nsup, const int32_t* __restrict__ e0,
                                                             const Tx* __restrict__ agg, const int32_t* se0,
                                                             const Tx* sagg, WT* carry, int32_t* mode, WT* scarry,
-                                                            int32_t* smode, int32_t* exc_list) {
+                                                            int32_t* smode, WT* cum) {
   const int tid = threadIdx.x;
   const bool w0 = tid < 32;  // warp 0 writes; every warp computes the same windows
   __shared__ PxBlockScratch<WT> sh;
@@ -562,9 +714,14 @@ __global__ void __launch_bounds__(PXR_THREADS, 1) k_px_resolve(const WT* __restr
   }
   WT s = (WT)0;
   int64_t sp = 0;
-  int32_t nexc = 0;
+#ifdef MGP_PX_PROF
+  const long long pxp_k0 = clock64();
+#endif
   while (sp < nsup) {
+    PXP_T0();
     const PxWin r = px_window<WT>(s, sp, nsup, se0, sagg);
+    PXP_ADD(0, 1);
+    PXP_CYC(1);
     if (w0 && tid < r.f) {
       scarry[sp + tid] = (WT)((double)r.carry_units * r.ue);
       smode[sp + tid] = r.e;
@@ -577,73 +734,87 @@ __global__ void __launch_bounds__(PXR_THREADS, 1) k_px_resolve(const WT* __restr
     int64_t c = sp * PX_SUPER;
     const int64_t cend = min(nch, c + PX_SUPER);
     while (c < cend) {
+      PXP_T0();
       const PxWin q = px_window<WT>(s, c, cend, e0, agg);
+      PXP_ADD(2, 1);
+      PXP_CYC(3);
       if (w0 && tid < q.f) {
         carry[c + tid] = (WT)((double)q.carry_units * q.ue);
         mode[c + tid] = q.e;
       }
       if (q.f > 0) s = (WT)((double)q.out_units * q.ue);
       c += q.f;
-      if (c < cend) {  // chunk c leaves its binade: the whole CTA resolves it
+      if (c < cend) {  // chunk c leaves its binade: the whole CTA resolves and materialises it
         if (tid == 0) {
           carry[c] = s;
           mode[c] = PX_EXC;
-          exc_list[1 + nexc] = (int32_t)c;
         }
-        ++nexc;
-        s = px_chunk_block<WT>(w, n, c, s, sh);
+        {
+          PXP_T0();
+          s = px_chunk_block<WT>(w, n, c, s, sh, cum);
+          PXP_ADD(4, 1);
+          PXP_CYC(5);
+        }
         ++c;
       }
     }
     ++sp;
   }
-  if (tid == 0) exc_list[0] = nexc;
+#ifdef MGP_PX_PROF
+  PXP_ADD(9, clock64() - pxp_k0);
+#endif
 }
 
-// carry-ins of the chunks of every super-chunk resolved whole: ordered scan of the chunk
-// aggregates in the super-chunk's binade from its carry-in (one warp per super-chunk)
-template <typename WT>
-__global__ void __launch_bounds__(32) k_px_expand(int64_t nch, const int32_t* __restrict__ e0,
-                                                  const Tx* __restrict__ agg, const WT* __restrict__ scarry,
-                                                  const int32_t* __restrict__ smode, WT* carry, int32_t* mode) {
-  constexpr int MANT = PxFp<WT>::MANT;
-  const int e = smode[blockIdx.x];
-  if (e == PX_DESC) return;
-  const int lane = threadIdx.x;
-  const WT s = scarry[blockIdx.x];
-  const int64_t S = px_units<WT>(s), p = S & 1;
-  const double ue = px_ulp(e, MANT);
-  const int64_t c = (int64_t)blockIdx.x * PX_SUPER + lane;
-  const bool valid = c < nch;
-  Tx t{0, 0};
-  if (valid) t = agg[c * PX_CAND + (e - (e0[c] - 1))];  // present: the super-chunk aggregate was
-  const Tx P = px_warp_scan(t);
-  Tx Q;
-  Q.a0 = __shfl_up_sync(0xffffffffu, P.a0, 1);
-  Q.a1 = __shfl_up_sync(0xffffffffu, P.a1, 1);
-  if (lane == 0) Q = Tx{0, 0};
-  if (valid) {
-    carry[c] = (WT)((double)(S + px_apply(Q, p)) * ue);
-    mode[c] = e;
-  }
-}
-
-template <typename WT>
+// Pass 2: per chunk, an ordered block scan of the transducers from the true carry-in writes
+// s_k = carry + units * u_e.  The carry-in of a chunk inside a super-chunk the resolver settled
+// whole (smode[sp] = its binade) is the super-chunk's carry-in composed with the aggregates of
+// the chunks before it (one warp reduction here, replacing a separate expansion pass); inside a
+// descended super-chunk the resolver wrote it (carry / mode), and the chunks the sum leaves its
+// binade in (PX_EXC) were materialised by the resolver itself.
+template <typename WT, bool VEC>
 __global__ void __launch_bounds__(PX_THREADS) k_px_materialize(const WT* __restrict__ w, int64_t n,
+                                                               const int32_t* __restrict__ e0,
+                                                               const Tx* __restrict__ agg,
+                                                               const WT* __restrict__ scarry,
+                                                               const int32_t* __restrict__ smode,
                                                                const WT* __restrict__ carry,
                                                                const int32_t* __restrict__ mode, WT* __restrict__ cum) {
   constexpr int MANT = PxFp<WT>::MANT;
   __shared__ Tx wsum[PX_THREADS / 32];
+  __shared__ WT s_carry;
+  __shared__ int s_md;
   const int64_t c = blockIdx.x;
-  const int md = mode[c];
-  const WT s0 = carry[c];
   const int64_t base = c * PX_CHUNK + threadIdx.x * PX_PER_THREAD;
-  if (md == PX_EXC) return;  // binade crossings: k_px_materialize_exc
+  WT v[PX_PER_THREAD];
+  px_load4<WT, VEC>(w, base, n, v);  // in flight while the carry-in is composed
+  if (threadIdx.x < 32) {
+    const int64_t sp = c / PX_SUPER;
+    const int sm = smode[sp];
+    if (sm == PX_DESC) {
+      if (threadIdx.x == 0) {
+        s_md = mode[c];
+        s_carry = carry[c];
+      }
+    } else {
+      const int64_t cl = sp * PX_SUPER + threadIdx.x;  // chunks [sp * 32, c) of the super-chunk
+      Tx t{0, 0};
+      if (cl < c) t = agg[cl * PX_CAND + (sm - (e0[cl] - 1))];
+      t = px_warp_reduce(t);
+      if (threadIdx.x == 0) {
+        const int64_t S = px_units<WT>(scarry[sp]);
+        s_md = sm;
+        s_carry = (WT)((double)(S + px_apply(t, S & 1)) * px_ulp(sm, MANT));
+      }
+    }
+  }
+  __syncthreads();
+  const int md = s_md;
+  const WT s0 = s_carry;
+  if (md == PX_EXC) return;  // materialised by the resolver
   const int e = md;
   const double ue = px_ulp(e, MANT);
   const int64_t S = px_units<WT>(s0);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  WT v[PX_PER_THREAD];
   int64_t inc[PX_PER_THREAD];
   int64_t tsum = 0;
   bool tie = false;
@@ -654,7 +825,6 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_materialize(const WT* __restr
     uint32_t i32[PX_PER_THREAD], t32 = 0;
 #pragma unroll
     for (int j = 0; j < PX_PER_THREAD; ++j) {
-      v[j] = base + j < n ? w[base + j] : 0.0f;
       const PxInc32 d = px_inc32(v[j], e);
       i32[j] = d.v;
       tie |= d.tie;
@@ -674,11 +844,13 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_materialize(const WT* __restr
       for (int q = 0; q < wid; ++q) U += wt32[q];
       const int xe = e - 23;
       const float uef = xe >= -126 ? __uint_as_float((uint32_t)(xe + 127) << 23) : __uint_as_float(1u << (xe + 149));
+      WT o[PX_PER_THREAD];
 #pragma unroll
       for (int j = 0; j < PX_PER_THREAD; ++j) {
         U += i32[j];
-        if (base + j < n) cum[base + j] = (WT)__fmul_rn((float)U, uef);
+        o[j] = (WT)__fmul_rn((float)U, uef);
       }
+      px_store4<WT, VEC>(cum, base, n, o);
       return;
     }
 #pragma unroll
@@ -686,7 +858,6 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_materialize(const WT* __restr
   } else {
 #pragma unroll
     for (int j = 0; j < PX_PER_THREAD; ++j) {
-      v[j] = base + j < n ? w[base + j] : (WT)0;
       bool tj;
       inc[j] = px_inc<WT>(v[j], e, tj);
       tie |= tj;
@@ -705,11 +876,13 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_materialize(const WT* __restr
     __syncthreads();
     int64_t U = S + x - tsum;
     for (int q = 0; q < wid; ++q) U += wtot[q];
+    WT o[PX_PER_THREAD];
 #pragma unroll
     for (int j = 0; j < PX_PER_THREAD; ++j) {
       U += inc[j];
-      if (base + j < n) cum[base + j] = (WT)((double)U * ue);
+      o[j] = (WT)((double)U * ue);
     }
+    px_store4<WT, VEC>(cum, base, n, o);
     return;
   }
   // exclusive ordered block scan of the per-thread transducers
@@ -738,19 +911,6 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_materialize(const WT* __restr
   }
 }
 
-
-// the binade-crossing chunks: one warp each, writing every value (separate launch, so the
-// warp routine's registers do not limit the block scan's occupancy)
-template <typename WT>
-__global__ void __launch_bounds__(32) k_px_materialize_exc(const WT* __restrict__ w, int64_t n,
-                                                          const WT* __restrict__ carry,
-                                                          const int32_t* __restrict__ exc_list, WT* __restrict__ cum) {
-  const int cnt = exc_list[0];
-  for (int q = blockIdx.x; q < cnt; q += gridDim.x) {
-    const int64_t c = exc_list[1 + q];
-    px_chunk_seq<WT, true>(w, n, c, carry[c], cum);
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Searches.  multinomial (M/resample.py:295-304): key_i = WT(uniform01_at(seed, i, 0) *
