@@ -495,16 +495,23 @@ int px_cumsum(const WT* w, int64_t n, WT* cum, cudaStream_t st) {
   CUDA_TRY(sc.alloc(&csum, sizeof(double) * nch));
   CUDA_TRY(sc.alloc(&est, sizeof(double) * nch));
   CUDA_TRY(sc.alloc(&e0, sizeof(int32_t) * nch));
-  CUDA_TRY(sc.alloc(&mode, sizeof(int32_t) * nch));
+
   CUDA_TRY(sc.alloc(&agg, sizeof(Tx) * PX_CAND * nch));
-  CUDA_TRY(sc.alloc(&carry, sizeof(WT) * nch));
+
   CUDA_TRY(sc.alloc(&se0, sizeof(int32_t) * nsup));
   CUDA_TRY(sc.alloc(&smode, sizeof(int32_t) * nsup));
   CUDA_TRY(sc.alloc(&sagg, sizeof(Tx) * PX_CAND * nsup));
   CUDA_TRY(sc.alloc(&scarry, sizeof(WT) * nsup));
-  CUDA_TRY(sc.alloc(&scnt, sizeof(int32_t) * nsup));
+  // zeroed together: the super-chunk counters and the resolver's per-chunk carry / mode
+  // (k_px_materialize loads them before it knows whether the resolver wrote them)
+  const size_t zbytes = sizeof(WT) * nch + sizeof(int32_t) * (nch + nsup);
+  unsigned char* zero = nullptr;
+  CUDA_TRY(sc.alloc(&zero, zbytes));
+  carry = reinterpret_cast<WT*>(zero);
+  mode = reinterpret_cast<int32_t*>(zero + sizeof(WT) * nch);
+  scnt = mode + nch;
   CUDA_TRY(sc.alloc(&tmp, tmp_bytes + 16));
-  CUDA_TRY(cudaMemsetAsync(scnt, 0, sizeof(int32_t) * nsup, st));
+  CUDA_TRY(cudaMemsetAsync(zero, 0, zbytes, st));
   // 16-byte vector accesses in the streaming passes when both arrays allow them
   const bool vec = ((uintptr_t)w % 16 == 0) && ((uintptr_t)cum % 16 == 0);
   if (vec) k_px_chunk_sum<WT, true><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, csum);

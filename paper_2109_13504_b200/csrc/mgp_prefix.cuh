@@ -114,6 +114,42 @@ __device__ __forceinline__ PxInc32 px_inc32(float w, int e) {
   return d;
 }
 
+// float32, four elements at once on the FMA pipe (the integer form above is ~13 ALU instructions
+// per element and binade; the aggregate pass was ALU-bound at 82%): t = w * 2^(23-e) is exact,
+// fl(t + 2^23) is t rounded to the nearest integer (ties to even) with unit spacing because
+// t < 2^22, its low mantissa bits are that integer, and t - round(t) = +-0.5 (exact) flags a
+// tie -- the same increments and tie flags as px_inc32.  Valid when every element is below
+// 2^(e-1) (wmax_bits: the largest bit pattern; negative, non-finite and saturating elements fail
+// it) and e >= -104 (2^(23-e) a normal float); otherwise the integer form.
+__device__ __forceinline__ uint32_t px_inc4_f32(const float* v, int e, uint32_t wmax_bits, uint32_t* inc, bool& tie,
+                                                bool& sat) {
+  uint32_t s = 0;
+  if (e >= -104 && wmax_bits < ((uint32_t)(e + 126) << 23)) {
+    const float scale = __uint_as_float((uint32_t)(150 - e) << 23);  // 2^(23-e)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float y = __fmaf_rn(v[j], scale, 0x1p23f);
+      const float r = __fadd_rn(y, -0x1p23f);
+      tie |= fabsf(__fmaf_rn(v[j], scale, -r)) == 0.5f;
+      inc[j] = __float_as_uint(y) - 0x4B000000u;
+      s += inc[j];
+    }
+    return s;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const PxInc32 d = px_inc32(v[j], e);
+    inc[j] = d.v;
+    s += d.v;
+    tie |= d.tie;
+    sat |= d.sat;
+  }
+  return s;
+}
+__device__ __forceinline__ uint32_t px_wmax_bits(const float* v) {
+  return max(max(__float_as_uint(v[0]), __float_as_uint(v[1])), max(__float_as_uint(v[2]), __float_as_uint(v[3])));
+}
+
 // float64: the same branch-free form in 64 bits (M < 2^53; k clamped to [0, 63], k > 54 gives
 // q = v = 0 because M < 2^53 <= half)
 struct PxInc64 {
@@ -290,6 +326,8 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_aggregate(const WT* __restric
   WT v[PX_PER_THREAD];
   px_load4<WT, VEC>(w, c * PX_CHUNK + tid * PX_PER_THREAD, n, v);
   const int e0 = PxFp<WT>::expo((WT)est[c]);
+  uint32_t wmax = 0;
+  if constexpr (sizeof(WT) == 4) wmax = px_wmax_bits(reinterpret_cast<const float*>(v));
 #pragma unroll
   for (int k = 0; k < PX_CAND; ++k) {
     const int e = e0 - 1 + k;
@@ -299,15 +337,9 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_aggregate(const WT* __restric
     if constexpr (sizeof(WT) == 4) {
       // float32: every increment is < 2^24, so a warp's 128 of them sum exactly in 32 bits
       // (one REDUX); any saturating element saturates the warp's aggregate
-      uint32_t s32 = 0;
       bool sat = false;
-#pragma unroll
-      for (int j = 0; j < PX_PER_THREAD; ++j) {
-        const PxInc32 d = px_inc32(v[j], e);
-        s32 += d.v;
-        tie |= d.tie;
-        sat |= d.sat;
-      }
+      uint32_t incs[PX_PER_THREAD];
+      const uint32_t s32 = px_inc4_f32(reinterpret_cast<const float*>(v), e, wmax, incs, tie, sat);
       if (!__any_sync(0xffffffffu, tie)) {
         const bool any_sat = __any_sync(0xffffffffu, sat);
         const int64_t tot = (int64_t)__reduce_add_sync(0xffffffffu, s32);
@@ -340,10 +372,10 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_aggregate(const WT* __restric
     Tx t{0, 0};
     for (int q = 0; q < PX_THREADS / 32; ++q) t = px_compose(t, red[tid][q]);
     agg[c * PX_CAND + tid] = t;
+    if (tid == 0) e0_out[c] = e0;
+    __threadfence();  // the writers' stores are visible before the counter moves
   }
-  if (tid == 0) e0_out[c] = e0;
   // the last chunk of super-chunk sp to finish composes its aggregates
-  __threadfence();
   __syncthreads();
   const int64_t sp = c / PX_SUPER;
   if (tid == 0) {
@@ -788,20 +820,32 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_materialize(const WT* __restr
   WT v[PX_PER_THREAD];
   px_load4<WT, VEC>(w, base, n, v);  // in flight while the carry-in is composed
   if (threadIdx.x < 32) {
+    // everything the carry-in may need in one round trip (independent loads), then select
     const int64_t sp = c / PX_SUPER;
+    const int64_t cl = sp * PX_SUPER + threadIdx.x;  // chunks [sp * 32, c) of the super-chunk
+    const bool in = cl < c;
     const int sm = smode[sp];
+    const int ecl = in ? e0[cl] : 0;
+    Tx cand[PX_CAND];
+#pragma unroll
+    for (int q = 0; q < PX_CAND; ++q) cand[q] = in ? agg[cl * PX_CAND + q] : Tx{0, 0};
+    const WT sc = scarry[sp];
+    const int md_c = mode[c];
+    const WT carry_c = carry[c];
     if (sm == PX_DESC) {
       if (threadIdx.x == 0) {
-        s_md = mode[c];
-        s_carry = carry[c];
+        s_md = md_c;
+        s_carry = carry_c;
       }
     } else {
-      const int64_t cl = sp * PX_SUPER + threadIdx.x;  // chunks [sp * 32, c) of the super-chunk
       Tx t{0, 0};
-      if (cl < c) t = agg[cl * PX_CAND + (sm - (e0[cl] - 1))];
+      const int kq = sm - (ecl - 1);
+#pragma unroll
+      for (int q = 0; q < PX_CAND; ++q)
+        if (in && kq == q) t = cand[q];
       t = px_warp_reduce(t);
       if (threadIdx.x == 0) {
-        const int64_t S = px_units<WT>(scarry[sp]);
+        const int64_t S = px_units<WT>(sc);
         s_md = sm;
         s_carry = (WT)((double)(S + px_apply(t, S & 1)) * px_ulp(sm, MANT));
       }
@@ -822,14 +866,10 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_materialize(const WT* __restr
     // float32: a resolved chunk keeps the running sum inside binade e, so every prefix is
     // U * 2^(e-23) with U < 2^24 -- 32-bit scan, and U is exact as a float (one FMUL by the
     // power of two, subnormal spacing included)
-    uint32_t i32[PX_PER_THREAD], t32 = 0;
-#pragma unroll
-    for (int j = 0; j < PX_PER_THREAD; ++j) {
-      const PxInc32 d = px_inc32(v[j], e);
-      i32[j] = d.v;
-      tie |= d.tie;
-      t32 += d.v;
-    }
+    uint32_t i32[PX_PER_THREAD];
+    bool sat = false;  // a resolved chunk stays inside its binade: never set
+    const float* vf = reinterpret_cast<const float*>(v);
+    const uint32_t t32 = px_inc4_f32(vf, e, px_wmax_bits(vf), i32, tie, sat);
     if (!__syncthreads_or(tie)) {
       __shared__ uint32_t wt32[PX_THREADS / 32];
       uint32_t x = t32;
@@ -840,8 +880,9 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_materialize(const WT* __restr
       }
       if (lane == 31) wt32[wid] = x;
       __syncthreads();
-      uint32_t U = (uint32_t)S + x - t32;
-      for (int q = 0; q < wid; ++q) U += wt32[q];
+      // warps before this one: the 8 totals on lanes 0..7, one masked REDUX
+      const uint32_t wq = (lane < wid) ? wt32[lane & (PX_THREADS / 32 - 1)] : 0u;
+      uint32_t U = (uint32_t)S + x - t32 + __reduce_add_sync(0xffffffffu, wq);
       const int xe = e - 23;
       const float uef = xe >= -126 ? __uint_as_float((uint32_t)(xe + 127) << 23) : __uint_as_float(1u << (xe + 149));
       WT o[PX_PER_THREAD];
@@ -874,8 +915,10 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_materialize(const WT* __restr
     }
     if (lane == 31) wtot[wid] = x;
     __syncthreads();
-    int64_t U = S + x - tsum;
-    for (int q = 0; q < wid; ++q) U += wtot[q];
+    int64_t wq = (lane < wid) ? wtot[lane & (PX_THREADS / 32 - 1)] : 0;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) wq += __shfl_xor_sync(0xffffffffu, wq, o);  // lanes 0..7 hold them
+    int64_t U = S + x - tsum + __shfl_sync(0xffffffffu, wq, 0);
     WT o[PX_PER_THREAD];
 #pragma unroll
     for (int j = 0; j < PX_PER_THREAD; ++j) {
