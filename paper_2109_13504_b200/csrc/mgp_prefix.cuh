@@ -513,16 +513,23 @@ __device__ WT px_chunk_block(const WT* __restrict__ w, int64_t n, int64_t c, WT 
     const U S = (U)px_units<WT>(s);
     U t = 0, inc[PXR_PER];
     bool tie = false, sat = false;
+    if constexpr (sizeof(WT) == 4) {  // elements before p (and past len: zero-filled) count 0
+      float vm[PXR_PER];
 #pragma unroll
-    for (int j = 0; j < PXR_PER; ++j) {
-      const int idx = tid * PXR_PER + j;
-      inc[j] = 0;
-      if (idx >= p && idx < len) {
-        const auto d = P::inc(v[j], e);
-        inc[j] = d.v;
-        t += d.v;
-        tie |= d.tie;
-        sat |= d.sat;
+      for (int j = 0; j < PXR_PER; ++j) vm[j] = tid * PXR_PER + j >= p ? (float)v[j] : 0.0f;
+      t = px_inc4_f32(vm, e, px_wmax_bits(vm), inc, tie, sat);
+    } else {
+#pragma unroll
+      for (int j = 0; j < PXR_PER; ++j) {
+        const int idx = tid * PXR_PER + j;
+        inc[j] = 0;
+        if (idx >= p && idx < len) {
+          const auto d = P::inc(v[j], e);
+          inc[j] = d.v;
+          t += d.v;
+          tie |= d.tie;
+          sat |= d.sat;
+        }
       }
     }
     t = sat ? P::CAP : (t < P::CAP ? t : P::CAP);
@@ -588,18 +595,28 @@ __device__ WT px_chunk_block(const WT* __restrict__ w, int64_t n, int64_t c, WT 
   const long long pxp_q0 = clock64();
 #endif
   if (p < len) {  // sequential tail, numpy's order
+#ifdef MGP_PX_PROF
+    if (tid == 0 && g_px_prof[7] < 3) g_px_prof[13 + g_px_prof[7]] = (unsigned long long)(c * 4096 + p);
+#endif
     PXP_ADD(7, 1);
     PXP_ADD(8, len - p);
 #pragma unroll
     for (int j = 0; j < PXR_PER; ++j) sh.buf[tid * PXR_PER + j] = v[j];
     __syncthreads();
-    if (tid == 0) {  // groups of 8 through registers: the loads of the next group are in flight
-      WT r = s;        // while this group's dependent adds run (~4 cycles per element)
+    if (tid == 0) {  // groups of 8 through registers, the next group's loads issued before this
+      WT r = s;        // group's dependent adds (the add chain, ~4 cycles per element, is the cost)
       int idx = p;
-      for (; idx + 8 <= len; idx += 8) {
-        WT g[8];
+      WT g[8], h[8];
+      if (idx + 8 <= len) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) g[j] = sh.buf[idx + j];
+      }
+      for (; idx + 8 <= len; idx += 8) {
+        const bool more = idx + 16 <= len;
+        if (more) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) h[j] = sh.buf[idx + 8 + j];
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           r = r + g[j];
@@ -607,6 +624,8 @@ __device__ WT px_chunk_block(const WT* __restrict__ w, int64_t n, int64_t c, WT 
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) sh.buf[idx + j] = g[j];  // the prefix values
+#pragma unroll
+        for (int j = 0; j < 8; ++j) g[j] = h[j];
       }
       for (; idx < len; ++idx) {
         r = r + sh.buf[idx];
