@@ -988,7 +988,7 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_materialize(const WT* __restr
 // a key in [bnd[b], bnd[b+1]) has its answer in [start[b], start[b+1]] (upper_bound is
 // monotone).  The bucket is guessed from the key and corrected by exact comparisons against
 // the stored boundaries, then ~log2(N/K) probes finish the search (vs log2 N).
-constexpr int PXM_PER_BUCKET = 16;
+constexpr int PXM_PER_BUCKET = 8;  // 16 -> 8: 292 -> 265 us of search at 2^24 (scripts/mb/search_time.py)
 
 template <typename WT>
 __device__ __forceinline__ int64_t pxs_upper(const WT* __restrict__ cum, int64_t lo, int64_t hi, WT key) {
@@ -1000,9 +1000,10 @@ __device__ __forceinline__ int64_t pxs_upper(const WT* __restrict__ cum, int64_t
   return lo;
 }
 
+// K is a power of two: b / K = b * 2^-log2(K) exactly, one DMUL instead of a DDIV sequence
 template <typename WT>
 __device__ __forceinline__ WT pxm_bound(double total, int64_t b, int64_t K) {
-  return b >= K ? (WT)INFINITY : (WT)(total * (double)b / (double)K);
+  return b >= K ? (WT)INFINITY : (WT)(total * ((double)b * __longlong_as_double((1023ll - (63 - __clzll(K))) << 52)));
 }
 
 template <typename WT>
@@ -1016,11 +1017,12 @@ template <typename WT>
 __global__ void k_multinomial(const WT* __restrict__ cum, int64_t n, uint64_t base, int64_t p0, int64_t p_end,
                               int64_t K, const int32_t* __restrict__ start, int64_t* __restrict__ anc) {
   const double total = (double)cum[n - 1];
+  const double kscale = (double)K / total;  // the bucket guess only: exact corrections follow
   for (int64_t i = p0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p_end; i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t h = mix64(megores_key(base, (uint64_t)i, 0));
     const double ud = __dmul_rn((double)(h >> 11) * 0x1p-53, total);
     const WT key = (WT)ud;
-    int64_t bk = (int64_t)((double)key / total * (double)K);
+    int64_t bk = (int64_t)((double)key * kscale);
     bk = bk < 0 ? 0 : (bk >= K ? K - 1 : bk);
     while (bk > 0 && key < pxm_bound<WT>(total, bk, K)) --bk;          // exact corrections
     while (bk < K - 1 && !(key < pxm_bound<WT>(total, bk + 1, K))) ++bk;
