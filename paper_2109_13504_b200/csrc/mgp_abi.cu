@@ -501,14 +501,16 @@ int px_cumsum(const WT* w, int64_t n, WT* cum, cudaStream_t st) {
   CUDA_TRY(sc.alloc(&se0, sizeof(int32_t) * nsup));
   CUDA_TRY(sc.alloc(&smode, sizeof(int32_t) * nsup));
   CUDA_TRY(sc.alloc(&sagg, sizeof(Tx) * PX_CAND * nsup));
-  CUDA_TRY(sc.alloc(&scarry, sizeof(WT) * nsup));
-  // zeroed together: the super-chunk counters and the resolver's per-chunk carry / mode
-  // (k_px_materialize loads them before it knows whether the resolver wrote them)
-  const size_t zbytes = sizeof(WT) * nch + sizeof(int32_t) * (nch + nsup);
+
+  // zeroed together: the super-chunk counters and the resolver's per-chunk carry / mode and
+  // per-super-chunk carry (k_px_materialize loads them all before it knows which ones the
+  // resolver wrote)
+  const size_t zbytes = sizeof(WT) * (nch + nsup) + sizeof(int32_t) * (nch + nsup);
   unsigned char* zero = nullptr;
   CUDA_TRY(sc.alloc(&zero, zbytes));
   carry = reinterpret_cast<WT*>(zero);
-  mode = reinterpret_cast<int32_t*>(zero + sizeof(WT) * nch);
+  scarry = carry + nch;
+  mode = reinterpret_cast<int32_t*>(scarry + nsup);
   scnt = mode + nch;
   CUDA_TRY(sc.alloc(&tmp, tmp_bytes + 16));
   CUDA_TRY(cudaMemsetAsync(zero, 0, zbytes, st));

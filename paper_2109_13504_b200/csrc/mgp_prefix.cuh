@@ -146,6 +146,23 @@ __device__ __forceinline__ uint32_t px_inc4_f32(const float* v, int e, uint32_t 
   }
   return s;
 }
+// float64, the same on the FP64 pipe: t = w * 2^(52-e), fl(t + 2^52) for w < 2^(e-1), e >= -970.
+// Returns false (nothing computed) when an element needs the integer form.
+__device__ __forceinline__ bool px_inc4_f64(const double* v, int e, int64_t* inc, int64_t& sum, bool& tie) {
+  const uint64_t wmax = max(max((uint64_t)__double_as_longlong(v[0]), (uint64_t)__double_as_longlong(v[1])),
+                            max((uint64_t)__double_as_longlong(v[2]), (uint64_t)__double_as_longlong(v[3])));
+  if (!(e >= -970 && wmax < ((uint64_t)(e + 1022) << 52))) return false;
+  const double scale = __longlong_as_double((long long)(1075 - e) << 52);  // 2^(52-e)
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double y = __fma_rn(v[j], scale, 0x1p52);
+    const double r = __dadd_rn(y, -0x1p52);
+    tie |= fabs(__fma_rn(v[j], scale, -r)) == 0.5;
+    inc[j] = (int64_t)((uint64_t)__double_as_longlong(y) - 0x4330000000000000ull);
+    sum += inc[j];
+  }
+  return true;
+}
 __device__ __forceinline__ uint32_t px_wmax_bits(const float* v) {
   return max(max(__float_as_uint(v[0]), __float_as_uint(v[1])), max(__float_as_uint(v[2]), __float_as_uint(v[3])));
 }
@@ -348,11 +365,14 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_aggregate(const WT* __restric
         continue;
       }
     } else {
+      int64_t incs[PX_PER_THREAD];
+      if (!px_inc4_f64(reinterpret_cast<const double*>(v), e, incs, sum, tie)) {
 #pragma unroll
-      for (int j = 0; j < PX_PER_THREAD; ++j) {
-        bool tj;
-        sum = px_sat_add(sum, px_inc<WT>(v[j], e, tj));
-        tie |= tj;
+        for (int j = 0; j < PX_PER_THREAD; ++j) {
+          bool tj;
+          sum = px_sat_add(sum, px_inc<WT>(v[j], e, tj));
+          tie |= tj;
+        }
       }
     }
     if (__any_sync(0xffffffffu, tie)) {  // rounding ties in this warp: parity transducers
@@ -916,12 +936,14 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_materialize(const WT* __restr
 #pragma unroll
     for (int j = 0; j < PX_PER_THREAD; ++j) inc[j] = i32[j];
   } else {
+    if (!px_inc4_f64(reinterpret_cast<const double*>(v), e, inc, tsum, tie)) {
 #pragma unroll
-    for (int j = 0; j < PX_PER_THREAD; ++j) {
-      bool tj;
-      inc[j] = px_inc<WT>(v[j], e, tj);
-      tie |= tj;
-      tsum += inc[j];  // a resolved chunk stays inside its binade: no saturation here
+      for (int j = 0; j < PX_PER_THREAD; ++j) {
+        bool tj;
+        inc[j] = px_inc<WT>(v[j], e, tj);
+        tie |= tj;
+        tsum += inc[j];  // a resolved chunk stays inside its binade: no saturation here
+      }
     }
   }
   if (!__syncthreads_or(tie)) {  // no rounding ties in the chunk: plain exclusive integer scan
