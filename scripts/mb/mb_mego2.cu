@@ -148,6 +148,46 @@ __global__ void __launch_bounds__(256) k_w(const __grid_constant__ ResampleArgs 
   a.anc[i] = (int64_t)k;
 }
 
+// PFMA: the accept updates as predicated FMA-pipe instructions (FFMA wj*1+0, IMAD t*1+0 with
+// opaque 1 / 0 from the parameter space, so ptxas cannot turn them back into FSEL / SEL);
+// AMBB: ambiguity as a bool (predicate accumulation) instead of a recorded round
+template <bool PFMA, bool AMBB, bool ADDW, int UNR>
+__global__ void __launch_bounds__(256) k_p(const __grid_constant__ ResampleArgs a, const __grid_constant__ OffChunk oc,
+                                          float onef, float zerof, uint32_t onei, uint32_t zeroi) {
+  const uint32_t i = a.p0 + blockIdx.x * 256 + threadIdx.x;
+  const uint32_t lane = threadIdx.x & 31u, cmask = (a.n - 1) & ~31u, ial = i - lane;
+  float wk = tex1Dfetch<float>(a.tex, (int)i);
+  const float wk0 = wk;
+  int bstar = -1, ambt = -1;
+  bool amb = false;
+  uint64_t x = megores_key(a.base, i, (uint64_t)a.b0);
+#pragma unroll UNR
+  for (int t = 0; t < a.cnt; ++t) {
+    const uint2 o = oc.o[t];
+    const uint32_t j = mux3(ial + o.x, lane + o.y, cmask);
+    const float wj = tex1Dfetch<float>(a.tex, (int)j);
+    const float u1 = __uint_as_float(0x3F800000u + (mix64_mhi(x) >> 9));
+    const float lo = __fmaf_rd(u1, wk, -wk);
+    const float hi = __fmaf_ru(wk, 0x1p-22f, lo);
+    if (AMBB) amb |= (lo <= wj) && !(hi <= wj);
+    else if (!(hi <= wj) && lo <= wj) ambt = t;
+    if (PFMA) {
+      asm("{\n\t.reg .pred p;\n\t"
+          "setp.le.f32 p, %2, %3;\n\t"
+          "@p fma.rn.f32 %0, %3, %5, %6;\n\t"
+          "@p mad.lo.u32 %1, %4, %7, %8;\n\t}"
+          : "+f"(wk), "+r"(bstar) : "f"(hi), "f"(wj), "r"(t), "f"(onef), "f"(zerof), "r"(onei), "r"(zeroi));
+    } else {
+      if (hi <= wj) { wk = wj; bstar = t; }
+    }
+    x = ADDW ? add64_fma(x, a.one) : x + M_CTR;
+  }
+  if (AMBB ? amb : ambt >= 0) bstar = megores_exact_rounds(a, oc, i, wk0, true);
+  uint32_t k = i;
+  if (bstar >= 0) k = mux3(ial + oc.o[bstar].x, lane + oc.o[bstar].y, cmask);
+  a.anc[i] = (int64_t)k;
+}
+
 template <class K>
 float time_it(K launch, int reps) {
   cudaEvent_t e0, e1;
@@ -212,30 +252,13 @@ int main(int argc, char** argv) {
     printf("%-18s %.3f ms  %.1f Gcmp/s  speedup %.3f  mismatches %zu\n", name, ms, cmp / ms / 1e6, t0 / ms, bad);
     CK(cudaMemset(anc1, 0xff, 8ull * n));
   };
-  static OffT ot;
-  for (int t = 0; t < 1024; ++t) ot.t[t] = (uint32_t)t;
   for (int rep = 0; rep < 2; ++rep) {
-    check("w base", time_it([&]() { k_w<false, 0, false, 8><<<grid, 256>>>(b, oc, ot, 4, 32); }, 7));
-    check("w XC", time_it([&]() { k_w<true, 0, false, 8><<<grid, 256>>>(b, oc, ot, 4, 32); }, 7));
-    check("w SH1", time_it([&]() { k_w<false, 1, false, 8><<<grid, 256>>>(b, oc, ot, 4, 32); }, 7));
-    check("w SH2", time_it([&]() { k_w<false, 2, false, 8><<<grid, 256>>>(b, oc, ot, 4, 32); }, 7));
-    check("w I2F", time_it([&]() { k_w<false, 0, true, 8><<<grid, 256>>>(b, oc, ot, 4, 32); }, 7));
-    check("w XC I2F", time_it([&]() { k_w<true, 0, true, 8><<<grid, 256>>>(b, oc, ot, 4, 32); }, 7));
-    check("w SH1 I2F", time_it([&]() { k_w<false, 1, true, 8><<<grid, 256>>>(b, oc, ot, 4, 32); }, 7));
-    check("w XC SH1", time_it([&]() { k_w<true, 1, false, 8><<<grid, 256>>>(b, oc, ot, 4, 32); }, 7));
-    check("w XC SH1 I2F", time_it([&]() { k_w<true, 1, true, 8><<<grid, 256>>>(b, oc, ot, 4, 32); }, 7));
-    check("w XC SH3 I2F", time_it([&]() { k_w<true, 3, true, 8><<<grid, 256>>>(b, oc, ot, 4, 32); }, 7));
-    check("w XC I2F u4", time_it([&]() { k_w<true, 0, true, 4><<<grid, 256>>>(b, oc, ot, 4, 32); }, 7));
-  }
-  for (int rep = 0; rep < 1; ++rep) {
-    check("base u8", time_it([&]() { k_v<false, false, 1, 8><<<grid, 256>>>(b, oc); }, 7));
-    check("PMOV u8", time_it([&]() { k_v<true, false, 1, 8><<<grid, 256>>>(b, oc); }, 7));
-    check("ADDW u8", time_it([&]() { k_v<false, true, 1, 8><<<grid, 256>>>(b, oc); }, 7));
-    check("PMOV ADDW u8", time_it([&]() { k_v<true, true, 1, 8><<<grid, 256>>>(b, oc); }, 7));
-    check("PMOV u4", time_it([&]() { k_v<true, false, 1, 4><<<grid, 256>>>(b, oc); }, 7));
-    check("PMOV PPT2 u4", time_it([&]() { k_v<true, false, 2, 4><<<grid, 128>>>(b, oc); }, 7));
-    check("PMOV ADDW PPT2 u4", time_it([&]() { k_v<true, true, 2, 4><<<grid, 128>>>(b, oc); }, 7));
-    check("base PPT2 u4", time_it([&]() { k_v<false, false, 2, 4><<<grid, 128>>>(b, oc); }, 7));
+    check("p base ADDW", time_it([&]() { k_p<false, false, true, 8><<<grid, 256>>>(b, oc, 1.f, 0.f, 1u, 0u); }, 7));
+    check("p PFMA ADDW", time_it([&]() { k_p<true, false, true, 8><<<grid, 256>>>(b, oc, 1.f, 0.f, 1u, 0u); }, 7));
+    check("p AMBB ADDW", time_it([&]() { k_p<false, true, true, 8><<<grid, 256>>>(b, oc, 1.f, 0.f, 1u, 0u); }, 7));
+    check("p PFMA AMBB ADDW", time_it([&]() { k_p<true, true, true, 8><<<grid, 256>>>(b, oc, 1.f, 0.f, 1u, 0u); }, 7));
+    check("p PFMA AMBB", time_it([&]() { k_p<true, true, false, 8><<<grid, 256>>>(b, oc, 1.f, 0.f, 1u, 0u); }, 7));
+    check("p PFMA AMBB ADDW u4", time_it([&]() { k_p<true, true, true, 4><<<grid, 256>>>(b, oc, 1.f, 0.f, 1u, 0u); }, 7));
   }
   return 0;
 }
