@@ -290,9 +290,10 @@ int mgp_debug_megores_fallbacks(int64_t *h_count, int reset);
  * sequential tails and their cycles. */
 int mgp_debug_px_prof(int64_t *h_out16, int reset);
 
-/* Measurement switch for mgp_offspring: 1 = the int32 global-atomic histogram (round 1), 0 = the
- * bucketed shared-memory histogram (default).  Process-wide; for A/B timing and tests only. */
-int mgp_debug_offspring_mode(int atomic_histogram);
+/* Measurement switch for mgp_offspring: 0 = the queued shared-memory histogram (default), 1 = the
+ * int32 global-atomic histogram (round 1), 2 = the count-matrix bucketed histogram.  Process-wide;
+ * for A/B timing and tests only. */
+int mgp_debug_offspring_mode(int mode);
 
 #ifdef __cplusplus
 }

@@ -1261,8 +1261,9 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
 #define MGP_OFFSPRING_I32_MIN (1ll << 20)
 #endif
 
-// measurement switch (mgp_debug_offspring_mode): 1 = the round-1 int32 atomic histogram, for A/B
-static std::atomic<int> g_offspring_atomic{0};
+// measurement switch (mgp_debug_offspring_mode): 0 = queued (default), 1 = the round-1 int32 atomic
+// histogram, 2 = the count-matrix bucketed histogram (round 2 first version), for A/B
+static std::atomic<int> g_offspring_mode{0};
 
 int mgp_offspring(const int64_t* d_anc, int64_t n_anc, int64_t n, int64_t* d_counts, int32_t* d_bad, void* stream) {
   if (n < 0 || n_anc < 0) return set_err(MGP_EINVAL, "negative size");
@@ -1275,8 +1276,43 @@ int mgp_offspring(const int64_t* d_anc, int64_t n_anc, int64_t n, int64_t* d_cou
   // Large histograms: bucketed (no per-particle global atomics; mgp_kernels.cuh k_offb_*)
   const int64_t K = (n + OFFB_BINS - 1) / OFFB_BINS;
   const int64_t tiles = (n_anc + OFFB_TILE - 1) / OFFB_TILE;
+  const int mode = g_offspring_mode.load();
+  // Large histograms: queued (mgp_kernels.cuh k_offq_*): one read of the ancestors, no count pass
+  if (n >= MGP_OFFSPRING_I32_MIN && K <= OFFB_KMAX && n_anc > 0 && n_anc <= MAX_N && mode == 0 &&
+      (((uintptr_t)d_anc) & 15) == 0 && K * (2 * ((n_anc + K - 1) / K) + 1032) < (1ll << 31)) {
+    constexpr int THR = 512, PER = 16;
+    constexpr int64_t TILE = (int64_t)PER * THR;
+    const bool small_k = 20 * K + 16 + 4 * TILE <= 200 * 1024;  // shared memory per CTA, else half tiles
+    const int64_t tile = small_k ? TILE : TILE / 2;
+    const int64_t qt = (n_anc + tile - 1) / tile;
+    const int64_t avg = (n_anc + K - 1) / K;
+    const uint32_t cap = (uint32_t)(((2 * avg + 1024) + 7) & ~7ll);  // queue capacity (uint16 entries)
+    uint32_t *ctr = nullptr, *ovf = nullptr;  // ctr: K queue cursors, then the overflow length
+    uint16_t* queue = nullptr;
+    CUDA_TRY(sc.alloc(&ctr, sizeof(uint32_t) * (K + 1)));
+    CUDA_TRY(sc.alloc(&ovf, sizeof(uint32_t) * n_anc));
+    CUDA_TRY(sc.alloc(&queue, sizeof(uint16_t) * (size_t)K * cap));
+    CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(uint32_t) * (K + 1), st));
+    const size_t ssm = 20 * K + 16 + 4 * tile;
+    if (small_k) {
+      CUDA_TRY(cudaFuncSetAttribute(k_offq_scatter<THR, PER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+      k_offq_scatter<THR, PER><<<(unsigned)qt, THR, ssm, st>>>(d_anc, n_anc, n, (int)K, cap, ctr, queue, ctr + K, ovf, bad);
+    } else {
+      CUDA_TRY(cudaFuncSetAttribute(k_offq_scatter<THR, PER / 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+      k_offq_scatter<THR, PER / 2><<<(unsigned)qt, THR, ssm, st>>>(d_anc, n_anc, n, (int)K, cap, ctr, queue, ctr + K, ovf,
+                                                                   bad);
+    }
+    LAUNCH_CHECK("k_offq_scatter");
+    const size_t hsm = sizeof(uint32_t) * OFFB_BINS;
+    CUDA_TRY(cudaFuncSetAttribute(k_offq_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+    k_offq_hist<<<(unsigned)K, 512, hsm, st>>>(queue, cap, ctr, n, d_counts);
+    LAUNCH_CHECK("k_offq_hist");
+    k_offq_overflow<<<148 * 2, 256, 0, st>>>(ovf, ctr + K, d_counts);
+    LAUNCH_CHECK("k_offq_overflow");
+    return 0;
+  }
   if (n >= MGP_OFFSPRING_I32_MIN && K <= OFFB_KMAX && n_anc > 0 && n_anc <= MAX_N && K * tiles < (1ll << 30) &&
-      !g_offspring_atomic) {
+      mode != 1) {
     const int64_t m = K * tiles + 1;  // the bucket-major count matrix plus the total
     uint32_t *mat = nullptr, *off = nullptr;
     uint16_t* runs = nullptr;
@@ -1979,8 +2015,9 @@ extern "C" int mgp_philox_selftest(uint64_t key, uint32_t c1, uint32_t c2, uint3
   return 0;
 }
 
-extern "C" int mgp_debug_offspring_mode(int atomic_histogram) {
-  g_offspring_atomic.store(atomic_histogram ? 1 : 0);
+extern "C" int mgp_debug_offspring_mode(int mode) {
+  if (mode < 0 || mode > 2) return set_err(MGP_EINVAL, "offspring mode must be 0, 1 or 2");
+  g_offspring_mode.store(mode);
   return 0;
 }
 

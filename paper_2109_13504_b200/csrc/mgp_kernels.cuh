@@ -148,18 +148,19 @@ __device__ __forceinline__ P4 philox_keys(uint32_t c0, uint32_t c1, uint32_t c2,
   return P4{c0, c1, c2, c3};
 }
 
-// x + M_CTR computed as IMAD.WIDE.U32(one, M_CTR_lo, x) + IMAD(one, M_CTR_hi, hi): the FMA pipe
-// does the 64-bit add; `one` (== 1) comes from the parameter space so ptxas cannot fold it.
+// x + M_CTR as IADD3 (low word, carry out) + IMAD.X (high word: x_hi * one + M_CTR_hi + carry,
+// the FMA pipe); `one` (== 1) comes from the parameter space so ptxas cannot fold the multiply
+// into an IADD3.X on the ALU pipe.  Two instructions (the mad.wide form it replaces compiled to
+// IADD3 + IMAD.X + IMAD: ptxas hoisted one * M_CTR_lo and added one * M_CTR_hi separately).
 __device__ __forceinline__ uint64_t add64_fma(uint64_t x, uint32_t one) {
-  uint64_t r;
-  asm("{\n\t.reg .u32 lo, hi;\n\t"
-      "mad.wide.u32 %0, %1, %2, %3;\n\t"
-      "mov.b64 {lo, hi}, %0;\n\t"
-      "mad.lo.u32 hi, %1, %4, hi;\n\t"
-      "mov.b64 %0, {lo, hi};\n\t}"
-      : "=l"(r)
-      : "r"(one), "r"((uint32_t)M_CTR), "l"(x), "r"((uint32_t)(M_CTR >> 32)));
-  return r;
+  uint32_t lo, hi;
+  asm("{\n\t.reg .u32 xl, xh;\n\t"
+      "mov.b64 {xl, xh}, %2;\n\t"
+      "add.cc.u32 %0, xl, %4;\n\t"
+      "madc.lo.u32 %1, xh, %3, %5;\n\t}"
+      : "=r"(lo), "=r"(hi)
+      : "l"(x), "r"(one), "n"((uint32_t)M_CTR), "n"((uint32_t)(M_CTR >> 32)));
+  return ((uint64_t)hi << 32) | lo;
 }
 
 // exact (double)w * 2^-32 for a 32-bit word: (2^52 + w) * 2^-32 - 2^20 in one DFMA
@@ -1120,6 +1121,204 @@ __global__ void __launch_bounds__(512) k_offb_hist(const uint16_t* __restrict__ 
   const int64_t c0 = (int64_t)b << OFFB_BITS;
   const int nb = (int)min((int64_t)OFFB_BINS, n - c0);
   for (int q = threadIdx.x; q < nb; q += 512) __stcs(counts + c0 + q, (int64_t)bins[q]);
+}
+
+// ---------------------------------------------------------------------------
+// Queued offspring histogram (the default for 2^20 <= n <= 2^27): the bucketed histogram above
+// without its count pass and scan.  A histogram does not care in which order a bucket's ancestors
+// arrive, so every bucket gets a fixed-capacity queue and a tile reserves its run in it with one
+// global atomic (the arrival order is the atomic order; the counts are still exact):
+//   k_offq_scatter   per tile of 8192 ancestors (4096 for n > 2^25; one read of the ancestors,
+//                    16-byte loads held in registers): range check (bad flag), bucket counts by
+//                    shared-memory atomics, block scan, one atomicAdd per non-empty bucket on its
+//                    queue cursor, counting sort of the tile by bucket in shared memory, then every
+//                    (tile, bucket) run leaves as one contiguous uint16 store of the low 14 bits.
+//                    Positions past a queue's capacity (skewed inputs: one-hot ancestors, weights
+//                    that grow with the index) go to an overflow list instead, one atomicAdd on its
+//                    length per spilling run.
+//   k_offq_hist      one CTA per bucket: shared-memory histogram of its queue (8 uint16 per
+//                    16-byte load), 2^14 int64 counts out with streaming stores.
+//   k_offq_overflow  the overflow list (usually empty: one uniform load and exit) as
+//                    warp-aggregated int64 atomics into the finished counts.
+// HBM traffic per call: 8N (ancestors, read once) + 8N (counts) = the algorithmic 16N; the 2N-byte
+// queues stay in L2.
+constexpr int OFFQ_DEFER = 4;                 // queue reservations held in registers per thread (K <= 4 * THREADS)
+constexpr uint32_t OFFQ_SPILL = 0xFFFFFFFFu;  // run reaching past its queue's capacity
+
+// One tile of PER * THREADS ancestors per CTA, read with 16-byte loads held in registers.  Invalid
+// (out-of-range) ancestors go to a trash bucket K so that every per-element step is branch-free.
+// (Measured alternatives, scripts/mb/probe_offq*.sh: persistent CTAs streaming the next tiles
+// through a two-slot shared-memory ring by bulk copy (TMA) 0.138-0.155 ms; 32 ancestors per
+// thread, 256-thread CTAs, 2-4 CTAs per SM forced: 0.130-0.170 ms; the queue loads of
+// k_offq_hist batched four per thread: 0.180 ms.  This shape: 0.130 ms.)
+template <int THREADS, int PER>
+__global__ void __launch_bounds__(THREADS) k_offq_scatter(const int64_t* __restrict__ anc, int64_t n_anc, int64_t n,
+                                                          int K, uint32_t cap, uint32_t* __restrict__ gcur,
+                                                          uint16_t* __restrict__ queue, uint32_t* __restrict__ novf,
+                                                          uint32_t* __restrict__ ovf, int* bad) {
+  constexpr int TILE = PER * THREADS;
+  extern __shared__ __align__(16) unsigned char offq_smem[];
+  uint32_t* sorted = reinterpret_cast<uint32_t*>(offq_smem);  // TILE, sorted by bucket
+  uint32_t* cnt = sorted + TILE;  // K + 1: bucket counts (K: the trash bucket), then cursors
+  uint32_t* loc = cnt + K + 1;    // K: local run starts
+  uint32_t* gb = loc + K;         // K: queue position of the run
+  uint32_t* ob = gb + K;          // K: overflow-list position of the spill
+  uint32_t* dst = ob + K;         // K: queue index base of the run (or OFFQ_SPILL)
+  __shared__ uint32_t wsum[THREADS / 32];
+  const uint32_t trash = (uint32_t)K << OFFB_BITS;
+  bool oob = false;
+  {
+    for (int b = threadIdx.x; b <= K; b += THREADS) cnt[b] = 0;
+    const int64_t t0 = (int64_t)blockIdx.x * TILE;
+    const bool full = t0 + TILE <= n_anc;
+    __syncthreads();
+    uint32_t key[PER];
+#pragma unroll
+    for (int q = 0; q < PER / 2; ++q) {  // element pair 2 * (q * THREADS + tid) + {0, 1} of the tile
+      const int e = 2 * (q * THREADS + (int)threadIdx.x);
+      int64_t a0 = -1, a1 = -1;
+      bool l0 = true, l1 = true;
+      if (full) {
+        const longlong2 v = __ldcs(reinterpret_cast<const longlong2*>(anc + t0 + e));
+        a0 = v.x;
+        a1 = v.y;
+      } else {
+        l0 = t0 + e < n_anc;
+        l1 = t0 + e + 1 < n_anc;
+        if (l0) a0 = anc[t0 + e];
+        if (l1) a1 = anc[t0 + e + 1];
+      }
+      const bool v0 = a0 >= 0 && a0 < n, v1 = a1 >= 0 && a1 < n;
+      oob |= (l0 && !v0) || (l1 && !v1);
+      key[2 * q] = v0 ? (uint32_t)a0 : trash;  // trash >> OFFB_BITS == K
+      key[2 * q + 1] = v1 ? (uint32_t)a1 : trash;
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) atomicAdd(&cnt[key[q] >> OFFB_BITS], 1u);
+    __syncthreads();  // counts complete
+    // exclusive scan of the bucket counts; the queue reservations are issued here and their
+    // results consumed after the shared-memory sort, which hides the contended atomics' latency
+    const bool defer = K <= OFFQ_DEFER * THREADS;
+    uint32_t gres[OFFQ_DEFER];
+    uint32_t carry = 0;
+    for (int c0 = 0, it = 0; c0 < K; c0 += THREADS, ++it) {
+      const int b = c0 + threadIdx.x;
+      const uint32_t v = b < K ? cnt[b] : 0u;
+      uint32_t x = v;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+        if ((threadIdx.x & 31) >= d) x += y;
+      }
+      if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = x;
+      __syncthreads();
+      uint32_t wb = 0, tot = 0;
+#pragma unroll
+      for (int q = 0; q < THREADS / 32; ++q) {
+        wb += q < (int)(threadIdx.x >> 5) ? wsum[q] : 0u;
+        tot += wsum[q];
+      }
+      if (b < K) {
+        const uint32_t l = carry + wb + x - v;
+        loc[b] = l;
+        cnt[b] = l;  // cursor
+        const uint32_t g = v ? atomicAdd(&gcur[b], v) : 0u;
+        if (defer) {
+#pragma unroll
+          for (int r = 0; r < OFFQ_DEFER; ++r)
+            if (r == it) gres[r] = g;
+        } else {
+          gb[b] = g;
+        }
+      }
+      carry += tot;
+      if (c0 + THREADS >= K && threadIdx.x == 0) cnt[K] = carry;  // the trash run follows the valid ones
+      __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) sorted[atomicAdd(&cnt[key[q] >> OFFB_BITS], 1u)] = key[q];
+    // runs past a queue's capacity: positions [max(g, cap), g + v) go to the overflow list
+    for (int c0 = 0, it = 0; c0 < K; c0 += THREADS, ++it) {
+      const int b = c0 + threadIdx.x;
+      if (b >= K) break;
+      uint32_t g = gb[b];
+      if (defer) {
+#pragma unroll
+        for (int r = 0; r < OFFQ_DEFER; ++r)
+          if (r == it) g = gres[r];
+        gb[b] = g;
+      }
+      const uint32_t l = loc[b], v = (b + 1 < K ? loc[b + 1] : carry) - l;
+      uint32_t o = 0;
+      if (g + v > cap) {
+        const uint32_t from = g > cap ? g : cap;
+        o = atomicAdd(novf, g + v - from) - (from - g);  // ovf index = o + r for run offset r
+      }
+      ob[b] = o;
+      // queue index of sorted element q of this run = dst + q (K * cap < 2^31); SPILL: the run
+      // reaches past the capacity, take the checked path
+      dst[b] = g + v > cap ? OFFQ_SPILL : (uint32_t)b * cap + g - l;
+    }
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < carry; q += THREADS) {
+      const uint32_t k = sorted[q], b = k >> OFFB_BITS, d = dst[b];
+      if (d != OFFQ_SPILL) {
+        queue[d + q] = (uint16_t)(k & (OFFB_BINS - 1));
+      } else {
+        const uint32_t r = q - loc[b], pos = gb[b] + r;
+        if (pos < cap) queue[(size_t)b * cap + pos] = (uint16_t)(k & (OFFB_BINS - 1));
+        else ovf[ob[b] + r] = k;
+      }
+    }
+  }
+  if (oob) atomicExch(bad, 1);
+}
+
+__global__ void __launch_bounds__(512) k_offq_hist(const uint16_t* __restrict__ queue, uint32_t cap,
+                                                   const uint32_t* __restrict__ gcur, int64_t n,
+                                                   int64_t* __restrict__ counts) {
+  extern __shared__ __align__(16) unsigned char offq_smem[];
+  uint32_t* bins = reinterpret_cast<uint32_t*>(offq_smem);
+  const int b = blockIdx.x;
+  for (int q = threadIdx.x; q < OFFB_BINS / 4; q += 512) reinterpret_cast<uint4*>(bins)[q] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  const uint32_t m = min(gcur[b], cap);
+  const uint16_t* __restrict__ qb = queue + (size_t)b * cap;  // cap % 8 == 0: 16-byte aligned
+  const uint32_t m8 = m >> 3;
+  for (uint32_t q = threadIdx.x; q < m8; q += 512) {
+    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(qb) + q);
+    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      atomicAdd(&bins[w4[h] & 0xFFFFu], 1u);
+      atomicAdd(&bins[w4[h] >> 16], 1u);
+    }
+  }
+  for (uint32_t q = (m8 << 3) + threadIdx.x; q < m; q += 512) atomicAdd(&bins[qb[q]], 1u);
+  __syncthreads();
+  const int64_t c0 = (int64_t)b << OFFB_BITS;
+  const int nb = (int)min((int64_t)OFFB_BINS, n - c0);
+  if (nb == OFFB_BINS) {
+    for (int q = threadIdx.x; q < OFFB_BINS / 2; q += 512)
+      __stcs(reinterpret_cast<longlong2*>(counts + c0) + q, make_longlong2(bins[2 * q], bins[2 * q + 1]));
+  } else {
+    for (int q = threadIdx.x; q < nb; q += 512) __stcs(counts + c0 + q, (int64_t)bins[q]);
+  }
+}
+
+__global__ void k_offq_overflow(const uint32_t* __restrict__ ovf, const uint32_t* __restrict__ novf,
+                                int64_t* __restrict__ counts) {
+  const uint32_t m = *novf;
+  for (uint32_t q0 = blockIdx.x * blockDim.x; q0 < m; q0 += gridDim.x * blockDim.x) {
+    const uint32_t q = q0 + threadIdx.x;
+    const bool live = q < m;
+    const uint32_t k = live ? ovf[q] : 0xFFFFFFFFu;
+    const unsigned act = __ballot_sync(0xffffffffu, live);
+    if (!live) continue;
+    const unsigned peers = __match_any_sync(act, k);
+    if ((int)(threadIdx.x & 31) == __ffs(peers) - 1)
+      atomicAdd(reinterpret_cast<unsigned long long*>(counts) + k, (unsigned long long)__popc(peers));
+  }
 }
 
 // int32 histogram -> the int64 counts of the ABI (4 counts per thread, 16-byte loads)

@@ -1,5 +1,5 @@
 """CUDA-event time of mgp_offspring at 2^24 (Megopolis ancestors, y = 4) per histogram mode
-(0 = bucketed, 1 = int32 global atomics), through the C ABI (no Python-side sync)."""
+(0 = queued, 1 = int32 global atomics, 2 = count-matrix bucketed), through the C ABI (no Python-side sync)."""
 import os
 import sys
 
@@ -16,7 +16,7 @@ c = torch.empty(n, dtype=torch.int64, device="cuda")
 bad = torch.zeros(1, dtype=torch.int32, device="cuda")
 L = _lib.lib()
 s = torch.cuda.current_stream().cuda_stream
-for mode in (0, 1, 0, 1):
+for mode in (0, 1, 2, 0, 1, 2):
     L.mgp_debug_offspring_mode(mode)
     for _ in range(3):
         _lib.check(L.mgp_offspring(a.data_ptr(), n, n, c.data_ptr(), bad.data_ptr(), s))
