@@ -229,6 +229,7 @@ void offsets_host(uint64_t seed, int64_t n, int32_t b, int rng, int64_t* out) {
 #ifndef MGP_PPT_MEGORES
 #define MGP_PPT_MEGORES 1
 #endif
+
 template <int RNG>
 constexpr int mego_ppt() { return RNG == RNG_PHILOX ? MGP_PPT_PHILOX : MGP_PPT_MEGORES; }
 

@@ -424,7 +424,9 @@ __device__ __noinline__ int megores_exact_rounds(const ResampleArgs& a, const Of
 }
 
 // One particle per thread (2 or 4 particles per thread, with or without the half split, measured
-// no faster: scripts/mb/mb_mego.cu "z H--- 2 / 2h / 4h").
+// no faster: scripts/mb/mb_mego.cu "z H--- 2 / 2h / 4h"; re-measured after the 2-instruction key
+// add: a half-split kernel with four particles per thread, 30 instead of 32 instructions per
+// comparison, ran 6.64 ms against 6.48, scripts/mb/probe_mh.sh).
 template <bool POW2, bool ROWS = false>
 __global__ void __launch_bounds__(RS_THREADS) k_megopolis_megores_f32(const __grid_constant__ ResampleArgs a,
                                                                      const __grid_constant__ OffChunk oc) {
@@ -1298,7 +1300,7 @@ __global__ void __launch_bounds__(512) k_offq_hist(const uint16_t* __restrict__ 
   __syncthreads();
   const int64_t c0 = (int64_t)b << OFFB_BITS;
   const int nb = (int)min((int64_t)OFFB_BINS, n - c0);
-  if (nb == OFFB_BINS) {
+  if (nb == OFFB_BINS && (reinterpret_cast<uintptr_t>(counts + c0) & 15) == 0) {
     for (int q = threadIdx.x; q < OFFB_BINS / 2; q += 512)
       __stcs(reinterpret_cast<longlong2*>(counts + c0) + q, make_longlong2(bins[2 * q], bins[2 * q + 1]));
   } else {
