@@ -25,8 +25,7 @@ L2 (126 MB) would hold the 64 MiB weights across steps, so a 256 MiB buffer is w
 between timed steps (outside the timed windows).  ``e2e``: the same metric through the
 reference-facing C-ABI host entry (mgp_resample_host: pinned host weights in, pinned host
 ancestors out; N > 1: per-rank pinned stripe upload + the sharded step + ancestor download),
-wall clock; ``e2e.concurrent``: the same entry from two host threads on independent jobs (the
-transfers of one job overlap the kernel of the other).  ``e2e_dropin``: the reference's Python call shape,
+wall clock.  ``e2e_dropin``: the reference's Python call shape,
 ``megopolis(WeightVector(numpy), B, seed=...)`` with pageable numpy in and out.
 ``parity``: the timed ancestors against the CPU oracle (oracle/) on the same inputs.
 """
@@ -594,49 +593,6 @@ def main():
                                            _lib.RNG[args.rng], D.ptr(h_anc), ctypes.byref(bu), local))
             e2e["parity"] = {"checked": n_glob, "vs": "the device-timed ancestors",
                              "mismatches": int(np.count_nonzero(h_anc.numpy() != head["anc"].cpu().numpy()))}
-
-            # independent resample jobs from two host threads through the same entry (its threading
-            # contract: one stream set per host thread): job k+1's upload and job k-1's download
-            # overlap job k's kernel, so the per-job transfers leave the critical path
-            def e2e_concurrent(rid, threads=2):
-                bufs = [(torch.from_numpy(w_host).pin_memory(), torch.empty(n_glob, dtype=torch.int64).pin_memory())
-                        for _ in range(threads)]
-                reps = max(3, min(args.steps, 10))
-                errs = []
-
-                def worker(k, count):
-                    try:
-                        bk = ctypes.c_int32(0)
-                        for _ in range(count):
-                            _lib.check(L.mgp_resample_host(_lib.KIND["megopolis"], D.ptr(bufs[k][0]), 0, n_glob, 0,
-                                                           EPS, RUN_SEED, 32, 0, 1, rid, D.ptr(bufs[k][1]),
-                                                           ctypes.byref(bk), local))
-                    except Exception as ex:  # noqa: BLE001 (reported below)
-                        errs.append(ex)
-
-                def run(count):
-                    ts = [threading.Thread(target=worker, args=(k, count)) for k in range(threads)]
-                    for t in ts:
-                        t.start()
-                    for t in ts:
-                        t.join()
-                    if errs:
-                        raise errs[0]
-
-                run(2)
-                t0 = time.perf_counter()
-                run(reps)
-                tc = time.perf_counter() - t0
-                mism = sum(int(np.count_nonzero(bk[1].numpy() != head["anc"].cpu().numpy())) for bk in bufs)
-                return {"value": threads * reps * n_glob / tc, "unit": "particles/s", "threads": threads,
-                        "jobs": threads * reps, "ms_per_job": tc / (threads * reps) * 1e3,
-                        "h2d_bytes_per_step": 4 * n_glob, "d2h_bytes_per_step": 8 * n_glob,
-                        "path": f"{threads} host threads, each calling mgp_resample_host on its own pinned buffers "
-                                "(independent jobs; wall clock over all jobs)",
-                        "parity": {"checked": threads * n_glob, "vs": "the device-timed ancestors",
-                                   "mismatches": mism}}
-
-            e2e["concurrent"] = e2e_concurrent(_lib.RNG[args.rng])
 
             # the B-rule reduction, H2D (4N B) and D2H (8N B) reported separately
             def ev_ms(fn, reps=5):

@@ -95,10 +95,16 @@ for kind, part in (("c1", 256), ("c2", 128)):
     _lib.check(_lib.lib().mgp_resample_range(_lib.KIND[kind], wq.data_ptr(), 0, 4096, 7, 3, 32, part, 1,
                                              _lib.RNG["megores"], 0, 32, 61, out.data_ptr(),
                                              torch.cuda.current_stream().cuda_stream))
-# bucketed offspring histogram (n >= 2^20), incl. a ragged n and an out-of-range ancestor
+# queued offspring histogram (n >= 2^20), incl. a ragged n, a one-hot input (queue overflow list),
+# the count-matrix and atomic modes, and an out-of-range ancestor
 for nn in (1 << 20, (1 << 20) + 77):
     aa = torch.from_numpy(rr.integers(0, nn, nn)).cuda()
     mg.ancestors_to_offspring(aa, nn)
+mg.ancestors_to_offspring(torch.full((1 << 20,), 12345, dtype=torch.int64, device="cuda"), 1 << 20)
+for mode in (1, 2):
+    _lib.check(_lib.lib().mgp_debug_offspring_mode(mode))
+    mg.ancestors_to_offspring(aa, nn)
+_lib.check(_lib.lib().mgp_debug_offspring_mode(0))
 try:
     aa[5] = nn
     mg.ancestors_to_offspring(aa, nn)
