@@ -118,7 +118,7 @@ def load_peaks():
 
 
 class ClockSampler:
-    """NVML clock / throttle-reason sampling during the timed region."""
+    """NVML clock / throttle-reason / board-power sampling during the timed region."""
 
     REASONS = {
         0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
@@ -127,7 +127,7 @@ class ClockSampler:
     }
 
     def __init__(self, index: int):
-        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.samples, self.reasons, self.max_mhz, self.power_mw = [], set(), None, []
         self._stop = threading.Event()
         try:
             import pynvml
@@ -143,6 +143,7 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.power_mw.append(self.nv.nvmlDeviceGetPowerUsage(self.h))
                 r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.REASONS.items():
                     if r & bit and bit != 0x1:
@@ -165,8 +166,11 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
-        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        out = {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+               "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        if self.power_mw:
+            out["power_w"] = round(statistics.median(self.power_mw) / 1000.0, 1)
+        return out
 
 
 # ---------------------------------------------------------------------------
