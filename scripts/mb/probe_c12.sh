@@ -1,0 +1,11 @@
+# C1/C2 megores: float32 bracket + m_hi-only draws (new) against the float64 path (old); C1/C2 tests
+set -x
+mkdir -p gpurun_out
+cp paper_2109_13504_b200/libmgp.so /tmp/libmgp_keep.so
+for v in c12old c12new; do
+  cp scripts/mb/libmgp_$v.so paper_2109_13504_b200/libmgp.so
+  echo "== $v" >> gpurun_out/c12_time.txt
+  timeout 600 python scripts/mb/c12_time.py >> gpurun_out/c12_time.txt 2>&1
+done
+cp /tmp/libmgp_keep.so paper_2109_13504_b200/libmgp.so
+timeout 1500 python -m pytest tests/test_parity_gpu.py tests/test_reference_suite_gpu.py tests/test_reference_unmodified_gpu.py -q -p no:cacheprovider > gpurun_out/c12_tests.log 2>&1; tail -3 gpurun_out/c12_tests.log
