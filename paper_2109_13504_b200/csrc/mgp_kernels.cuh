@@ -522,6 +522,27 @@ __device__ __forceinline__ uint32_t below_n(uint64_t h_or_word, uint32_t n, uint
   return __umulhi((uint32_t)h_or_word, n);
 }
 
+// C1 / C2 on the megores stream with the exact float64 rule (power-of-two partitions, no zero
+// weight): the fallback of the float32-bracket path below when one of the particle's rounds is
+// ambiguous; C2's per-round partition is drawn directly instead of by the warp's shuffle.
+template <bool C2>
+__device__ __noinline__ uint32_t c12_exact_rounds(const ResampleArgs& a, uint32_t i, uint32_t k, float wk, uint32_t lo) {
+  atomicAdd(&g_megores_fallbacks, 1ull);
+  const float* __restrict__ w = reinterpret_cast<const float*>(a.w);
+  const uint64_t wlane = WARP_LANE_BASE + (i >> 5);
+  uint64_t x = megores_key(a.base, i, 2ull * (uint64_t)a.b0);
+  for (int t = 0; t < a.cnt; ++t) {
+    if (C2) lo = (uint32_t)draw_below<RNG_MEGORES>(a.base, a.seed, wlane, (uint64_t)(a.b0 + t), (int64_t)a.n_part) * a.n_w;
+    const double u = (double)mix64_m53(x) * 0x1p-53;  // u01 (M/rng.py:105-108)
+    x += M_CTR;
+    const uint32_t jl = below_n<RNG_MEGORES>(mix64(x), a.n_w, a.log2, true);
+    x += M_CTR;
+    const float wj = __ldg(w + lo + jl);
+    if (u * (double)wk <= (double)wj) { wk = wj; k = lo + jl; }
+  }
+  return k;
+}
+
 template <int RNG, typename WT, bool POW2, bool NOZERO, bool C2, bool STAGE>
 __global__ void __launch_bounds__(RS_THREADS) k_c12_w32(const __grid_constant__ ResampleArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -547,7 +568,38 @@ __global__ void __launch_bounds__(RS_THREADS) k_c12_w32(const __grid_constant__ 
     }
   }
   uint32_t preg = 0;
-  if constexpr (RNG == RNG_MEGORES) {
+  if constexpr (RNG == RNG_MEGORES && sizeof(WT) == 4 && NOZERO && POW2) {
+    // float32 weights, no zero weight, power-of-two partitions: the float32 bracket of the float64
+    // decision of k_megopolis_megores_f32 (exact re-run of the particle's rounds when a round is
+    // ambiguous), and only the high word m_hi of each draw's second splitmix product: the u draw
+    // needs its top 23 bits, and uint_below(2^k) = h >> (64 - k) reads bits [32 - k, 32) of h's
+    // high word, which equal m_hi's (h = m ^ (m >> 31) changes bit 0 of the high word only).
+    const float wk0 = (float)wk;
+    const uint32_t k0 = k, lo0 = lo, sh = 32u - a.log2;
+    bool amb = false;
+    uint64_t x = megores_key(a.base, i, 2ull * (uint64_t)a.b0);
+#pragma unroll 4
+    for (int t = 0; t < a.cnt; ++t) {
+      if constexpr (C2) {
+        if ((t & 31) == 0)
+          preg = (uint32_t)draw_below<RNG>(a.base, a.seed, wlane, (uint64_t)(a.b0 + t + (int)lane), (int64_t)a.n_part);
+        lo = __shfl_sync(0xffffffffu, preg, t & 31) * n_w;
+      }
+      const uint32_t mu = mix64_mhi(x);  // u at counter 2b
+      x = add64_fma(x, a.one);
+      const uint32_t mj = mix64_mhi(x);  // j at counter 2b + 1
+      x = add64_fma(x, a.one);
+      const uint32_t jl = a.log2 ? mj >> sh : 0u;
+      const float wj = (STAGE && !C2) ? part[jl] : __ldg(w + lo + jl);
+      const float u1 = __uint_as_float(0x3F800000u + (mu >> 9));  // 1 + u23
+      const float flo = __fmaf_rd(u1, wk, -wk);
+      const float fhi = __fmaf_ru(wk, 0x1p-22f, flo);
+      const bool acc = fhi <= wj;
+      amb |= !acc && flo <= wj;
+      if (acc) { wk = wj; k = lo + jl; }
+    }
+    if (amb && live) k = c12_exact_rounds<C2>(a, i, k0, wk0, lo0);
+  } else if constexpr (RNG == RNG_MEGORES) {
     uint64_t x = megores_key(a.base, i, 2ull * (uint64_t)a.b0);
     for (int t = 0; t < a.cnt; ++t) {
       if constexpr (C2) {
