@@ -177,6 +177,16 @@ __device__ __forceinline__ double u1_from_word(uint32_t w) {
   return __hiloint2double((int)((w >> 12) + 0x3FF00000u), (int)(w << 20));
 }
 
+// high word of mix64's second product m = v * MIX2 (mod 2^64), v = z ^ (z >> 27)
+__device__ __forceinline__ uint32_t mix64_mhi(uint64_t x) {
+  x = (x ^ (x >> 30)) * MIX1;
+  x ^= x >> 27;
+  const uint32_t vlo = (uint32_t)x, vhi = (uint32_t)(x >> 32);
+  return __umulhi(vlo, (uint32_t)MIX2) + vlo * (uint32_t)(MIX2 >> 32) + vhi * (uint32_t)MIX2;
+}
+
+__device__ unsigned long long g_megores_fallbacks;  // diagnostic count (mgp_debug_megores_fallbacks)
+
 // ---------------------------------------------------------------------------
 // Megopolis, W = 32 (the hot path).  One particle per thread; the warp's 32 partner
 // weights for round b are one 128-byte line (4 sectors) -- the paper's coalescing.
@@ -385,7 +395,10 @@ __global__ void __launch_bounds__(64, 1) k_megopolis_philox_half(const __grid_co
 //   lo = fl_down((1 + u23) wk - wk) <= u23 wk <= u wk,
 //   hi = fl_up(lo + 2^-22 wk) >= u23 wk + 2^-23 wk > u wk     (lo >= u23 wk - ulp(u23 wk) and
 //        ulp(u23 wk) <= 2^-23 wk).
-// hi <= wj  => u wk <= wj => fl64(u wk) <= wj: accept.
+// hi <  wj  => u wk <= wj => fl64(u wk) <= wj: accept.  The comparison is strict because the
+//              bound hi >= u wk needs 2^-23 wk >= ulp32(u23 wk), which fails for subnormal wk
+//              (spacing 2^-149): there u wk < hi + 2^-149, and hi < wj means wj >= hi + 2^-149
+//              (wj is a float), so u wk < wj still holds.  wj == hi is left to the exact re-run.
 // lo >  wj  => u wk >= lo >= wj + ulp32(wj) > wj + ulp64(wj) / 2 => fl64(u wk) > wj: reject.
 // Otherwise (probability ~2^-21 per comparison) the round is ambiguous: the lane records it,
 // and after the loop every lane that saw one re-runs its rounds with the exact float64 rule
@@ -393,17 +406,9 @@ __global__ void __launch_bounds__(64, 1) k_megopolis_philox_half(const __grid_co
 // needs neither the low half of the second product, the final xorshift, the 64-bit integer
 // conversion (I2F.F64.U64, conversion pipe) nor any float64 instruction: 32.5 instructions
 // per round instead of 38.75 (scripts/mb/mb_mego.cu "z H--- 1u8": 7.82 -> 6.78 ms at 2^24,
-// B = 354).  Subnormal weights are exact too: the FFMAs are IEEE with denormals (no ftz).
+// B = 354).  Subnormal weights are exact too: the FFMAs are IEEE with denormals (no ftz), and the
+// strict accept comparison above covers the bound's one-spacing slack there.
 
-// high word of mix64's second product m = v * MIX2 (mod 2^64), v = z ^ (z >> 27)
-__device__ __forceinline__ uint32_t mix64_mhi(uint64_t x) {
-  x = (x ^ (x >> 30)) * MIX1;
-  x ^= x >> 27;
-  const uint32_t vlo = (uint32_t)x, vhi = (uint32_t)(x >> 32);
-  return __umulhi(vlo, (uint32_t)MIX2) + vlo * (uint32_t)(MIX2 >> 32) + vhi * (uint32_t)MIX2;
-}
-
-__device__ unsigned long long g_megores_fallbacks;  // diagnostic count (mgp_debug_megores_fallbacks)
 
 // One particle's rounds [0, cnt) of a launch with the exact float64 decision; returns the last
 // accepted round (-1: none).  wk is the weight of the particle's state at the launch start.
@@ -445,7 +450,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_megopolis_megores_f32(const __gr
     const float u1 = __uint_as_float(0x3F800000u + (mix64_mhi(x) >> 9));  // 1 + u23
     const float lo = __fmaf_rd(u1, wk, -wk);
     const float hi = __fmaf_ru(wk, 0x1p-22f, lo);
-    const bool acc = hi <= wj;
+    const bool acc = hi < wj;  // strict: see the subnormal note above k_megopolis_megores_f32
     if (!acc && lo <= wj) amb = t;
     if (acc) { wk = wj; bstar = t; }
     // x += M_CTR: ptxas hoists one * M_CTR and splits the add into IADD3 (ALU) + IMAD.X (FMA
@@ -594,7 +599,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_c12_w32(const __grid_constant__ 
       const float u1 = __uint_as_float(0x3F800000u + (mu >> 9));  // 1 + u23
       const float flo = __fmaf_rd(u1, wk, -wk);
       const float fhi = __fmaf_ru(wk, 0x1p-22f, flo);
-      const bool acc = fhi <= wj;
+      const bool acc = fhi < wj;  // strict: see the subnormal note above k_megopolis_megores_f32
       amb |= !acc && flo <= wj;
       if (acc) { wk = wj; k = lo + jl; }
     }
