@@ -1,6 +1,7 @@
 """Wall time of the reference's call shape at 2^24 (megopolis(WeightVector(numpy float32), 354,
 seed), pageable numpy in) with the returned array page-locked (MGP_PINNED_OUTPUT=1, default) or
-plain numpy (0); ancestors compared between the two."""
+plain numpy (0); ancestors compared between the two.  The page-locked variant measured slower and
+was removed, so both modes now run the plain-numpy path."""
 import os
 import sys
 import time
