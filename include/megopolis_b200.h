@@ -281,9 +281,10 @@ int mgp_systematic_oracle(const void *d_w, int dtype, int64_t n, double u, int64
  * Writes 4*n words each; returns the number of mismatching words in *h_mismatch. */
 int mgp_philox_selftest(uint64_t key, uint32_t c1, uint32_t c2, uint32_t c3, int64_t n, int64_t *h_mismatch);
 
-/* Diagnostic: the number of particles whose megores-stream float32 decision bracket was
- * ambiguous in some round and that were re-run with the exact float64 rule (the current device,
- * since the last reset).  reset != 0 zeroes the counter after reading it. */
+/* Diagnostic: the number of particles whose megores-stream float32 decision bracket (Megopolis,
+ * Metropolis-C1 and -C2 on float32 weights) was ambiguous in some round and that were re-run with
+ * the exact float64 rule (the current device, since the last reset).  reset != 0 zeroes the
+ * counter after reading it. */
 int mgp_debug_megores_fallbacks(int64_t *h_count, int reset);
 /* Exact-cumsum resolver profile (16 counters; non-zero only in a -DMGP_PX_PROF build of the
  * library, scripts/mb/px_prof.sh): super windows, chunk windows, crossing chunks, block passes,
