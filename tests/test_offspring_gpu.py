@@ -66,3 +66,17 @@ def test_ragged_and_errors(mg):
     bad[12345] = -3
     with pytest.raises(ValueError):
         mg.ancestors_to_offspring(bad, 1 << 20)
+
+
+def test_queued_histogram_many_buckets(mg):
+    """n > 2^25: more than 2048 buckets (queue reservations stored in shared memory instead of
+    registers) and, at n = 2^27, 8192 buckets with the tile still at 8192 ancestors; skewed inputs
+    so some queues overflow."""
+    rs = np.random.default_rng(99)
+    for n in ((1 << 26) + 12345, 1 << 27):
+        a = rs.integers(0, n, n)
+        a[: n // 4] = rs.integers(0, 1 << 16, n // 4)  # the first 4 buckets take a quarter: overflow
+        got = mg.ancestors_to_offspring(torch.from_numpy(a).cuda(), n)
+        assert np.array_equal(got.cpu().numpy(), np.bincount(a, minlength=n))
+        del got
+        torch.cuda.empty_cache()
