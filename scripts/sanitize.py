@@ -88,6 +88,11 @@ mg.gen_gamma_weights(mg.GammaWeightParams(0.5, 2.0, 777), 4, "double", device="c
 wp = rr.random(1 << 20).astype(np.float32)
 mg.megopolis(mg.WeightVector(wp, "single"), 3, seed=2, rng="philox")  # half-split, staged in and out
 mg.metropolis_c1(mg.WeightVector(wp[:1 << 19], "single"), 3, mg.PartitionConfig(256), seed=2)
+# the megores float32 brackets and their exact re-runs (subnormal multiples of 2^-149: frequent)
+ws = torch.from_numpy(rr.integers(1, 17, 1 << 16).astype(np.float32) * np.float32(2.0 ** -149)).cuda()
+mg.megopolis(mg.WeightVector(ws, "single"), 24, seed=3)
+mg.metropolis_c1(mg.WeightVector(ws, "single"), 24, mg.PartitionConfig(128), seed=3)
+mg.metropolis_c2(mg.WeightVector(ws, "single"), 24, mg.PartitionConfig(128), seed=3)
 for k in range(70):
     mg.megopolis(mg.WeightVector(torch.rand(512, device="cuda"), "single"), 2, seed=k)
 for kind, part in (("c1", 256), ("c2", 128)):
