@@ -1291,7 +1291,7 @@ int mgp_offspring(const int64_t* d_anc, int64_t n_anc, int64_t n, int64_t* d_cou
   // Large histograms: queued (mgp_kernels.cuh k_offq_*): one read of the ancestors, no count pass
   if (n >= MGP_OFFSPRING_I32_MIN && K <= OFFB_KMAX && n_anc > 0 && n_anc <= MAX_N && mode == 0 &&
       (((uintptr_t)d_anc) & 15) == 0 && K * (2 * ((n_anc + K - 1) / K) + 1032) < (1ll << 31)) {
-    constexpr int THR = 512, PER = 16;
+    constexpr int THR = MGP_OFFQ_THR, PER = MGP_OFFQ_PER;
     constexpr int64_t TILE = (int64_t)PER * THR;
     const bool small_k = 20 * K + 16 + 4 * TILE <= 200 * 1024;  // shared memory per CTA, else half tiles
     const int64_t tile = small_k ? TILE : TILE / 2;

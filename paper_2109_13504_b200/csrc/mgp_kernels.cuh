@@ -1201,17 +1201,28 @@ __global__ void __launch_bounds__(512) k_offb_hist(const uint16_t* __restrict__ 
 //                    warp-aggregated int64 atomics into the finished counts.
 // HBM traffic per call: 8N (ancestors, read once) + 8N (counts) = the algorithmic 16N; the 2N-byte
 // queues stay in L2.
+// three 512-thread CTAs per SM (registers capped at 40, a few bytes of spill): 0.123 -> 0.109 ms at
+// 2^24 against two per SM (scripts/mb/probe_oq.sh: 4 per SM or 256-/384-thread CTAs were slower)
+#ifndef MGP_OFFQ_MINB
+#define MGP_OFFQ_MINB 3
+#endif
+#ifndef MGP_OFFQ_THR
+#define MGP_OFFQ_THR 512
+#endif
+#ifndef MGP_OFFQ_PER
+#define MGP_OFFQ_PER 16
+#endif
 constexpr int OFFQ_DEFER = 4;                 // queue reservations held in registers per thread (K <= 4 * THREADS)
 constexpr uint32_t OFFQ_SPILL = 0xFFFFFFFFu;  // run reaching past its queue's capacity
 
 // One tile of PER * THREADS ancestors per CTA, read with 16-byte loads held in registers.  Invalid
 // (out-of-range) ancestors go to a trash bucket K so that every per-element step is branch-free.
-// (Measured alternatives, scripts/mb/probe_offq*.sh: persistent CTAs streaming the next tiles
-// through a two-slot shared-memory ring by bulk copy (TMA) 0.138-0.155 ms; 32 ancestors per
-// thread, 256-thread CTAs, 2-4 CTAs per SM forced: 0.130-0.170 ms; the queue loads of
-// k_offq_hist batched four per thread: 0.180 ms.  This shape: 0.130 ms.)
+// (Measured alternatives, scripts/mb/probe_offq*.sh, probe_oq.sh: persistent CTAs streaming the
+// next tiles through a two-slot shared-memory ring by bulk copy (TMA) 0.138-0.155 ms; 32 ancestors
+// per thread 0.13-0.17 ms; the queue loads of k_offq_hist batched four per thread: 0.180 ms.  This
+// shape with three CTAs per SM: 0.109 ms.)
 template <int THREADS, int PER>
-__global__ void __launch_bounds__(THREADS) k_offq_scatter(const int64_t* __restrict__ anc, int64_t n_anc, int64_t n,
+__global__ void __launch_bounds__(THREADS, MGP_OFFQ_MINB) k_offq_scatter(const int64_t* __restrict__ anc, int64_t n_anc, int64_t n,
                                                           int K, uint32_t cap, uint32_t* __restrict__ gcur,
                                                           uint16_t* __restrict__ queue, uint32_t* __restrict__ novf,
                                                           uint32_t* __restrict__ ovf, int* bad) {
