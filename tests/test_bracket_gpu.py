@@ -114,3 +114,27 @@ def test_bracket_accept_bound_is_strict(mg, kind):
     assert want[i] == i
     assert got[i] == i and np.array_equal(got, want)
     assert fallbacks() > 0
+
+
+@pytest.mark.parametrize("kind", ["megopolis", "c1", "c2"])
+def test_bracket_multi_launch(mg, kind):
+    """B > 1024: the bracket paths across several launches (the carried ancestor state, the round
+    counters of each launch's exact re-run), on weights with a tight bracket (subnormal multiples)
+    and on ordinary ones, device and host entries."""
+    from oracle import oracle as ora
+
+    n = 1 << 12
+    for w in (subnormal_weights(n, 5), (np.random.default_rng(6).random(n) ** 4 + 1e-3).astype(np.float32)):
+        for b in (1025, 2049):
+            if kind == "megopolis":
+                want = ora.megopolis(w, b, seed=b)
+                got_h = mg.megopolis(w, b, seed=b)
+                got_d = mg.megopolis(mg.WeightVector(torch.from_numpy(w).cuda(), "single"), b, seed=b)
+            else:
+                fn = mg.metropolis_c1 if kind == "c1" else mg.metropolis_c2
+                ofn = ora.metropolis_c1 if kind == "c1" else ora.metropolis_c2
+                want = ofn(w, b, 128, seed=b)
+                got_h = fn(w, b, mg.PartitionConfig(128), seed=b)
+                got_d = fn(mg.WeightVector(torch.from_numpy(w).cuda(), "single"), b, mg.PartitionConfig(128), seed=b)
+            assert np.array_equal(got_h, want), (kind, b, "host")
+            assert np.array_equal(got_d.cpu().numpy(), want), (kind, b, "device")
