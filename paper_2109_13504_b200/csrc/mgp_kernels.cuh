@@ -1201,7 +1201,7 @@ __global__ void __launch_bounds__(512) k_offb_hist(const uint16_t* __restrict__ 
 //                    warp-aggregated int64 atomics into the finished counts.
 // HBM traffic per call: 8N (ancestors, read once) + 8N (counts) = the algorithmic 16N; the 2N-byte
 // queues stay in L2.
-// three 512-thread CTAs per SM (registers capped at 40, a few bytes of spill): 0.123 -> 0.109 ms at
+// three 512-thread CTAs per SM (registers capped at 40, no spill with OFFQ_DEFER = 2): 0.123 -> 0.109 ms at
 // 2^24 against two per SM (scripts/mb/probe_oq.sh: 4 per SM or 256-/384-thread CTAs were slower)
 #ifndef MGP_OFFQ_MINB
 #define MGP_OFFQ_MINB 3
@@ -1212,7 +1212,7 @@ __global__ void __launch_bounds__(512) k_offb_hist(const uint16_t* __restrict__ 
 #ifndef MGP_OFFQ_PER
 #define MGP_OFFQ_PER 16
 #endif
-constexpr int OFFQ_DEFER = 4;                 // queue reservations held in registers per thread (K <= 4 * THREADS)
+constexpr int OFFQ_DEFER = 2;                 // queue reservations held in registers per thread (K <= 2 * THREADS)
 constexpr uint32_t OFFQ_SPILL = 0xFFFFFFFFu;  // run reaching past its queue's capacity
 
 // One tile of PER * THREADS ancestors per CTA, read with 16-byte loads held in registers.  Invalid
