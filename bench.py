@@ -25,7 +25,9 @@ L2 (126 MB) would hold the 64 MiB weights across steps, so a 256 MiB buffer is w
 between timed steps (outside the timed windows).  ``e2e``: the same metric through the
 reference-facing C-ABI host entry (mgp_resample_host: pinned host weights in, pinned host
 ancestors out; N > 1: per-rank pinned stripe upload + the sharded step + ancestor download),
-wall clock.  ``e2e_dropin``: the reference's Python call shape,
+wall clock; ``e2e.batched``: independent jobs through the pipelined batch entry
+(mgp_resample_host_batch; each job's copies overlap the neighbouring jobs' kernels).
+``e2e_dropin``: the reference's Python call shape,
 ``megopolis(WeightVector(numpy), B, seed=...)`` with pageable numpy in and out.
 ``parity``: the timed ancestors against the CPU oracle (oracle/) on the same inputs.
 """
@@ -597,6 +599,37 @@ def main():
                                            _lib.RNG[args.rng], D.ptr(h_anc), ctypes.byref(bu), local))
             e2e["parity"] = {"checked": n_glob, "vs": "the device-timed ancestors",
                              "mismatches": int(np.count_nonzero(h_anc.numpy() != head["anc"].cpu().numpy()))}
+
+            # independent jobs through the pipelined batch entry (mgp_resample_host_batch): job k+1's
+            # upload and job k-1's download overlap job k's kernel; every job still uploads its
+            # 4N bytes and downloads its 8N bytes inside the timed region
+            def e2e_batched(rid, count=8):
+                outs = [torch.empty(n_glob, dtype=torch.int64).pin_memory() for _ in range(2)]
+                hw = (ctypes.c_void_p * count)(*([D.ptr(h_w)] * count))
+                ha = (ctypes.c_void_p * count)(*[D.ptr(outs[k & 1]) for k in range(count)])
+                sd = (ctypes.c_uint64 * count)(*([RUN_SEED] * count))
+                bu = (ctypes.c_int32 * count)()
+
+                def batch():
+                    _lib.check(L.mgp_resample_host_batch(_lib.KIND["megopolis"], hw, 0, n_glob, count, 0, EPS, sd, 32,
+                                                         0, 1, rid, ha, bu, local))
+
+                batch()
+                ts = []
+                for _ in range(3):
+                    t0 = time.perf_counter()
+                    batch()
+                    ts.append(time.perf_counter() - t0)
+                tb = statistics.median(ts)
+                mism = sum(int(np.count_nonzero(o.numpy() != head["anc"].cpu().numpy())) for o in outs)
+                return {"value": count * n_glob / tb, "unit": "particles/s", "jobs": count,
+                        "ms_per_job": tb / count * 1e3, "h2d_bytes_per_step": 4 * n_glob, "d2h_bytes_per_step": 8 * n_glob,
+                        "path": f"mgp_resample_host_batch: {count} independent jobs (pinned host weights in, pinned "
+                                "ancestors out), uploads/downloads overlapped with the neighbouring jobs' kernels; "
+                                "wall clock over the batch, median of 3",
+                        "parity": {"checked": 2 * n_glob, "vs": "the device-timed ancestors", "mismatches": mism}}
+
+            e2e["batched"] = e2e_batched(_lib.RNG[args.rng])
 
             # the B-rule reduction, H2D (4N B) and D2H (8N B) reported separately
             def ev_ms(fn, reps=5):

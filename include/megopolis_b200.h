@@ -172,6 +172,15 @@ int mgp_resample_host(int kind, const void *h_w, int dtype, int64_t n, int32_t b
                       int32_t warp, int32_t partition_bytes, int strict, int rng, int64_t *h_anc, int32_t *b_used,
                       int device);
 
+/* Independent resamples of `count` host weight vectors of n elements (h_w[k] -> h_anc[k], seeds[k];
+ * b <= 0: each job's B from epsilon, reported in b_used[k]), pipelined over two device buffer slots:
+ * job k+1's upload and statistics and job k-1's download overlap job k's kernel.  Same ancestors
+ * as `count` calls of mgp_resample_host.  The overlap needs page-locked host buffers (pageable ones
+ * are correct, their copies synchronous).  Output buffers may repeat every other job. */
+int mgp_resample_host_batch(int kind, const void *const *h_w, int dtype, int64_t n, int32_t count, int32_t b,
+                            double epsilon, const uint64_t *seeds, int32_t warp, int32_t partition_bytes, int strict,
+                            int rng, int64_t *const *h_anc, int32_t *b_used, int device);
+
 /* ancestors_to_offspring (M/resample.py:361-368): d_counts[j] = #{i : anc[i] == j};
  * *d_bad set to 1 if an ancestor is outside [0, n) (the reference's ValueError). */
 int mgp_offspring(const int64_t *d_anc, int64_t n_anc, int64_t n, int64_t *d_counts, int32_t *d_bad,

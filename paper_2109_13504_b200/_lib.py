@@ -49,6 +49,8 @@ SIGNATURES = {
     "mgp_resample_stripes": (_i32, [_i32, _vp, _i32, _i64, _i32, _u64, _i32, _i32, _i32, _i32, _i32, _i64, _i64,
                                      _vp, _vp]),
     "mgp_resample_host": (_i32, [_i32, _vp, _i32, _i64, _i32, _dbl, _u64, _i32, _i32, _i32, _i32, _vp, _vp, _i32]),
+    "mgp_resample_host_batch": (_i32, [_i32, _vp, _i32, _i64, _i32, _i32, _dbl, _vp, _i32, _i32, _i32, _i32, _vp, _vp,
+                                       _i32]),
     "mgp_offspring": (_i32, [_vp, _i64, _i64, _vp, _vp, _vp]),
     "mgp_expected_offspring": (_i32, [_vp, _i32, _i64, _vp, _vp, _vp]),
     "mgp_expected_offspring_slice": (_i32, [_vp, _i32, _i64, _i64, _dbl, _vp, _vp]),

@@ -1268,6 +1268,105 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
   return 0;
 }
 
+// Independent resamples of `count` host weight vectors, pipelined across two device buffer slots:
+// job k's upload and statistics run on st2 while job k-1's kernel runs on st, and job k-1's
+// download runs on cp while job k's kernel runs.  The host round trip for B (the reference derives
+// it on the host) happens while the previous kernel is still running, so consecutive kernels are
+// queued back to back.  Same ancestors as `count` calls of mgp_resample_host.
+int mgp_resample_host_batch(int kind, const void* const* h_w, int dtype, int64_t n, int32_t count, int32_t b,
+                            double epsilon, const uint64_t* seeds, int32_t warp, int32_t partition_bytes, int strict,
+                            int rng, int64_t* const* h_anc, int32_t* b_used, int device) {
+  if (count < 0) return set_err(MGP_EINVAL, "count must be non-negative");
+  if (count == 0) return 0;
+  if (!h_w || !h_anc || !seeds) return set_err(MGP_EINVAL, "null pointer");
+  if (dtype != MGP_F32 && dtype != MGP_F64) return set_err(MGP_EINVAL, "dtype must be MGP_F32 or MGP_F64");
+  if (n < 1) return set_err(MGP_EINVAL, "weights must be a non-empty 1-d sequence");
+  if (n > MAX_N) return set_err(MGP_EUNSUPPORTED, "N exceeds 2^31-1");
+  for (int32_t k = 0; k < count; ++k)
+    if (!h_w[k] || !h_anc[k]) return set_err(MGP_EINVAL, "null pointer (job %d)", (int)k);
+  struct DeviceGuard {
+    int prev = -1;
+    ~DeviceGuard() {
+      if (prev >= 0) cudaSetDevice(prev);
+    }
+  } guard;
+  if (device >= 0) {
+    CUDA_TRY(cudaGetDevice(&guard.prev));
+    CUDA_TRY(cudaSetDevice(device));
+  }
+  HostCtx* hc = nullptr;
+  if (int rc0 = host_ctx(&hc)) return rc0;
+  cudaStream_t st = hc->st, st2 = hc->st2, cp = hc->cp;
+  const size_t wbytes = (size_t)n * (dtype == MGP_F32 ? 4 : 8);
+  void* d_w[2] = {nullptr, nullptr};
+  int64_t* d_anc[2] = {nullptr, nullptr};
+  mgp_weight_stats_t* d_stats[2] = {nullptr, nullptr};
+  cudaEvent_t kern_done[2] = {hc->ev[0], hc->ev[1]}, d2h_done[2] = {hc->ev[2], hc->ev[3]};
+  Plan plans[2];
+  int rc = 0;
+  auto cleanup = [&]() {
+    cudaStreamSynchronize(cp);
+    cudaStreamSynchronize(st2);
+    cudaStreamSynchronize(st);
+    for (int q = 0; q < 2; ++q) {
+      if (d_w[q]) cudaFreeAsync(d_w[q], st);
+      if (d_anc[q]) cudaFreeAsync(d_anc[q], st);
+      if (d_stats[q]) cudaFreeAsync(d_stats[q], st);
+      plan_free(plans[q], st);
+    }
+    cudaStreamSynchronize(st);
+  };
+#define BTRY(x)                           \
+  do {                                    \
+    rc = (x);                             \
+    if (rc) { cleanup(); return rc; }     \
+  } while (0)
+#define BCUDA(x)                                                              \
+  do {                                                                        \
+    cudaError_t e_ = (x);                                                     \
+    if (e_ != cudaSuccess) { rc = cuda_err(e_, #x); cleanup(); return rc; }   \
+  } while (0)
+  for (int q = 0; q < 2 && q < count; ++q) {
+    BCUDA(pool_malloc(&d_w[q], wbytes, st));
+    BCUDA(pool_malloc(&d_anc[q], sizeof(int64_t) * n, st));
+    BCUDA(pool_malloc(&d_stats[q], sizeof(mgp_weight_stats_t), st));
+  }
+  BCUDA(cudaStreamSynchronize(st));  // the slots exist before st2 / cp use them
+  for (int32_t k = 0; k < count; ++k) {
+    const int q = k & 1;
+    if (k >= 2) {
+      BCUDA(cudaStreamWaitEvent(st2, kern_done[q], 0));  // job k-2's kernel has read d_w[q]
+      BCUDA(cudaStreamWaitEvent(st, d2h_done[q], 0));    // job k-2's download has read d_anc[q]
+      BTRY(plan_free(plans[q], st));
+    }
+    BCUDA(cudaMemcpyAsync(d_w[q], h_w[k], wbytes, cudaMemcpyHostToDevice, st2));
+    BTRY(mgp_weight_stats(d_w[q], dtype, n, d_stats[q], st2));
+    mgp_weight_stats_t hs{};
+    BCUDA(cudaMemcpyAsync(&hs, d_stats[q], sizeof hs, cudaMemcpyDeviceToHost, st2));
+    BCUDA(cudaStreamSynchronize(st2));  // job k's weights are on the device and checked
+    if (hs.n_nonfinite) { rc = set_err(MGP_EINVAL, "weights must be finite (job %d)", (int)k); cleanup(); return rc; }
+    if (hs.n_neg) { rc = set_err(MGP_EINVAL, "weights must be non-negative (job %d)", (int)k); cleanup(); return rc; }
+    if (hs.n_pos == 0) { rc = set_err(MGP_EINVAL, "all weights are zero (job %d)", (int)k); cleanup(); return rc; }
+    int32_t bk = b;
+    if (bk <= 0) BTRY(mgp_compute_iterations(epsilon, hs.mean, hs.max, &bk));
+    if (b_used) b_used[k] = bk;
+    const int flags = (hs.n_zero == 0) ? MGP_FLAG_NONZERO : 0;
+    BTRY(make_plan(plans[q], kind, d_w[q], dtype, n, bk, seeds[k], warp, partition_bytes, strict, rng, flags));
+    BTRY(plan_alloc(plans[q], st));
+    BTRY(run_range(plans[q], 0, n, d_anc[q], st));
+    BCUDA(cudaEventRecord(kern_done[q], st));
+    BCUDA(cudaStreamWaitEvent(cp, kern_done[q], 0));
+    BCUDA(cudaMemcpyAsync(h_anc[k], d_anc[q], sizeof(int64_t) * n, cudaMemcpyDeviceToHost, cp));
+    BCUDA(cudaEventRecord(d2h_done[q], cp));
+  }
+  BCUDA(cudaStreamSynchronize(cp));
+  BCUDA(cudaStreamSynchronize(st));
+  cleanup();
+#undef BTRY
+#undef BCUDA
+  return 0;
+}
+
 #ifndef MGP_OFFSPRING_I32_MIN
 #define MGP_OFFSPRING_I32_MIN (1ll << 20)
 #endif

@@ -162,6 +162,40 @@ def _resample(kind, w, b, seed, warp, part, strict, rng, name):
     return out
 
 
+def resample_batch(kind: str, weights, b: int, seeds, warp: WarpConfig = WarpConfig(), part=None,
+                   strict: bool = True, *, rng: str = "megores", epsilon: float = 0.01, out=None):
+    """Independent host-buffer resamples (the reference's call shape repeated over a batch, e.g. the
+    repetitions of a quality grid point), pipelined on the device: job k+1's upload and job k-1's
+    download overlap job k's kernel (mgp_resample_host_batch).  ``weights``: numpy arrays of one
+    length and dtype (page-locked ones give the overlap); ``b <= 0`` derives each job's B from
+    ``epsilon``.  Returns (ancestor arrays, B per job); the same ancestors as one
+    ``make_resampler(kind)`` call per job.  ``out``: optional output arrays (may repeat every other
+    job)."""
+    D.require_cuda()
+    kind = {"metropolis_c1": "c1", "metropolis_c2": "c2", "systematic_improved": "systematic"}.get(kind, kind)
+    vals = [np.ascontiguousarray(getattr(w, "values", w)) for w in weights]
+    seeds = [int(s) & (2**64 - 1) for s in seeds]
+    if len(seeds) != len(vals):
+        raise ValueError(f"{len(vals)} weight vectors but {len(seeds)} seeds")
+    if not vals:
+        return [], []
+    n, dt = len(vals[0]), vals[0].dtype
+    if any(len(v) != n or v.dtype != dt for v in vals):
+        raise ValueError("every weight vector of a batch must have the same length and dtype")
+    outs = list(out) if out is not None else [np.empty(n, dtype=np.int64) for _ in vals]
+    if len(outs) != len(vals) or any(o.dtype != np.int64 or len(o) != n or not o.flags.c_contiguous for o in outs):
+        raise ValueError("out must hold one contiguous int64 array of N elements per job")
+    pb = abi_partition_bytes(part.partition_bytes, warp) if part is not None else 0
+    k = len(vals)
+    hw = (ctypes.c_void_p * k)(*[v.ctypes.data for v in vals])
+    ha = (ctypes.c_void_p * k)(*[o.ctypes.data for o in outs])
+    sd = (ctypes.c_uint64 * k)(*seeds)
+    bu = (ctypes.c_int32 * k)()
+    _lib.check(_lib.lib().mgp_resample_host_batch(_lib.KIND[kind], hw, D.wdtype(vals[0]), n, k, int(b), float(epsilon),
+                                                  sd, warp.warp_size, pb, int(bool(strict)), _rng(rng), ha, bu, -1))
+    return outs, [int(x) for x in bu]
+
+
 def metropolis(w, b: int, seed, *, rng: str = "megores"):
     """Independent per-particle random comparisons; fully random access (M/resample.py:201-206)."""
     return _resample("metropolis", w, b, seed, None, None, False, rng, "metropolis")
