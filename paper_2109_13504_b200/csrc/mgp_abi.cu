@@ -13,6 +13,7 @@
 #include <cstring>
 #include <string>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <deque>
 #include <functional>
@@ -791,8 +792,15 @@ class HostPool {
     Ticket left;
   };
   HostPool() {
+    // Half the hardware threads, at most 8.  A pool as wide as the machine (16 workers on the 16
+    // vCPUs of the B200 boxes) slows the staged downloads to ~9 GB/s: the drop-in call at 2^24
+    // takes 21-27 ms (bimodal) instead of 7.6, even when only 8 of the 16 workers take copy
+    // pieces (the rest are woken and compete with the thread driving the copy engine and the
+    // driver's threads).  4 workers: 7.3-9.4 ms (scripts/mb/dropin_threads.sh).  The weight
+    // validation pass costs 1.4 ms at 8 workers against 0.8 at 16.  MGP_HOST_THREADS overrides.
     const unsigned hw = std::thread::hardware_concurrency();
-    nthreads_ = (int)std::max(2u, std::min(hw ? hw : 4u, 16u));
+    nthreads_ = (int)std::max(2u, std::min((hw ? hw : 4u) / 2, 8u));
+    if (const char* e = getenv("MGP_HOST_THREADS")) nthreads_ = std::max(1, std::min(64, atoi(e)));
     for (int t = 0; t < nthreads_ - 1; ++t) th_.emplace_back([this] { run(); });
   }
   ~HostPool() {
@@ -873,17 +881,32 @@ int stage_ready(HostCtx* c) {
 
 // pageable h_src -> device, through the staging slots on stream st (returns after the last
 // slot is queued; the DMA of slot k overlaps the host copy into slot k+1)
+// MGP_HOST_TRACE=1: per-call phase times of the staged copies on stderr (probes only)
+static bool host_trace() {
+  static const bool on = getenv("MGP_HOST_TRACE") != nullptr;
+  return on;
+}
+static double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 int staged_h2d(HostCtx* c, void* d_dst, const void* h_src, size_t n, cudaStream_t st) {
   if (int rc = stage_ready(c)) return rc;
+  const bool tr = host_trace();
+  double t_ev = 0, t_cp = 0, t0 = tr ? now_ms() : 0;
   int k = 0;
   for (size_t off = 0; off < n; off += STAGE_SLOT, k = (k + 1) % STAGE_SLOTS) {
     const size_t len = std::min(STAGE_SLOT, n - off);
     char* slot = c->stage + (size_t)k * STAGE_SLOT;
+    double ta = tr ? now_ms() : 0;
     CUDA_TRY(cudaEventSynchronize(c->slot_ev[k]));  // the slot's previous DMA has drained
+    double tb = tr ? now_ms() : 0;
     HostPool::get().copy(slot, (const char*)h_src + off, len);
+    if (tr) { const double tc = now_ms(); t_ev += tb - ta; t_cp += tc - tb; }
     CUDA_TRY(cudaMemcpyAsync((char*)d_dst + off, slot, len, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaEventRecord(c->slot_ev[k], st));
   }
+  if (tr) fprintf(stderr, "[mgp trace] staged_h2d %zu B: %.2f ms (slot waits %.2f, host copies %.2f)\n", n, now_ms() - t0, t_ev, t_cp);
   return 0;
 }
 
@@ -912,13 +935,33 @@ int staged_d2h(HostCtx* c, void* h_dst, const void* d_src, const std::vector<Sta
     if (e != cudaSuccess) return e;
     return cudaEventRecord(c->slot_ev[k], cp);
   };
+  const bool tr = host_trace();
+  cudaEvent_t td[2] = {};  // trace: DMA span on cp
+  if (tr) {
+    for (auto& e : td) cudaEventCreate(&e);
+    cudaEventRecord(td[0], cp);
+  }
   for (; issued < segs.size() && issued < (size_t)STAGE_SLOTS - 1; ++issued) CUDA_TRY(issue(issued));
+  double t0 = tr ? now_ms() : 0, t_ev = 0, t_cp = 0, t_first = 0;
   HostPool::get().wait(faulted);  // the output's pages are resident before the first host copy
+  const double t_fault = tr ? now_ms() - t0 : 0;
   for (size_t q = 0; q < segs.size(); ++q) {
     if (issued < segs.size()) CUDA_TRY(issue(issued++));  // keep the next slots' DMAs in flight
     const int k = (int)(q % STAGE_SLOTS);
+    double ta = tr ? now_ms() : 0;
     CUDA_TRY(cudaEventSynchronize(c->slot_ev[k]));
+    double tb = tr ? now_ms() : 0;
     HostPool::get().copy((char*)h_dst + segs[q].dst, c->stage + (size_t)k * STAGE_SLOT, segs[q].len);
+    if (tr) { const double tc = now_ms(); t_ev += tb - ta; t_cp += tc - tb; if (q == 0) t_first = tb - t0; }
+  }
+  if (tr) {
+    float dm = 0;
+    cudaEventRecord(td[1], cp);
+    cudaEventSynchronize(td[1]);
+    cudaEventElapsedTime(&dm, td[0], td[1]);
+    for (auto& e : td) cudaEventDestroy(e);
+    fprintf(stderr, "[mgp trace] staged_d2h %zu segs: %.2f ms (prefault wait %.2f, first slot ready %.2f, slot waits %.2f, host copies %.2f; cp stream span %.2f ms)\n",
+            segs.size(), now_ms() - t0, t_fault, t_first, t_ev, t_cp, dm);
   }
   return 0;
 }
@@ -1220,6 +1263,11 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
     cudaEvent_t ready = new_event();
     HCUDA(cudaEventRecord(ready, st));
     HCUDA(cudaStreamWaitEvent(st2, ready, 0));
+    cudaEvent_t tk[3] = {};  // MGP_HOST_TRACE: kernel span (start, last chunk on st, on st2)
+    if (host_trace()) {
+      for (auto& e : tk) cudaEventCreate(&e);
+      cudaEventRecord(tk[0], st);
+    }
     int k = 0;
     for (int64_t c0 = 0; c0 < half; c0 += step, ++k) {
       const int64_t c1 = std::min(half, c0 + step);
@@ -1230,10 +1278,18 @@ int mgp_resample_host(int kind, const void* h_w, int dtype, int64_t n, int32_t b
       HCUDA(d2h(c0, c0, c1 - c0, ev));
       HCUDA(d2h(half + c0, half + c0, c1 - c0, ev));
     }
+    if (tk[0]) { cudaEventRecord(tk[1], st); cudaEventRecord(tk[2], st2); }
     HTRY(flush_pending());
     HCUDA(cudaStreamSynchronize(cp));
     HCUDA(cudaStreamSynchronize(st2));
     HCUDA(cudaStreamSynchronize(st));
+    if (tk[0]) {
+      float a = 0, b2 = 0;
+      cudaEventElapsedTime(&a, tk[0], tk[1]);
+      cudaEventElapsedTime(&b2, tk[0], tk[2]);
+      fprintf(stderr, "[mgp trace] chunk kernels: %.2f ms (st), %.2f ms (st2) after the upload\n", a, b2);
+      for (auto& e : tk) cudaEventDestroy(e);
+    }
     cleanup();
     return 0;
   }
