@@ -1434,18 +1434,19 @@ static std::atomic<int> g_offspring_mode{0};
 int mgp_offspring(const int64_t* d_anc, int64_t n_anc, int64_t n, int64_t* d_counts, int32_t* d_bad, void* stream) {
   if (n < 0 || n_anc < 0) return set_err(MGP_EINVAL, "negative size");
   cudaStream_t st = S(stream);
-  if (d_bad) CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int32_t), st));
-  Scratch sc(st);
-  int32_t* bad = d_bad;
-  if (!bad && n_anc) CUDA_TRY(sc.alloc(&bad, sizeof(int32_t)));
-  const unsigned grid = (unsigned)((n_anc + 255) / 256);
   // Large histograms: bucketed (no per-particle global atomics; mgp_kernels.cuh k_offb_*)
   const int64_t K = (n + OFFB_BINS - 1) / OFFB_BINS;
   const int64_t tiles = (n_anc + OFFB_TILE - 1) / OFFB_TILE;
   const int mode = g_offspring_mode.load();
+  const bool queued = n >= MGP_OFFSPRING_I32_MIN && K <= OFFB_KMAX && n_anc > 0 && n_anc <= MAX_N && mode == 0 &&
+                      (((uintptr_t)d_anc) & 15) == 0 && K * (2 * ((n_anc + K - 1) / K) + 1032) < (1ll << 31);
+  if (d_bad && !(queued && MGP_OFFQ_PDL)) CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int32_t), st));
+  Scratch sc(st);
+  int32_t* bad = d_bad;
+  if (!bad && n_anc) CUDA_TRY(sc.alloc(&bad, sizeof(int32_t)));
+  const unsigned grid = (unsigned)((n_anc + 255) / 256);
   // Large histograms: queued (mgp_kernels.cuh k_offq_*): one read of the ancestors, no count pass
-  if (n >= MGP_OFFSPRING_I32_MIN && K <= OFFB_KMAX && n_anc > 0 && n_anc <= MAX_N && mode == 0 &&
-      (((uintptr_t)d_anc) & 15) == 0 && K * (2 * ((n_anc + K - 1) / K) + 1032) < (1ll << 31)) {
+  if (queued) {
     constexpr int THR = MGP_OFFQ_THR, PER = MGP_OFFQ_PER;
     constexpr int64_t TILE = (int64_t)PER * THR;
     const bool small_k = 20 * K + 16 + 4 * TILE <= 200 * 1024;  // shared memory per CTA, else half tiles
@@ -1458,8 +1459,43 @@ int mgp_offspring(const int64_t* d_anc, int64_t n_anc, int64_t n, int64_t* d_cou
     CUDA_TRY(sc.alloc(&ctr, sizeof(uint32_t) * (K + 1)));
     CUDA_TRY(sc.alloc(&ovf, sizeof(uint32_t) * n_anc));
     CUDA_TRY(sc.alloc(&queue, sizeof(uint16_t) * (size_t)K * cap));
-    CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(uint32_t) * (K + 1), st));
     const size_t ssm = 20 * K + 16 + 4 * tile;
+    const size_t hsm = sizeof(uint32_t) * OFFB_BINS;
+    CUDA_TRY(cudaFuncSetAttribute(k_offq_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+#if MGP_OFFQ_PDL
+    // k_offq_zero (cursors, overflow length, the caller's flag), then each kernel launched as a
+    // programmatic dependent of the one before: the scatter's tile loads overlap the zeroing and
+    // the launch gaps disappear (mgp_kernels.cuh, MGP_OFFQ_PDL)
+    k_offq_zero<<<1, 1024, 0, st>>>(ctr, (int)K + 1, d_bad);
+    LAUNCH_CHECK("k_offq_zero");
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3((unsigned)qt);
+    lc.blockDim = dim3(THR);
+    lc.dynamicSmemBytes = ssm;
+    lc.stream = st;
+    lc.attrs = pdl;
+    lc.numAttrs = 1;
+    if (small_k) {
+      CUDA_TRY(cudaFuncSetAttribute(k_offq_scatter<THR, PER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+      CUDA_TRY(cudaLaunchKernelEx(&lc, k_offq_scatter<THR, PER>, d_anc, n_anc, n, (int)K, cap, ctr, queue, ctr + K, ovf, bad));
+    } else {
+      CUDA_TRY(cudaFuncSetAttribute(k_offq_scatter<THR, PER / 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+      CUDA_TRY(cudaLaunchKernelEx(&lc, k_offq_scatter<THR, PER / 2>, d_anc, n_anc, n, (int)K, cap, ctr, queue, ctr + K, ovf,
+                                  bad));
+    }
+    lc.gridDim = dim3((unsigned)K);
+    lc.blockDim = dim3(512);
+    lc.dynamicSmemBytes = hsm;
+    CUDA_TRY(cudaLaunchKernelEx(&lc, k_offq_hist, (const uint16_t*)queue, cap, (const uint32_t*)ctr, n, d_counts));
+    lc.gridDim = dim3(148 * 2);
+    lc.blockDim = dim3(256);
+    lc.dynamicSmemBytes = 0;
+    CUDA_TRY(cudaLaunchKernelEx(&lc, k_offq_overflow, (const uint32_t*)ovf, (const uint32_t*)(ctr + K), d_counts));
+#else
+    CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(uint32_t) * (K + 1), st));
     if (small_k) {
       CUDA_TRY(cudaFuncSetAttribute(k_offq_scatter<THR, PER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
       k_offq_scatter<THR, PER><<<(unsigned)qt, THR, ssm, st>>>(d_anc, n_anc, n, (int)K, cap, ctr, queue, ctr + K, ovf, bad);
@@ -1469,12 +1505,11 @@ int mgp_offspring(const int64_t* d_anc, int64_t n_anc, int64_t n, int64_t* d_cou
                                                                    bad);
     }
     LAUNCH_CHECK("k_offq_scatter");
-    const size_t hsm = sizeof(uint32_t) * OFFB_BINS;
-    CUDA_TRY(cudaFuncSetAttribute(k_offq_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
     k_offq_hist<<<(unsigned)K, 512, hsm, st>>>(queue, cap, ctr, n, d_counts);
     LAUNCH_CHECK("k_offq_hist");
     k_offq_overflow<<<148 * 2, 256, 0, st>>>(ovf, ctr + K, d_counts);
     LAUNCH_CHECK("k_offq_overflow");
+#endif
     return 0;
   }
   if (n >= MGP_OFFSPRING_I32_MIN && K <= OFFB_KMAX && n_anc > 0 && n_anc <= MAX_N && K * tiles < (1ll << 30) &&

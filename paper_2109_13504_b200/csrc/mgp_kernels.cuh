@@ -1203,6 +1203,11 @@ __global__ void __launch_bounds__(512) k_offb_hist(const uint16_t* __restrict__ 
 // queues stay in L2.
 // three 512-thread CTAs per SM (registers capped at 40, no spill with OFFQ_DEFER = 2): 0.123 -> 0.109 ms at
 // 2^24 against two per SM (scripts/mb/probe_oq.sh: 4 per SM or 256-/384-thread CTAs were slower)
+// Programmatic dependent launch of k_offq_hist and k_offq_overflow (their launch latency and the
+// histogram CTAs' bin zeroing overlap the previous kernel's last wave)
+#ifndef MGP_OFFQ_PDL
+#define MGP_OFFQ_PDL 1
+#endif
 #ifndef MGP_OFFQ_MINB
 #define MGP_OFFQ_MINB 3
 #endif
@@ -1237,6 +1242,11 @@ __global__ void __launch_bounds__(THREADS, MGP_OFFQ_MINB) k_offq_scatter(const i
   __shared__ uint32_t wsum[THREADS / 32];
   const uint32_t trash = (uint32_t)K << OFFB_BITS;
   bool oob = false;
+#if MGP_OFFQ_PDL
+  // let k_offq_hist's CTAs become resident in the slots the last scatter wave leaves free (they
+  // zero their bins, then wait for this grid's completion in griddepcontrol.wait)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
   {
     for (int b = threadIdx.x; b <= K; b += THREADS) cnt[b] = 0;
     const int64_t t0 = (int64_t)blockIdx.x * TILE;
@@ -1265,6 +1275,9 @@ __global__ void __launch_bounds__(THREADS, MGP_OFFQ_MINB) k_offq_scatter(const i
     }
 #pragma unroll
     for (int q = 0; q < PER; ++q) atomicAdd(&cnt[key[q] >> OFFB_BITS], 1u);
+#if MGP_OFFQ_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // k_offq_zero complete: cursors and flag zeroed
+#endif
     __syncthreads();  // counts complete
     // exclusive scan of the bucket counts; the queue reservations are issued here and their
     // results consumed after the shared-memory sort, which hides the contended atomics' latency
@@ -1344,6 +1357,15 @@ __global__ void __launch_bounds__(THREADS, MGP_OFFQ_MINB) k_offq_scatter(const i
   if (oob) atomicExch(bad, 1);
 }
 
+// zero the queue cursors + overflow length (k1 words) and the caller's out-of-range flag
+__global__ void __launch_bounds__(1024) k_offq_zero(uint32_t* __restrict__ ctr, int k1, int* bad) {
+#if MGP_OFFQ_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+  for (int q = threadIdx.x; q < k1; q += 1024) ctr[q] = 0u;
+  if (bad && threadIdx.x == 0) *bad = 0;
+}
+
 __global__ void __launch_bounds__(512) k_offq_hist(const uint16_t* __restrict__ queue, uint32_t cap,
                                                    const uint32_t* __restrict__ gcur, int64_t n,
                                                    int64_t* __restrict__ counts) {
@@ -1351,6 +1373,10 @@ __global__ void __launch_bounds__(512) k_offq_hist(const uint16_t* __restrict__ 
   uint32_t* bins = reinterpret_cast<uint32_t*>(offq_smem);
   const int b = blockIdx.x;
   for (int q = threadIdx.x; q < OFFB_BINS / 4; q += 512) reinterpret_cast<uint4*>(bins)[q] = make_uint4(0, 0, 0, 0);
+#if MGP_OFFQ_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // k_offq_scatter complete, its queues visible
+#endif
   __syncthreads();
   const uint32_t m = min(gcur[b], cap);
   const uint16_t* __restrict__ qb = queue + (size_t)b * cap;  // cap % 8 == 0: 16-byte aligned
@@ -1378,6 +1404,9 @@ __global__ void __launch_bounds__(512) k_offq_hist(const uint16_t* __restrict__ 
 
 __global__ void k_offq_overflow(const uint32_t* __restrict__ ovf, const uint32_t* __restrict__ novf,
                                 int64_t* __restrict__ counts) {
+#if MGP_OFFQ_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // k_offq_hist complete (the counts it adds to)
+#endif
   const uint32_t m = *novf;
   for (uint32_t q0 = blockIdx.x * blockDim.x; q0 < m; q0 += gridDim.x * blockDim.x) {
     const uint32_t q = q0 + threadIdx.x;

@@ -80,3 +80,27 @@ def test_queued_histogram_many_buckets(mg):
         assert np.array_equal(got.cpu().numpy(), np.bincount(a, minlength=n))
         del got
         torch.cuda.empty_cache()
+
+
+def test_flag_reset_by_the_call(mg):
+    """mgp_offspring zeroes the caller's out-of-range flag itself (the queued path does it in
+    k_offq_zero, ahead of the programmatically launched scatter): a flag left at 1 by an earlier
+    call reads 0 after a valid call and 1 after an invalid one."""
+    from paper_2109_13504_b200 import _device as D
+    from paper_2109_13504_b200 import _lib
+
+    n = 1 << 21
+    rs = np.random.default_rng(5)
+    a = torch.from_numpy(rs.integers(0, n, n)).cuda()
+    counts = torch.empty(n, dtype=torch.int64, device="cuda")
+    flag = torch.ones(1, dtype=torch.int32, device="cuda")
+    L = _lib.lib()
+    _lib.check(L.mgp_offspring(D.ptr(a), n, n, D.ptr(counts), D.ptr(flag), D.stream_ptr()))
+    assert int(flag.item()) == 0
+    assert np.array_equal(counts.cpu().numpy(), np.bincount(a.cpu().numpy(), minlength=n))
+    a[777] = n
+    _lib.check(L.mgp_offspring(D.ptr(a), n, n, D.ptr(counts), D.ptr(flag), D.stream_ptr()))
+    assert int(flag.item()) == 1
+    a[777] = 0
+    _lib.check(L.mgp_offspring(D.ptr(a), n, n, D.ptr(counts), D.ptr(flag), D.stream_ptr()))
+    assert int(flag.item()) == 0
