@@ -441,7 +441,11 @@ __global__ void __launch_bounds__(RS_THREADS) k_megopolis_megores_f32(const __gr
   const uint32_t k0 = a.first ? i : (uint32_t)a.kstate[i];
   const float wk0 = tex1Dfetch<float>(a.tex, (int)k0);
   float wk = wk0;
-  int bstar = -1, amb = -1;
+  // the accepted partner index itself is carried (j is live for the fetch anyway): no per-round
+  // round-index register (one VIADD per round; 6.476 -> 6.456 ms, scripts/mb/probe_cj.sh) and the
+  // ambiguity is a flag
+  uint32_t kacc = k0;
+  bool amb = false;
   uint64_t x = megores_key(a.base, i, (uint64_t)a.b0);
 #pragma unroll 8
   for (int t = 0; t < a.cnt; ++t) {
@@ -451,18 +455,19 @@ __global__ void __launch_bounds__(RS_THREADS) k_megopolis_megores_f32(const __gr
     const float lo = __fmaf_rd(u1, wk, -wk);
     const float hi = __fmaf_ru(wk, 0x1p-22f, lo);
     const bool acc = hi < wj;  // strict: see the subnormal note above k_megopolis_megores_f32
-    if (!acc && lo <= wj) amb = t;
-    if (acc) { wk = wj; bstar = t; }
+    if (!acc && lo <= wj) amb = true;
+    if (acc) { wk = wj; kacc = j; }
     // x += M_CTR: ptxas hoists one * M_CTR and splits the add into IADD3 (ALU) + IMAD.X (FMA
     // pipe) -- 3% faster than IADD3 + IADD3.X (scripts/mb/mb_mego2.cu "ADDW u8": 6.84 -> 6.69 ms);
     // moving more of the hash to the heavy FMA pipe (IMAD.WIDE adds, IMAD.HI shifts, I2F for
     // the bracket) measured 1-12% slower there.
     x = add64_fma(x, a.one);
   }
-  if (amb >= 0) bstar = megores_exact_rounds(a, oc, i, wk0, POW2);
-  uint32_t k = k0;
-  if (bstar >= 0) k = mego_j<POW2>(ial, lane, oc.o[bstar], n);
-  store_result<ROWS>(a, (int64_t)i, i, k);
+  if (amb) {
+    const int bstar = megores_exact_rounds(a, oc, i, wk0, POW2);
+    kacc = bstar >= 0 ? mego_j<POW2>(ial, lane, oc.o[bstar], n) : k0;
+  }
+  store_result<ROWS>(a, (int64_t)i, i, kacc);
 }
 
 // ---------------------------------------------------------------------------
