@@ -515,25 +515,69 @@ int px_cumsum(const WT* w, int64_t n, WT* cum, cudaStream_t st) {
   mode = reinterpret_cast<int32_t*>(scarry + nsup);
   scnt = mode + nch;
   CUDA_TRY(sc.alloc(&tmp, tmp_bytes + 16));
-  CUDA_TRY(cudaMemsetAsync(zero, 0, zbytes, st));
   // 16-byte vector accesses in the streaming passes when both arrays allow them
   const bool vec = ((uintptr_t)w % 16 == 0) && ((uintptr_t)cum % 16 == 0);
-  if (vec) k_px_chunk_sum<WT, true><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, csum);
-  else k_px_chunk_sum<WT, false><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, csum);
+  // k_px_chunk_sum also zeroes `zero` (zbytes is a multiple of 4)
+  uint32_t* zw = reinterpret_cast<uint32_t*>(zero);
+  const int64_t zwords = (int64_t)(zbytes / 4);
+  if (vec) k_px_chunk_sum<WT, true><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, csum, zw, zwords);
+  else k_px_chunk_sum<WT, false><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, csum, zw, zwords);
   LAUNCH_CHECK("k_px_chunk_sum");
   CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, csum, est, (int)nch, st));
+#if MGP_PX_PDL
+  {  // programmatic dependent of the scan: the weight loads overlap its tail
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t la{};
+    la.gridDim = dim3((unsigned)nch);
+    la.blockDim = dim3(PX_THREADS);
+    la.stream = st;
+    la.attrs = at;
+    la.numAttrs = 1;
+    if (vec)
+      CUDA_TRY(cudaLaunchKernelEx(&la, k_px_aggregate<WT, true>, w, n, nch, (const double*)est, scnt, e0, agg, se0, sagg));
+    else
+      CUDA_TRY(cudaLaunchKernelEx(&la, k_px_aggregate<WT, false>, w, n, nch, (const double*)est, scnt, e0, agg, se0, sagg));
+  }
+#else
   if (vec) k_px_aggregate<WT, true><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, nch, est, scnt, e0, agg, se0, sagg);
   else k_px_aggregate<WT, false><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, nch, est, scnt, e0, agg, se0, sagg);
   LAUNCH_CHECK("k_px_aggregate");
+#endif
   const int64_t stage = px_stage_bytes(nsup);
   if (stage > 0)
     CUDA_TRY(cudaFuncSetAttribute(k_px_resolve<WT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PX_STAGE_MAX));
+#if MGP_PX_PDL
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(1);
+  lc.blockDim = dim3(PXR_THREADS);
+  lc.dynamicSmemBytes = (size_t)stage;
+  lc.stream = st;
+  lc.attrs = pdl;
+  lc.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&lc, k_px_resolve<WT>, w, n, nch, nsup, (const int32_t*)e0, (const Tx*)agg,
+                              (const int32_t*)se0, (const Tx*)sagg, carry, mode, scarry, smode, cum));
+  lc.gridDim = dim3((unsigned)nch);
+  lc.blockDim = dim3(PX_THREADS);
+  lc.dynamicSmemBytes = 0;
+  if (vec)
+    CUDA_TRY(cudaLaunchKernelEx(&lc, k_px_materialize<WT, true>, w, n, (const int32_t*)e0, (const Tx*)agg,
+                                (const WT*)scarry, (const int32_t*)smode, (const WT*)carry, (const int32_t*)mode, cum));
+  else
+    CUDA_TRY(cudaLaunchKernelEx(&lc, k_px_materialize<WT, false>, w, n, (const int32_t*)e0, (const Tx*)agg,
+                                (const WT*)scarry, (const int32_t*)smode, (const WT*)carry, (const int32_t*)mode, cum));
+#else
   k_px_resolve<WT><<<1, PXR_THREADS, (size_t)stage, st>>>(w, n, nch, nsup, e0, agg, se0, sagg, carry, mode, scarry,
                                                           smode, cum);
   LAUNCH_CHECK("k_px_resolve");
   if (vec) k_px_materialize<WT, true><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, e0, agg, scarry, smode, carry, mode, cum);
   else k_px_materialize<WT, false><<<(unsigned)nch, PX_THREADS, 0, st>>>(w, n, e0, agg, scarry, smode, carry, mode, cum);
   LAUNCH_CHECK("k_px_materialize");
+#endif
   return 0;
 }
 

@@ -44,6 +44,11 @@
 
 namespace mgp {
 
+// k_px_resolve and k_px_materialize launched as programmatic dependents of the kernel before
+#ifndef MGP_PX_PDL
+#define MGP_PX_PDL 1
+#endif
+
 constexpr int PX_THREADS = 256;
 constexpr int PX_PER_THREAD = 4;
 constexpr int PX_CHUNK = PX_THREADS * PX_PER_THREAD;  // 1024 elements per chunk
@@ -308,10 +313,14 @@ __device__ __forceinline__ Tx px_warp_scan(Tx t) {
 }
 
 template <typename WT, bool VEC>
-__global__ void __launch_bounds__(PX_THREADS) k_px_chunk_sum(const WT* __restrict__ w, int64_t n, double* csum) {
+__global__ void __launch_bounds__(PX_THREADS) k_px_chunk_sum(const WT* __restrict__ w, int64_t n, double* csum,
+                                                             uint32_t* __restrict__ zero, int64_t zwords) {
   __shared__ double red[PX_THREADS / 32];
   WT v[PX_PER_THREAD];
   px_load4<WT, VEC>(w, (int64_t)blockIdx.x * PX_CHUNK + threadIdx.x * PX_PER_THREAD, n, v);
+  // the counters / carries / modes the later passes expect zeroed (replaces a memset node)
+  for (int64_t q = (int64_t)blockIdx.x * PX_THREADS + threadIdx.x; q < zwords; q += (int64_t)gridDim.x * PX_THREADS)
+    zero[q] = 0u;
   double s = 0.0;
 #pragma unroll
   for (int j = 0; j < PX_PER_THREAD; ++j) s += (double)v[j];
@@ -342,6 +351,9 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_aggregate(const WT* __restric
   const int64_t c = blockIdx.x;
   WT v[PX_PER_THREAD];
   px_load4<WT, VEC>(w, c * PX_CHUNK + tid * PX_PER_THREAD, n, v);
+#if MGP_PX_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the scan of the chunk sums complete
+#endif
   const int e0 = PxFp<WT>::expo((WT)est[c]);
   uint32_t wmax = 0;
   if constexpr (sizeof(WT) == 4) wmax = px_wmax_bits(reinterpret_cast<const float*>(v));
@@ -773,6 +785,12 @@ __global__ void __launch_bounds__(PXR_THREADS, 1) k_px_resolve(const WT* __restr
   // super-chunk aggregates staged in shared memory when the launch provides room (one bulk
   // copy instead of a global round trip per super window)
   extern __shared__ __align__(16) unsigned char px_smem[];
+#if MGP_PX_PDL
+  // k_px_materialize may launch now: its first wave loads its weights while this CTA runs and
+  // then waits in griddepcontrol.wait for this grid
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // k_px_aggregate complete
+#endif
   const bool staged = px_stage_bytes(nsup) != 0 && dyn_smem_size() >= px_stage_bytes(nsup);
   if (staged) {
     Tx* ssagg = reinterpret_cast<Tx*>(px_smem);
@@ -858,6 +876,9 @@ __global__ void __launch_bounds__(PX_THREADS) k_px_materialize(const WT* __restr
   const int64_t base = c * PX_CHUNK + threadIdx.x * PX_PER_THREAD;
   WT v[PX_PER_THREAD];
   px_load4<WT, VEC>(w, base, n, v);  // in flight while the carry-in is composed
+#if MGP_PX_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // k_px_resolve complete (carries, modes)
+#endif
   if (threadIdx.x < 32) {
     // everything the carry-in may need in one round trip (independent loads), then select
     const int64_t sp = c / PX_SUPER;
