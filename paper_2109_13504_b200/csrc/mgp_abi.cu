@@ -600,20 +600,43 @@ int px_search(int kind, const void* cum, int dtype, int64_t n, uint64_t seed, in
     int32_t* start = nullptr;
     CUDA_TRY(sc.alloc(&start, sizeof(int32_t) * (K + 1)));
     const unsigned kg = (unsigned)std::min<int64_t>((K + 256) / 256, 148 * 16);
+    // each kernel a programmatic dependent of the one before (griddepcontrol.wait at its top):
+    // the launch latency overlaps the previous kernel's tail (MGP_PX_PDL)
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = MGP_PX_PDL;
+    cudaLaunchConfig_t la{};
+    la.blockDim = dim3(256);
+    la.stream = st;
+    la.attrs = at;
+    la.numAttrs = 1;
     if (dtype == MGP_F32) {
-      k_multinomial_buckets<float><<<kg, 256, 0, st>>>((const float*)cum, n, K, start);
-      k_multinomial<float><<<grid, 256, 0, st>>>((const float*)cum, n, base, p0, p_end, K, start, anc);
+      la.gridDim = dim3(kg);
+      CUDA_TRY(cudaLaunchKernelEx(&la, k_multinomial_buckets<float>, (const float*)cum, n, K, start));
+      la.gridDim = dim3(grid);
+      CUDA_TRY(cudaLaunchKernelEx(&la, k_multinomial<float>, (const float*)cum, n, base, p0, p_end, K,
+                                  (const int32_t*)start, anc));
     } else {
-      k_multinomial_buckets<double><<<kg, 256, 0, st>>>((const double*)cum, n, K, start);
-      k_multinomial<double><<<grid, 256, 0, st>>>((const double*)cum, n, base, p0, p_end, K, start, anc);
+      la.gridDim = dim3(kg);
+      CUDA_TRY(cudaLaunchKernelEx(&la, k_multinomial_buckets<double>, (const double*)cum, n, K, start));
+      la.gridDim = dim3(grid);
+      CUDA_TRY(cudaLaunchKernelEx(&la, k_multinomial<double>, (const double*)cum, n, base, p0, p_end, K,
+                                  (const int32_t*)start, anc));
     }
-    LAUNCH_CHECK("k_multinomial");
   } else {
     const double u0 = (double)(mix64(megores_key(megores_base(seed), GLOBAL_OFFSET_LANE, 0)) >> 11) * 0x1p-53;
     const unsigned sg = (unsigned)std::min<int64_t>((cnt / PXS_RUN + 256) / 256, 148 * 64);
-    if (dtype == MGP_F32) k_systematic<float><<<sg, 256, 0, st>>>((const float*)cum, n, u0, p0, p_end, anc);
-    else k_systematic<double><<<sg, 256, 0, st>>>((const double*)cum, n, u0, p0, p_end, anc);
-    LAUNCH_CHECK("k_systematic");
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = MGP_PX_PDL;
+    cudaLaunchConfig_t la{};
+    la.gridDim = dim3(sg);
+    la.blockDim = dim3(256);
+    la.stream = st;
+    la.attrs = at;
+    la.numAttrs = 1;
+    if (dtype == MGP_F32) CUDA_TRY(cudaLaunchKernelEx(&la, k_systematic<float>, (const float*)cum, n, u0, p0, p_end, anc));
+    else CUDA_TRY(cudaLaunchKernelEx(&la, k_systematic<double>, (const double*)cum, n, u0, p0, p_end, anc));
   }
   return 0;
 }

@@ -1051,6 +1051,9 @@ __device__ __forceinline__ WT pxm_bound(double total, int64_t b, int64_t K) {
 
 template <typename WT>
 __global__ void k_multinomial_buckets(const WT* __restrict__ cum, int64_t n, int64_t K, int32_t* __restrict__ start) {
+#if MGP_PX_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // launched as a programmatic dependent (px_search)
+#endif
   const double total = (double)cum[n - 1];
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= K; b += (int64_t)gridDim.x * blockDim.x)
     start[b] = (int32_t)(b == 0 ? pxs_upper(cum, 0, n, (WT)0) - 0 : pxs_upper(cum, 0, n, pxm_bound<WT>(total, b, K)));
@@ -1059,6 +1062,9 @@ __global__ void k_multinomial_buckets(const WT* __restrict__ cum, int64_t n, int
 template <typename WT>
 __global__ void k_multinomial(const WT* __restrict__ cum, int64_t n, uint64_t base, int64_t p0, int64_t p_end,
                               int64_t K, const int32_t* __restrict__ start, int64_t* __restrict__ anc) {
+#if MGP_PX_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // launched as a programmatic dependent (px_search)
+#endif
   const double total = (double)cum[n - 1];
   const double kscale = (double)K / total;  // the bucket guess only: exact corrections follow
   for (int64_t i = p0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p_end; i += (int64_t)gridDim.x * blockDim.x) {
@@ -1086,6 +1092,9 @@ constexpr int PXS_RUN = 16;
 template <typename WT>
 __global__ void k_systematic(const WT* __restrict__ cum, int64_t n, double u0, int64_t p0, int64_t p_end,
                              int64_t* __restrict__ anc) {
+#if MGP_PX_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // launched as a programmatic dependent (px_search)
+#endif
   const double total = (double)cum[n - 1];
   const int64_t nrun = (p_end - p0 + PXS_RUN - 1) / PXS_RUN;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrun; r += (int64_t)gridDim.x * blockDim.x) {
