@@ -201,8 +201,16 @@ int pw_reduce(const Elem& e, const WT* wraw, int64_t n, PwOut out, cudaStream_t 
   else
     k_pw_chunks<Elem, WT, STATS><<<(unsigned)nch, PW_THREADS, 0, st>>>(e, wraw, n, depth, heap, cst);
   LAUNCH_CHECK("k_pw_chunks");
-  k_pw_final<<<1, 1024, 0, st>>>(heap, depth, n, cst, out);
-  LAUNCH_CHECK("k_pw_final");
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = MGP_PW_PDL;
+  cudaLaunchConfig_t la{};
+  la.gridDim = dim3(1);
+  la.blockDim = dim3(1024);
+  la.stream = st;
+  la.attrs = at;
+  la.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&la, k_pw_final, heap, depth, n, (const WStats*)cst, out));
   return 0;
 }
 

@@ -829,9 +829,17 @@ __device__ __forceinline__ void wtally_observe(WTally<WT>& c, WT v) {
 // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) by xor-shuffles (IEEE addition commutes exactly),
 // then the n % 8 tail sequentially -- numpy's leaf order.  Internal nodes are combined
 // bottom-up.  heap[2^D + c] receives the chunk sum.
+// k_pw_final launched as a programmatic dependent of the chunk pass (its launch and residency
+// overlap the chunk pass's last wave)
+#ifndef MGP_PW_PDL
+#define MGP_PW_PDL 1
+#endif
 template <class Elem, typename WT, bool STATS>
 __global__ void __launch_bounds__(PW_THREADS) k_pw_chunks(Elem e, const WT* wraw, int64_t n, int depth,
                                                           double* heap, WStats* cstats) {
+#if MGP_PW_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // k_pw_final may become resident
+#endif
   __shared__ double s_el[pw_sidx(PW_CHUNK)];
   __shared__ int32_t s_lo[PW_HEAP];
   __shared__ int32_t s_len[PW_HEAP];
@@ -936,6 +944,9 @@ __global__ void __launch_bounds__(PW_THREADS) k_pw_chunks(Elem e, const WT* wraw
 template <class Elem, typename WT, bool STATS>
 __global__ void __launch_bounds__(PW_THREADS) k_pw_chunks4096(Elem e, const WT* wraw, int depth, double* heap,
                                                               WStats* cstats) {
+#if MGP_PW_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // k_pw_final may become resident
+#endif
   __shared__ double s_leaf[32];
   __shared__ WStats s_red[PW_THREADS / 32];
   const int64_t lo0 = (int64_t)blockIdx.x * PW_CHUNK;
@@ -1003,6 +1014,9 @@ struct PwOut {
 
 __global__ void __launch_bounds__(1024) k_pw_final(double* heap, int depth, int64_t n, const WStats* cstats,
                                                    PwOut out) {
+#if MGP_PW_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the chunk pass complete
+#endif
   for (int lvl = depth - 1; lvl >= 0; --lvl) {
     const int64_t h0 = 1ll << lvl, h1 = 2ll << lvl;
     for (int64_t h = h0 + threadIdx.x; h < h1; h += blockDim.x) heap[h] = __dadd_rn(heap[2 * h], heap[2 * h + 1]);
