@@ -802,6 +802,9 @@ int plan_free(Plan& p, cudaStream_t st) {
 #ifndef MGP_HOST_CHUNKS
 #define MGP_HOST_CHUNKS 16  // lower/upper chunk pairs of the half-split host path
 #endif
+#ifndef MGP_BATCH_LAST_CHUNKED
+#define MGP_BATCH_LAST_CHUNKED 1
+#endif
 #ifndef MGP_HOST_TAIL_SPLIT
 #define MGP_HOST_TAIL_SPLIT 1
 #endif
@@ -1512,7 +1515,46 @@ int mgp_resample_host_batch(int kind, const void* const* h_w, int dtype, int64_t
     const int flags = (hs.n_zero == 0) ? MGP_FLAG_NONZERO : 0;
     BTRY(make_plan(plans[q], kind, d_w[q], dtype, n, bk, seeds[k], warp, partition_bytes, strict, rng, flags));
     BTRY(plan_alloc(plans[q], st));
-    BTRY(run_range(plans[q], 0, n, d_anc[q], st));
+    Plan& pl = plans[q];
+    const bool half_ok = plan_half_ok(pl);
+    const bool chunk_ok = !(plan_uses_w32(pl) && pl.kind == MGP_KIND_MEGOPOLIS && pl.b > OFF_CAP);
+    if (MGP_BATCH_LAST_CHUNKED && k == count - 1 && count > 1 && (n >> 20) > 1 && (half_ok || chunk_ok)) {
+      // The last job has no next kernel to hide its download behind: run it in particle chunks
+      // (the single-call host entry's schedule, last chunk split) with each chunk's download
+      // queued behind its kernel, so only a fraction of the 8N-byte download follows the last
+      // kernel instead of all of it (earlier jobs' downloads overlap the next job's kernel).
+      const int64_t nchunk = std::min<int64_t>(MGP_HOST_CHUNKS, n >> 20);
+      int e = 4;  // hc->ev[0..3] are kern_done / d2h_done
+      if (half_ok) {
+        pl.half = true;
+        const int64_t half = n / 2;
+        const std::vector<int64_t> bnd = host_chunk_bounds(half, nchunk, 128, true);
+        for (size_t c = 0; c + 1 < bnd.size(); ++c) {
+          const int64_t c0 = bnd[c], c1 = bnd[c + 1];
+          BTRY(run_range(pl, c0, c1, d_anc[q], st));
+          cudaEvent_t ev = hc->ev[e++];
+          BCUDA(cudaEventRecord(ev, st));
+          BCUDA(cudaStreamWaitEvent(cp, ev, 0));
+          BCUDA(cudaMemcpyAsync(h_anc[k] + c0, d_anc[q] + c0, sizeof(int64_t) * (c1 - c0), cudaMemcpyDeviceToHost, cp));
+          BCUDA(cudaMemcpyAsync(h_anc[k] + half + c0, d_anc[q] + half + c0, sizeof(int64_t) * (c1 - c0),
+                                cudaMemcpyDeviceToHost, cp));
+        }
+      } else {
+        const std::vector<int64_t> bnd = host_chunk_bounds(n, nchunk, 256, true);
+        for (size_t c = 0; c + 1 < bnd.size(); ++c) {
+          const int64_t c0 = bnd[c], c1 = bnd[c + 1];
+          BTRY(run_range(pl, c0, c1, d_anc[q], st));
+          cudaEvent_t ev = hc->ev[e++];
+          BCUDA(cudaEventRecord(ev, st));
+          BCUDA(cudaStreamWaitEvent(cp, ev, 0));
+          BCUDA(cudaMemcpyAsync(h_anc[k] + c0, d_anc[q] + c0, sizeof(int64_t) * (c1 - c0), cudaMemcpyDeviceToHost, cp));
+        }
+      }
+      BCUDA(cudaEventRecord(kern_done[q], st));
+      BCUDA(cudaEventRecord(d2h_done[q], cp));
+      continue;
+    }
+    BTRY(run_range(pl, 0, n, d_anc[q], st));
     BCUDA(cudaEventRecord(kern_done[q], st));
     BCUDA(cudaStreamWaitEvent(cp, kern_done[q], 0));
     BCUDA(cudaMemcpyAsync(h_anc[k], d_anc[q], sizeof(int64_t) * n, cudaMemcpyDeviceToHost, cp));

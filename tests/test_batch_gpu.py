@@ -71,3 +71,31 @@ def test_batch_pinned_aliased_outputs_and_errors(mg):
         mg.resample_batch("megopolis", bad, 0, [1, 2, 3])
     with pytest.raises(ValueError):
         mg.resample_batch("megopolis", ws[:2], 0, [1])
+
+
+@pytest.mark.parametrize("kind,part,rng,n", [("megopolis", None, "philox", 1 << 22), ("megopolis", None, "megores", 1 << 21),
+                                             ("megopolis", None, "megores", (1 << 21) + 4096),
+                                             ("c2", 128, "philox", 3 << 20), ("systematic", None, "megores", 1 << 21)])
+def test_batch_last_job_chunked(mg, kind, part, rng, n):
+    """n >= 2^21: the batch's last job runs in particle chunks (last chunk split) with per-chunk
+    downloads (MGP_BATCH_LAST_CHUNKED); every job, the chunked last one included, equals one
+    mgp_resample_host call, into page-locked outputs."""
+    import ctypes
+
+    from paper_2109_13504_b200 import _lib
+    from paper_2109_13504_b200.resample import abi_partition_bytes
+
+    count = 3
+    ws = [torch.from_numpy(w).pin_memory().numpy() for w in jobs(n, count, 9)]
+    outs = [torch.empty(n, dtype=torch.int64).pin_memory().numpy() for _ in range(count)]
+    seeds = [5 * k + 2 for k in range(count)]
+    pc = mg.PartitionConfig(part) if part else None
+    got, bs = mg.resample_batch(kind, ws, 0, seeds, part=pc, rng=rng, out=outs)
+    pb = abi_partition_bytes(part, mg.WarpConfig()) if part else 0
+    for k in range(count):
+        one = np.empty(n, dtype=np.int64)
+        bu = ctypes.c_int32(0)
+        _lib.check(_lib.lib().mgp_resample_host(_lib.KIND[kind], ws[k].ctypes.data, 0, n, 0, 0.01, seeds[k], 32, pb, 1,
+                                                _lib.RNG[rng], one.ctypes.data, ctypes.byref(bu), -1))
+        assert bs[k] == bu.value, k
+        assert np.array_equal(got[k], one), (kind, rng, n, k)
