@@ -21,6 +21,12 @@
 #include <mutex>
 #include <thread>
 #include <vector>
+#if defined(__x86_64__)
+#include <emmintrin.h>
+#endif
+#ifndef MGP_COPY_NT
+#define MGP_COPY_NT 1
+#endif
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -886,13 +892,40 @@ class HostPool {
   // n bytes in parallel pieces of at least 1 MiB
   void copy(void* dst, const void* src, size_t n) {
     const size_t piece = std::max<size_t>(1 << 20, (n + nthreads_ - 1) / nthreads_);
-    if (n <= piece) { std::memcpy(dst, src, n); return; }
+    if (n <= piece) { copy_nt(dst, src, n); return; }
     std::vector<std::function<void()>> tasks;
     for (size_t off = 0; off < n; off += piece) {
       const size_t len = std::min(piece, n - off);
-      tasks.push_back([=] { std::memcpy((char*)dst + off, (const char*)src + off, len); });
+      tasks.push_back([=] { copy_nt((char*)dst + off, (const char*)src + off, len); });
     }
     wait(submit(std::move(tasks)));
+  }
+  // memcpy with streaming (non-temporal) stores for the 16-byte-aligned body: the staged data is
+  // written once and not read back by this thread, so the stores skip the read-for-ownership of
+  // every destination line (glibc's memcpy switches to streaming stores only far above the
+  // 1 MiB pieces used here)
+  static void copy_nt(void* dst, const void* src, size_t n) {
+#if MGP_COPY_NT && defined(__x86_64__)
+    char* d = (char*)dst;
+    const char* s = (const char*)src;
+    const size_t head = (16 - ((uintptr_t)d & 15)) & 15;
+    if (n < 4096 || head > n) { std::memcpy(d, s, n); return; }
+    std::memcpy(d, s, head);
+    d += head; s += head; n -= head;
+    const size_t body = n & ~(size_t)63;
+    for (size_t q = 0; q < body; q += 64) {
+      const __m128i a = _mm_loadu_si128((const __m128i*)(s + q)), b = _mm_loadu_si128((const __m128i*)(s + q + 16));
+      const __m128i c = _mm_loadu_si128((const __m128i*)(s + q + 32)), e = _mm_loadu_si128((const __m128i*)(s + q + 48));
+      _mm_stream_si128((__m128i*)(d + q), a);
+      _mm_stream_si128((__m128i*)(d + q + 16), b);
+      _mm_stream_si128((__m128i*)(d + q + 32), c);
+      _mm_stream_si128((__m128i*)(d + q + 48), e);
+    }
+    _mm_sfence();
+    std::memcpy(d + body, s + body, n - body);
+#else
+    std::memcpy(dst, src, n);
+#endif
   }
 
  private:
